@@ -1,0 +1,248 @@
+// One-CTA symmetric eigen-solver (parallel cyclic Jacobi) and the
+// re-orthonormalisation used by basis expansion.
+//
+// The reference truncates with a thin SVD of each unfolding
+// (Eigen::BDCSVD, truncated_svd.hpp:29-45). Here the same spectrum is taken
+// from the Gram G = M M^T (lambda = sigma^2, eigenvectors = left singular
+// vectors), which the streaming kernels produce in one pass over the batch;
+// the n x n eigenproblem (n <= a few hundred) runs in a single CTA.
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace htr {
+namespace {
+
+constexpr int kJacobiThreads = 1024;
+constexpr int64_t kSmemMaxN = 112;  // 2 * 112^2 * 8 B = 196 KB of shared memory
+
+__global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __restrict__ G, int n,
+                                                                double* __restrict__ lambda,
+                                                                double* __restrict__ Vout, double* gwork,
+                                                                int in_smem) {
+    extern __shared__ double smem[];
+    __shared__ int pos[1024];
+    __shared__ double cs[512], sn[512];
+    __shared__ int prs[512], qrs[512];
+    __shared__ int rotated;
+
+    const int tid = threadIdx.x, nt = blockDim.x;
+    double* A = in_smem ? smem : gwork;
+    double* V = in_smem ? smem + static_cast<int64_t>(n) * n : gwork + static_cast<int64_t>(n) * n;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    for (int64_t i = tid; i < nn; i += nt) {
+        const int64_t r = i % n, c = i / n;
+        // symmetrise defensively: the Gram kernels are exact mirrors already
+        A[i] = 0.5 * (G[r + n * c] + G[c + n * r]);
+        V[i] = r == c ? 1.0 : 0.0;
+    }
+    const int m = n + (n & 1);
+    for (int i = tid; i < m; i += nt) pos[i] = i;
+    __syncthreads();
+
+    const int half = m / 2;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        if (tid == 0) rotated = 0;
+        __syncthreads();
+        for (int round = 0; round < m - 1; ++round) {
+            // phase 1: rotations for the disjoint pairs of this round
+            for (int i = tid; i < half; i += nt) {
+                int p = pos[i], q = pos[m - 1 - i];
+                if (p > q) { const int t = p; p = q; q = t; }
+                double c = 1.0, s = 0.0;
+                if (q < n) {
+                    const double app = A[p + static_cast<int64_t>(n) * p];
+                    const double aqq = A[q + static_cast<int64_t>(n) * q];
+                    const double apq = A[p + static_cast<int64_t>(n) * q];
+                    if (fabs(apq) > 1e-300 && fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
+                        const double tau = (aqq - app) / (2.0 * apq);
+                        double t;
+                        if (fabs(tau) > 1e150) t = 0.5 / tau;
+                        else t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                        rotated = 1;
+                    }
+                }
+                cs[i] = c; sn[i] = s; prs[i] = p; qrs[i] = q;
+            }
+            __syncthreads();
+            // phase 2: rows p, q of A  (A <- J^T A)
+            const int64_t items = static_cast<int64_t>(half) * n;
+            for (int64_t it = tid; it < items; it += nt) {
+                const int i = static_cast<int>(it / n), j = static_cast<int>(it % n);
+                const double s = sn[i];
+                if (s == 0.0) continue;
+                const double c = cs[i];
+                const int p = prs[i], q = qrs[i];
+                const double ap = A[p + static_cast<int64_t>(n) * j], aq = A[q + static_cast<int64_t>(n) * j];
+                A[p + static_cast<int64_t>(n) * j] = c * ap - s * aq;
+                A[q + static_cast<int64_t>(n) * j] = s * ap + c * aq;
+            }
+            __syncthreads();
+            // phase 3: columns p, q of A and V  (A <- A J, V <- V J)
+            for (int64_t it = tid; it < items; it += nt) {
+                const int i = static_cast<int>(it / n), j = static_cast<int>(it % n);
+                const double s = sn[i];
+                if (s == 0.0) continue;
+                const double c = cs[i];
+                const int p = prs[i], q = qrs[i];
+                double* cp = A + static_cast<int64_t>(n) * p;
+                double* cq = A + static_cast<int64_t>(n) * q;
+                const double ap = cp[j], aq = cq[j];
+                cp[j] = c * ap - s * aq;
+                cq[j] = s * ap + c * aq;
+                double* vp = V + static_cast<int64_t>(n) * p;
+                double* vq = V + static_cast<int64_t>(n) * q;
+                const double xp = vp[j], xq = vq[j];
+                vp[j] = c * xp - s * xq;
+                vq[j] = s * xp + c * xq;
+            }
+            __syncthreads();
+            // the annihilated pair entries are exactly zero by construction
+            for (int i = tid; i < half; i += nt) {
+                if (sn[i] != 0.0) {
+                    const int p = prs[i], q = qrs[i];
+                    A[p + static_cast<int64_t>(n) * q] = 0.0;
+                    A[q + static_cast<int64_t>(n) * p] = 0.0;
+                }
+            }
+            // rotate the tournament positions (pos[0] fixed)
+            if (tid == 0) {
+                const int last = pos[m - 1];
+                for (int k = m - 1; k > 1; --k) pos[k] = pos[k - 1];
+                pos[1] = last;
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+        if (!rotated) break;
+        __syncthreads();
+    }
+
+    // sort eigenpairs by descending eigenvalue (stable on index)
+    for (int i = tid; i < n; i += nt) {
+        const double li = A[i + static_cast<int64_t>(n) * i];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+            const double lj = A[j + static_cast<int64_t>(n) * j];
+            rank += (lj > li) || (lj == li && j < i);
+        }
+        lambda[rank] = li;
+        for (int r = 0; r < n; ++r) Vout[r + static_cast<int64_t>(n) * rank] = V[r + static_cast<int64_t>(n) * i];
+    }
+}
+
+// --------------------------------------------------------------------------
+// Re-orthonormalisation of new directions (expand_core, ht_rise.hpp:53-79):
+// W <- (I - U U^T) W twice, then CholeskyQR2. One CTA; all sizes small.
+// --------------------------------------------------------------------------
+__device__ void block_project_out(const double* U, int64_t alpha, int64_t r, double* W, int64_t q, double* T) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int64_t ab = tid; ab < r * q; ab += nt) {
+        const int64_t a = ab % r, b = ab / r;
+        double s = 0.0;
+        for (int64_t i = 0; i < alpha; ++i) s = fma(U[i + alpha * a], W[i + alpha * b], s);
+        T[ab] = s;
+    }
+    __syncthreads();
+    for (int64_t ib = tid; ib < alpha * q; ib += nt) {
+        const int64_t i = ib % alpha, b = ib / alpha;
+        double s = 0.0;
+        for (int64_t a = 0; a < r; ++a) s = fma(U[i + alpha * a], T[a + r * b], s);
+        W[ib] -= s;
+    }
+    __syncthreads();
+}
+
+__device__ void block_cholqr(int64_t alpha, double* W, int64_t q, double* Gm) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int64_t ab = tid; ab < q * q; ab += nt) {
+        const int64_t a = ab % q, b = ab / q;
+        double s = 0.0;
+        for (int64_t i = 0; i < alpha; ++i) s = fma(W[i + alpha * a], W[i + alpha * b], s);
+        Gm[ab] = s;
+    }
+    __syncthreads();
+    // in-place lower Cholesky G = L L^T (right-looking)
+    for (int64_t k = 0; k < q; ++k) {
+        if (tid == 0) Gm[k + q * k] = sqrt(fmax(Gm[k + q * k], 1e-300));
+        __syncthreads();
+        const double dkk = Gm[k + q * k];
+        for (int64_t i = k + 1 + tid; i < q; i += nt) Gm[i + q * k] /= dkk;
+        __syncthreads();
+        const int64_t rem = q - k - 1;
+        for (int64_t ij = tid; ij < rem * rem; ij += nt) {
+            const int64_t i = k + 1 + ij % rem, j = k + 1 + ij / rem;
+            if (j <= i) Gm[i + q * j] -= Gm[i + q * k] * Gm[j + q * k];
+        }
+        __syncthreads();
+    }
+    // W <- W L^{-T}: each row w solves L x = w^T (forward substitution)
+    for (int64_t i = tid; i < alpha; i += nt) {
+        for (int64_t j = 0; j < q; ++j) {
+            double s = W[i + alpha * j];
+            for (int64_t k = 0; k < j; ++k) s -= Gm[j + q * k] * W[i + alpha * k];
+            W[i + alpha * j] = s / Gm[j + q * j];
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(512) orthonormalize_kernel(const double* U, int64_t alpha, int64_t r, double* W,
+                                                             int64_t q, double* info, double* work) {
+    double* T = work;                 // r * q
+    double* Gm = work + r * q;        // q * q
+    if (r > 0) {
+        block_project_out(U, alpha, r, W, q, T);
+        block_project_out(U, alpha, r, W, q, T);
+    }
+    block_cholqr(alpha, W, q, Gm);
+    block_cholqr(alpha, W, q, Gm);
+    // defect ||U^T W||_F and ||W||_F (expand_core's orthogonality check)
+    __shared__ double red[2][16];
+    double d = 0.0, w = 0.0;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int64_t ab = tid; ab < r * q; ab += nt) {
+        const int64_t a = ab % r, b = ab / r;
+        double s = 0.0;
+        for (int64_t i = 0; i < alpha; ++i) s = fma(U[i + alpha * a], W[i + alpha * b], s);
+        d = fma(s, s, d);
+    }
+    for (int64_t i = tid; i < alpha * q; i += nt) w = fma(W[i], W[i], w);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+        w += __shfl_xor_sync(0xffffffffu, w, o);
+    }
+    if ((tid & 31) == 0) { red[0][tid >> 5] = d; red[1][tid >> 5] = w; }
+    __syncthreads();
+    if (tid == 0) {
+        double sd = 0.0, sw = 0.0;
+        for (int k = 0; k < nt / 32; ++k) { sd += red[0][k]; sw += red[1][k]; }
+        info[0] = sqrt(sd);
+        info[1] = sqrt(sw);
+    }
+}
+
+}  // namespace
+
+void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, double* work, cudaStream_t s,
+                       int64_t* launches) {
+    const bool in_smem = n <= kSmemMaxN;
+    const size_t smem = in_smem ? 2 * sizeof(double) * static_cast<size_t>(n * n) : 0;
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    }
+    const int threads = n <= 32 ? 128 : (n <= 64 ? 256 : kJacobiThreads);
+    jacobi_kernel<<<1, threads, smem, s>>>(G, static_cast<int>(n), lambda, V, work, in_smem ? 1 : 0);
+    ++*launches;
+}
+
+void launch_orthonormalize_new(const double* U, int64_t alpha, int64_t r, double* W, int64_t q, double* info,
+                               double* work, cudaStream_t s, int64_t* launches) {
+    orthonormalize_kernel<<<1, 512, 0, s>>>(U, alpha, r, W, q, info, work);
+    ++*launches;
+}
+
+}  // namespace htr

@@ -1,0 +1,107 @@
+// htrise-b200 device kernels: declarations shared by the launch sites.
+//
+// All kernels are f64 and deterministic (fixed reduction trees, no FP64
+// atomics): every rank of a sharded run computes bit-identical results from
+// bit-identical inputs, which keeps the redundant per-rank eigen-truncations
+// in lock-step.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace htr {
+
+constexpr int kNumSMs = 148;  // B200; the launchers query the device anyway
+
+// ---------------------------------------------------------------------------
+// Generic strided contraction ("mode product engine").
+//   C(m, n1, n2) = alpha * sum_{k1<K1, k2<K2} A(m, k1, k2) * B(k1, k2, n1, n2)
+//                  + beta * C(m, n1, n2)
+// Offsets: A = m*sam + k1*sak1 + k2*sak2, B = k1*sbk1 + k2*sbk2 + n1*sbn1 +
+// n2*sbn2, C = m*scm + n1*scn1 + n2*scn2. Covers every mode product (leaf
+// projection U^T, reconstruction U, transfer split) and every mode-k Gram
+// Y_(k) Y_(k)^T of a canonical tensor without materialising an unfolding.
+// ---------------------------------------------------------------------------
+struct GemmDesc {
+    int64_t M = 1, N1 = 1, N2 = 1, K1 = 1, K2 = 1;
+    const double* A = nullptr;
+    int64_t sam = 0, sak1 = 0, sak2 = 0;
+    const double* B = nullptr;
+    int64_t sbk1 = 0, sbk2 = 0, sbn1 = 0, sbn2 = 0;
+    double* C = nullptr;
+    int64_t scm = 0, scn1 = 0, scn2 = 0;
+    double alpha = 1.0, beta = 0.0;
+    // residual-energy epilogue: instead of storing, accumulate
+    // sum (D(m,n) - acc)^2 with D addressed like C; one partial per CTA.
+    const double* D = nullptr;
+    double* energy_partials = nullptr;  // >= grid size entries
+};
+
+// Enqueue; returns the number of CTAs used for the energy epilogue (0 when
+// storing). `workspace` must hold gemm_workspace_doubles(desc) doubles.
+int64_t gemm_workspace_doubles(const GemmDesc& d, int num_sms);
+int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t s, int64_t* launches);
+
+// Sum of squares of n doubles -> out[0] (deterministic two-pass). partials
+// needs kReduceBlocks doubles. Also writes out[1] = 1.0 if any entry is
+// non-finite, else 0.0.
+constexpr int kReduceBlocks = 592;
+void launch_sumsq(const double* x, int64_t n, double* partials, double* out, cudaStream_t s,
+                  int64_t* launches);
+// out[0] = sum of n partials in index order (deterministic).
+void launch_sum_partials(const double* partials, int64_t n, double* out, cudaStream_t s, int64_t* launches);
+
+// Symmetric eigen-decomposition of an n x n column-major matrix G by
+// parallel cyclic Jacobi in one CTA. Writes eigenvalues (descending) to
+// lambda and the matching eigenvectors as columns of V (n x n, col-major).
+// `work` must hold 2*n*n doubles when n exceeds the shared-memory limit.
+void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, double* work, cudaStream_t s,
+                       int64_t* launches);
+
+// Rank rule of truncated_svd.hpp:74-99 on k = min(rows, cols) values
+// sigma_i^2 = max(lambda_i, 0). info[0] = rank, info[1] = discarded norm,
+// info[2] = trace (sum of lambda) used for the zero-input test.
+void launch_rank_rule(const double* lambda, int64_t k, int64_t n, double eps_abs, int64_t min_rank,
+                      const double* trace_src, double* info, cudaStream_t s, int64_t* launches);
+
+// Copy the first r columns of V (n x n) to U (n x r); when zero_input != 0
+// writes identity columns instead (truncated_svd.hpp:66-72).
+void launch_take_columns(const double* V, int64_t n, int64_t r, double* U, const double* info,
+                         cudaStream_t s, int64_t* launches);
+
+// dst (outer x (a_ext+extra) x inner-block) <- zero-padded copy along one axis:
+// src viewed as [inner, ext, outer] -> dst [inner, ext+extra, outer].
+void launch_pad_axis(const double* src, int64_t inner, int64_t ext, int64_t outer, int64_t extra, double* dst,
+                     cudaStream_t s, int64_t* launches);
+
+// Orthogonalise W (alpha x q) against U (alpha x r) twice, then CholeskyQR2,
+// in one CTA (ht_rise.hpp:53-79 expand_core with SURVEY §7.3 item 4). Writes
+// the orthonormal result back into W and the defect ||U^T W||_F, ||W||_F to
+// info[0..1].
+void launch_orthonormalize_new(const double* U, int64_t alpha, int64_t r, double* W, int64_t q, double* info,
+                               double* work, cudaStream_t s, int64_t* launches);
+
+// Fill dst[i] = value for n entries.
+void launch_fill(double* dst, int64_t n, double value, cudaStream_t s, int64_t* launches);
+
+// Fused all-leaf projection for 3-way batches [N0, N1, n2, S] on the FP64
+// tensor cores (DMMA): Z[a0,a1,a2,s] = sum X[i0,i1,i2,s] U0[i0,a0] U1[i1,a1]
+// U2[i2,a2] and sum X^2, in one read of X (K1).
+struct Fused3Args {
+    const double* Y = nullptr;
+    int64_t n2 = 0, S = 0;
+    const double* U0 = nullptr;  // N0 x r0
+    const double* U1 = nullptr;  // N1 x r1
+    const double* U2 = nullptr;  // n2 x r2
+    int r0 = 0, r1 = 0, r2 = 0;
+    double* Z = nullptr;          // r0*r1*r2 x S
+    double* zpart = nullptr;      // workspace
+    double* ysq_partials = nullptr;  // grid entries
+};
+// Whether the fused kernel supports this shape; returns the grid size used.
+bool fused3_supported(int64_t n0, int64_t n1, int r0, int r1, int r2);
+int64_t fused3_workspace_doubles(int64_t n0, int64_t n1, int64_t n2, int64_t S, int r0, int r1, int r2,
+                                 int num_sms);
+int launch_fused3(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches);
+
+}  // namespace htr

@@ -1,0 +1,945 @@
+// htrise-b200 native runtime: the reference's Alg. 1 (BHT-l2r, bht.hpp:251-350)
+// and Alg. 2 (HT-RISE, ht_rise.hpp:99-186) orchestrated on device-resident
+// data. The host walks the dimension tree (integer metadata) and enqueues
+// kernels on one stream; the only host round trips are the scalars that
+// decide control flow (ranks after a truncation, the skip test).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "runtime.hpp"
+
+namespace htr {
+
+void raise(htr_status code, const std::string& msg) { throw Error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) raise(HTR_ERR_CUDA, std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what);
+}
+
+Stream::Stream(int dev) : device(dev) {
+    HTR_CUDA(cudaSetDevice(dev));
+    HTR_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+}
+Stream::~Stream() {
+    if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    }
+}
+
+Buf::Buf(StreamPtr st_, int64_t n_) : st(std::move(st_)), n(n_) {
+    if (n > 0) HTR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(n) * sizeof(double), st->s));
+}
+Buf::~Buf() {
+    if (p && owned) cudaFreeAsync(p, st->s);
+}
+
+Index Rep::rank(NodeId id) const {
+    const TreeNode& n = tree.node(id);
+    if (n.kind == NodeKind::Root) raise(HTR_ERR_INVALID_ARGUMENT, "rank: root has no own rank");
+    const DT& c = core(id);
+    return n.kind == NodeKind::Leaf ? c.shape[1] : c.shape[2];
+}
+
+RankMap Rep::ranks() const {
+    RankMap r;
+    for (Index l = 1; l <= tree.depth(); ++l)
+        for (const TreeNode& n : tree.layer(l)) r[n.id] = rank(n.id);
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL (dlopen'd so that the process uses whichever libnccl torch loaded)
+// ---------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+    void* lib = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.lib) {
+        api.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!api.lib) raise(HTR_ERR_RUNTIME, std::string("cannot load libnccl.so.2: ") + dlerror());
+        api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(api.lib, "ncclGetUniqueId"));
+        api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(api.lib, "ncclCommInitRank"));
+        api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(api.lib, "ncclAllReduce"));
+        api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(api.lib, "ncclCommDestroy"));
+        api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(dlsym(api.lib, "ncclGetErrorString"));
+        if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy)
+            raise(HTR_ERR_RUNTIME, "libnccl.so.2 lacks required symbols");
+    }
+    return api;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) {
+        const char* m = nccl().getErrorString ? nccl().getErrorString(r) : "?";
+        raise(HTR_ERR_RUNTIME, std::string("NCCL error ") + m + " at " + what);
+    }
+}
+}  // namespace
+
+void comm_unique_id(uint8_t out[128]) {
+    ncclUniqueId id;
+    nccl_check(nccl().getUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, 128);
+}
+
+void comm_init(Context& c, const uint8_t uid[128], int nranks, int rank) {
+    if (nranks <= 1) {
+        c.nranks = 1;
+        c.rank = 0;
+        return;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, uid, 128);
+    ncclComm_t comm;
+    HTR_CUDA(cudaSetDevice(c.device));
+    nccl_check(nccl().commInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
+    c.nccl_comm = comm;
+    c.nranks = nranks;
+    c.rank = rank;
+}
+
+Context::Context(int dev) : device(dev) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        raise(HTR_ERR_NO_DEVICE, "htrise-b200 needs a CUDA device (sm_100a); none is visible");
+    if (dev < 0 || dev >= count) raise(HTR_ERR_NO_DEVICE, "device index out of range");
+    st = std::make_shared<Stream>(dev);
+    s = st->s;
+    HTR_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    cudaMemPool_t pool;
+    HTR_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    HTR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    HTR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_sc), 1024 * sizeof(double)));
+    d_sc = alloc(1024);
+    for (auto& e : ev) HTR_CUDA(cudaEventCreate(&e));
+}
+
+Context::~Context() {
+    if (s) cudaStreamSynchronize(s);
+    if (nccl_comm) nccl().commDestroy(static_cast<ncclComm_t>(nccl_comm));
+    for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+    if (h_sc) cudaFreeHost(h_sc);
+}
+
+void Context::allreduce(double* d, int64_t n) {
+    if (nranks <= 1 || n == 0) return;
+    nccl_check(nccl().allReduce(d, d, static_cast<size_t>(n), ncclDouble, ncclSum,
+                                static_cast<ncclComm_t>(nccl_comm), s),
+               "ncclAllReduce");
+}
+
+void Context::fetch(const double* d, int64_t n, double* host) {
+    if (n <= 0) return;
+    HTR_CUDA(cudaMemcpyAsync(host, d, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    HTR_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---------------------------------------------------------------------------
+// building blocks
+// ---------------------------------------------------------------------------
+
+void run_gemm(Context& c, const GemmDesc& d) {
+    const int64_t ws = gemm_workspace_doubles(d, c.num_sms);
+    BufPtr w = ws > 0 ? c.alloc(ws) : nullptr;
+    launch_gemm(d, w ? w->p : nullptr, c.num_sms, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+}
+
+namespace {
+struct Split {
+    int64_t I = 1, J = 1, O = 1;
+};
+Split split_at(const Shape& s, int mode) {
+    Split p;
+    for (int k = 0; k < mode; ++k) p.I *= s[static_cast<size_t>(k)];
+    p.J = s[static_cast<size_t>(mode)];
+    for (size_t k = static_cast<size_t>(mode) + 1; k < s.size(); ++k) p.O *= s[k];
+    return p;
+}
+}  // namespace
+
+DT mode_mul(Context& c, const DT& t, int mode, const double* Mp, int64_t Q, int64_t smq, int64_t smj) {
+    const Split sp = split_at(t.shape, mode);
+    Shape os = t.shape;
+    os[static_cast<size_t>(mode)] = Q;
+    DT out = c.tensor(os);
+    GemmDesc d;
+    d.M = Q;
+    d.N1 = sp.I;
+    d.N2 = sp.O;
+    d.K1 = sp.J;
+    d.K2 = 1;
+    d.A = Mp;
+    d.sam = smq;
+    d.sak1 = smj;
+    d.B = t.data();
+    d.sbk1 = sp.I;
+    d.sbn1 = 1;
+    d.sbn2 = sp.I * sp.J;
+    d.C = out.data();
+    d.scm = sp.I;
+    d.scn1 = 1;
+    d.scn2 = sp.I * Q;
+    run_gemm(c, d);
+    return out;
+}
+
+void residual_energy(Context& c, const DT& t, int mode, const double* U, int64_t r, const DT& coeff,
+                     double* slot) {
+    // D = t, acc = U * coeff along `mode`: sum (t - U coeff)^2 (bht.hpp:361)
+    const Split sp = split_at(t.shape, mode);
+    GemmDesc d;
+    d.M = sp.J;
+    d.N1 = sp.I;
+    d.N2 = sp.O;
+    d.K1 = r;
+    d.A = U;
+    d.sam = 1;
+    d.sak1 = sp.J;
+    d.B = coeff.data();
+    d.sbk1 = sp.I;
+    d.sbn1 = 1;
+    d.sbn2 = sp.I * r;
+    d.D = t.data();
+    d.scm = sp.I;
+    d.scn1 = 1;
+    d.scn2 = sp.I * sp.J;
+    const int64_t tiles = ((sp.I * sp.O + 63) / 64) * ((sp.J + 63) / 64);
+    BufPtr parts = c.alloc(tiles);
+    d.energy_partials = parts->p;
+    launch_gemm(d, nullptr, c.num_sms, c.s, &c.launches);
+    launch_sum_partials(parts->p, tiles, slot, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+}
+
+DT gram(Context& c, const DT& t, int mode, bool reduce) {
+    const Split sp = split_at(t.shape, mode);
+    DT G = c.tensor({sp.J, sp.J});
+    GemmDesc d;
+    d.M = sp.J;
+    d.N1 = sp.J;
+    d.N2 = 1;
+    d.K1 = sp.I;
+    d.K2 = sp.O;
+    d.A = t.data();
+    d.sam = sp.I;
+    d.sak1 = 1;
+    d.sak2 = sp.I * sp.J;
+    d.B = t.data();
+    d.sbk1 = 1;
+    d.sbk2 = sp.I * sp.J;
+    d.sbn1 = sp.I;
+    d.C = G.data();
+    d.scm = 1;
+    d.scn1 = sp.J;
+    run_gemm(c, d);
+    if (reduce) c.allreduce(G.data(), sp.J * sp.J);
+    return G;
+}
+
+void norm_sq(Context& c, const double* x, int64_t n, double* ysq, bool* nonfinite, bool reduce) {
+    BufPtr parts = c.alloc(kReduceBlocks);
+    launch_sumsq(x, n, parts->p, c.d_sc->p, c.s, &c.launches);
+    if (reduce) c.allreduce(c.d_sc->p, 2);
+    c.fetch(c.d_sc->p, 2, c.h_sc);
+    *ysq = c.h_sc[0];
+    if (nonfinite) *nonfinite = c.h_sc[1] != 0.0;
+}
+
+Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
+                         bool want_basis) {
+    const int64_t n = rows;
+    const int64_t k = std::min(rows, cols);
+    BufPtr lam = c.alloc(n);
+    BufPtr V = c.alloc(n * n);
+    BufPtr work = c.alloc(2 * n * n);
+    BufPtr info = c.alloc(4);
+    launch_jacobi_eig(G.data(), n, lam->p, V->p, work->p, c.s, &c.launches);
+    launch_rank_rule(lam->p, k, n, eps_abs, min_rank, nullptr, info->p, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+    double h[4];
+    c.fetch(info->p, 3, h);
+    Truncation t;
+    t.rank = static_cast<int64_t>(h[0]);
+    t.discarded = h[1];
+    const bool zero = h[2] == 0.0;
+    if (t.rank > 0) {
+        std::vector<double> l(static_cast<size_t>(t.rank));
+        c.fetch(lam->p, t.rank, l.data());
+        t.sigma.resize(static_cast<size_t>(t.rank));
+        for (int64_t i = 0; i < t.rank; ++i) t.sigma[static_cast<size_t>(i)] = zero ? 0.0 : std::sqrt(std::max(0.0, l[static_cast<size_t>(i)]));
+    }
+    if (want_basis) {
+        t.u = c.tensor({rows, t.rank});
+        launch_take_columns(V->p, n, t.rank, t.u.data(), info->p, c.s, &c.launches);
+        HTR_CUDA(cudaGetLastError());
+    }
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// input checks (bht.hpp:187-213) and tree plumbing
+// ---------------------------------------------------------------------------
+
+void check_batch_input(const Shape& ys, const DimensionTree& tree, const Shape* dims, const char* who) {
+    const Index order = static_cast<Index>(ys.size());
+    if (order != tree.dims() + 1)
+        raise(HTR_ERR_INVALID_ARGUMENT, std::string(who) + ": tensor order " + std::to_string(order) +
+                                            " does not match tree over " + std::to_string(tree.dims()) +
+                                            " dims plus batch");
+    if (order < 3) raise(HTR_ERR_INVALID_ARGUMENT, std::string(who) + ": need d >= 2 plus a batch axis");
+    for (Index e : ys)
+        if (e < 1) raise(HTR_ERR_INVALID_ARGUMENT, std::string(who) + ": extent < 1");
+    if (dims) {
+        for (Index k = 0; k < tree.dims(); ++k)
+            if (ys[static_cast<size_t>(k)] != (*dims)[static_cast<size_t>(k)])
+                raise(HTR_ERR_INVALID_ARGUMENT, std::string(who) + ": shape mismatch at mode " + std::to_string(k) +
+                                                    ": " + std::to_string(ys[static_cast<size_t>(k)]) + " vs " +
+                                                    std::to_string((*dims)[static_cast<size_t>(k)]));
+    }
+}
+
+DimensionTree tree_from_nodes(const htr_node* nodes, int64_t n) {
+    int32_t depth = -1;
+    for (int64_t i = 0; i < n; ++i) depth = std::max(depth, nodes[i].layer);
+    if (depth < 0) raise(HTR_ERR_INVALID_ARGUMENT, "DimensionTree: need a single root");
+    std::vector<std::vector<TreeNode>> layers(static_cast<size_t>(depth) + 1);
+    for (int64_t i = 0; i < n; ++i) {
+        const htr_node& h = nodes[i];
+        if (h.layer < 0) raise(HTR_ERR_INVALID_ARGUMENT, "DimensionTree: negative layer");
+        auto& layer = layers[static_cast<size_t>(h.layer)];
+        if (static_cast<int64_t>(layer.size()) <= h.pos) layer.resize(static_cast<size_t>(h.pos) + 1);
+        TreeNode t;
+        t.id = {h.layer, h.pos};
+        t.kind = h.kind == HTR_KIND_ROOT ? NodeKind::Root : h.kind == HTR_KIND_TRANSFER ? NodeKind::Transfer : NodeKind::Leaf;
+        t.leaf_dim = h.leaf_dim;
+        if (h.succ0 >= 0) t.successors = {{h.layer + 1, h.succ0}, {h.layer + 1, h.succ1}};
+        layer[static_cast<size_t>(h.pos)] = t;
+    }
+    try {
+        return DimensionTree::from_layers(std::move(layers));
+    } catch (const std::invalid_argument& e) {
+        raise(HTR_ERR_INVALID_ARGUMENT, e.what());
+    } catch (const std::out_of_range& e) {
+        raise(HTR_ERR_OUT_OF_RANGE, e.what());
+    }
+}
+
+void nodes_from_tree(const DimensionTree& t, std::vector<htr_node>& out) {
+    out.clear();
+    for (Index l = 0; l <= t.depth(); ++l)
+        for (const TreeNode& n : t.layer(l)) {
+            htr_node h;
+            h.layer = static_cast<int32_t>(n.id.layer);
+            h.pos = static_cast<int32_t>(n.id.pos);
+            h.kind = n.kind == NodeKind::Root ? HTR_KIND_ROOT : n.kind == NodeKind::Transfer ? HTR_KIND_TRANSFER : HTR_KIND_LEAF;
+            h.leaf_dim = static_cast<int32_t>(n.leaf_dim);
+            h.succ0 = n.successors.empty() ? -1 : static_cast<int32_t>(n.successors[0].pos);
+            h.succ1 = n.successors.empty() ? -1 : static_cast<int32_t>(n.successors[1].pos);
+            out.push_back(h);
+        }
+}
+
+namespace {
+
+double effective_eps_rel(double eps_rel) {
+    // bht.hpp:20-27
+    if (!(eps_rel >= 0) || eps_rel >= 1.0) raise(HTR_ERR_INVALID_ARGUMENT, "relative tolerance must lie in [0, 1)");
+    return eps_rel > 0 ? eps_rel : 1e-14;
+}
+
+double adaptive_budget(double eps_abs, double achieved_sq, Index remaining) {
+    // bht.hpp:227-245
+    if (remaining < 1) raise(HTR_ERR_INVALID_ARGUMENT, "adaptive_budget: no SVDs remaining");
+    const double budget = eps_abs * eps_abs;
+    double rem = budget - achieved_sq;
+    if (rem < 0) {
+        if (achieved_sq > budget * (1.0 + 1e-9) + 1e-300)
+            raise(HTR_ERR_RUNTIME, "adaptive_budget: error budget exhausted (achieved^2 = " +
+                                       std::to_string(achieved_sq) + " > eps_abs^2 = " + std::to_string(budget) + ")");
+        rem = 0.0;
+    }
+    return std::sqrt(rem) / std::sqrt(static_cast<double>(remaining));
+}
+
+Index svds_below(const DimensionTree& t, Index l) {
+    Index n = 0;
+    for (Index k = 1; k < l; ++k) n += t.layer_size(k);
+    return n;
+}
+
+/// Basis matrix view (alpha x r) of a non-root core (bht.hpp:81-86).
+struct Basis {
+    const double* p;
+    int64_t alpha, r;
+};
+Basis basis_of(const Rep& h, NodeId id) {
+    const DT& c = h.core(id);
+    if (h.tree.node(id).kind == NodeKind::Leaf) return {c.data(), c.shape[0], c.shape[1]};
+    return {c.data(), c.shape[0] * c.shape[1], c.shape[2]};
+}
+
+/// Layer extent list with the batch last (bht.hpp:312-321); leaves already
+/// projected by the fused kernel report their rank.
+Shape layer_extents(const Rep& h, Index l, const RankMap& ranks, int64_t batch, bool leaves_projected) {
+    Shape ext;
+    for (const TreeNode& n : h.tree.layer(l)) {
+        if (n.kind == NodeKind::Leaf)
+            ext.push_back(leaves_projected ? ranks.at(n.id) : h.dims[static_cast<size_t>(n.leaf_dim)]);
+        else
+            ext.push_back(ranks.at(n.successors[0]) * ranks.at(n.successors[1]));
+    }
+    ext.push_back(batch);
+    return ext;
+}
+
+DT project(Context& c, const DT& t, int mode, const Basis& b, double* energy_slot) {
+    if (b.alpha != t.shape[static_cast<size_t>(mode)])
+        raise(HTR_ERR_INVALID_ARGUMENT, "mode_multiply: factor/extent mismatch");
+    DT coeff = mode_mul(c, t, mode, b.p, b.r, b.alpha, 1);  // U^T
+    if (energy_slot) residual_energy(c, t, mode, b.p, b.r, coeff, energy_slot);
+    return coeff;
+}
+
+int64_t global_batch(Context& c, int64_t local) {
+    if (c.nranks <= 1) return local;
+    c.h_sc[0] = static_cast<double>(local);
+    HTR_CUDA(cudaMemcpyAsync(c.d_sc->p + 8, c.h_sc, sizeof(double), cudaMemcpyHostToDevice, c.s));
+    c.allreduce(c.d_sc->p + 8, 1);
+    double g = 0.0;
+    c.fetch(c.d_sc->p + 8, 1, &g);
+    return static_cast<int64_t>(std::llround(g));
+}
+
+std::shared_ptr<RootStore> new_root(Context& c, int64_t r11, int64_t r12, int64_t cap) {
+    auto rs = std::make_shared<RootStore>();
+    rs->r11 = r11;
+    rs->r12 = r12;
+    rs->cap = std::max<int64_t>(cap, 1);
+    rs->buf = c.alloc(r11 * r12 * rs->cap);
+    rs->committed = 0;
+    return rs;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// BHT-l2r (bht.hpp:251-350)
+// ---------------------------------------------------------------------------
+
+BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_rel, bool adaptive) {
+    check_batch_input(y.shape, tree, nullptr, "bht_l2r");
+    const Index d = tree.dims(), p = tree.depth();
+    const int64_t batch = y.shape[static_cast<size_t>(d)];
+    const int64_t gbatch = global_batch(c, batch);
+    double ysq = 0.0;
+    bool bad = false;
+    norm_sq(c, y.data(), y.size(), &ysq, &bad);
+    if (bad) raise(HTR_ERR_INVALID_ARGUMENT, "bht_l2r: non-finite input");
+    const double norm_y = std::sqrt(ysq);
+    const double eps_abs = effective_eps_rel(eps_rel) * norm_y;
+
+    BuildOut out;
+    std::memset(&out.report, 0, sizeof(out.report));
+    htr_build_report& rep = out.report;
+    rep.eps_nw_initial = eps_abs / std::sqrt(static_cast<double>(2 * d - 2));
+    rep.layer_norms[rep.n_layer_norms++] = norm_y;
+
+    auto h = std::make_shared<Rep>();
+    h->st = c.st;
+    h->tree = tree;
+    h->dims = Shape(y.shape.begin(), y.shape.end() - 1);
+    h->cores.resize(static_cast<size_t>(p) + 1);
+    for (Index l = 0; l <= p; ++l) h->cores[static_cast<size_t>(l)].resize(static_cast<size_t>(tree.layer_size(l)));
+    h->eps_rel = eps_rel;
+
+    auto record = [&](NodeId id, int64_t rank, double disc) {
+        if (rep.n_records < HTR_MAX_NODES) {
+            rep.rec_layer[rep.n_records] = static_cast<int32_t>(id.layer);
+            rep.rec_pos[rep.n_records] = static_cast<int32_t>(id.pos);
+            rep.rec_rank[rep.n_records] = rank;
+            rep.rec_discarded[rep.n_records] = disc;
+            ++rep.n_records;
+        }
+    };
+    auto push_norm = [&](const DT& t) {
+        double s = 0.0;
+        norm_sq(c, t.data(), t.size(), &s, nullptr);
+        if (rep.n_layer_norms < HTR_MAX_LAYERS) rep.layer_norms[rep.n_layer_norms++] = std::sqrt(s);
+        return std::sqrt(s);
+    };
+
+    double eps_nw = rep.eps_nw_initial;
+    DT cur = y;
+    const double col_scale = static_cast<double>(gbatch) / static_cast<double>(batch);
+    auto cols_of = [&](const DT& t, int mode) {
+        const int64_t J = t.shape[static_cast<size_t>(mode)];
+        return static_cast<int64_t>(std::llround(static_cast<double>(t.size() / J) * col_scale));
+    };
+
+    // deepest layer: plain HOSVD of y over all leaves, then sequential projections
+    std::vector<Truncation> bases;
+    for (const TreeNode& n : tree.layer(p)) {
+        DT G = gram(c, cur, static_cast<int>(n.leaf_dim));
+        bases.push_back(truncate_gram(c, G, G.shape[0], cols_of(cur, static_cast<int>(n.leaf_dim)), eps_nw, 1));
+    }
+    RankMap ranks;
+    for (size_t i = 0; i < bases.size(); ++i) {
+        const TreeNode& n = tree.layer(p)[i];
+        DT core = bases[i].u;
+        h->cores[static_cast<size_t>(p)][i] = core;
+        ranks[n.id] = bases[i].rank;
+        record(n.id, bases[i].rank, bases[i].discarded);
+    }
+    for (size_t i = 0; i < bases.size(); ++i) {
+        const TreeNode& n = tree.layer(p)[i];
+        cur = project(c, cur, static_cast<int>(n.leaf_dim), {bases[i].u.data(), bases[i].u.shape[0], bases[i].rank},
+                      nullptr);
+    }
+    push_norm(cur);
+
+    for (Index l = p - 1; l >= 1; --l) {
+        if (adaptive) {
+            const double cn = rep.layer_norms[rep.n_layer_norms - 1];
+            eps_nw = adaptive_budget(eps_abs, std::max(0.0, ysq - cn * cn), svds_below(tree, l + 1));
+        }
+        cur.shape = layer_extents(*h, l, ranks, batch, false);
+        std::vector<Truncation> lb;
+        for (Index j = 0; j < tree.layer_size(l); ++j) {
+            DT G = gram(c, cur, static_cast<int>(j));
+            lb.push_back(truncate_gram(c, G, G.shape[0], cols_of(cur, static_cast<int>(j)), eps_nw, 1));
+        }
+        for (Index j = 0; j < tree.layer_size(l); ++j) {
+            const TreeNode& n = tree.layer(l)[static_cast<size_t>(j)];
+            Truncation& b = lb[static_cast<size_t>(j)];
+            DT core = b.u;
+            if (n.kind != NodeKind::Leaf) core.shape = {ranks[n.successors[0]], ranks[n.successors[1]], b.rank};
+            h->cores[static_cast<size_t>(l)][static_cast<size_t>(j)] = core;
+            ranks[n.id] = b.rank;
+            record(n.id, b.rank, b.discarded);
+        }
+        for (Index j = 0; j < tree.layer_size(l); ++j) {
+            const Truncation& b = lb[static_cast<size_t>(j)];
+            cur = project(c, cur, static_cast<int>(j), {b.u.data(), b.u.shape[0], b.rank}, nullptr);
+        }
+        push_norm(cur);
+    }
+
+    const TreeNode& rootn = tree.node({0, 0});
+    const int64_t r11 = ranks[rootn.successors[0]], r12 = ranks[rootn.successors[1]];
+    h->root = new_root(c, r11, r12, batch);
+    HTR_CUDA(cudaMemcpyAsync(h->root->buf->p, cur.data(), sizeof(double) * static_cast<size_t>(r11 * r12 * batch),
+                             cudaMemcpyDeviceToDevice, c.s));
+    h->root->committed = batch;
+    h->acc = batch;
+    h->acc_global = gbatch;
+    out.rep = h;
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// encode (bht.hpp:373-401)
+// ---------------------------------------------------------------------------
+
+EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
+    const DimensionTree& tree = h.tree;
+    const Index d = tree.dims(), p = tree.depth();
+    const int64_t batch = y.shape[static_cast<size_t>(d)];
+    EncodeOut out;
+    out.exact = exact;
+    const RankMap ranks = h.ranks();
+    double* sc = c.d_sc->p;  // [0] ysq, [1] nonfinite, [2] latent^2, [16..] step energies
+    int nslots = 0;
+    HTR_CUDA(cudaMemsetAsync(sc, 0, 512 * sizeof(double), c.s));
+
+    DT cur = y;
+    bool leaves_done = false;
+    if (!exact && c.fused && d == 3) {
+        NodeId leaf_of[3];
+        for (Index l = 1; l <= p; ++l)
+            for (const TreeNode& n : tree.layer(l))
+                if (n.kind == NodeKind::Leaf) leaf_of[n.leaf_dim] = n.id;
+        const int r0 = static_cast<int>(ranks.at(leaf_of[0])), r1 = static_cast<int>(ranks.at(leaf_of[1])),
+                  r2 = static_cast<int>(ranks.at(leaf_of[2]));
+        if (fused3_supported(y.shape[0], y.shape[1], r0, r1, r2)) {
+            Fused3Args fa;
+            fa.Y = y.data();
+            fa.n2 = y.shape[2];
+            fa.S = batch;
+            fa.U0 = h.core(leaf_of[0]).data();
+            fa.U1 = h.core(leaf_of[1]).data();
+            fa.U2 = h.core(leaf_of[2]).data();
+            fa.r0 = r0;
+            fa.r1 = r1;
+            fa.r2 = r2;
+            DT Z = c.tensor({r0, r1, r2, batch});
+            fa.Z = Z.data();
+            const int64_t ws = fused3_workspace_doubles(y.shape[0], y.shape[1], fa.n2, batch, r0, r1, r2, c.num_sms);
+            BufPtr w = c.alloc(ws);
+            fa.zpart = w->p;
+            fa.ysq_partials = w->p + (ws - std::min<int64_t>(c.num_sms, fa.n2 * batch));
+            if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[0], c.s));
+            const int grid = launch_fused3(y.shape[0], y.shape[1], fa, c.num_sms, c.s, &c.launches);
+            if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[1], c.s));
+            HTR_CUDA(cudaGetLastError());
+            launch_sum_partials(fa.ysq_partials, grid, sc + 0, c.s, &c.launches);
+            cur = Z;
+            leaves_done = true;
+            out.fused = true;
+        }
+    }
+    if (!leaves_done) {
+        for (const TreeNode& n : tree.layer(p))
+            cur = project(c, cur, static_cast<int>(n.leaf_dim), basis_of(h, n.id), exact ? sc + 16 + nslots++ : nullptr);
+    }
+    for (Index l = p - 1; l >= 1; --l) {
+        cur.shape = layer_extents(h, l, ranks, batch, leaves_done);
+        for (Index j = 0; j < tree.layer_size(l); ++j) {
+            const TreeNode& n = tree.layer(l)[static_cast<size_t>(j)];
+            if (leaves_done && n.kind == NodeKind::Leaf) continue;
+            cur = project(c, cur, static_cast<int>(j), basis_of(h, n.id), exact ? sc + 16 + nslots++ : nullptr);
+        }
+    }
+    out.latent = cur;
+
+    // ||y||^2 unless the fused kernel produced it, plus ||latent||^2
+    BufPtr parts = c.alloc(kReduceBlocks);
+    if (!leaves_done) {
+        launch_sumsq(y.data(), y.size(), parts->p, sc + 0, c.s, &c.launches);
+    }
+    BufPtr parts2 = c.alloc(kReduceBlocks);
+    launch_sumsq(cur.data(), cur.size(), parts2->p, sc + 2, c.s, &c.launches);  // writes sc[2], sc[3]
+    HTR_CUDA(cudaGetLastError());
+    c.allreduce(sc, 16 + nslots);
+    c.fetch(sc, 16 + nslots, c.h_sc);
+    if (c.profile && leaves_done) {
+        float ms = 0.f;
+        HTR_CUDA(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
+        c.fused_ms += ms;
+        ++c.fused_calls;
+    }
+    out.ysq = c.h_sc[0];
+    out.nonfinite = !leaves_done ? c.h_sc[1] != 0.0 : !std::isfinite(out.ysq);
+    const double latsq = c.h_sc[2];
+    if (exact) {
+        double loss = 0.0;
+        for (int i = 0; i < nslots; ++i) loss += c.h_sc[16 + i];
+        out.proj_sq = loss;
+    } else {
+        out.proj_sq = std::max(0.0, out.ysq - latsq);
+    }
+    if (out.nonfinite && leaves_done) {
+        // the fused pass saw inf/nan in ||y||^2: distinguish overflow from
+        // non-finite input with the explicit scan
+        double s = 0.0;
+        bool bad = false;
+        norm_sq(c, y.data(), y.size(), &s, &bad);
+        out.nonfinite = bad;
+        out.ysq = s;
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// root append / pad
+// ---------------------------------------------------------------------------
+
+void append_root(Context& c, Rep& out, const Rep& in, const DT& latent) {
+    const int64_t r11 = latent.shape[0], r12 = latent.shape[1], n = latent.shape[2];
+    const std::shared_ptr<RootStore>& rs = in.root;
+    const int64_t slice = r11 * r12;
+    if (rs && rs->r11 == r11 && rs->r12 == r12 && rs->committed == in.acc && in.acc + n <= rs->cap) {
+        // tip of the shared store: append in place, O(batch)
+        HTR_CUDA(cudaMemcpyAsync(rs->buf->p + slice * in.acc, latent.data(), sizeof(double) * static_cast<size_t>(slice * n),
+                                 cudaMemcpyDeviceToDevice, c.s));
+        rs->committed = in.acc + n;
+        out.root = rs;
+    } else {
+        const int64_t cap = std::max<int64_t>(2 * (in.acc + n), rs ? rs->cap : 0);
+        auto ns = new_root(c, r11, r12, cap);
+        if (in.acc > 0) {
+            if (!rs || rs->r11 != r11 || rs->r12 != r12) raise(HTR_ERR_RUNTIME, "append_root: rank mismatch");
+            HTR_CUDA(cudaMemcpyAsync(ns->buf->p, rs->buf->p, sizeof(double) * static_cast<size_t>(slice * in.acc),
+                                     cudaMemcpyDeviceToDevice, c.s));
+        }
+        HTR_CUDA(cudaMemcpyAsync(ns->buf->p + slice * in.acc, latent.data(), sizeof(double) * static_cast<size_t>(slice * n),
+                                 cudaMemcpyDeviceToDevice, c.s));
+        ns->committed = in.acc + n;
+        out.root = ns;
+    }
+    out.acc = in.acc + n;
+}
+
+// ---------------------------------------------------------------------------
+// HT-RISE update (ht_rise.hpp:99-186)
+// ---------------------------------------------------------------------------
+
+namespace {
+
+/// G_R = (I - U U^T) G (I - U U^T): the Gram of the residual
+/// compute_residual(U, C) (ht_rise.hpp:31-38) without forming it.
+void residual_gram(Context& c, DT& G, const Basis& U) {
+    const int64_t a = U.alpha, r = U.r;
+    DT X1 = c.tensor({r, a});
+    {
+        GemmDesc d;  // X1 = U^T G
+        d.M = r; d.N1 = a; d.K1 = a;
+        d.A = U.p; d.sam = a; d.sak1 = 1;
+        d.B = G.data(); d.sbk1 = 1; d.sbn1 = a;
+        d.C = X1.data(); d.scm = 1; d.scn1 = r;
+        run_gemm(c, d);
+    }
+    {
+        GemmDesc d;  // G -= U X1
+        d.M = a; d.N1 = a; d.K1 = r;
+        d.A = U.p; d.sam = 1; d.sak1 = a;
+        d.B = X1.data(); d.sbk1 = 1; d.sbn1 = r;
+        d.C = G.data(); d.scm = 1; d.scn1 = a;
+        d.alpha = -1.0; d.beta = 1.0;
+        run_gemm(c, d);
+    }
+    DT X2 = c.tensor({a, r});
+    {
+        GemmDesc d;  // X2 = G U
+        d.M = a; d.N1 = r; d.K1 = a;
+        d.A = G.data(); d.sam = 1; d.sak1 = a;
+        d.B = U.p; d.sbk1 = 1; d.sbn1 = a;
+        d.C = X2.data(); d.scm = 1; d.scn1 = a;
+        run_gemm(c, d);
+    }
+    {
+        GemmDesc d;  // G -= X2 U^T
+        d.M = a; d.N1 = a; d.K1 = r;
+        d.A = X2.data(); d.sam = 1; d.sak1 = a;
+        d.B = U.p; d.sbk1 = a; d.sbn1 = 1;
+        d.C = G.data(); d.scm = 1; d.scn1 = a;
+        d.alpha = -1.0; d.beta = 1.0;
+        run_gemm(c, d);
+    }
+}
+
+}  // namespace
+
+UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_override, bool adaptive) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int64_t l0 = c.launches;
+    check_batch_input(y.shape, h.tree, &h.dims, "ht_rise_update");
+    const DimensionTree& tree = h.tree;
+    const Index d = tree.dims(), p = tree.depth();
+    const int64_t batch = y.shape[static_cast<size_t>(d)];
+    const double eps_rel = effective_eps_rel(eps_override >= 0 ? eps_override : h.eps_rel);
+
+    UpdateOut res;
+    std::memset(&res.report, 0, sizeof(res.report));
+    htr_update_report& rep = res.report;
+
+    EncodeOut enc = encode(c, h, y, c.exact_loss);
+    if (enc.nonfinite) raise(HTR_ERR_INVALID_ARGUMENT, "ht_rise_update: non-finite input");
+    double norm_y = std::sqrt(enc.ysq);
+    rep.eps_des = eps_rel * norm_y;
+    if (!enc.exact) {
+        // guard band around the skip threshold: the telescoped loss
+        // ||y||^2 - ||latent||^2 carries ~u*||y||^2 absolute error, so a
+        // decision that close to the boundary is re-taken with the
+        // reference's explicit per-step residuals (bht.hpp:357-365)
+        const double guard = 1e-12 * enc.ysq;
+        if (std::abs(enc.proj_sq - rep.eps_des * rep.eps_des) <= guard) {
+            enc = encode(c, h, y, true);
+        }
+    }
+    rep.proj_error = std::sqrt(enc.proj_sq);
+    rep.used_fused_path = enc.fused ? 1 : 0;
+    rep.used_exact_loss = enc.exact ? 1 : 0;
+    const int64_t gbatch = global_batch(c, batch);
+
+    auto finish = [&](std::shared_ptr<Rep> out) {
+        RankMap nr = out->ranks();
+        RankMap old = h.ranks();
+        int i = 0;
+        for (const auto& [id, r] : nr) {
+            if (i >= HTR_MAX_NODES) break;
+            rep.node_layer[i] = static_cast<int32_t>(id.layer);
+            rep.node_pos[i] = static_cast<int32_t>(id.pos);
+            rep.new_ranks[i] = r;
+            rep.added_ranks[i] = r - old.at(id);
+            ++i;
+        }
+        rep.n_nodes = i;
+        out->acc_global = h.acc_global + gbatch;
+        HTR_CUDA(cudaStreamSynchronize(c.s));
+        rep.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        rep.kernel_launches = c.launches - l0;
+        res.rep = std::move(out);
+        return res;
+    };
+
+    if (rep.proj_error <= rep.eps_des) {
+        rep.skipped = 1;
+        auto out = std::make_shared<Rep>(h);
+        append_root(c, *out, h, enc.latent);
+        return finish(out);
+    }
+
+    // ---- EXPAND ----------------------------------------------------------
+    auto out = std::make_shared<Rep>(h);
+    RankMap ranks = h.ranks();
+    double eps_nw = rep.eps_des / std::sqrt(static_cast<double>(2 * d - 2));
+    const double ysq = enc.ysq;
+    const double col_scale = static_cast<double>(gbatch) / static_cast<double>(batch);
+    // the root is re-padded lazily: remember pending layer-1 growth
+    int64_t pad0 = 0, pad1 = 0;
+
+    auto expand_node = [&](const TreeNode& n, const DT& cur, int mode) {
+        const Basis U = basis_of(*out, n.id);
+        DT G = gram(c, cur, mode);
+        residual_gram(c, G, U);
+        const int64_t cols = static_cast<int64_t>(
+            std::llround(static_cast<double>(cur.size() / cur.shape[static_cast<size_t>(mode)]) * col_scale));
+        Truncation tb = truncate_gram(c, G, U.alpha, cols, eps_nw, 0);
+        if (tb.rank == 0) return;
+        // re-orthonormalise the new directions against the old basis and
+        // append (expand_core, ht_rise.hpp:53-79)
+        BufPtr info = c.alloc(4);
+        BufPtr work = c.alloc(U.r * tb.rank + tb.rank * tb.rank + 16);
+        launch_orthonormalize_new(U.p, U.alpha, U.r, tb.u.data(), tb.rank, info->p, work->p, c.s, &c.launches);
+        HTR_CUDA(cudaGetLastError());
+        double hinfo[2];
+        c.fetch(info->p, 2, hinfo);
+        if (!(hinfo[0] <= 1e-8 * std::max(1.0, hinfo[1])))
+            raise(HTR_ERR_INVALID_ARGUMENT, "expand_core: new directions not orthogonal to existing basis (defect " +
+                                                std::to_string(hinfo[0]) + ")");
+        const int64_t rn = U.r + tb.rank;
+        DT joined = c.tensor({U.alpha, rn});
+        HTR_CUDA(cudaMemcpyAsync(joined.data(), U.p, sizeof(double) * static_cast<size_t>(U.alpha * U.r),
+                                 cudaMemcpyDeviceToDevice, c.s));
+        HTR_CUDA(cudaMemcpyAsync(joined.data() + U.alpha * U.r, tb.u.data(),
+                                 sizeof(double) * static_cast<size_t>(U.alpha * tb.rank), cudaMemcpyDeviceToDevice, c.s));
+        if (n.kind != NodeKind::Leaf) {
+            const Shape& s = out->core(n.id).shape;
+            joined.shape = {s[0], s[1], rn};
+        }
+        out->cores[static_cast<size_t>(n.id.layer)][static_cast<size_t>(n.id.pos)] = joined;
+        ranks[n.id] += tb.rank;
+        // pad the parent's successor slot with zeros (pad_with_zeros, ht_rise.hpp:83-92)
+        const Index slot = tree.parent_slot(n.id);
+        const TreeNode& par = tree.node(n.parent);
+        if (par.kind == NodeKind::Root) {
+            (slot == 0 ? pad0 : pad1) += tb.rank;
+        } else {
+            const DT& pc = out->core(n.parent);
+            const int64_t inner = slot == 0 ? 1 : pc.shape[0];
+            const int64_t ext = pc.shape[static_cast<size_t>(slot)];
+            const int64_t outer = slot == 0 ? pc.shape[1] * pc.shape[2] : pc.shape[2];
+            Shape ns = pc.shape;
+            ns[static_cast<size_t>(slot)] += tb.rank;
+            DT padded = c.tensor(ns);
+            launch_pad_axis(pc.data(), inner, ext, outer, tb.rank, padded.data(), c.s, &c.launches);
+            HTR_CUDA(cudaGetLastError());
+            out->cores[static_cast<size_t>(n.parent.layer)][static_cast<size_t>(n.parent.pos)] = padded;
+        }
+    };
+
+    DT cur = y;
+    for (const TreeNode& n : tree.layer(p)) expand_node(n, cur, static_cast<int>(n.leaf_dim));
+    for (const TreeNode& n : tree.layer(p)) cur = project(c, cur, static_cast<int>(n.leaf_dim), basis_of(*out, n.id), nullptr);
+
+    for (Index l = p - 1; l >= 1; --l) {
+        if (adaptive) {
+            double cn2 = 0.0;
+            norm_sq(c, cur.data(), cur.size(), &cn2, nullptr);
+            eps_nw = adaptive_budget(rep.eps_des, std::max(0.0, ysq - cn2), svds_below(tree, l + 1));
+        }
+        cur.shape = layer_extents(*out, l, ranks, batch, false);
+        for (Index j = 0; j < tree.layer_size(l); ++j) expand_node(tree.layer(l)[static_cast<size_t>(j)], cur, static_cast<int>(j));
+        for (Index j = 0; j < tree.layer_size(l); ++j)
+            cur = project(c, cur, static_cast<int>(j), basis_of(*out, tree.layer(l)[static_cast<size_t>(j)].id), nullptr);
+    }
+
+    // root: zero-pad the stored slices to the grown layer-1 ranks, then append
+    if (pad0 || pad1) {
+        const std::shared_ptr<RootStore>& rs = h.root;
+        const int64_t r11 = rs->r11 + pad0, r12 = rs->r12 + pad1;
+        auto ns = new_root(c, r11, r12, std::max<int64_t>(rs->cap, 2 * (h.acc + batch)));
+        if (h.acc > 0) {
+            BufPtr tmp = c.alloc(r11 * rs->r12 * h.acc);
+            // axis 0 then axis 1 of [r11_old, r12_old, acc]
+            launch_pad_axis(rs->buf->p, 1, rs->r11, rs->r12 * h.acc, pad0, tmp->p, c.s, &c.launches);
+            launch_pad_axis(tmp->p, r11, rs->r12, h.acc, pad1, ns->buf->p, c.s, &c.launches);
+            HTR_CUDA(cudaGetLastError());
+        }
+        ns->committed = h.acc;
+        Rep padded_in = h;
+        padded_in.root = ns;
+        out->root = ns;
+        append_root(c, *out, padded_in, cur);
+    } else {
+        append_root(c, *out, h, cur);
+    }
+    return finish(out);
+}
+
+// ---------------------------------------------------------------------------
+// decode (bht.hpp:406-456)
+// ---------------------------------------------------------------------------
+
+DT decode(Context& c, const Rep& h, const DT& latent) {
+    const int64_t r11 = h.root->r11, r12 = h.root->r12;
+    if (latent.shape.size() != 3 || latent.shape[0] != r11 || latent.shape[1] != r12)
+        raise(HTR_ERR_INVALID_ARGUMENT, "decode: latent ranks " + htrise::shape_to_string(latent.shape) +
+                                            " do not match root [" + std::to_string(r11) + "x" + std::to_string(r12) + "]");
+    struct Tag {
+        NodeId node;
+        bool open;
+        Index dim;
+    };
+    const TreeNode& rootn = h.tree.node({0, 0});
+    std::vector<Tag> tags = {{rootn.successors[0], true, -1}, {rootn.successors[1], true, -1}};
+    DT cur = latent;
+    for (Index l = 1; l <= h.tree.depth(); ++l) {
+        for (size_t pos = 0; pos < tags.size(); ++pos) {
+            Tag& tg = tags[pos];
+            if (!tg.open || tg.node.layer != l) continue;
+            const TreeNode& n = h.tree.node(tg.node);
+            const Basis b = basis_of(h, n.id);
+            // multiply mode `pos` by the basis (alpha x r): M(q, j) = B[q + alpha j]
+            DT next = mode_mul(c, cur, static_cast<int>(pos), b.p, b.alpha, 1, b.alpha);
+            if (n.kind == NodeKind::Leaf) {
+                tg.open = false;
+                tg.dim = n.leaf_dim;
+                cur = next;
+            } else {
+                const Shape& cs = h.core(n.id).shape;
+                Shape split = next.shape;
+                split[pos] = cs[0];
+                split.insert(split.begin() + static_cast<std::ptrdiff_t>(pos) + 1, cs[1]);
+                next.shape = split;
+                cur = next;
+                const NodeId s0 = n.successors[0], s1 = n.successors[1];
+                tags[pos] = {s0, true, -1};
+                tags.insert(tags.begin() + static_cast<std::ptrdiff_t>(pos) + 1, Tag{s1, true, -1});
+                ++pos;
+            }
+        }
+    }
+    // validate() forces in-order spans, so the modes already carry dims in order
+    for (size_t k = 0; k < tags.size(); ++k)
+        if (tags[k].dim != static_cast<Index>(k)) raise(HTR_ERR_RUNTIME, "decode: unexpected mode order");
+    return cur;
+}
+
+}  // namespace htr

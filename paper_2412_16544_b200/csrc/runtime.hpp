@@ -1,0 +1,187 @@
+// htrise-b200 native runtime: device memory, representations, algorithms.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "htrise/dimension_tree.hpp"
+#include "htrise_cuda.h"
+#include "kernels.cuh"
+
+namespace htr {
+
+using htrise::DimensionTree;
+using htrise::Index;
+using htrise::NodeId;
+using htrise::NodeKind;
+using htrise::RankMap;
+using htrise::Shape;
+using htrise::TreeNode;
+
+struct Error {
+    htr_status code;
+    std::string msg;
+};
+[[noreturn]] void raise(htr_status code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+#define HTR_CUDA(x) ::htr::cuda_check((x), #x)
+
+/// Owns the context's CUDA stream; shared by every buffer allocated on it so
+/// stream-ordered frees stay valid after the context handle is destroyed.
+struct Stream {
+    cudaStream_t s = nullptr;
+    int device = 0;
+    explicit Stream(int dev);
+    ~Stream();
+};
+using StreamPtr = std::shared_ptr<Stream>;
+
+/// Stream-ordered device allocation of n doubles.
+struct Buf {
+    StreamPtr st;
+    double* p = nullptr;
+    int64_t n = 0;
+    bool owned = true;
+    Buf(StreamPtr st_, int64_t n_);
+    /// Non-owning wrapper around caller memory (device pointers handed in
+    /// through the C-ABI).
+    Buf(StreamPtr st_, double* external, int64_t n_) : st(std::move(st_)), p(external), n(n_), owned(false) {}
+    ~Buf();
+    Buf(const Buf&) = delete;
+    Buf& operator=(const Buf&) = delete;
+};
+using BufPtr = std::shared_ptr<Buf>;
+
+/// Device tensor view: canonical layout, shared immutable storage.
+struct DT {
+    BufPtr buf;
+    Shape shape;
+    int64_t offset = 0;
+    double* data() const { return buf->p + offset; }
+    int64_t size() const { return htrise::shape_product(shape); }
+};
+
+/// Append-only root core r11 x r12 x capacity (batch axis last). Several
+/// representation values may share it; each sees its first `acc` slices.
+struct RootStore {
+    BufPtr buf;
+    int64_t r11 = 0, r12 = 0, cap = 0, committed = 0;
+};
+
+struct Rep {
+    StreamPtr st;
+    DimensionTree tree;
+    Shape dims;
+    std::vector<std::vector<DT>> cores;  // non-root cores; cores[0] unused
+    std::shared_ptr<RootStore> root;
+    int64_t acc = 0;         // slices held locally (this rank's shard)
+    int64_t acc_global = 0;  // total tensors streamed (all ranks)
+    double eps_rel = 0.0;
+
+    const DT& core(NodeId id) const {
+        return cores.at(static_cast<size_t>(id.layer)).at(static_cast<size_t>(id.pos));
+    }
+    Index rank(NodeId id) const;
+    RankMap ranks() const;
+};
+
+struct Context {
+    int device = 0;
+    StreamPtr st;
+    cudaStream_t s = nullptr;
+    int num_sms = kNumSMs;
+    std::string err;
+    int64_t launches = 0;
+    bool exact_loss = false;
+    bool fused = true;
+    bool profile = false;
+    double* h_sc = nullptr;  // pinned scalars
+    BufPtr d_sc;             // device scalars
+    // timing of the fused encode kernel and of the generic GEMMs
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    double fused_ms = 0.0, gemm_ms = 0.0;
+    int64_t fused_calls = 0, gemm_calls = 0;
+    // batch-axis sharding over NCCL (dlopen'd)
+    int nranks = 1, rank = 0;
+    void* nccl_comm = nullptr;
+
+    explicit Context(int dev);
+    ~Context();
+
+    BufPtr alloc(int64_t n) { return std::make_shared<Buf>(st, n); }
+    DT tensor(const Shape& shape) {
+        DT t;
+        t.shape = shape;
+        t.buf = alloc(htrise::shape_product(shape));
+        return t;
+    }
+    /// Sum n doubles over all ranks in place (no-op on one rank).
+    void allreduce(double* d, int64_t n);
+    /// Copy n device doubles to host (synchronises the stream).
+    void fetch(const double* d, int64_t n, double* host);
+};
+
+// ---- building blocks -------------------------------------------------------
+void run_gemm(Context& c, const GemmDesc& d);
+/// out = t x_mode M with M(q, j) = Mp[q*smq + j*smj] (q < Q).
+DT mode_mul(Context& c, const DT& t, int mode, const double* Mp, int64_t Q, int64_t smq, int64_t smj);
+/// Sum over the fibres of (t - U (U^T t)) along `mode`, given coeff = U^T t;
+/// result added into the device scalar `slot`.
+void residual_energy(Context& c, const DT& t, int mode, const double* U, int64_t r, const DT& coeff,
+                     double* slot);
+/// Gram of the mode-`mode` unfolding (extent x extent), all-reduced.
+DT gram(Context& c, const DT& t, int mode, bool reduce = true);
+/// ||x||^2 (all-reduced) and the non-finite flag.
+void norm_sq(Context& c, const double* x, int64_t n, double* ysq, bool* nonfinite, bool reduce = true);
+
+struct Truncation {
+    DT u;  // rows x rank
+    int64_t rank = 0;
+    double discarded = 0.0;
+    std::vector<double> sigma;  // retained singular values
+};
+/// Error-truncated basis of a symmetric Gram (truncated_svd.hpp:53-100 on the
+/// matrix whose Gram this is). k = min(rows, cols).
+Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
+                         bool want_basis = true);
+
+// ---- algorithms --------------------------------------------------------------
+struct BuildOut {
+    std::shared_ptr<Rep> rep;
+    htr_build_report report;
+};
+BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_rel, bool adaptive);
+
+struct EncodeOut {
+    DT latent;
+    double ysq = 0.0;       // ||y||^2 (global)
+    double proj_sq = 0.0;   // projection error^2
+    bool fused = false;
+    bool exact = false;
+    bool nonfinite = false;
+};
+EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact);
+
+struct UpdateOut {
+    std::shared_ptr<Rep> rep;
+    htr_update_report report;
+};
+UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_override, bool adaptive);
+
+DT decode(Context& c, const Rep& h, const DT& latent);
+
+/// Append latent slices [r11, r12, N] to a representation's root (value
+/// semantics: returns the new root view).
+void append_root(Context& c, Rep& out, const Rep& in, const DT& latent);
+
+// validation shared with the C-ABI
+DimensionTree tree_from_nodes(const htr_node* nodes, int64_t n);
+void nodes_from_tree(const DimensionTree& t, std::vector<htr_node>& out);
+void check_batch_input(const Shape& y_shape, const DimensionTree& tree, const Shape* dims, const char* who);
+
+}  // namespace htr
