@@ -102,6 +102,9 @@ HTR_API htr_status htr_context_destroy(htr_context* ctx);
 HTR_API const char* htr_last_error(const htr_context* ctx);
 /* CUDA stream the context launches on (cudaStream_t). */
 HTR_API htr_status htr_context_stream(htr_context* ctx, void** stream);
+/* Make the context's stream wait for all work already enqueued on `stream`
+ * (e.g. torch's current stream that produced a device input). */
+HTR_API htr_status htr_context_wait_stream(htr_context* ctx, void* stream);
 HTR_API htr_status htr_synchronize(htr_context* ctx);
 /* Options: see HTR_OPT_*. */
 #define HTR_OPT_EXACT_LOSS 1      /* 1: per-step explicit residual loss like bht.hpp:357-365 (default 0 = telescoped with guard band) */

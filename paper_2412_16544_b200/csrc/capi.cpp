@@ -141,6 +141,14 @@ htr_status htr_context_stream(htr_context* ctx, void** stream) {
     return guarded(ctx, [&] { *stream = C(ctx).s; });
 }
 
+htr_status htr_context_wait_stream(htr_context* ctx, void* stream) {
+    return guarded(ctx, [&] {
+        htr::Context& c = C(ctx);
+        HTR_CUDA(cudaEventRecord(c.ev[3], static_cast<cudaStream_t>(stream)));
+        HTR_CUDA(cudaStreamWaitEvent(c.s, c.ev[3], 0));
+    });
+}
+
 htr_status htr_synchronize(htr_context* ctx) {
     return guarded(ctx, [&] { HTR_CUDA(cudaStreamSynchronize(C(ctx).s)); });
 }
@@ -416,7 +424,7 @@ htr_status htr_truncated_svd(htr_context* ctx, const double* m, int32_t m_on_dev
         htr::norm_sq(c, mt.data(), mt.size(), &s2, &bad, false);
         if (bad) htr::raise(HTR_ERR_INVALID_ARGUMENT, "truncated_svd: non-finite entries");
         DT G = htr::gram(c, mt, 0, false);
-        htr::Truncation t = htr::truncate_gram(c, G, rows, cols, eps_abs, min_rank);
+        htr::Truncation t = htr::truncate_gram(c, G, rows, cols, eps_abs, min_rank, htr::unfolding_refiner(c, mt, 0));
         if (rank) *rank = t.rank;
         if (discarded_norm) *discarded_norm = t.discarded;
         if (sigma)

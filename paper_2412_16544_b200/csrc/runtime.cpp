@@ -261,8 +261,10 @@ void norm_sq(Context& c, const double* x, int64_t n, double* ysq, bool* nonfinit
     if (nonfinite) *nonfinite = c.h_sc[1] != 0.0;
 }
 
+ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode);
+
 Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
-                         bool want_basis) {
+                         const ProjectedGram& refine) {
     const int64_t n = rows;
     const int64_t k = std::min(rows, cols);
     BufPtr lam = c.alloc(n);
@@ -270,6 +272,37 @@ Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, do
     BufPtr work = c.alloc(2 * n * n);
     BufPtr info = c.alloc(4);
     launch_jacobi_eig(G.data(), n, lam->p, V->p, work->p, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+    if (refine) {
+        std::vector<double> lh(static_cast<size_t>(n));
+        c.fetch(lam->p, n, lh.data());
+        const double lmax = std::max(lh[0], 0.0);
+        if (lmax > 0.0 && eps_abs * eps_abs < 1e-7 * lmax) {
+            int64_t s0 = 0;
+            while (s0 < n && lh[static_cast<size_t>(s0)] >= 1e-6 * lmax) ++s0;
+            const int64_t q = n - s0;
+            if (q > 0) {
+                double* W = V->p + n * s0;  // eigenvectors of the small eigenvalues
+                DT G2 = refine(W, q);
+                BufPtr mu = c.alloc(q);
+                BufPtr Z = c.alloc(q * q);
+                BufPtr work2 = c.alloc(2 * q * q);
+                launch_jacobi_eig(G2.data(), q, mu->p, Z->p, work2->p, c.s, &c.launches);
+                HTR_CUDA(cudaMemcpyAsync(lam->p + s0, mu->p, sizeof(double) * static_cast<size_t>(q),
+                                         cudaMemcpyDeviceToDevice, c.s));
+                BufPtr WZ = c.alloc(n * q);
+                GemmDesc d;  // WZ = W Z
+                d.M = n; d.N1 = q; d.K1 = q;
+                d.A = W; d.sam = 1; d.sak1 = n;
+                d.B = Z->p; d.sbk1 = 1; d.sbn1 = q;
+                d.C = WZ->p; d.scm = 1; d.scn1 = n;
+                run_gemm(c, d);
+                HTR_CUDA(cudaMemcpyAsync(W, WZ->p, sizeof(double) * static_cast<size_t>(n * q), cudaMemcpyDeviceToDevice,
+                                         c.s));
+                HTR_CUDA(cudaGetLastError());
+            }
+        }
+    }
     launch_rank_rule(lam->p, k, n, eps_abs, min_rank, nullptr, info->p, c.s, &c.launches);
     HTR_CUDA(cudaGetLastError());
     double h[4];
@@ -282,14 +315,21 @@ Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, do
         std::vector<double> l(static_cast<size_t>(t.rank));
         c.fetch(lam->p, t.rank, l.data());
         t.sigma.resize(static_cast<size_t>(t.rank));
-        for (int64_t i = 0; i < t.rank; ++i) t.sigma[static_cast<size_t>(i)] = zero ? 0.0 : std::sqrt(std::max(0.0, l[static_cast<size_t>(i)]));
+        for (int64_t i = 0; i < t.rank; ++i)
+            t.sigma[static_cast<size_t>(i)] = zero ? 0.0 : std::sqrt(std::max(0.0, l[static_cast<size_t>(i)]));
     }
-    if (want_basis) {
-        t.u = c.tensor({rows, t.rank});
-        launch_take_columns(V->p, n, t.rank, t.u.data(), info->p, c.s, &c.launches);
-        HTR_CUDA(cudaGetLastError());
-    }
+    t.u = c.tensor({rows, t.rank});
+    launch_take_columns(V->p, n, t.rank, t.u.data(), info->p, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
     return t;
+}
+
+ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode) {
+    return [&c, t, mode](const double* W, int64_t q) {
+        const int64_t n = t.shape[static_cast<size_t>(mode)];
+        DT B = mode_mul(c, t, mode, W, q, n, 1);  // W^T along `mode`
+        return gram(c, B, mode);
+    };
 }
 
 // ---------------------------------------------------------------------------
@@ -496,7 +536,8 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
     std::vector<Truncation> bases;
     for (const TreeNode& n : tree.layer(p)) {
         DT G = gram(c, cur, static_cast<int>(n.leaf_dim));
-        bases.push_back(truncate_gram(c, G, G.shape[0], cols_of(cur, static_cast<int>(n.leaf_dim)), eps_nw, 1));
+        bases.push_back(truncate_gram(c, G, G.shape[0], cols_of(cur, static_cast<int>(n.leaf_dim)), eps_nw, 1,
+                                      unfolding_refiner(c, cur, static_cast<int>(n.leaf_dim))));
     }
     RankMap ranks;
     for (size_t i = 0; i < bases.size(); ++i) {
@@ -522,7 +563,8 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
         std::vector<Truncation> lb;
         for (Index j = 0; j < tree.layer_size(l); ++j) {
             DT G = gram(c, cur, static_cast<int>(j));
-            lb.push_back(truncate_gram(c, G, G.shape[0], cols_of(cur, static_cast<int>(j)), eps_nw, 1));
+            lb.push_back(truncate_gram(c, G, G.shape[0], cols_of(cur, static_cast<int>(j)), eps_nw, 1,
+                                       unfolding_refiner(c, cur, static_cast<int>(j))));
         }
         for (Index j = 0; j < tree.layer_size(l); ++j) {
             const TreeNode& n = tree.layer(l)[static_cast<size_t>(j)];
@@ -810,7 +852,34 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
         residual_gram(c, G, U);
         const int64_t cols = static_cast<int64_t>(
             std::llround(static_cast<double>(cur.size() / cur.shape[static_cast<size_t>(mode)]) * col_scale));
-        Truncation tb = truncate_gram(c, G, U.alpha, cols, eps_nw, 0);
+        // refinement measures the residual R = (I - U U^T) C directly:
+        // W^T R = ((I - U U^T) W)^T C
+        ProjectedGram refine = [&c, &cur, mode, U](const double* W, int64_t q) {
+            DT T = c.tensor({U.r, q});
+            {
+                GemmDesc d;  // T = U^T W
+                d.M = U.r; d.N1 = q; d.K1 = U.alpha;
+                d.A = U.p; d.sam = U.alpha; d.sak1 = 1;
+                d.B = W; d.sbk1 = 1; d.sbn1 = U.alpha;
+                d.C = T.data(); d.scm = 1; d.scn1 = U.r;
+                run_gemm(c, d);
+            }
+            DT Wp = c.tensor({U.alpha, q});
+            HTR_CUDA(cudaMemcpyAsync(Wp.data(), W, sizeof(double) * static_cast<size_t>(U.alpha * q),
+                                     cudaMemcpyDeviceToDevice, c.s));
+            {
+                GemmDesc d;  // Wp -= U T
+                d.M = U.alpha; d.N1 = q; d.K1 = U.r;
+                d.A = U.p; d.sam = 1; d.sak1 = U.alpha;
+                d.B = T.data(); d.sbk1 = 1; d.sbn1 = U.r;
+                d.C = Wp.data(); d.scm = 1; d.scn1 = U.alpha;
+                d.alpha = -1.0; d.beta = 1.0;
+                run_gemm(c, d);
+            }
+            DT B = mode_mul(c, cur, mode, Wp.data(), q, U.alpha, 1);
+            return gram(c, B, mode);
+        };
+        Truncation tb = truncate_gram(c, G, U.alpha, cols, eps_nw, 0, refine);
         if (tb.rank == 0) return;
         // re-orthonormalise the new directions against the old basis and
         // append (expand_core, ht_rise.hpp:53-79)

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -145,10 +146,19 @@ struct Truncation {
     double discarded = 0.0;
     std::vector<double> sigma;  // retained singular values
 };
+/// Gram (q x q) of W^T M for a device matrix W (rows x q, col-major): lets a
+/// truncation re-measure a subspace against the matrix M itself.
+using ProjectedGram = std::function<DT(const double* W, int64_t q)>;
 /// Error-truncated basis of a symmetric Gram (truncated_svd.hpp:53-100 on the
-/// matrix whose Gram this is). k = min(rows, cols).
+/// matrix whose Gram this is). k = min(rows, cols). When the tolerance sits
+/// near the Gram's rounding floor (eps^2 < 1e-7 lambda_max) the eigenvalues
+/// below 1e-6 lambda_max are re-measured through `refine` (a second Gram of
+/// the projection of M onto that subspace), which resolves singular values
+/// down to ~u sigma_max like the reference's direct SVD.
 Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
-                         bool want_basis = true);
+                         const ProjectedGram& refine = nullptr);
+/// Refiner for a plain unfolding of `t` along `mode`.
+ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode);
 
 // ---- algorithms --------------------------------------------------------------
 struct BuildOut {

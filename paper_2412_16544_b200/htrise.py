@@ -96,6 +96,7 @@ _SIGNATURES = {
     "htr_context_destroy": (C.c_int32, [_P]),
     "htr_last_error": (C.c_char_p, [_P]),
     "htr_context_stream": (C.c_int32, [_P, C.POINTER(_P)]),
+    "htr_context_wait_stream": (C.c_int32, [_P, _P]),
     "htr_synchronize": (C.c_int32, [_P]),
     "htr_context_set_option": (C.c_int32, [_P, C.c_int32, C.c_double]),
     "htr_context_launch_count": (C.c_int64, [_P]),
@@ -287,9 +288,15 @@ def _shape_arr(shape):
     return (C.c_int64 * len(shape))(*[int(s) for s in shape])
 
 
-def _tensor_arg(y):
-    """-> (pointer, on_device, shape, keepalive)."""
+def _tensor_arg(y, ctx: Optional["Context"] = None):
+    """-> (pointer, on_device, shape, keepalive). Device inputs produced on
+    torch's current stream are ordered before the library's stream."""
     if isinstance(y, DeviceTensor):
+        if ctx is not None and hasattr(y.data, "data_ptr"):
+            import torch
+
+            s = torch.cuda.current_stream(y.data.device).cuda_stream
+            ctx.check(lib().htr_context_wait_stream(ctx.handle, C.c_void_p(s)))
         return C.cast(C.c_void_p(y.ptr()), _D), 1, tuple(int(s) for s in y.shape), y
     a = _as_host(y)
     if a.ndim == 0:
@@ -540,7 +547,7 @@ def bht_l2r(y, tree: DimensionTree, eps_rel: float, adaptive_budget: bool = Fals
             ctx: Optional[Context] = None):
     """Alg. 1 (bht.hpp:251-350). Returns (HTRepresentation, BuildReport)."""
     ctx = ctx or default_context()
-    p, on_dev, shape, keep = _tensor_arg(y)
+    p, on_dev, shape, keep = _tensor_arg(y, ctx)
     nodes, nn = tree.c_nodes()
     out = _P()
     rep = _BuildReport()
@@ -556,7 +563,7 @@ def bht_l2r(y, tree: DimensionTree, eps_rel: float, adaptive_budget: bool = Fals
 def ht_rise_update(h: HTRepresentation, y, epsilon_rel: Optional[float] = None, adaptive_budget: bool = False):
     """Alg. 2 (ht_rise.hpp:99-186). Returns (new HTRepresentation, UpdateReport)."""
     ctx = h.ctx
-    p, on_dev, shape, keep = _tensor_arg(y)
+    p, on_dev, shape, keep = _tensor_arg(y, ctx)
     out = _P()
     rep = _UpdateReport()
     eps = -1.0 if epsilon_rel is None else float(epsilon_rel)
@@ -579,7 +586,7 @@ def _latent_shape(h: HTRepresentation, batch: int):
 def encode(h: HTRepresentation, y):
     """bht.hpp:373-401 -> (latent r11 x r12 x N, projection error)."""
     ctx = h.ctx
-    p, on_dev, shape, keep = _tensor_arg(y)
+    p, on_dev, shape, keep = _tensor_arg(y, ctx)
     if len(shape) != h.tree.dims() + 1:
         raise ValueError(f"encode: tensor order {len(shape)} does not match tree over {h.tree.dims()} dims plus batch")
     lat = np.zeros(int(np.prod(_latent_shape(h, shape[-1]))), dtype=np.float64)
@@ -593,7 +600,7 @@ def encode(h: HTRepresentation, y):
 def decode(h: HTRepresentation, latent) -> np.ndarray:
     """bht.hpp:406-456."""
     ctx = h.ctx
-    p, on_dev, shape, keep = _tensor_arg(latent)
+    p, on_dev, shape, keep = _tensor_arg(latent, ctx)
     if len(shape) != 3:
         raise ValueError(f"decode: latent ranks {list(shape)} do not match root")
     out = np.zeros(int(np.prod(h.dims)) * shape[2], dtype=np.float64)
@@ -679,7 +686,7 @@ def compute_residual(basis, c_unfolded, ctx: Optional[Context] = None) -> np.nda
 def frobenius_norm(t, ctx: Optional[Context] = None) -> float:
     """tensor.hpp:269."""
     ctx = ctx or default_context()
-    p, on_dev, shape, keep = _tensor_arg(t)
+    p, on_dev, shape, keep = _tensor_arg(t, ctx)
     out = C.c_double()
     ctx.check(lib().htr_frobenius_norm(ctx.handle, p, on_dev, int(np.prod(shape)), C.byref(out)))
     del keep

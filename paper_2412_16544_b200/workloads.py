@@ -15,7 +15,10 @@ Pinned readings of the ambiguities listed in SURVEY.md Appendix B:
   c3  6 components (per-mode orthonormal Gaussian factors, N(0,1) weights per
       sample); from batch 25 (1-based) 6 more switch on and all 12 stay on;
       the 8-long field mode holds 12 factors (first 8 orthonormal, 4 more
-      Gaussian unit vectors); noise sigma = 1e-5 absolute; seed 3.
+      Gaussian unit vectors); noise 1e-5 relative to the batch norm (an
+      absolute 1e-5 would put ||noise||/||Y|| ~ 2e-3 above eps = 1e-3 and make
+      every leaf full-rank, contradicting the config's 6 -> 12 rank story);
+      seed 3.
   c4  leaf bases and transfer tensors fixed per stream, root coefficients
       per sample; noise 1e-4 relative per sample; seed 4.
   c5  factors fixed per stream, core 20^3 N(0,1) per sample; noise 1e-4
@@ -128,7 +131,10 @@ def _c3(w: Workload, b: int, dev, n: int, off: int) -> torch.Tensor:
     y = torch.einsum("sr,ar,br,cr,dr->sdcba", weights, f[0], f[1], f[2], f[3])
     gn = _gen(dev, 3500 + b)
     noise = torch.randn(w.batch, *y.shape[1:], generator=gn, device=dev, dtype=torch.float64)[off:off + n]
-    return (y + 1e-5 * noise).contiguous().reshape(-1)
+    # relative to the full batch's signal norm (weights of all samples)
+    wfull = torch.randn(w.batch, 12, generator=_gen(dev, 3000 + b), device=dev, dtype=torch.float64)[:, :active]
+    scale = 1e-5 * float(wfull.norm()) / math.sqrt(w.batch * math.prod(w.dims))
+    return (y + scale * noise).contiguous().reshape(-1)
 
 
 # ---- c4 -------------------------------------------------------------------
