@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
     const int R = R01 * a.r2;
     double* Wbuf = reinterpret_cast<double*>(U1f + (N1 / 8) * MT1 * 32);  // [2][kWarps][R01]
     double* Zs = Wbuf + 2 * kWarps * R01;                                   // [R]
+    double* U2s = Zs + R;                                                   // [n2 * r2]
     __shared__ double red[kWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -91,6 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
         U1f[idx] = v;
     }
     for (int e = tid; e < R; e += kThreads) Zs[e] = 0.0;
+    for (int64_t e = tid; e < a.n2 * a.r2; e += kThreads) U2s[e] = a.U2[e];
     __syncthreads();
 
     const int64_t B = gridDim.x, b = blockIdx.x;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
 #pragma unroll
     for (int k = 0; k < kPrefetch; ++k) pf_issue(ring[k]);
 
-    double ysq0 = 0.0, ysq1 = 0.0;
+    double ysq0 = 0.0, ysq1 = 0.0, ysq2 = 0.0, ysq3 = 0.0;
     int64_t cur_s = -1;
     const int64_t maxs = ri.maxs;
 
@@ -153,15 +155,23 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
                     const int c = c0 + cc;
                     const double2 x0 = ring[cc][0], x1 = ring[cc][1];
                     pf_issue(ring[cc]);  // refill with the chunk kPrefetch steps ahead
-                    ysq0 = fma(x0.x, x0.x, fma(x0.y, x0.y, ysq0));
-                    ysq1 = fma(x1.x, x1.x, fma(x1.y, x1.y, ysq1));
+                    ysq0 = fma(x0.x, x0.x, ysq0);
+                    ysq1 = fma(x0.y, x0.y, ysq1);
+                    ysq2 = fma(x1.x, x1.x, ysq2);
+                    ysq3 = fma(x1.y, x1.y, ysq3);
+                    double2 u[MT0];
+#pragma unroll
+                    for (int ma = 0; ma < MT0; ++ma) u[ma] = U0f[(c * MT0 + ma) * 32 + lane];
+                    // dependent MMAs on one accumulator are 2*MT0 issues apart
 #pragma unroll
                     for (int ma = 0; ma < MT0; ++ma) {
-                        const double2 u = U0f[(c * MT0 + ma) * 32 + lane];
-                        dmma(pacc[ma][0], u.x, x0.x);
-                        dmma(pacc[ma][1], u.x, x1.x);
-                        dmma(pacc[ma][0], u.y, x0.y);
-                        dmma(pacc[ma][1], u.y, x1.y);
+                        dmma(pacc[ma][0], u[ma].x, x0.x);
+                        dmma(pacc[ma][1], u[ma].x, x1.x);
+                    }
+#pragma unroll
+                    for (int ma = 0; ma < MT0; ++ma) {
+                        dmma(pacc[ma][0], u[ma].y, x0.y);
+                        dmma(pacc[ma][1], u[ma].y, x1.y);
                     }
                 }
             }
@@ -169,15 +179,16 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
                 const int ntile = 2 * pair + nt;
+                double2 u[MT1];
 #pragma unroll
-                for (int mb = 0; mb < MT1; ++mb) {
-                    const double2 u = U1f[(ntile * MT1 + mb) * 32 + lane];
+                for (int mb = 0; mb < MT1; ++mb) u[mb] = U1f[(ntile * MT1 + mb) * 32 + lane];
 #pragma unroll
-                    for (int ma = 0; ma < MT0; ++ma) {
-                        dmma(wacc[ma][mb], pacc[ma][nt][0], u.x);
-                        dmma(wacc[ma][mb], pacc[ma][nt][1], u.y);
-                    }
-                }
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int mb = 0; mb < MT1; ++mb)
+#pragma unroll
+                        for (int ma = 0; ma < MT0; ++ma)
+                            dmma(wacc[ma][mb], pacc[ma][nt][j], j ? u[mb].y : u[mb].x);
             }
         }
 
@@ -196,12 +207,18 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
         }
         __syncthreads();
 
-        // step 3: Z_s += W (x) U2[i2, :] for the group's slabs, in slab order
+        // step 3: Z_s += W (x) U2[i2, :] over the group's slabs; runs of
+        // slabs of one sample accumulate in registers, one Z pass per run
         const double* wsrc = Wbuf + (g & 1) * kWarps * R01;
-        for (int w = 0; w < kWarps; ++w) {
-            const int64_t tw = tb + kWarps * g + w;
-            if (tw >= te) break;
-            const int64_t s = tw / a.n2, i2 = tw - s * a.n2;
+        const int64_t rem_slabs = te - (tb + kWarps * g);
+        const int nact = static_cast<int>(rem_slabs < kWarps ? rem_slabs : kWarps);
+        int w0 = 0;
+        while (w0 < nact) {
+            const int64_t t0 = tb + kWarps * g + w0;
+            const int64_t s = t0 / a.n2;
+            const int64_t i20 = t0 - s * a.n2;
+            int w1 = w0 + 1;
+            while (w1 < nact && (t0 + (w1 - w0)) / a.n2 == s) ++w1;
             if (s != cur_s) {
                 if (cur_s >= 0) {
                     double* zp = a.zpart + ((b * maxs) + (cur_s - s_first)) * R;
@@ -212,10 +229,19 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
                 }
                 cur_s = s;
             }
+            int p = tid % R01, a2 = tid / R01;
             for (int e = tid; e < R; e += kThreads) {
-                const int a2 = e / R01, p = e - a2 * R01;
-                Zs[e] = fma(wsrc[w * R01 + p], __ldg(a.U2 + i2 + a.n2 * a2), Zs[e]);
+                double acc = Zs[e];
+                const double* u2 = U2s + i20 + a.n2 * a2;
+                for (int w = w0; w < w1; ++w) acc = fma(wsrc[w * R01 + p], u2[w - w0], acc);
+                Zs[e] = acc;
+                p += kThreads;
+                while (p >= R01) {
+                    p -= R01;
+                    ++a2;
+                }
             }
+            w0 = w1;
         }
     }
     if (cur_s >= 0) {
@@ -224,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
     }
 
     // ||Y||^2 partial of this CTA (fixed shuffle tree, fixed warp order)
-    double ys = ysq0 + ysq1;
+    double ys = (ysq0 + ysq1) + (ysq2 + ysq3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ys += __shfl_xor_sync(0xffffffffu, ys, o);
     if (lane == 0) red[warp] = ys;
@@ -236,27 +262,33 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
     }
 }
 
-// Z[e + R s] = sum over the CTAs whose slab range meets sample s, in CTA order.
+// Z[e + R s] = sum over the CTAs whose slab range meets sample s, in CTA
+// order. One CTA per sample; the contributing CTA range is found once.
 __global__ void fused3_reduce_kernel(const Fused3Args a, RangeInfo ri, int64_t B) {
+    __shared__ int64_t range[2];
     const int64_t R = static_cast<int64_t>(a.r0) * a.r1 * a.r2;
-    const int64_t total = R * a.S;
-    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t s = idx / R, e = idx - s * R;
-        const int64_t lo = s * a.n2, hi = lo + a.n2;  // slabs of sample s
-        // first CTA whose range ends after lo
-        int64_t bl = (lo * B) / ri.T;
-        while (bl > 0 && cta_begin(ri.T, bl, B) > lo) --bl;
-        while (cta_begin(ri.T, bl + 1, B) <= lo) ++bl;
-        double acc = 0.0;
-        for (int64_t bb = bl; bb < B; ++bb) {
-            const int64_t tb = cta_begin(ri.T, bb, B), te = cta_begin(ri.T, bb + 1, B);
-            if (tb >= hi) break;
-            if (te <= tb) continue;
-            const int64_t sf = tb / a.n2;
-            acc += a.zpart[((bb * ri.maxs) + (s - sf)) * R + e];
+    for (int64_t s = blockIdx.x; s < a.S; s += gridDim.x) {
+        if (threadIdx.x == 0) {
+            const int64_t lo = s * a.n2, hi = lo + a.n2;
+            int64_t bl = (lo * B) / ri.T;
+            while (bl > 0 && cta_begin(ri.T, bl, B) > lo) --bl;
+            while (cta_begin(ri.T, bl + 1, B) <= lo) ++bl;
+            int64_t bh = bl;
+            while (bh + 1 < B && cta_begin(ri.T, bh + 1, B) < hi) ++bh;
+            range[0] = bl;
+            range[1] = bh;
         }
-        a.Z[idx] = acc;
+        __syncthreads();
+        const int64_t bl = range[0], bh = range[1];
+        for (int64_t e = threadIdx.x; e < R; e += blockDim.x) {
+            double acc = 0.0;
+            for (int64_t bb = bl; bb <= bh; ++bb) {
+                const int64_t tb = cta_begin(ri.T, bb, B);
+                acc += a.zpart[((bb * ri.maxs) + (s - tb / a.n2)) * R + e];
+            }
+            a.Z[e + R * s] = acc;
+        }
+        __syncthreads();
     }
 }
 
@@ -268,12 +300,11 @@ int launch_impl(const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launc
     RangeInfo ri{T, (per + a.n2 - 1) / a.n2 + 1};
     const int64_t R01 = static_cast<int64_t>(a.r0) * a.r1;
     const size_t smem = sizeof(double) * (static_cast<size_t>(N0 / 8) * MT0 * 64 + static_cast<size_t>(N1 / 8) * MT1 * 64 +
-                                          2 * kWarps * R01 + R01 * a.r2);
+                                          2 * kWarps * R01 + R01 * a.r2 + a.n2 * a.r2);
     auto kfn = fused3_kernel<N0, N1, MT0, MT1>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kfn<<<static_cast<unsigned>(B), kThreads, smem, s>>>(a, ri);
-    const int64_t total = R01 * a.r2 * a.S;
-    const int rb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 4 * num_sms)));
+    const int rb = static_cast<int>(std::min<int64_t>(a.S, 65535));
     fused3_reduce_kernel<<<rb, 256, 0, s>>>(a, ri, B);
     *launches += 2;
     return static_cast<int>(B);
@@ -291,13 +322,14 @@ int dispatch_mt(int mt, const Fused3Args& a, int num_sms, cudaStream_t s, int64_
 
 }  // namespace
 
-bool fused3_supported(int64_t n0, int64_t n1, int r0, int r1, int r2) {
+bool fused3_supported(int64_t n0, int64_t n1, int64_t n2, int r0, int r1, int r2) {
     if (n0 != n1 || (n0 != 64 && n0 != 128)) return false;
     if (r0 < 1 || r1 < 1 || r2 < 1 || r0 > 24 || r1 > 24) return false;
     if (static_cast<int64_t>(r0) * r1 * r2 > kMaxZ) return false;
     const int64_t R01 = static_cast<int64_t>(r0) * r1;
     const int mt = (std::max(r0, r1) + 7) / 8;
-    const size_t smem = sizeof(double) * (static_cast<size_t>(n0 / 8) * mt * 64 * 2 + 2 * kWarps * R01 + R01 * r2);
+    const size_t smem =
+        sizeof(double) * (static_cast<size_t>(n0 / 8) * mt * 64 * 2 + 2 * kWarps * R01 + R01 * r2 + n2 * r2);
     return smem <= 227 * 1024;
 }
 

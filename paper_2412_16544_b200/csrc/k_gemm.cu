@@ -17,7 +17,7 @@
 namespace htr {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
+constexpr int BM = 64, BN = 64, BK = 16, NT = 128;
 
 struct Flags {
     int a_kfast;
@@ -43,70 +43,89 @@ __device__ __forceinline__ int64_t c_off(const GemmDesc& d, int64_t m, int64_t n
     return m * d.scm + n1 * d.scn1 + n2 * d.scn2;
 }
 
+// FP64 tensor-core tile: 64x64 outputs per CTA, 4 warps each owning a
+// 32x32 quadrant as 4x4 DMMA 8x8 accumulators, K staged 16 at a time through
+// shared memory (row pitch 68 doubles: conflict-free fragment reads).
+constexpr int PITCH = BM + 4;
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c[0]), "+d"(c[1])
+        : "d"(a), "d"(b));
+}
+
 __global__ void __launch_bounds__(NT) gemm_kernel(const GemmDesc d, const int64_t kchunk, double* partial,
                                                   const Flags fl) {
-    __shared__ double As[BK][BM + 1];
-    __shared__ double Bs[BK][BN + 1];
+    __shared__ __align__(16) double As[2][BK][PITCH];
+    __shared__ __align__(16) double Bs[2][BK][PITCH];
     __shared__ double red[NT / 32];
 
-    const int t = threadIdx.x;
-    const int tx = t & 15, ty = t >> 4;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
     const int64_t M = d.M, N = d.N1 * d.N2, K = d.K1 * d.K2;
     const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
     const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
     const int64_t kbeg = static_cast<int64_t>(blockIdx.z) * kchunk;
     const int64_t kend = min(K, kbeg + kchunk);
 
-    double acc[4][4];
+    double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    double ra[4], rb[4];
+    constexpr int PER = BM * BK / NT;  // 8 elements of each operand per thread
+    double ra[PER], rb[PER];
     auto load = [&](int64_t k0) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < PER; ++j) {
             int kk, mm;
-            if (fl.a_kfast) { kk = t & 15; mm = (t >> 4) + 16 * j; }
-            else { mm = t & 63; kk = (t >> 6) + 4 * j; }
+            if (fl.a_kfast) { kk = t & 15; mm = (t >> 4) + 8 * j; }
+            else { mm = t & 63; kk = (t >> 6) + 2 * j; }
             const int64_t m = m0 + mm, k = k0 + kk;
             ra[j] = (m < M && k < kend) ? __ldg(d.A + a_off(d, m, k)) : 0.0;
             int nn;
-            if (fl.b_kfast) { kk = t & 15; nn = (t >> 4) + 16 * j; }
-            else { nn = t & 63; kk = (t >> 6) + 4 * j; }
+            if (fl.b_kfast) { kk = t & 15; nn = (t >> 4) + 8 * j; }
+            else { nn = t & 63; kk = (t >> 6) + 2 * j; }
             const int64_t n = n0 + nn, k2 = k0 + kk;
             rb[j] = (n < N && k2 < kend) ? __ldg(d.B + b_off(d, k2, n)) : 0.0;
         }
     };
-    auto stash = [&]() {
+    auto stash = [&](int buf) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (fl.a_kfast) As[t & 15][(t >> 4) + 16 * j] = ra[j];
-            else As[(t >> 6) + 4 * j][t & 63] = ra[j];
-            if (fl.b_kfast) Bs[t & 15][(t >> 4) + 16 * j] = rb[j];
-            else Bs[(t >> 6) + 4 * j][t & 63] = rb[j];
+        for (int j = 0; j < PER; ++j) {
+            if (fl.a_kfast) As[buf][t & 15][(t >> 4) + 8 * j] = ra[j];
+            else As[buf][(t >> 6) + 2 * j][t & 63] = ra[j];
+            if (fl.b_kfast) Bs[buf][t & 15][(t >> 4) + 8 * j] = rb[j];
+            else Bs[buf][(t >> 6) + 2 * j][t & 63] = rb[j];
         }
     };
 
-    if (kbeg < kend) load(kbeg);
+    int buf = 0;
+    if (kbeg < kend) {
+        load(kbeg);
+        stash(0);
+    }
+    __syncthreads();
     for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
-        stash();
-        __syncthreads();
-        if (k0 + BK < kend) load(k0 + BK);
+        const bool more = k0 + BK < kend;
+        if (more) load(k0 + BK);  // global loads in flight during the MMAs
 #pragma unroll
-        for (int kk = 0; kk < BK; ++kk) {
+        for (int ks = 0; ks < BK; ks += 4) {
             double a[4], b[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+            for (int i = 0; i < 4; ++i) a[i] = As[buf][ks + t4][wm + 8 * i + g4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+            for (int j = 0; j < 4; ++j) b[j] = Bs[buf][ks + t4][wn + 8 * j + g4];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < 4; ++j) dmma884(acc[i][j], a[i], b[j]);
         }
+        if (more) stash(buf ^ 1);
         __syncthreads();
+        buf ^= 1;
     }
 
     if (fl.energy) {
@@ -114,16 +133,18 @@ __global__ void __launch_bounds__(NT) gemm_kernel(const GemmDesc d, const int64_
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
-                if (m < M && n < N) {
-                    const double r = d.D[c_off(d, m, n)] - acc[i][j];
-                    e = fma(r, r, e);
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t m = m0 + wm + 8 * i + g4, n = n0 + wn + 8 * j + 2 * t4 + h;
+                    if (m < M && n < N) {
+                        const double r = d.D[c_off(d, m, n)] - acc[i][j][h];
+                        e = fma(r, r, e);
+                    }
                 }
-            }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-        if ((t & 31) == 0) red[t >> 5] = e;
+        if (lane == 0) red[warp] = e;
         __syncthreads();
         if (t == 0) {
             double s = 0.0;
@@ -136,17 +157,19 @@ __global__ void __launch_bounds__(NT) gemm_kernel(const GemmDesc d, const int64_
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int64_t m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
-            if (m < M && n < N) {
-                if (partial) {
-                    partial[(static_cast<int64_t>(blockIdx.z) * M + m) * N + n] = acc[i][j];
-                } else {
-                    double* c = d.C + c_off(d, m, n);
-                    *c = d.beta == 0.0 ? d.alpha * acc[i][j] : fma(d.alpha, acc[i][j], d.beta * *c);
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t m = m0 + wm + 8 * i + g4, n = n0 + wn + 8 * j + 2 * t4 + h;
+                if (m < M && n < N) {
+                    if (partial) {
+                        partial[(static_cast<int64_t>(blockIdx.z) * M + m) * N + n] = acc[i][j][h];
+                    } else {
+                        double* c = d.C + c_off(d, m, n);
+                        *c = d.beta == 0.0 ? d.alpha * acc[i][j][h] : fma(d.alpha, acc[i][j][h], d.beta * *c);
+                    }
                 }
             }
-        }
 }
 
 __global__ void splitk_reduce_kernel(const GemmDesc d, const double* partial, int splits) {

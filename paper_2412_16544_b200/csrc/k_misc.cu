@@ -67,12 +67,18 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const double* __restrict__ x
 }
 
 __global__ void sumsq_finish_kernel(const double* partials, int nb, double* out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double t = 0.0, b = 0.0;
-        for (int i = 0; i < nb; ++i) {
-            t += partials[2 * i];
-            b = fmax(b, partials[2 * i + 1]);
-        }
+    // one warp, fixed lane striding and shuffle tree: deterministic
+    double t = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 32) {
+        t += partials[2 * i];
+        b = fmax(b, partials[2 * i + 1]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        t += __shfl_xor_sync(0xffffffffu, t, o);
+        b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (threadIdx.x == 0) {
         out[0] = t;
         out[1] = b;
     }

@@ -99,7 +99,7 @@ struct Fused3Args {
     double* ysq_partials = nullptr;  // grid entries
 };
 // Whether the fused kernel supports this shape; returns the grid size used.
-bool fused3_supported(int64_t n0, int64_t n1, int r0, int r1, int r2);
+bool fused3_supported(int64_t n0, int64_t n1, int64_t n2, int r0, int r1, int r2);
 int64_t fused3_workspace_doubles(int64_t n0, int64_t n1, int64_t n2, int64_t S, int r0, int r1, int r2,
                                  int num_sms);
 int launch_fused3(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches);

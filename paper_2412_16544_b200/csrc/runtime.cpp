@@ -618,7 +618,7 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
                 if (n.kind == NodeKind::Leaf) leaf_of[n.leaf_dim] = n.id;
         const int r0 = static_cast<int>(ranks.at(leaf_of[0])), r1 = static_cast<int>(ranks.at(leaf_of[1])),
                   r2 = static_cast<int>(ranks.at(leaf_of[2]));
-        if (fused3_supported(y.shape[0], y.shape[1], r0, r1, r2)) {
+        if (fused3_supported(y.shape[0], y.shape[1], y.shape[2], r0, r1, r2)) {
             Fused3Args fa;
             fa.Y = y.data();
             fa.n2 = y.shape[2];
