@@ -10,22 +10,30 @@
 //
 // which is the leaf-projected working tensor of encode for every 3-way tree
 // ((1,(2,3)) and ((1,2),3)); the interior transfer projection then runs on
-// the 1/(N0 N1 n2 / r0 r1 r2)-size Z.
+// the r0 r1 r2 / (N0 N1 n2)-size Z.
 //
-// Data path per warp and slab X = Y[:, :, i2, s] (N0 x N1, contiguous):
-//   step 1  P = U0^T X     (8x4x8 DMMA tiles; X fragments come straight from
-//                           HBM into registers with 16-byte ld.global.nc, each
-//                           element loaded exactly once, prefetched 8 chunks
-//                           ahead; U0^T fragments from shared memory)
-//   step 2  W = P U1       (P's accumulator fragments are re-used in
-//                           registers as the A operand: the k index of the
-//                           MMA is permuted to match the C layout)
-//   step 3  Z_s += W (x) U2[i2, :]   (CTA-wide, shared-memory accumulators,
-//                           flushed per sample to a partial buffer that a
-//                           second kernel reduces in a fixed order).
+// Structure (one CTA per SM, no CTA barriers in the main loop). Each of 8
+// warps owns every 8th slab X = Y[:, :, i2, s] (N0 x N1, contiguous) of its
+// CTA's slab range and walks it in steps of 16 columns x 32 rows; each step
+// arrives by two TMA tensor copies (cp.async.bulk.tensor.3d over a
+// [N0, N1, slabs] tensor map, 16x16 boxes, 128-byte swizzle) into the warp's
+// own 4-deep shared-memory ring, issued by one lane three steps ahead and
+// completed on a per-stage mbarrier. The MMA's
+// column order is permuted (n-index g -> physical column pi(g)) so that the
+// swizzled fragment reads are bank-conflict-free; step 2 undoes the
+// permutation through the order of the U1 fragments;
+//   * step 1  P = U0^T X    DMMA 8x8x4 with U0^T fragments from shared memory;
+//   * step 2  W += P U1     P's accumulator fragments re-used in registers as
+//                           the A operand (MMA k index permuted to the C layout);
+//   * per slab the warp writes W (r0 x r1) to global memory; a DMMA GEMM
+//     then contracts the slab axis with U2:  Z_s = sum_i2 W_(s,i2) (x) U2[i2,:].
 // Everything is deterministic: no atomics, fixed reduction trees.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 
 #include "kernels.cuh"
 
@@ -34,45 +42,93 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int kPrefetch = 8;  // chunks of 8 rows in flight per warp
-constexpr int kMaxZ = 8192;   // r0*r1*r2 accumulators kept in shared memory
+constexpr int kStages = 4;         // per-warp ring depth
+constexpr int kRows = 32;          // rows (i0) per step
+constexpr int kCols = 16;          // columns (i1) per step = 2 DMMA n-tiles
+constexpr int kBoxRows = 16;      // TMA box: 16 doubles (128 B, the swizzle span) x 16 columns
+constexpr int kBoxDoubles = kBoxRows * kCols;
+constexpr int kStageDoubles = kCols * kRows;  // two boxes
+constexpr uint32_t kStageBytes = kCols * kRows * sizeof(double);
+
+// physical column (within an 8-column MMA n-tile) of MMA n-index g: lanes
+// g and g+1 of a quarter-warp land in columns differing in bit 2, whose
+// 128-byte swizzle XOR sends them to disjoint 16-byte bank groups
+__host__ __device__ __forceinline__ int col_perm(int g) { return (g >> 1) + 4 * (g & 1); }
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(c[0]), "+d"(c[1])
-                 : "d"(a), "d"(b));
+        : "+d"(c[0]), "+d"(c[1])
+        : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ double2 ldg_stream(const double* p) {
-    double2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    return v;
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// global -> shared tensor copy (TMA engine), completion counted on `bar`;
+// the batch is read exactly once, so it is marked evict-first in L2
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 
 struct RangeInfo {
-    int64_t T;      // total slabs = n2 * S
-    int64_t maxs;   // sample slots per CTA
+    int64_t T;  // total slabs = n2 * S
 };
 
 __host__ __device__ __forceinline__ int64_t cta_begin(int64_t T, int64_t b, int64_t B) { return (T * b) / B; }
 
 template <int N0, int N1, int MT0, int MT1>
-__global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a, const RangeInfo ri) {
-    constexpr int NC = N0 / 8;   // k-chunks (8 rows of i0) per column block
-    constexpr int NP = N1 / 16;  // n-tile pairs per slab
-    constexpr int STEPS = NP * NC;
-    extern __shared__ __align__(16) double smem[];
-    double2* U0f = reinterpret_cast<double2*>(smem);                 // [NC][MT0][32]
-    double2* U1f = U0f + NC * MT0 * 32;                              // [N1/8][MT1][32]
-    const int R01 = a.r0 * a.r1;
-    const int R = R01 * a.r2;
-    double* Wbuf = reinterpret_cast<double*>(U1f + (N1 / 8) * MT1 * 32);  // [2][kWarps][R01]
-    double* Zs = Wbuf + 2 * kWarps * R01;                                   // [R]
-    double* U2s = Zs + R;                                                   // [n2 * r2]
+__global__ void __launch_bounds__(kThreads, 1)
+    fused3_kernel(const Fused3Args a, const RangeInfo ri, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int NC = N0 / 8;      // 8-row chunks per column block
+    constexpr int NQ = N0 / kRows;  // steps per column pair
+    constexpr int NP = N1 / kCols;  // column pairs per slab
+    constexpr int IPS = NP * NQ;    // steps per slab
+    extern __shared__ __align__(1024) double smem_raw[];
+    // stages first: the 128-byte swizzle needs 1024-byte aligned boxes
+    double* stages = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u) / sizeof(double);  // [warp][stage][box][col][16]
+    double2* U0f = reinterpret_cast<double2*>(stages + kWarps * kStages * kStageDoubles);  // [NC][MT0][32]
+    double2* U1f = U0f + NC * MT0 * 32;                                              // [N1/8][MT1][32]
+    uint64_t* full = reinterpret_cast<uint64_t*>(U1f + (N1 / 8) * MT1 * 32);  // [warp][stage]
     __shared__ double red[kWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g4 = lane >> 2, t4 = lane & 3;
+    const int R01 = a.r0 * a.r1;
 
     // ---- stage basis fragments (zero-padded to 8-multiples) ----
     for (int idx = tid; idx < NC * MT0 * 32; idx += kThreads) {
@@ -85,97 +141,102 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
     }
     for (int idx = tid; idx < (N1 / 8) * MT1 * 32; idx += kThreads) {
         const int l = idx & 31, mt = (idx >> 5) % MT1, nt = idx / (32 * MT1);
-        const int i1 = 8 * nt + 2 * (l & 3), col = 8 * mt + (l >> 2);
+        const int i1x = 8 * nt + col_perm(2 * (l & 3)), i1y = 8 * nt + col_perm(2 * (l & 3) + 1);
+        const int col = 8 * mt + (l >> 2);
         double2 v;
-        v.x = col < a.r1 ? a.U1[i1 + static_cast<int64_t>(N1) * col] : 0.0;
-        v.y = col < a.r1 ? a.U1[i1 + 1 + static_cast<int64_t>(N1) * col] : 0.0;
+        v.x = col < a.r1 ? a.U1[i1x + static_cast<int64_t>(N1) * col] : 0.0;
+        v.y = col < a.r1 ? a.U1[i1y + static_cast<int64_t>(N1) * col] : 0.0;
         U1f[idx] = v;
     }
-    for (int e = tid; e < R; e += kThreads) Zs[e] = 0.0;
-    for (int64_t e = tid; e < a.n2 * a.r2; e += kThreads) U2s[e] = a.U2[e];
+    if (tid < kWarps * kStages) mbar_init(&full[tid], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
     const int64_t B = gridDim.x, b = blockIdx.x;
     const int64_t tb = cta_begin(ri.T, b, B), te = cta_begin(ri.T, b + 1, B);
-    const int64_t ngroups = (te - tb + kWarps - 1) / kWarps;
-    const int64_t s_first = tb / a.n2;
     const int64_t slab_elems = static_cast<int64_t>(N0) * N1;
-
-    // prefetch stream: (group, pair, chunk) counters of the chunk kPrefetch
-    // steps ahead of the one being consumed
-    const int lane_off = 2 * t4 + N0 * g4;  // row offset in a chunk + column in an n-tile
-    int64_t pf_g = 0;
-    int pf_pair = 0, pf_c = 0;
-    auto pf_issue = [&](double2 (&dst)[2]) {
-        const int64_t t = tb + kWarps * pf_g + warp;
-        if (t < te) {
-            const double* p = a.Y + t * slab_elems + static_cast<int64_t>(16 * N0) * pf_pair + 8 * pf_c + lane_off;
-            dst[0] = ldg_stream(p);
-            dst[1] = ldg_stream(p + 8 * N0);
-        } else {
-            dst[0] = make_double2(0.0, 0.0);
-            dst[1] = make_double2(0.0, 0.0);
-        }
-        if (++pf_c == NC) {
-            pf_c = 0;
-            if (++pf_pair == NP) {
-                pf_pair = 0;
-                ++pf_g;
-            }
-        }
+    auto steps_of = [&](int w) -> int64_t {
+        return (te - tb > w ? (te - tb - w + kWarps - 1) / kWarps : 0) * IPS;
     };
 
-    double2 ring[kPrefetch][2];
-#pragma unroll
-    for (int k = 0; k < kPrefetch; ++k) pf_issue(ring[k]);
+    const int64_t total = steps_of(warp);
+    double* my_stages = stages + warp * kStages * kStageDoubles;
+    uint64_t* my_full = full + warp * kStages;
+    const uint64_t policy = evict_first_policy();
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+
+    auto issue = [&](int64_t i) {  // lane 0 only
+        const int st = static_cast<int>(i % kStages);
+        const int64_t j = i / IPS;
+        const int rem = static_cast<int>(i - j * IPS);
+        const int pair = rem / NQ, q = rem - pair * NQ;
+        const int t = static_cast<int>(tb + warp + kWarps * j);
+        mbar_expect_tx(&my_full[st], kStageBytes);
+        double* dst = my_stages + st * kStageDoubles;
+        tma_load_3d(dst, &tmap, kRows * q, kCols * pair, t, &my_full[st], policy);
+        tma_load_3d(dst + kBoxDoubles, &tmap, kRows * q + kBoxRows, kCols * pair, t, &my_full[st], policy);
+    };
+    if (lane == 0)
+        for (int k = 0; k < kStages; ++k)
+            if (k < total) issue(k);
 
     double ysq0 = 0.0, ysq1 = 0.0, ysq2 = 0.0, ysq3 = 0.0;
-    int64_t cur_s = -1;
-    const int64_t maxs = ri.maxs;
+    double wacc[MT0][MT1][2];
+    double pacc[MT0][2][2];
+#pragma unroll
+    for (int i = 0; i < MT0; ++i)
+#pragma unroll
+        for (int j = 0; j < MT1; ++j) wacc[i][j][0] = wacc[i][j][1] = 0.0;
 
-    for (int64_t g = 0; g < ngroups; ++g) {
-        const int64_t t = tb + kWarps * g + warp;
-        const bool active = t < te;
-        double wacc[MT0][MT1][2];
+    for (int64_t i = 0; i < total; ++i) {
+        const int st = static_cast<int>(i % kStages);
+        const int64_t j = i / IPS;
+        const int rem = static_cast<int>(i - j * IPS);
+        const int pair = rem / NQ, q = rem - pair * NQ;
+        if (q == 0) {
 #pragma unroll
-        for (int i = 0; i < MT0; ++i)
+            for (int x = 0; x < MT0; ++x)
 #pragma unroll
-            for (int j = 0; j < MT1; ++j) wacc[i][j][0] = wacc[i][j][1] = 0.0;
-
-        for (int pair = 0; pair < NP; ++pair) {
-            double pacc[MT0][2][2];
+                for (int y = 0; y < 2; ++y) pacc[x][y][0] = pacc[x][y][1] = 0.0;
+        }
+        mbar_wait(&my_full[st], static_cast<uint32_t>((i / kStages) & 1));
+        const double* sb = my_stages + st * kStageDoubles;
+        const int pc0 = col_perm(g4), pc1 = 8 + col_perm(g4);
 #pragma unroll
-            for (int i = 0; i < MT0; ++i)
+        for (int cc = 0; cc < kRows / 8; ++cc) {
+            const int c = q * (kRows / 8) + cc;
+            const int box = cc >> 1, chunk = 4 * (cc & 1) + t4;  // 16-byte chunk within the 128-byte column
+            const double* bb = sb + box * kBoxDoubles;
+            const double2 x0 = *reinterpret_cast<const double2*>(bb + pc0 * kBoxRows + 2 * (chunk ^ (pc0 & 7)));
+            const double2 x1 = *reinterpret_cast<const double2*>(bb + pc1 * kBoxRows + 2 * (chunk ^ (pc1 & 7)));
+            double2 u[MT0];
 #pragma unroll
-                for (int j = 0; j < 2; ++j) pacc[i][j][0] = pacc[i][j][1] = 0.0;
-#pragma unroll 1
-            for (int c0 = 0; c0 < NC; c0 += kPrefetch) {
+            for (int ma = 0; ma < MT0; ++ma) u[ma] = U0f[(c * MT0 + ma) * 32 + lane];
+            ysq0 = fma(x0.x, x0.x, ysq0);
+            ysq1 = fma(x0.y, x0.y, ysq1);
+            ysq2 = fma(x1.x, x1.x, ysq2);
+            ysq3 = fma(x1.y, x1.y, ysq3);
 #pragma unroll
-                for (int cc = 0; cc < kPrefetch; ++cc) {
-                    const int c = c0 + cc;
-                    const double2 x0 = ring[cc][0], x1 = ring[cc][1];
-                    pf_issue(ring[cc]);  // refill with the chunk kPrefetch steps ahead
-                    ysq0 = fma(x0.x, x0.x, ysq0);
-                    ysq1 = fma(x0.y, x0.y, ysq1);
-                    ysq2 = fma(x1.x, x1.x, ysq2);
-                    ysq3 = fma(x1.y, x1.y, ysq3);
-                    double2 u[MT0];
-#pragma unroll
-                    for (int ma = 0; ma < MT0; ++ma) u[ma] = U0f[(c * MT0 + ma) * 32 + lane];
-                    // dependent MMAs on one accumulator are 2*MT0 issues apart
-#pragma unroll
-                    for (int ma = 0; ma < MT0; ++ma) {
-                        dmma(pacc[ma][0], u[ma].x, x0.x);
-                        dmma(pacc[ma][1], u[ma].x, x1.x);
-                    }
-#pragma unroll
-                    for (int ma = 0; ma < MT0; ++ma) {
-                        dmma(pacc[ma][0], u[ma].y, x0.y);
-                        dmma(pacc[ma][1], u[ma].y, x1.y);
-                    }
-                }
+            for (int ma = 0; ma < MT0; ++ma) {
+                dmma(pacc[ma][0], u[ma].x, x0.x);
+                dmma(pacc[ma][1], u[ma].x, x1.x);
             }
-            // step 2: W += P U1 over the pair's 16 columns
+#pragma unroll
+            for (int ma = 0; ma < MT0; ++ma) {
+                dmma(pacc[ma][0], u[ma].y, x0.y);
+                dmma(pacc[ma][1], u[ma].y, x1.y);
+            }
+        }
+        // the stage is consumed (its values fed warp-collective MMAs): order
+        // the generic-proxy reads before the async-proxy refill
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (i + kStages < total) issue(i + kStages);
+        }
+
+        if (q == NQ - 1) {
+            // step 2: W += P U1 over this pair's 16 columns
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
                 const int ntile = 2 * pair + nt;
@@ -183,70 +244,29 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
 #pragma unroll
                 for (int mb = 0; mb < MT1; ++mb) u[mb] = U1f[(ntile * MT1 + mb) * 32 + lane];
 #pragma unroll
-                for (int j = 0; j < 2; ++j)
+                for (int h = 0; h < 2; ++h)
 #pragma unroll
                     for (int mb = 0; mb < MT1; ++mb)
 #pragma unroll
                         for (int ma = 0; ma < MT0; ++ma)
-                            dmma(wacc[ma][mb], pacc[ma][nt][j], j ? u[mb].y : u[mb].x);
+                            dmma(wacc[ma][mb], pacc[ma][nt][h], h ? u[mb].y : u[mb].x);
+            }
+            if (pair == NP - 1) {
+                // slab done: publish W (compact a0 + r0 a1) and reset
+                const int64_t t = tb + warp + kWarps * j;
+                double* wdst = a.wslab + t * R01;
+#pragma unroll
+                for (int ma = 0; ma < MT0; ++ma)
+#pragma unroll
+                    for (int mb = 0; mb < MT1; ++mb)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int a0 = 8 * ma + g4, a1 = 8 * mb + 2 * t4 + h;
+                            if (a0 < a.r0 && a1 < a.r1) wdst[a0 + a.r0 * a1] = wacc[ma][mb][h];
+                            wacc[ma][mb][h] = 0.0;
+                        }
             }
         }
-
-        // publish this warp's W (compact a0 + r0*a1 layout)
-        double* wdst = Wbuf + ((g & 1) * kWarps + warp) * R01;
-        if (active) {
-#pragma unroll
-            for (int ma = 0; ma < MT0; ++ma)
-#pragma unroll
-                for (int mb = 0; mb < MT1; ++mb)
-#pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const int a0 = 8 * ma + g4, a1 = 8 * mb + 2 * t4 + j;
-                        if (a0 < a.r0 && a1 < a.r1) wdst[a0 + a.r0 * a1] = wacc[ma][mb][j];
-                    }
-        }
-        __syncthreads();
-
-        // step 3: Z_s += W (x) U2[i2, :] over the group's slabs; runs of
-        // slabs of one sample accumulate in registers, one Z pass per run
-        const double* wsrc = Wbuf + (g & 1) * kWarps * R01;
-        const int64_t rem_slabs = te - (tb + kWarps * g);
-        const int nact = static_cast<int>(rem_slabs < kWarps ? rem_slabs : kWarps);
-        int w0 = 0;
-        while (w0 < nact) {
-            const int64_t t0 = tb + kWarps * g + w0;
-            const int64_t s = t0 / a.n2;
-            const int64_t i20 = t0 - s * a.n2;
-            int w1 = w0 + 1;
-            while (w1 < nact && (t0 + (w1 - w0)) / a.n2 == s) ++w1;
-            if (s != cur_s) {
-                if (cur_s >= 0) {
-                    double* zp = a.zpart + ((b * maxs) + (cur_s - s_first)) * R;
-                    for (int e = tid; e < R; e += kThreads) {
-                        zp[e] = Zs[e];
-                        Zs[e] = 0.0;
-                    }
-                }
-                cur_s = s;
-            }
-            int p = tid % R01, a2 = tid / R01;
-            for (int e = tid; e < R; e += kThreads) {
-                double acc = Zs[e];
-                const double* u2 = U2s + i20 + a.n2 * a2;
-                for (int w = w0; w < w1; ++w) acc = fma(wsrc[w * R01 + p], u2[w - w0], acc);
-                Zs[e] = acc;
-                p += kThreads;
-                while (p >= R01) {
-                    p -= R01;
-                    ++a2;
-                }
-            }
-            w0 = w1;
-        }
-    }
-    if (cur_s >= 0) {
-        double* zp = a.zpart + ((b * maxs) + (cur_s - s_first)) * R;
-        for (int e = tid; e < R; e += kThreads) zp[e] = Zs[e];
     }
 
     // ||Y||^2 partial of this CTA (fixed shuffle tree, fixed warp order)
@@ -262,51 +282,71 @@ __global__ void __launch_bounds__(kThreads, 1) fused3_kernel(const Fused3Args a,
     }
 }
 
-// Z[e + R s] = sum over the CTAs whose slab range meets sample s, in CTA
-// order. One CTA per sample; the contributing CTA range is found once.
-__global__ void fused3_reduce_kernel(const Fused3Args a, RangeInfo ri, int64_t B) {
-    __shared__ int64_t range[2];
-    const int64_t R = static_cast<int64_t>(a.r0) * a.r1 * a.r2;
-    for (int64_t s = blockIdx.x; s < a.S; s += gridDim.x) {
-        if (threadIdx.x == 0) {
-            const int64_t lo = s * a.n2, hi = lo + a.n2;
-            int64_t bl = (lo * B) / ri.T;
-            while (bl > 0 && cta_begin(ri.T, bl, B) > lo) --bl;
-            while (cta_begin(ri.T, bl + 1, B) <= lo) ++bl;
-            int64_t bh = bl;
-            while (bh + 1 < B && cta_begin(ri.T, bh + 1, B) < hi) ++bh;
-            range[0] = bl;
-            range[1] = bh;
-        }
-        __syncthreads();
-        const int64_t bl = range[0], bh = range[1];
-        for (int64_t e = threadIdx.x; e < R; e += blockDim.x) {
-            double acc = 0.0;
-            for (int64_t bb = bl; bb <= bh; ++bb) {
-                const int64_t tb = cta_begin(ri.T, bb, B);
-                acc += a.zpart[((bb * ri.maxs) + (s - tb / a.n2)) * R + e];
-            }
-            a.Z[e + R * s] = acc;
-        }
-        __syncthreads();
+template <int N0, int N1, int MT0, int MT1>
+size_t smem_bytes() {
+    return sizeof(double) * (static_cast<size_t>(N0 / 8) * MT0 * 64 + static_cast<size_t>(N1 / 8) * MT1 * 64 +
+                             static_cast<size_t>(kWarps) * kStages * kStageDoubles) +
+           sizeof(uint64_t) * kWarps * kStages + 1024;  // + alignment slack
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
     }
+    return fn;
+}
+
+/// [N0, N1, T] view of the batch (T = n2 * S slabs), 16 x 16 x 1 boxes.
+bool make_batch_map(CUtensorMap* map, const double* Y, int64_t N0, int64_t N1, int64_t T) {
+    auto enc = tensor_map_encoder();
+    if (!enc || (reinterpret_cast<uintptr_t>(Y) & 15) || T > (int64_t{1} << 31)) return false;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(N0), static_cast<cuuint64_t>(N1), static_cast<cuuint64_t>(T)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(N0 * 8), static_cast<cuuint64_t>(N0 * N1 * 8)};
+    cuuint32_t box[3] = {kBoxRows, kCols, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(Y), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int N0, int N1, int MT0, int MT1>
 int launch_impl(const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {
     const int64_t T = a.n2 * a.S;
     const int64_t B = std::min<int64_t>(num_sms, T);
-    const int64_t per = (T + B - 1) / B;
-    RangeInfo ri{T, (per + a.n2 - 1) / a.n2 + 1};
-    const int64_t R01 = static_cast<int64_t>(a.r0) * a.r1;
-    const size_t smem = sizeof(double) * (static_cast<size_t>(N0 / 8) * MT0 * 64 + static_cast<size_t>(N1 / 8) * MT1 * 64 +
-                                          2 * kWarps * R01 + R01 * a.r2 + a.n2 * a.r2);
+    RangeInfo ri{T};
+    alignas(64) CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    if (!make_batch_map(&map, a.Y, N0, N1, T)) return -1;
+    const size_t smem = smem_bytes<N0, N1, MT0, MT1>();
     auto kfn = fused3_kernel<N0, N1, MT0, MT1>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    kfn<<<static_cast<unsigned>(B), kThreads, smem, s>>>(a, ri);
-    const int rb = static_cast<int>(std::min<int64_t>(a.S, 65535));
-    fused3_reduce_kernel<<<rb, 256, 0, s>>>(a, ri, B);
-    *launches += 2;
+    kfn<<<static_cast<unsigned>(B), kThreads, smem, s>>>(a, ri, map);
+    ++*launches;
+    // Z_s[p, a2] = sum_i2 W[(s, i2), p] U2[i2, a2]: the slab-axis (mode 2)
+    // contraction, one small GEMM per sample
+    GemmDesc d;
+    const int64_t R01 = static_cast<int64_t>(a.r0) * a.r1;
+    d.M = R01;
+    d.N1 = a.r2;
+    d.K1 = a.n2;
+    d.batch = a.S;
+    d.A = a.wslab;
+    d.sam = 1;
+    d.sak1 = R01;
+    d.sab = R01 * a.n2;
+    d.B = a.U2;
+    d.sbk1 = 1;
+    d.sbn1 = a.n2;
+    d.C = a.Z;
+    d.scm = 1;
+    d.scn1 = R01;
+    d.scb = R01 * a.r2;
+    launch_gemm(d, nullptr, num_sms, s, launches);
     return static_cast<int>(B);
 }
 
@@ -323,25 +363,20 @@ int dispatch_mt(int mt, const Fused3Args& a, int num_sms, cudaStream_t s, int64_
 }  // namespace
 
 bool fused3_supported(int64_t n0, int64_t n1, int64_t n2, int r0, int r1, int r2) {
+    (void)n2;
     if (n0 != n1 || (n0 != 64 && n0 != 128)) return false;
     if (r0 < 1 || r1 < 1 || r2 < 1 || r0 > 24 || r1 > 24) return false;
-    if (static_cast<int64_t>(r0) * r1 * r2 > kMaxZ) return false;
-    const int64_t R01 = static_cast<int64_t>(r0) * r1;
-    const int mt = (std::max(r0, r1) + 7) / 8;
-    const size_t smem =
-        sizeof(double) * (static_cast<size_t>(n0 / 8) * mt * 64 * 2 + 2 * kWarps * R01 + R01 * r2 + n2 * r2);
-    return smem <= 227 * 1024;
+    return true;
 }
 
 int64_t fused3_workspace_doubles(int64_t n0, int64_t n1, int64_t n2, int64_t S, int r0, int r1, int r2,
                                  int num_sms) {
     (void)n0;
     (void)n1;
+    (void)r2;
     const int64_t T = n2 * S;
     const int64_t B = std::min<int64_t>(num_sms, T);
-    const int64_t per = (T + B - 1) / B;
-    const int64_t maxs = (per + n2 - 1) / n2 + 1;
-    return B * maxs * static_cast<int64_t>(r0) * r1 * r2 + B;  // zpart + ysq partials
+    return T * static_cast<int64_t>(r0) * r1 + B;  // per-slab W + ||Y||^2 partials
 }
 
 int launch_fused3(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {

@@ -1,14 +1,18 @@
-// Generic strided f64 contraction engine (see GemmDesc in kernels.cuh).
+// Generic strided f64 contraction engine on the FP64 tensor cores (DMMA).
 //
 // Replaces the Eigen GEMMs behind mode_multiply / unfold (reference
 // tensor.hpp:300-312, 150-172), the Gram of every unfolding that feeds a
 // truncated SVD (truncated_svd.hpp:53, bht.hpp:284/325, ht_rise.hpp:144) and
 // the explicit residual energy of project_mode (bht.hpp:357-365) — all
 // without materialising an unfolding: the unfolding is an index map
-// (k1, k2) / (n1, n2) over the canonical buffer.
+// (k1, k2) / (n1, n2) over the canonical buffer (see GemmDesc).
 //
-// Tile 64x64x16, 256 threads, 4x4 f64 accumulators per thread, register
-// prefetch of the next K tile, deterministic split-K through a workspace.
+// CTA tiles of BM x BN outputs (64x64, 64x32 or 32x64, picked per problem to
+// minimise padding), 4 warps each holding (BM/2)x(BN/2) as 8x8 DMMA
+// accumulators, K staged 16 at a time through double-buffered shared memory
+// (pitch = tile + 4 doubles: conflict-free fragment reads). Operand offsets
+// along m / n are precomputed per thread; the k offset needs one 32-bit
+// multiply-shift division at most. Deterministic split-K and batching.
 #include <algorithm>
 #include <cstdio>
 
@@ -17,36 +21,29 @@
 namespace htr {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, NT = 128;
+constexpr int BK = 16, NT = 128;
 
-struct Flags {
-    int a_kfast;
-    int b_kfast;
-    int energy;
+/// n / d for n < 2^31 via multiply-high (Granlund-Montgomery round-up).
+struct FastDiv {
+    uint32_t d = 1, magic = 0, shift = 0;
+    FastDiv() = default;
+    explicit FastDiv(uint32_t dv) : d(dv) {
+        shift = 0;
+        while ((uint64_t{1} << shift) < dv) ++shift;
+        magic = static_cast<uint32_t>(((uint64_t{1} << 32) * ((uint64_t{1} << shift) - dv)) / dv + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        const uint64_t hi = __umulhi(n, magic);
+        return static_cast<uint32_t>((hi + n) >> shift);
+    }
 };
 
-__device__ __forceinline__ int64_t a_off(const GemmDesc& d, int64_t m, int64_t k) {
-    const int64_t k2 = k / d.K1;
-    const int64_t k1 = k - k2 * d.K1;
-    return m * d.sam + k1 * d.sak1 + k2 * d.sak2;
-}
-__device__ __forceinline__ int64_t b_off(const GemmDesc& d, int64_t k, int64_t n) {
-    const int64_t k2 = k / d.K1;
-    const int64_t k1 = k - k2 * d.K1;
-    const int64_t n2 = n / d.N1;
-    const int64_t n1 = n - n2 * d.N1;
-    return k1 * d.sbk1 + k2 * d.sbk2 + n1 * d.sbn1 + n2 * d.sbn2;
-}
-__device__ __forceinline__ int64_t c_off(const GemmDesc& d, int64_t m, int64_t n) {
-    const int64_t n2 = n / d.N1;
-    const int64_t n1 = n - n2 * d.N1;
-    return m * d.scm + n1 * d.scn1 + n2 * d.scn2;
-}
-
-// FP64 tensor-core tile: 64x64 outputs per CTA, 4 warps each owning a
-// 32x32 quadrant as 4x4 DMMA 8x8 accumulators, K staged 16 at a time through
-// shared memory (row pitch 68 doubles: conflict-free fragment reads).
-constexpr int PITCH = BM + 4;
+struct Launch {
+    int a_kfast, b_kfast, energy;
+    int kmode;  // 0: K1 == 1 (k -> k2), 1: K2 == 1 (k -> k1), 2: general
+    FastDiv k1div, n1div;
+    int64_t splits;
+};
 
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -54,52 +51,81 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
         : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(NT) gemm_kernel(const GemmDesc d, const int64_t kchunk, double* partial,
-                                                  const Flags fl) {
-    __shared__ __align__(16) double As[2][BK][PITCH];
-    __shared__ __align__(16) double Bs[2][BK][PITCH];
+__device__ __forceinline__ int64_t k_part(const Launch& L, int64_t k, int64_t s1, int64_t s2, int64_t K1) {
+    if (L.kmode == 0) return k * s2;
+    if (L.kmode == 1) return k * s1;
+    const int64_t k2 = L.k1div.div(static_cast<uint32_t>(k));
+    return (k - k2 * K1) * s1 + k2 * s2;
+}
+
+__device__ __forceinline__ int64_t n_part(const Launch& L, int64_t n, int64_t s1, int64_t s2, int64_t N1) {
+    const int64_t n2 = L.n1div.div(static_cast<uint32_t>(n));
+    return (n - n2 * N1) * s1 + n2 * s2;
+}
+
+template <int BM, int BN>
+__global__ void __launch_bounds__(NT, 3) gemm_kernel(const GemmDesc d, const int64_t kchunk, double* partial,
+                                                     const Launch L) {
+    constexpr int WM = BM / 2, WN = BN / 2, FM = WM / 8, FN = WN / 8;
+    constexpr int PA = BM + 4, PB = BN + 4;
+    constexpr int EA = BM * BK / NT, EB = BN * BK / NT;  // elements per thread per tile
+    __shared__ __align__(16) double As[2][BK][PA];
+    __shared__ __align__(16) double Bs[2][BK][PB];
     __shared__ double red[NT / 32];
 
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int g4 = lane >> 2, t4 = lane & 3;
-    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    const int wm = (warp & 1) * WM, wn = (warp >> 1) * WN;
     const int64_t M = d.M, N = d.N1 * d.N2, K = d.K1 * d.K2;
+    const int64_t zb = blockIdx.z / L.splits, zs = blockIdx.z - zb * L.splits;
+    const double* A = d.A + zb * d.sab;
+    const double* B = d.B + zb * d.sbb;
     const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
     const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
-    const int64_t kbeg = static_cast<int64_t>(blockIdx.z) * kchunk;
+    const int64_t kbeg = zs * kchunk;
     const int64_t kend = min(K, kbeg + kchunk);
 
-    double acc[4][4][2];
+    // per-thread operand coordinates: the m / n parts never change with k
+    auto akk = [&](int j) { return L.a_kfast ? (t & 15) : t / BM + (NT / BM) * j; };
+    auto amm = [&](int j) { return L.a_kfast ? (t >> 4) + (NT / 16) * j : t % BM; };
+    auto bkk = [&](int j) { return L.b_kfast ? (t & 15) : t / BN + (NT / BN) * j; };
+    auto bnn = [&](int j) { return L.b_kfast ? (t >> 4) + (NT / 16) * j : t % BN; };
+    int64_t aoff[EA], boff[EB];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < EA; ++j) {
+        const int64_t m = m0 + amm(j);
+        aoff[j] = m < M ? m * d.sam : -1;
+    }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < EB; ++j) {
+        const int64_t n = n0 + bnn(j);
+        boff[j] = n < N ? n_part(L, n, d.sbn1, d.sbn2, d.N1) : -1;
+    }
 
-    constexpr int PER = BM * BK / NT;  // 8 elements of each operand per thread
-    double ra[PER], rb[PER];
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    double ra[EA], rb[EB];
     auto load = [&](int64_t k0) {
 #pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            int kk, mm;
-            if (fl.a_kfast) { kk = t & 15; mm = (t >> 4) + 8 * j; }
-            else { mm = t & 63; kk = (t >> 6) + 2 * j; }
-            const int64_t m = m0 + mm, k = k0 + kk;
-            ra[j] = (m < M && k < kend) ? __ldg(d.A + a_off(d, m, k)) : 0.0;
-            int nn;
-            if (fl.b_kfast) { kk = t & 15; nn = (t >> 4) + 8 * j; }
-            else { nn = t & 63; kk = (t >> 6) + 2 * j; }
-            const int64_t n = n0 + nn, k2 = k0 + kk;
-            rb[j] = (n < N && k2 < kend) ? __ldg(d.B + b_off(d, k2, n)) : 0.0;
+        for (int j = 0; j < EA; ++j) {
+            const int64_t k = k0 + akk(j);
+            ra[j] = (aoff[j] >= 0 && k < kend) ? __ldg(A + aoff[j] + k_part(L, k, d.sak1, d.sak2, d.K1)) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < EB; ++j) {
+            const int64_t k = k0 + bkk(j);
+            rb[j] = (boff[j] >= 0 && k < kend) ? __ldg(B + boff[j] + k_part(L, k, d.sbk1, d.sbk2, d.K1)) : 0.0;
         }
     };
     auto stash = [&](int buf) {
 #pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            if (fl.a_kfast) As[buf][t & 15][(t >> 4) + 8 * j] = ra[j];
-            else As[buf][(t >> 6) + 2 * j][t & 63] = ra[j];
-            if (fl.b_kfast) Bs[buf][t & 15][(t >> 4) + 8 * j] = rb[j];
-            else Bs[buf][(t >> 6) + 2 * j][t & 63] = rb[j];
-        }
+        for (int j = 0; j < EA; ++j) As[buf][akk(j)][amm(j)] = ra[j];
+#pragma unroll
+        for (int j = 0; j < EB; ++j) Bs[buf][bkk(j)][bnn(j)] = rb[j];
     };
 
     int buf = 0;
@@ -113,32 +139,33 @@ __global__ void __launch_bounds__(NT) gemm_kernel(const GemmDesc d, const int64_
         if (more) load(k0 + BK);  // global loads in flight during the MMAs
 #pragma unroll
         for (int ks = 0; ks < BK; ks += 4) {
-            double a[4], b[4];
+            double a[FM], b[FN];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = As[buf][ks + t4][wm + 8 * i + g4];
+            for (int i = 0; i < FM; ++i) a[i] = As[buf][ks + t4][wm + 8 * i + g4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = Bs[buf][ks + t4][wn + 8 * j + g4];
+            for (int j = 0; j < FN; ++j) b[j] = Bs[buf][ks + t4][wn + 8 * j + g4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < FM; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma884(acc[i][j], a[i], b[j]);
+                for (int j = 0; j < FN; ++j) dmma884(acc[i][j], a[i], b[j]);
         }
         if (more) stash(buf ^ 1);
         __syncthreads();
         buf ^= 1;
     }
 
-    if (fl.energy) {
+    if (L.energy) {
+        const double* D = d.D + zb * d.scb;
         double e = 0.0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < FM; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < FN; ++j)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int64_t m = m0 + wm + 8 * i + g4, n = n0 + wn + 8 * j + 2 * t4 + h;
                     if (m < M && n < N) {
-                        const double r = d.D[c_off(d, m, n)] - acc[i][j][h];
+                        const double r = D[m * d.scm + n_part(L, n, d.scn1, d.scn2, d.N1)] - acc[i][j][h];
                         e = fma(r, r, e);
                     }
                 }
@@ -149,15 +176,18 @@ __global__ void __launch_bounds__(NT) gemm_kernel(const GemmDesc d, const int64_
         if (t == 0) {
             double s = 0.0;
             for (int w = 0; w < NT / 32; ++w) s += red[w];
-            d.energy_partials[blockIdx.x + static_cast<int64_t>(gridDim.x) * blockIdx.y] = s;
+            d.energy_partials[blockIdx.x +
+                              static_cast<int64_t>(gridDim.x) * (blockIdx.y + static_cast<int64_t>(gridDim.y) * blockIdx.z)] =
+                s;
         }
         return;
     }
 
+    double* C = d.C + zb * d.scb;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < FN; ++j)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int64_t m = m0 + wm + 8 * i + g4, n = n0 + wn + 8 * j + 2 * t4 + h;
@@ -165,45 +195,57 @@ __global__ void __launch_bounds__(NT) gemm_kernel(const GemmDesc d, const int64_
                     if (partial) {
                         partial[(static_cast<int64_t>(blockIdx.z) * M + m) * N + n] = acc[i][j][h];
                     } else {
-                        double* c = d.C + c_off(d, m, n);
+                        double* c = C + m * d.scm + n_part(L, n, d.scn1, d.scn2, d.N1);
                         *c = d.beta == 0.0 ? d.alpha * acc[i][j][h] : fma(d.alpha, acc[i][j][h], d.beta * *c);
                     }
                 }
             }
 }
 
-__global__ void splitk_reduce_kernel(const GemmDesc d, const double* partial, int splits) {
-    const int64_t M = d.M, N = d.N1 * d.N2, MN = M * N;
-    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < MN;
+__global__ void splitk_reduce_kernel(const GemmDesc d, const double* partial, int64_t splits, const Launch L) {
+    const int64_t M = d.M, N = d.N1 * d.N2, MN = M * N, total = MN * d.batch;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t zb = idx / MN, r = idx - zb * MN;
         double s = 0.0;
-        for (int z = 0; z < splits; ++z) s += partial[z * MN + idx];
-        const int64_t m = idx / N, n = idx - m * N;
-        double* c = d.C + c_off(d, m, n);
+        for (int64_t z = 0; z < splits; ++z) s += partial[(zb * splits + z) * MN + r];
+        const int64_t m = r / N, n = r - m * N;
+        double* c = d.C + zb * d.scb + m * d.scm + n_part(L, n, d.scn1, d.scn2, d.N1);
         *c = d.beta == 0.0 ? d.alpha * s : fma(d.alpha, s, d.beta * *c);
     }
 }
 
 struct Plan {
+    int bm, bn;
     int64_t tiles_n, tiles_m, splits, kchunk;
 };
 
 Plan plan_for(const GemmDesc& d, int num_sms) {
     Plan p;
     const int64_t N = d.N1 * d.N2, K = d.K1 * d.K2;
-    p.tiles_n = (N + BN - 1) / BN;
-    p.tiles_m = (d.M + BM - 1) / BM;
-    const int64_t tiles = p.tiles_n * p.tiles_m;
+    // tile shape with the least padded area (ties: the square tile)
+    const int shapes[3][2] = {{64, 64}, {64, 32}, {32, 64}};
+    int64_t best = -1;
+    for (const auto& sh : shapes) {
+        const int64_t area = ((d.M + sh[0] - 1) / sh[0]) * sh[0] * ((N + sh[1] - 1) / sh[1]) * sh[1];
+        if (best < 0 || area < best) {
+            best = area;
+            p.bm = sh[0];
+            p.bn = sh[1];
+        }
+    }
+    p.tiles_n = (N + p.bn - 1) / p.bn;
+    p.tiles_m = (d.M + p.bm - 1) / p.bm;
+    const int64_t tiles = p.tiles_n * p.tiles_m * d.batch;
     const int64_t ktiles = (K + BK - 1) / BK;
     p.splits = 1;
     if (d.energy_partials == nullptr && tiles < 2 * num_sms && ktiles >= 16) {
-        p.splits = std::min<int64_t>((2 * num_sms + tiles - 1) / tiles, ktiles / 8);
+        p.splits = std::min<int64_t>((4 * num_sms + tiles - 1) / tiles, ktiles / 8);
         p.splits = std::max<int64_t>(1, std::min<int64_t>(p.splits, 4096));
     }
     const int64_t per = (ktiles + p.splits - 1) / p.splits;
     p.kchunk = std::max<int64_t>(per, 1) * BK;
-    p.splits = (K + p.kchunk - 1) / p.kchunk;
-    if (p.splits < 1) p.splits = 1;
+    p.splits = std::max<int64_t>(1, (K + p.kchunk - 1) / p.kchunk);
     return p;
 }
 
@@ -211,33 +253,44 @@ Plan plan_for(const GemmDesc& d, int num_sms) {
 
 int64_t gemm_workspace_doubles(const GemmDesc& d, int num_sms) {
     const Plan p = plan_for(d, num_sms);
-    return p.splits > 1 ? p.splits * d.M * d.N1 * d.N2 : 0;
+    return p.splits > 1 ? p.splits * d.batch * d.M * d.N1 * d.N2 : 0;
+}
+
+int64_t gemm_energy_partials(const GemmDesc& d, int num_sms) {
+    const Plan p = plan_for(d, num_sms);
+    return p.tiles_n * p.tiles_m * d.batch;
 }
 
 int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t s, int64_t* launches) {
     const int64_t N = d.N1 * d.N2, K = d.K1 * d.K2;
-    if (d.M <= 0 || N <= 0) return 0;
+    if (d.M <= 0 || N <= 0 || d.batch <= 0) return 0;
     if (K <= 0) return 0;  // extents are >= 1 by construction
     const Plan p = plan_for(d, num_sms);
     const bool a_kc = d.K1 > 1 ? d.sak1 == 1 : d.sak2 == 1;
     const bool b_kc = d.K1 > 1 ? d.sbk1 == 1 : d.sbk2 == 1;
     const bool b_nc = d.N1 > 1 ? d.sbn1 == 1 : d.sbn2 == 1;
-    Flags fl;
-    fl.a_kfast = a_kc ? 1 : (d.sam == 1 ? 0 : 1);
-    fl.b_kfast = b_kc ? 1 : (b_nc ? 0 : 1);
-    fl.energy = d.energy_partials != nullptr;
+    Launch L;
+    L.a_kfast = a_kc ? 1 : (d.sam == 1 ? 0 : 1);
+    L.b_kfast = b_kc ? 1 : (b_nc ? 0 : 1);
+    L.energy = d.energy_partials != nullptr;
+    L.kmode = d.K1 == 1 ? 0 : (d.K2 == 1 ? 1 : 2);
+    L.k1div = FastDiv(static_cast<uint32_t>(d.K1));
+    L.n1div = FastDiv(static_cast<uint32_t>(d.N1));
+    L.splits = p.splits;
     const dim3 grid(static_cast<unsigned>(p.tiles_n), static_cast<unsigned>(p.tiles_m),
-                    static_cast<unsigned>(p.splits));
+                    static_cast<unsigned>(p.splits * d.batch));
     double* partial = p.splits > 1 ? workspace : nullptr;
-    gemm_kernel<<<grid, NT, 0, s>>>(d, p.kchunk, partial, fl);
+    if (p.bm == 64 && p.bn == 64) gemm_kernel<64, 64><<<grid, NT, 0, s>>>(d, p.kchunk, partial, L);
+    else if (p.bm == 64) gemm_kernel<64, 32><<<grid, NT, 0, s>>>(d, p.kchunk, partial, L);
+    else gemm_kernel<32, 64><<<grid, NT, 0, s>>>(d, p.kchunk, partial, L);
     ++*launches;
     if (p.splits > 1) {
-        const int64_t MN = d.M * N;
-        const int blocks = static_cast<int>(std::min<int64_t>((MN + 255) / 256, 4 * num_sms));
-        splitk_reduce_kernel<<<blocks, 256, 0, s>>>(d, partial, static_cast<int>(p.splits));
+        const int64_t total = d.M * N * d.batch;
+        const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * num_sms));
+        splitk_reduce_kernel<<<blocks, 256, 0, s>>>(d, partial, p.splits, L);
         ++*launches;
     }
-    return fl.energy ? static_cast<int>(p.tiles_n * p.tiles_m) : 0;
+    return L.energy ? static_cast<int>(p.tiles_n * p.tiles_m * d.batch) : 0;
 }
 
 }  // namespace htr

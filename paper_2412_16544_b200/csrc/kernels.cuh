@@ -18,12 +18,15 @@ constexpr int kNumSMs = 148;  // B200; the launchers query the device anyway
 //   C(m, n1, n2) = alpha * sum_{k1<K1, k2<K2} A(m, k1, k2) * B(k1, k2, n1, n2)
 //                  + beta * C(m, n1, n2)
 // Offsets: A = m*sam + k1*sak1 + k2*sak2, B = k1*sbk1 + k2*sbk2 + n1*sbn1 +
-// n2*sbn2, C = m*scm + n1*scn1 + n2*scn2. Covers every mode product (leaf
+// n2*sbn2, C = m*scm + n1*scn1 + n2*scn2 (+ batch * sab/sbb/scb); N and K
+// must stay below 2^31. Covers every mode product (leaf
 // projection U^T, reconstruction U, transfer split) and every mode-k Gram
 // Y_(k) Y_(k)^T of a canonical tensor without materialising an unfolding.
 // ---------------------------------------------------------------------------
 struct GemmDesc {
     int64_t M = 1, N1 = 1, N2 = 1, K1 = 1, K2 = 1;
+    int64_t batch = 1;                   // independent problems, pointer strides below
+    int64_t sab = 0, sbb = 0, scb = 0;
     const double* A = nullptr;
     int64_t sam = 0, sak1 = 0, sak2 = 0;
     const double* B = nullptr;
@@ -40,6 +43,8 @@ struct GemmDesc {
 // Enqueue; returns the number of CTAs used for the energy epilogue (0 when
 // storing). `workspace` must hold gemm_workspace_doubles(desc) doubles.
 int64_t gemm_workspace_doubles(const GemmDesc& d, int num_sms);
+// Number of per-CTA partials the residual-energy epilogue writes.
+int64_t gemm_energy_partials(const GemmDesc& d, int num_sms);
 int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t s, int64_t* launches);
 
 // Sum of squares of n doubles -> out[0] (deterministic two-pass). partials
@@ -86,7 +91,8 @@ void launch_fill(double* dst, int64_t n, double value, cudaStream_t s, int64_t* 
 
 // Fused all-leaf projection for 3-way batches [N0, N1, n2, S] on the FP64
 // tensor cores (DMMA): Z[a0,a1,a2,s] = sum X[i0,i1,i2,s] U0[i0,a0] U1[i1,a1]
-// U2[i2,a2] and sum X^2, in one read of X (K1).
+// U2[i2,a2] and sum X^2, in one read of X (K1). Enqueues the
+// streaming kernel plus the small slab-axis contraction GEMM.
 struct Fused3Args {
     const double* Y = nullptr;
     int64_t n2 = 0, S = 0;
@@ -95,7 +101,7 @@ struct Fused3Args {
     const double* U2 = nullptr;  // n2 x r2
     int r0 = 0, r1 = 0, r2 = 0;
     double* Z = nullptr;          // r0*r1*r2 x S
-    double* zpart = nullptr;      // workspace
+    double* wslab = nullptr;      // workspace: per-slab W (r0 r1 per slab)
     double* ysq_partials = nullptr;  // grid entries
 };
 // Whether the fused kernel supports this shape; returns the grid size used.

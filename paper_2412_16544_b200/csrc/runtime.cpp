@@ -154,6 +154,8 @@ void Context::fetch(const double* d, int64_t n, double* host) {
 // ---------------------------------------------------------------------------
 
 void run_gemm(Context& c, const GemmDesc& d) {
+    if (d.N1 * d.N2 >= (int64_t{1} << 31) || d.K1 * d.K2 >= (int64_t{1} << 31))
+        raise(HTR_ERR_RUNTIME, "contraction extent exceeds 2^31 elements; split the batch");
     const int64_t ws = gemm_workspace_doubles(d, c.num_sms);
     BufPtr w = ws > 0 ? c.alloc(ws) : nullptr;
     launch_gemm(d, w ? w->p : nullptr, c.num_sms, c.s, &c.launches);
@@ -219,8 +221,10 @@ void residual_energy(Context& c, const DT& t, int mode, const double* U, int64_t
     d.scm = sp.I;
     d.scn1 = 1;
     d.scn2 = sp.I * sp.J;
-    const int64_t tiles = ((sp.I * sp.O + 63) / 64) * ((sp.J + 63) / 64);
-    BufPtr parts = c.alloc(tiles);
+    BufPtr parts = c.alloc(1);
+    d.energy_partials = parts->p;  // sized below once the tile plan is known
+    const int64_t tiles = gemm_energy_partials(d, c.num_sms);
+    parts = c.alloc(tiles);
     d.energy_partials = parts->p;
     launch_gemm(d, nullptr, c.num_sms, c.s, &c.launches);
     launch_sum_partials(parts->p, tiles, slot, c.s, &c.launches);
@@ -633,16 +637,18 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
             fa.Z = Z.data();
             const int64_t ws = fused3_workspace_doubles(y.shape[0], y.shape[1], fa.n2, batch, r0, r1, r2, c.num_sms);
             BufPtr w = c.alloc(ws);
-            fa.zpart = w->p;
-            fa.ysq_partials = w->p + (ws - std::min<int64_t>(c.num_sms, fa.n2 * batch));
+            fa.wslab = w->p;
+            fa.ysq_partials = w->p + fa.n2 * batch * static_cast<int64_t>(r0) * r1;
             if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[0], c.s));
             const int grid = launch_fused3(y.shape[0], y.shape[1], fa, c.num_sms, c.s, &c.launches);
             if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[1], c.s));
             HTR_CUDA(cudaGetLastError());
-            launch_sum_partials(fa.ysq_partials, grid, sc + 0, c.s, &c.launches);
-            cur = Z;
-            leaves_done = true;
-            out.fused = true;
+            if (grid > 0) {  // else (no tensor map for this pointer): generic kernels below
+                launch_sum_partials(fa.ysq_partials, grid, sc + 0, c.s, &c.launches);
+                cur = Z;
+                leaves_done = true;
+                out.fused = true;
+            }
         }
     }
     if (!leaves_done) {
