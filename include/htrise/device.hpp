@@ -1,0 +1,117 @@
+// htrise-b200 drop-in: the bridge from the header API to libhtrise_cuda.so.
+//
+// Every compute entry point of the reference headers (truncated_svd,
+// bht_l2r, encode, decode, reconstruct_slice, ht_rise_update,
+// compute_residual, ...) lands here and crosses the C-ABI of
+// include/htrise_cuda.h; status codes come back as the reference's exception
+// types (std::invalid_argument / std::out_of_range / std::runtime_error).
+// Link with -lhtrise_cuda. There is no CPU fallback: without a CUDA device
+// every call throws std::runtime_error.
+#pragma once
+
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "htrise/dimension_tree.hpp"
+#include "htrise/tensor.hpp"
+#include "htrise_cuda.h"
+
+namespace htrise {
+namespace device {
+
+[[noreturn]] inline void throw_status(htr_status code, const std::string& msg) {
+    switch (code) {
+        case HTR_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case HTR_ERR_OUT_OF_RANGE: throw std::out_of_range(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+/// Process-wide default context on device 0 (or $HTRISE_DEVICE).
+class Context {
+public:
+    static Context& instance() {
+        static Context c;
+        return c;
+    }
+    htr_context* get() {
+        std::call_once(once_, [this] {
+            int dev = 0;
+            if (const char* e = std::getenv("HTRISE_DEVICE")) dev = std::atoi(e);
+            htr_context* c = nullptr;
+            const htr_status st = htr_context_create(dev, &c);
+            if (st != HTR_OK) {
+                const std::string msg = c ? htr_last_error(c) : "htr_context_create failed";
+                htr_context_destroy(c);
+                error_ = msg;
+                code_ = st;
+                return;
+            }
+            ctx_ = c;
+        });
+        if (!ctx_) throw_status(code_, error_);
+        return ctx_;
+    }
+    void check(htr_status st) {
+        if (st != HTR_OK) throw_status(st, htr_last_error(ctx_));
+    }
+    ~Context() {
+        if (ctx_) htr_context_destroy(ctx_);
+    }
+
+private:
+    Context() = default;
+    std::once_flag once_;
+    htr_context* ctx_ = nullptr;
+    std::string error_;
+    htr_status code_ = HTR_OK;
+};
+
+inline htr_context* ctx() { return Context::instance().get(); }
+inline void check(htr_status st) { Context::instance().check(st); }
+
+/// Owning handle of a device-resident representation value.
+using RepHandle = std::shared_ptr<htr_rep>;
+inline RepHandle wrap(htr_rep* r) {
+    return RepHandle(r, [](htr_rep* p) { htr_rep_free(p); });
+}
+
+inline std::vector<htr_node> nodes_of(const DimensionTree& t) {
+    std::vector<htr_node> out;
+    for (Index l = 0; l <= t.depth(); ++l)
+        for (const TreeNode& n : t.layer(l)) {
+            htr_node h{};
+            h.layer = static_cast<int32_t>(n.id.layer);
+            h.pos = static_cast<int32_t>(n.id.pos);
+            h.kind = n.kind == NodeKind::Root ? HTR_KIND_ROOT : n.kind == NodeKind::Transfer ? HTR_KIND_TRANSFER : HTR_KIND_LEAF;
+            h.leaf_dim = static_cast<int32_t>(n.leaf_dim);
+            h.succ0 = n.successors.empty() ? -1 : static_cast<int32_t>(n.successors[0].pos);
+            h.succ1 = n.successors.empty() ? -1 : static_cast<int32_t>(n.successors[1].pos);
+            out.push_back(h);
+        }
+    return out;
+}
+
+inline Shape core_shape(const htr_rep* r, NodeId id) {
+    int64_t s[3] = {0, 0, 0};
+    int32_t order = 0;
+    check(htr_rep_core_shape(r, static_cast<int32_t>(id.layer), static_cast<int32_t>(id.pos), s, &order));
+    return Shape(s, s + order);
+}
+
+inline DenseTensor fetch_core(const htr_rep* r, NodeId id) {
+    Shape s = core_shape(r, id);
+    if (shape_product(s) == 0) {
+        // an empty root (no slice yet) is not representable as a DenseTensor
+        throw std::runtime_error("fetch_core: empty core at " + to_string(id));
+    }
+    DenseTensor t(s);
+    check(htr_rep_core_get(ctx(), r, static_cast<int32_t>(id.layer), static_cast<int32_t>(id.pos), t.data(), 0));
+    return t;
+}
+
+}  // namespace device
+}  // namespace htrise

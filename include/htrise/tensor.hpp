@@ -141,7 +141,7 @@ public:
     /// Copy of a column-major buffer (Eigen::Map<const Matrix> analogue).
     static Matrix from_buffer(const double* p, Index r, Index c) {
         Matrix m(r, c);
-        if (r * c) std::memcpy(m.a_.data(), p, sizeof(double) * static_cast<std::size_t>(r * c));
+        if (r > 0 && c > 0) std::memcpy(m.a_.data(), p, sizeof(double) * static_cast<std::size_t>(r * c));
         return m;
     }
 
@@ -179,7 +179,7 @@ public:
     }
     Matrix leftCols(Index n) const {
         Matrix m(rows_, n);
-        if (rows_ * n) std::memcpy(m.a_.data(), a_.data(), sizeof(double) * static_cast<std::size_t>(rows_ * n));
+        if (rows_ > 0 && n > 0) std::memcpy(m.a_.data(), a_.data(), sizeof(double) * static_cast<std::size_t>(rows_ * n));
         return m;
     }
     Matrix col(Index j) const { return block(0, j, rows_, 1); }

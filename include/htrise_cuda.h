@@ -1,6 +1,6 @@
 /* htrise-b200 C-ABI: the drop-in boundary beneath the htrise C++ API.
  *
- * The reference (/root/reference/proj/include/htrise/*.hpp) is header-only
+ * The reference (/root/reference/proj/include/htrise/ headers) is header-only
  * C++ with no plugin or FFI layer; its public entry points
  * are inline functions in namespace htrise. This library re-implements the
  * data-parallel core of those entry points as sm_100a kernels and exports it

@@ -66,5 +66,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+DROPIN_SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+DROPIN_BIN = os.path.join(ROOT, "tests", "cpp", "build", "test_dropin")
+
+
+def build_dropin_test() -> str:
+    """Compile the C++ drop-in test program (reference-style tests written
+    against include/htrise/*.hpp, linked to libhtrise_cuda.so)."""
+    os.makedirs(os.path.dirname(DROPIN_BIN), exist_ok=True)
+    cmd = [CXX, "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", CUDA_INC, DROPIN_SRC,
+           "-L", PKG, "-lhtrise_cuda", "-Wl,-rpath,$ORIGIN/../../../paper_2412_16544_b200", "-o", DROPIN_BIN]
+    subprocess.run(cmd, check=True)
+    return DROPIN_BIN
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build_dropin_test())

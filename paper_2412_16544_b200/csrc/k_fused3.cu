@@ -324,7 +324,11 @@ int launch_impl(const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launc
     if (!make_batch_map(&map, a.Y, N0, N1, T)) return -1;
     const size_t smem = smem_bytes<N0, N1, MT0, MT1>();
     auto kfn = fused3_kernel<N0, N1, MT0, MT1>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        configured = true;
+    }
     kfn<<<static_cast<unsigned>(B), kThreads, smem, s>>>(a, ri, map);
     ++*launches;
     // Z_s[p, a2] = sum_i2 W[(s, i2), p] U2[i2, a2]: the slab-axis (mode 2)

@@ -9,8 +9,9 @@
 //
 // CTA tiles of BM x BN outputs (64x64, 64x32 or 32x64, picked per problem to
 // minimise padding), 4 warps each holding (BM/2)x(BN/2) as 8x8 DMMA
-// accumulators, K staged 16 at a time through double-buffered shared memory
-// (pitch = tile + 4 doubles: conflict-free fragment reads). Operand offsets
+// accumulators, K staged 16 at a time through a 4-stage cp.async pipeline in
+// shared memory (pitch = tile + 4 doubles: conflict-free fragment reads;
+// zero-fill outside the problem). Operand offsets
 // along m / n are precomputed per thread; the k offset needs one 32-bit
 // multiply-shift division at most. Deterministic split-K and batching.
 #include <algorithm>
@@ -63,14 +64,27 @@ __device__ __forceinline__ int64_t n_part(const Launch& L, int64_t n, int64_t s1
     return (n - n2 * N1) * s1 + n2 * s2;
 }
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+
+constexpr int NSTAGE = 4;
+
+template <int BM, int BN>
+constexpr size_t gemm_smem_bytes() {
+    return sizeof(double) * NSTAGE * BK * ((BM + 4) + (BN + 4));
+}
+
 template <int BM, int BN>
 __global__ void __launch_bounds__(NT, 3) gemm_kernel(const GemmDesc d, const int64_t kchunk, double* partial,
                                                      const Launch L) {
     constexpr int WM = BM / 2, WN = BN / 2, FM = WM / 8, FN = WN / 8;
     constexpr int PA = BM + 4, PB = BN + 4;
     constexpr int EA = BM * BK / NT, EB = BN * BK / NT;  // elements per thread per tile
-    __shared__ __align__(16) double As[2][BK][PA];
-    __shared__ __align__(16) double Bs[2][BK][PB];
+    extern __shared__ __align__(16) double gsm[];
+    double* As = gsm;                        // [NSTAGE][BK][PA]
+    double* Bs = gsm + NSTAGE * BK * PA;     // [NSTAGE][BK][PB]
     __shared__ double red[NT / 32];
 
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -84,6 +98,7 @@ __global__ void __launch_bounds__(NT, 3) gemm_kernel(const GemmDesc d, const int
     const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
     const int64_t kbeg = zs * kchunk;
     const int64_t kend = min(K, kbeg + kchunk);
+    const int ntiles = static_cast<int>((kend - kbeg + BK - 1) / BK);
 
     // per-thread operand coordinates: the m / n parts never change with k
     auto akk = [&](int j) { return L.a_kfast ? (t & 15) : t / BM + (NT / BM) * j; };
@@ -108,51 +123,52 @@ __global__ void __launch_bounds__(NT, 3) gemm_kernel(const GemmDesc d, const int
 #pragma unroll
         for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    double ra[EA], rb[EB];
-    auto load = [&](int64_t k0) {
+    // async copy of K tile `kt` into stage `st` (zero-fill outside the problem)
+    auto issue = [&](int kt, int st) {
+        const int64_t k0 = kbeg + static_cast<int64_t>(kt) * BK;
+        double* as = As + st * BK * PA;
+        double* bs = Bs + st * BK * PB;
 #pragma unroll
         for (int j = 0; j < EA; ++j) {
             const int64_t k = k0 + akk(j);
-            ra[j] = (aoff[j] >= 0 && k < kend) ? __ldg(A + aoff[j] + k_part(L, k, d.sak1, d.sak2, d.K1)) : 0.0;
+            const bool ok = aoff[j] >= 0 && k < kend;
+            cp_async8(as + akk(j) * PA + amm(j), ok ? A + aoff[j] + k_part(L, k, d.sak1, d.sak2, d.K1) : A, ok);
         }
 #pragma unroll
         for (int j = 0; j < EB; ++j) {
             const int64_t k = k0 + bkk(j);
-            rb[j] = (boff[j] >= 0 && k < kend) ? __ldg(B + boff[j] + k_part(L, k, d.sbk1, d.sbk2, d.K1)) : 0.0;
+            const bool ok = boff[j] >= 0 && k < kend;
+            cp_async8(bs + bkk(j) * PB + bnn(j), ok ? B + boff[j] + k_part(L, k, d.sbk1, d.sbk2, d.K1) : B, ok);
         }
     };
-    auto stash = [&](int buf) {
-#pragma unroll
-        for (int j = 0; j < EA; ++j) As[buf][akk(j)][amm(j)] = ra[j];
-#pragma unroll
-        for (int j = 0; j < EB; ++j) Bs[buf][bkk(j)][bnn(j)] = rb[j];
-    };
 
-    int buf = 0;
-    if (kbeg < kend) {
-        load(kbeg);
-        stash(0);
+#pragma unroll
+    for (int st = 0; st < NSTAGE - 1; ++st) {
+        if (st < ntiles) issue(st, st);
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    __syncthreads();
-    for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
-        const bool more = k0 + BK < kend;
-        if (more) load(k0 + BK);  // global loads in flight during the MMAs
+    for (int kt = 0; kt < ntiles; ++kt) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(NSTAGE - 2) : "memory");
+        __syncthreads();
+        // the stage consumed in the previous iteration is free again
+        if (kt + NSTAGE - 1 < ntiles) issue(kt + NSTAGE - 1, (kt + NSTAGE - 1) % NSTAGE);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const double* as = As + (kt % NSTAGE) * BK * PA;
+        const double* bs = Bs + (kt % NSTAGE) * BK * PB;
 #pragma unroll
         for (int ks = 0; ks < BK; ks += 4) {
             double a[FM], b[FN];
 #pragma unroll
-            for (int i = 0; i < FM; ++i) a[i] = As[buf][ks + t4][wm + 8 * i + g4];
+            for (int i = 0; i < FM; ++i) a[i] = as[(ks + t4) * PA + wm + 8 * i + g4];
 #pragma unroll
-            for (int j = 0; j < FN; ++j) b[j] = Bs[buf][ks + t4][wn + 8 * j + g4];
+            for (int j = 0; j < FN; ++j) b[j] = bs[(ks + t4) * PB + wn + 8 * j + g4];
 #pragma unroll
             for (int i = 0; i < FM; ++i)
 #pragma unroll
                 for (int j = 0; j < FN; ++j) dmma884(acc[i][j], a[i], b[j]);
         }
-        if (more) stash(buf ^ 1);
-        __syncthreads();
-        buf ^= 1;
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 
     if (L.energy) {
         const double* D = d.D + zb * d.scb;
@@ -266,6 +282,16 @@ int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t 
     if (d.M <= 0 || N <= 0 || d.batch <= 0) return 0;
     if (K <= 0) return 0;  // extents are >= 1 by construction
     const Plan p = plan_for(d, num_sms);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(gemm_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(gemm_smem_bytes<64, 64>()));
+        cudaFuncSetAttribute(gemm_kernel<64, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(gemm_smem_bytes<64, 32>()));
+        cudaFuncSetAttribute(gemm_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(gemm_smem_bytes<32, 64>()));
+        configured = true;
+    }
     const bool a_kc = d.K1 > 1 ? d.sak1 == 1 : d.sak2 == 1;
     const bool b_kc = d.K1 > 1 ? d.sbk1 == 1 : d.sbk2 == 1;
     const bool b_nc = d.N1 > 1 ? d.sbn1 == 1 : d.sbn2 == 1;
@@ -280,9 +306,9 @@ int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t 
     const dim3 grid(static_cast<unsigned>(p.tiles_n), static_cast<unsigned>(p.tiles_m),
                     static_cast<unsigned>(p.splits * d.batch));
     double* partial = p.splits > 1 ? workspace : nullptr;
-    if (p.bm == 64 && p.bn == 64) gemm_kernel<64, 64><<<grid, NT, 0, s>>>(d, p.kchunk, partial, L);
-    else if (p.bm == 64) gemm_kernel<64, 32><<<grid, NT, 0, s>>>(d, p.kchunk, partial, L);
-    else gemm_kernel<32, 64><<<grid, NT, 0, s>>>(d, p.kchunk, partial, L);
+    if (p.bm == 64 && p.bn == 64) gemm_kernel<64, 64><<<grid, NT, gemm_smem_bytes<64, 64>(), s>>>(d, p.kchunk, partial, L);
+    else if (p.bm == 64) gemm_kernel<64, 32><<<grid, NT, gemm_smem_bytes<64, 32>(), s>>>(d, p.kchunk, partial, L);
+    else gemm_kernel<32, 64><<<grid, NT, gemm_smem_bytes<32, 64>(), s>>>(d, p.kchunk, partial, L);
     ++*launches;
     if (p.splits > 1) {
         const int64_t total = d.M * N * d.batch;

@@ -180,6 +180,7 @@ class Context:
             self._h = None
             _raise(code, msg)
         self.device = device
+        self.world = 1
 
     def check(self, code: int):
         if code != OK:
@@ -215,6 +216,7 @@ class Context:
     def init_comm(self, unique_id: bytes, nranks: int, rank: int):
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         self.check(lib().htr_context_init_comm(self._h, buf, nranks, rank))
+        self.world = nranks
 
     def close(self):
         if self._h:
@@ -442,22 +444,55 @@ class HTRepresentation:
     """Device-resident batch-HT value (bht.hpp:34-151). Updates return new
     values; cores are fetched to host lazily for inspection."""
 
-    def __init__(self, handle, ctx: Context):
+    def __init__(self, handle, ctx: Context, tree: Optional[DimensionTree] = None,
+                 dims: Optional[List[int]] = None, accumulated: Optional[int] = None,
+                 epsilon_rel: Optional[float] = None):
         self._h = handle
         self.ctx = ctx
+        self._tree = tree
+        self._dims = dims
+        self._acc = accumulated
+        self._eps = epsilon_rel
+        self._cache: Dict[Tuple[int, int], np.ndarray] = {}
+
+    def _info(self):
         d = C.c_int32()
         dims = (C.c_int64 * 64)()
         acc = C.c_int64()
         eps = C.c_double()
         nn = C.c_int64()
         self.ctx.check(lib().htr_rep_info(self._h, C.byref(d), dims, C.byref(acc), C.byref(eps), C.byref(nn)))
-        self.dims = [int(dims[i]) for i in range(d.value)]
-        self.accumulated = int(acc.value)
-        self.epsilon_rel = float(eps.value)
-        nodes = (_Node * nn.value)()
-        self.ctx.check(lib().htr_rep_nodes(self._h, nodes, nn.value))
-        self.tree = DimensionTree(nodes[:])
-        self._cache: Dict[Tuple[int, int], np.ndarray] = {}
+        self._dims = [int(dims[i]) for i in range(d.value)]
+        self._acc = int(acc.value)
+        self._eps = float(eps.value)
+        if self._tree is None:
+            nodes = (_Node * nn.value)()
+            self.ctx.check(lib().htr_rep_nodes(self._h, nodes, nn.value))
+            self._tree = DimensionTree(nodes[:])
+
+    @property
+    def tree(self) -> DimensionTree:
+        if self._tree is None:
+            self._info()
+        return self._tree
+
+    @property
+    def dims(self) -> List[int]:
+        if self._dims is None:
+            self._info()
+        return self._dims
+
+    @property
+    def accumulated(self) -> int:
+        if self._acc is None:
+            self._info()
+        return self._acc
+
+    @property
+    def epsilon_rel(self) -> float:
+        if self._eps is None:
+            self._info()
+        return self._eps
 
     @property
     def handle(self):
@@ -571,7 +606,8 @@ def ht_rise_update(h: HTRepresentation, y, epsilon_rel: Optional[float] = None, 
                                        int(bool(adaptive_budget)), C.byref(out), C.byref(rep)))
     del keep
     ids = [(rep.node_layer[i], rep.node_pos[i]) for i in range(rep.n_nodes)]
-    return HTRepresentation(out, ctx), UpdateReport(
+    acc = None if h._acc is None else h._acc + shape[-1] * getattr(ctx, "world", 1)
+    return HTRepresentation(out, ctx, h._tree, h._dims, acc, h._eps), UpdateReport(
         bool(rep.skipped), rep.proj_error, rep.eps_des,
         {ids[i]: int(rep.added_ranks[i]) for i in range(rep.n_nodes)},
         {ids[i]: int(rep.new_ranks[i]) for i in range(rep.n_nodes)},
