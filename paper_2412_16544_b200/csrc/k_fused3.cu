@@ -331,6 +331,7 @@ int launch_impl(const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launc
     }
     kfn<<<static_cast<unsigned>(B), kThreads, smem, s>>>(a, ri, map);
     ++*launches;
+    if (!a.slab_gemm) return static_cast<int>(B);
     // Z_s[p, a2] = sum_i2 W[(s, i2), p] U2[i2, a2]: the slab-axis (mode 2)
     // contraction, one small GEMM per sample
     GemmDesc d;

@@ -103,11 +103,27 @@ struct Fused3Args {
     double* Z = nullptr;          // r0*r1*r2 x S
     double* wslab = nullptr;      // workspace: per-slab W (r0 r1 per slab)
     double* ysq_partials = nullptr;  // grid entries
+    bool slab_gemm = true;        // also enqueue Z = sum_i2 W (x) U2 (else left to tail3)
 };
 // Whether the fused kernel supports this shape; returns the grid size used.
 bool fused3_supported(int64_t n0, int64_t n1, int64_t n2, int r0, int r1, int r2);
 int64_t fused3_workspace_doubles(int64_t n0, int64_t n1, int64_t n2, int64_t S, int r0, int r1, int r2,
                                  int num_sms);
 int launch_fused3(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches);
+
+// Skip-path tail for (1,(2,3)) trees, one CTA per sample: Z_s from the
+// per-slab W of fused3 and U2, then latent_s = Z_s B (B: r1 r2 x rt transfer
+// basis), latent [r0, rt, S] and ||latent_s||^2 per sample.
+struct Tail3Args {
+    const double* wslab = nullptr;
+    const double* U2 = nullptr;
+    const double* B = nullptr;
+    int r0 = 0, r1 = 0, r2 = 0, rt = 0;
+    int64_t n2 = 0, S = 0;
+    double* latent = nullptr;
+    double* latsq = nullptr;  // S entries
+};
+bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2);
+void launch_tail3(const Tail3Args& a, cudaStream_t s, int64_t* launches);
 
 }  // namespace htr

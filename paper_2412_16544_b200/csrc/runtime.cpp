@@ -615,6 +615,7 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
 
     DT cur = y;
     bool leaves_done = false;
+    bool tail_done = false;  // latent and ||latent||^2 already produced
     if (!exact && c.fused && d == 3) {
         NodeId leaf_of[3];
         for (Index l = 1; l <= p; ++l)
@@ -622,6 +623,11 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
                 if (n.kind == NodeKind::Leaf) leaf_of[n.leaf_dim] = n.id;
         const int r0 = static_cast<int>(ranks.at(leaf_of[0])), r1 = static_cast<int>(ranks.at(leaf_of[1])),
                   r2 = static_cast<int>(ranks.at(leaf_of[2]));
+        // (1,(2,3)) tree: layer 1 = [leaf d0, transfer(d1,d2)], layer 2 = [leaf d1, leaf d2]
+        const bool tree_123 = p == 2 && tree.layer(1)[0].kind == NodeKind::Leaf &&
+                              tree.layer(1)[1].kind == NodeKind::Transfer;
+        const int rt = tree_123 ? static_cast<int>(ranks.at(NodeId{1, 1})) : 0;
+        const bool use_tail = tree_123 && tail3_supported(r0, r1, r2, rt, y.shape[2]);
         if (fused3_supported(y.shape[0], y.shape[1], y.shape[2], r0, r1, r2)) {
             Fused3Args fa;
             fa.Y = y.data();
@@ -633,8 +639,12 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
             fa.r0 = r0;
             fa.r1 = r1;
             fa.r2 = r2;
-            DT Z = c.tensor({r0, r1, r2, batch});
-            fa.Z = Z.data();
+            DT Z;
+            if (!use_tail) {
+                Z = c.tensor({r0, r1, r2, batch});
+                fa.Z = Z.data();
+            }
+            fa.slab_gemm = !use_tail;
             const int64_t ws = fused3_workspace_doubles(y.shape[0], y.shape[1], fa.n2, batch, r0, r1, r2, c.num_sms);
             BufPtr w = c.alloc(ws);
             fa.wslab = w->p;
@@ -645,9 +655,31 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
             HTR_CUDA(cudaGetLastError());
             if (grid > 0) {  // else (no tensor map for this pointer): generic kernels below
                 launch_sum_partials(fa.ysq_partials, grid, sc + 0, c.s, &c.launches);
-                cur = Z;
                 leaves_done = true;
                 out.fused = true;
+                if (use_tail) {
+                    Tail3Args ta;
+                    ta.wslab = fa.wslab;
+                    ta.U2 = fa.U2;
+                    ta.B = h.core(NodeId{1, 1}).data();
+                    ta.r0 = r0;
+                    ta.r1 = r1;
+                    ta.r2 = r2;
+                    ta.rt = rt;
+                    ta.n2 = fa.n2;
+                    ta.S = batch;
+                    DT lat = c.tensor({r0, rt, batch});
+                    ta.latent = lat.data();
+                    BufPtr lsq = c.alloc(batch);
+                    ta.latsq = lsq->p;
+                    launch_tail3(ta, c.s, &c.launches);
+                    HTR_CUDA(cudaGetLastError());
+                    launch_sum_partials(lsq->p, batch, sc + 2, c.s, &c.launches);
+                    cur = lat;
+                    tail_done = true;
+                } else {
+                    cur = Z;
+                }
             }
         }
     }
@@ -655,7 +687,7 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
         for (const TreeNode& n : tree.layer(p))
             cur = project(c, cur, static_cast<int>(n.leaf_dim), basis_of(h, n.id), exact ? sc + 16 + nslots++ : nullptr);
     }
-    for (Index l = p - 1; l >= 1; --l) {
+    for (Index l = p - 1; l >= 1 && !tail_done; --l) {
         cur.shape = layer_extents(h, l, ranks, batch, leaves_done);
         for (Index j = 0; j < tree.layer_size(l); ++j) {
             const TreeNode& n = tree.layer(l)[static_cast<size_t>(j)];
@@ -671,7 +703,7 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
         launch_sumsq(y.data(), y.size(), parts->p, sc + 0, c.s, &c.launches);
     }
     BufPtr parts2 = c.alloc(kReduceBlocks);
-    launch_sumsq(cur.data(), cur.size(), parts2->p, sc + 2, c.s, &c.launches);  // writes sc[2], sc[3]
+    if (!tail_done) launch_sumsq(cur.data(), cur.size(), parts2->p, sc + 2, c.s, &c.launches);  // sc[2], sc[3]
     HTR_CUDA(cudaGetLastError());
     c.allreduce(sc, 16 + nslots);
     c.fetch(sc, 16 + nslots, c.h_sc);
