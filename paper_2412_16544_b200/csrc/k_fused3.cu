@@ -40,9 +40,9 @@
 namespace htr {
 namespace {
 
-constexpr int kWarps = 8;
+constexpr int kWarps = 12;
 constexpr int kThreads = kWarps * 32;
-constexpr int kStages = 4;         // per-warp ring depth
+constexpr int kStages = 3;         // per-warp ring depth
 constexpr int kRows = 32;          // rows (i0) per step
 constexpr int kCols = 16;          // columns (i1) per step = 2 DMMA n-tiles
 constexpr int kBoxRows = 16;      // TMA box: 16 doubles (128 B, the swizzle span) x 16 columns
