@@ -176,6 +176,109 @@ __global__ void fill_kernel(double* dst, int64_t n, double v) {
         dst[idx] = v;
 }
 
+// Small mode product out[i, q, o] = sum_j M(q, j) t[i, j, o] for J, Q <= 32:
+// one thread per (i, o) fibre, M broadcast from shared memory, every input
+// element read once and every output written once (HBM-bound; the DMMA
+// engine would pad such tiny extents to 32-64 rows). Optional residual
+// energy sum_fibre ||t - M^T (M t)||^2 for orthonormal-basis projections
+// (bht.hpp:361), written as one partial per CTA.
+template <int JM, int QM>
+__device__ __forceinline__ void small_fibre(const double (&x)[JM], const double* Ms, int J, double (&y)[QM],
+                                            double* energy_acc) {
+#pragma unroll
+    for (int q = 0; q < QM; ++q) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < JM; ++j) acc = fma(Ms[q + QM * j], x[j], acc);
+        y[q] = acc;
+    }
+    if (energy_acc) {
+        // residual of the projection: x - M^T y (bht.hpp:361)
+#pragma unroll
+        for (int j = 0; j < JM; ++j) {
+            if (j >= J) continue;
+            double back = 0.0;
+#pragma unroll
+            for (int q = 0; q < QM; ++q) back = fma(Ms[q + QM * j], y[q], back);
+            const double r = x[j] - back;
+            *energy_acc = fma(r, r, *energy_acc);
+        }
+    }
+}
+
+template <int JM, int QM, bool MODE0>
+__global__ void __launch_bounds__(256) mode_small_kernel(const double* __restrict__ t, int64_t I, int J, int64_t O,
+                                                          const double* __restrict__ M, int Q, int64_t smq, int64_t smj,
+                                                          double* __restrict__ out, double* energy) {
+    __shared__ double Ms[QM * JM];  // zero-padded to QM x JM
+    __shared__ double red[8];
+    // MODE0 (I == 1): per-warp staging of 32 consecutive fibres (coalesced)
+    __shared__ double stage[MODE0 ? 4 : 1][MODE0 ? 32 * (JM > QM ? JM : QM) + 32 : 1];  // 4 warps in MODE0
+    for (int e = threadIdx.x; e < QM * JM; e += blockDim.x) {
+        const int q = e % QM, j = e / QM;
+        Ms[e] = (q < Q && j < J) ? M[q * smq + j * smj] : 0.0;
+    }
+    __syncthreads();
+    double en = 0.0;
+    double* enp = energy ? &en : nullptr;
+    if constexpr (MODE0) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        double* st = stage[warp];
+        const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+        for (int64_t base = (blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + warp) * 32; base < O;
+             base += nwarps * 32) {
+            const int nf = static_cast<int>(O - base < 32 ? O - base : 32);
+            const double* src = t + base * J;
+            for (int e = lane; e < nf * J; e += 32) {
+                const int f = e / J, j = e - f * J;
+                st[f * (JM + 1) + j] = __ldg(src + e);
+            }
+            __syncwarp();
+            double x[JM], y[QM];
+#pragma unroll
+            for (int j = 0; j < JM; ++j) x[j] = (lane < nf && j < J) ? st[lane * (JM + 1) + j] : 0.0;
+            small_fibre<JM, QM>(x, Ms, J, y, lane < nf ? enp : nullptr);
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < QM; ++q)
+                if (q < Q) st[lane * (QM + 1) + q] = y[q];
+            __syncwarp();
+            double* dst = out + base * Q;
+            for (int e = lane; e < nf * Q; e += 32) {
+                const int f = e / Q, q = e - f * Q;
+                dst[e] = st[f * (QM + 1) + q];
+            }
+            __syncwarp();
+        }
+    } else {
+        const int64_t fibres = I * O;
+        for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; f < fibres;
+             f += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const int64_t o = f / I, i = f - o * I;
+            const double* src = t + i + I * J * o;
+            double x[JM], y[QM];
+#pragma unroll
+            for (int j = 0; j < JM; ++j) x[j] = j < J ? __ldg(src + I * j) : 0.0;
+            small_fibre<JM, QM>(x, Ms, J, y, enp);
+            double* dst = out + i + I * static_cast<int64_t>(Q) * o;
+#pragma unroll
+            for (int q = 0; q < QM; ++q)
+                if (q < Q) dst[I * q] = y[q];
+        }
+    }
+    if (energy) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) en += __shfl_xor_sync(0xffffffffu, en, off);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = en;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += red[w];
+            energy[blockIdx.x] = tot;
+        }
+    }
+}
+
 int blocks_for(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4096))); }
 
 }  // namespace
@@ -211,6 +314,35 @@ void launch_pad_axis(const double* src, int64_t inner, int64_t ext, int64_t oute
     if (total == 0) return;
     pad_axis_kernel<<<blocks_for(total), 256, 0, s>>>(src, inner, ext, outer, extra, dst);
     ++*launches;
+}
+
+int launch_mode_small(const double* t, int64_t I, int64_t J, int64_t O, const double* M, int64_t Q, int64_t smq,
+                      int64_t smj, double* out, double* energy, int num_sms, cudaStream_t s, int64_t* launches) {
+    if (J > 32 || Q > 32) return -1;
+    const bool mode0 = I == 1;
+    const int64_t units = mode0 ? (O + 31) / 32 * 32 : I * O;
+    const int per_block = mode0 ? 128 : 256;
+    const int blocks = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>((units + per_block - 1) / per_block, 8 * num_sms)));
+    const int jm = J <= 4 ? 4 : J <= 8 ? 8 : J <= 16 ? 16 : 32;
+    const int qm = Q <= 4 ? 4 : Q <= 8 ? 8 : Q <= 16 ? 16 : 32;
+#define HTR_SMALL(JJ, QQ)                                                                                       \
+    if (jm == JJ && qm == QQ) {                                                                                 \
+        if (mode0)                                                                                              \
+            mode_small_kernel<JJ, QQ, true><<<blocks, 128, 0, s>>>(t, I, static_cast<int>(J), O, M,              \
+                                                                    static_cast<int>(Q), smq, smj, out, energy); \
+        else                                                                                                    \
+            mode_small_kernel<JJ, QQ, false><<<blocks, 256, 0, s>>>(t, I, static_cast<int>(J), O, M,             \
+                                                                     static_cast<int>(Q), smq, smj, out, energy); \
+        ++*launches;                                                                                            \
+        return blocks;                                                                                          \
+    }
+    HTR_SMALL(4, 4) HTR_SMALL(4, 8) HTR_SMALL(4, 16) HTR_SMALL(4, 32)
+    HTR_SMALL(8, 4) HTR_SMALL(8, 8) HTR_SMALL(8, 16) HTR_SMALL(8, 32)
+    HTR_SMALL(16, 4) HTR_SMALL(16, 8) HTR_SMALL(16, 16) HTR_SMALL(16, 32)
+    HTR_SMALL(32, 4) HTR_SMALL(32, 8) HTR_SMALL(32, 16) HTR_SMALL(32, 32)
+#undef HTR_SMALL
+    return -1;
 }
 
 void launch_fill(double* dst, int64_t n, double value, cudaStream_t s, int64_t* launches) {

@@ -86,6 +86,13 @@ void launch_pad_axis(const double* src, int64_t inner, int64_t ext, int64_t oute
 void launch_orthonormalize_new(const double* U, int64_t alpha, int64_t r, double* W, int64_t q, double* info,
                                double* work, cudaStream_t s, int64_t* launches);
 
+// out[i, q, o] = sum_j M(q, j) t[i, j, o] with M(q, j) = M[q*smq + j*smj],
+// J, Q <= 32 (streaming, one thread per fibre). When energy != nullptr the
+// kernel also writes per-CTA partials of sum ||t_fibre - M^T (M t_fibre)||^2.
+// Returns the CTA count, or -1 when the extents are too large.
+int launch_mode_small(const double* t, int64_t I, int64_t J, int64_t O, const double* M, int64_t Q, int64_t smq,
+                      int64_t smj, double* out, double* energy, int num_sms, cudaStream_t s, int64_t* launches);
+
 // Fill dst[i] = value for n entries.
 void launch_fill(double* dst, int64_t n, double value, cudaStream_t s, int64_t* launches);
 

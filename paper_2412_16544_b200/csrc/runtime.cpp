@@ -180,6 +180,14 @@ DT mode_mul(Context& c, const DT& t, int mode, const double* Mp, int64_t Q, int6
     Shape os = t.shape;
     os[static_cast<size_t>(mode)] = Q;
     DT out = c.tensor(os);
+    if (sp.J <= 16 && Q <= 16 && sp.I * sp.O >= 4096) {
+        // tiny extents: streaming kernel (the MMA tiles would be mostly padding)
+        if (launch_mode_small(t.data(), sp.I, sp.J, sp.O, Mp, Q, smq, smj, out.data(), nullptr, c.num_sms, c.s,
+                              &c.launches) > 0) {
+            HTR_CUDA(cudaGetLastError());
+            return out;
+        }
+    }
     GemmDesc d;
     d.M = Q;
     d.N1 = sp.I;
@@ -455,6 +463,21 @@ Shape layer_extents(const Rep& h, Index l, const RankMap& ranks, int64_t batch, 
 DT project(Context& c, const DT& t, int mode, const Basis& b, double* energy_slot) {
     if (b.alpha != t.shape[static_cast<size_t>(mode)])
         raise(HTR_ERR_INVALID_ARGUMENT, "mode_multiply: factor/extent mismatch");
+    const Split sp = split_at(t.shape, mode);
+    if (energy_slot && sp.J <= 16 && b.r <= 16 && sp.I * sp.O >= 4096) {
+        // streaming projection with the explicit residual energy fused in
+        Shape os = t.shape;
+        os[static_cast<size_t>(mode)] = b.r;
+        DT coeff = c.tensor(os);
+        BufPtr parts = c.alloc(8 * c.num_sms);
+        const int nb = launch_mode_small(t.data(), sp.I, sp.J, sp.O, b.p, b.r, b.alpha, 1, coeff.data(), parts->p,
+                                         c.num_sms, c.s, &c.launches);
+        if (nb > 0) {
+            launch_sum_partials(parts->p, nb, energy_slot, c.s, &c.launches);
+            HTR_CUDA(cudaGetLastError());
+            return coeff;
+        }
+    }
     DT coeff = mode_mul(c, t, mode, b.p, b.r, b.alpha, 1);  // U^T
     if (energy_slot) residual_energy(c, t, mode, b.p, b.r, coeff, energy_slot);
     return coeff;

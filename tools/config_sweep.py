@@ -1,0 +1,41 @@
+"""Per-config timings on one GPU: BHT-l2r on batch 0, then the HT-RISE
+stream (skip / non-skip update latency from the library's own wall clock,
+like UpdateReport.seconds in ht_rise.hpp:117-121) and GB/s of streamed data."""
+import argparse, json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2412_16544_b200 import htrise as ht
+from paper_2412_16544_b200.workloads import CONFIGS
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
+ap.add_argument("--max-batches", type=int, default=40)
+a = ap.parse_args()
+ctx = ht.Context(0); ht.set_default_context(ctx)
+rows = []
+for name in a.configs.split(","):
+    w = CONFIGS[name]
+    y0 = w.make_batch(0, "cuda"); torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep, _ = ht.bht_l2r(ht.DeviceTensor(y0, w.shape), w.tree(), w.eps)
+    t_bht = time.perf_counter() - t0
+    del y0
+    skip_t, full_t, fused = [], [], 0
+    nb = min(w.n_batches, a.max_batches)
+    for b in range(1, nb):
+        yb = w.make_batch(b, "cuda"); torch.cuda.synchronize()
+        rep, upd = ht.ht_rise_update(rep, ht.DeviceTensor(yb, w.shape))
+        (skip_t if upd.skipped else full_t).append(upd.seconds)
+        fused += upd.used_fused_path
+        del yb
+    gb = w.bytes_per_batch / 1e9
+    row = {"config": name, "batch_GB": round(gb, 4), "bht_l2r_ms": round(1e3 * t_bht, 2),
+           "updates": nb - 1, "skips": len(skip_t), "fused_path": fused,
+           "skip_ms_mean": round(1e3 * sum(skip_t) / len(skip_t), 3) if skip_t else None,
+           "nonskip_ms_mean": round(1e3 * sum(full_t) / len(full_t), 3) if full_t else None,
+           "skip_GBps": round(gb / (sum(skip_t) / len(skip_t)), 1) if skip_t else None,
+           "ranks": {str(k): v for k, v in rep.ranks().items()}}
+    rows.append(row)
+    print(json.dumps(row), flush=True)
+    del rep
+    torch.cuda.empty_cache()
