@@ -250,12 +250,18 @@ def run_ours(args):
                "host_buffer": "pinned"}
 
     peak, peak_kind = _peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+            traffic = json.load(f)["traffic_bytes"] * (local_bytes / (8 * 128 ** 3 * 256))
+    except Exception:
+        pass
     roof = None
     if fused_calls:
         avg = fused_ms / fused_calls
         achieved = local_bytes / (avg * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "fused3_kernel (leaf projections + ||Y||^2, DMMA f64)",
+                "traffic": traffic, "kernel": "fused3_kernel (leaf projections + ||Y||^2, DMMA f64)",
                 "kernel_ms": avg, "share_of_step": avg / ms, "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": local_bytes}
 
