@@ -22,7 +22,8 @@ Pinned readings of the ambiguities listed in SURVEY.md Appendix B:
   c4  leaf bases and transfer tensors fixed per stream, root coefficients
       per sample; noise 1e-4 relative per sample; seed 4.
   c5  factors fixed per stream, core 20^3 N(0,1) per sample; noise 1e-4
-      relative per sample; seed 5.
+      relative per sample (drawn per group of 16 samples so that shards of a
+      multiple of 16 samples reproduce the unsharded bytes); seed 5.
 """
 from __future__ import annotations
 
@@ -174,26 +175,26 @@ def _c5(w: Workload, b: int, dev, n: int, off: int) -> torch.Tensor:
     A = [_orth(w.dims[k], r, g, dev) for k in range(3)]
     gc = _gen(dev, 5000 + b)
     out = torch.empty(n, w.dims[2], w.dims[1], w.dims[0], device=dev, dtype=torch.float64)
-    gn = _gen(dev, 5500 + b)
-    chunk = 16
-    # draw the whole batch's cores/noise deterministically, then slice the shard
-    cores = torch.randn(w.batch, r, r, r, generator=gc, device=dev, dtype=torch.float64)[off:off + n]
     numel = w.dims[0] * w.dims[1] * w.dims[2]
-    skip = off
-    for s0 in range(0, n, chunk):
-        s1 = min(n, s0 + chunk)
+    # cores for the whole batch from one stream, then the shard's slice
+    cores = torch.randn(w.batch, r, r, r, generator=gc, device=dev, dtype=torch.float64)[off:off + n]
+    # noise per group of 16 samples from its own seed: identical bytes for
+    # any sharding whose shard size is a multiple of 16
+    group = 16
+    s0 = 0
+    while s0 < n:
+        gidx = (off + s0) // group
+        s1 = min(n, (gidx + 1) * group - off)
         c = cores[s0:s1]  # (s, a2, a1, a0) C-order
         y = torch.einsum("szyx,ix->szyi", c, A[0])
         y = torch.einsum("szyi,jy->szji", y, A[1])
         y = torch.einsum("szji,kz->skji", y, A[2])
-        out[s0:s1] = y
-    # per-sample relative noise, generated for the full batch in order
-    if skip:
-        torch.randn(skip * numel, generator=gn, device=dev, dtype=torch.float64)
-    for s in range(n):
-        nz = torch.randn(numel, generator=gn, device=dev, dtype=torch.float64).reshape(out.shape[1:])
-        sc = 1e-4 * out[s].norm() / math.sqrt(numel)
-        out[s].add_(nz, alpha=float(sc))
+        gn = _gen(dev, 5500 * 4096 + b * 4096 + gidx)
+        lo = (off + s0) - gidx * group  # first sample of this piece within its group
+        nz = torch.randn(group, numel, generator=gn, device=dev, dtype=torch.float64)[lo:lo + (s1 - s0)]
+        sc = 1e-4 * y.reshape(s1 - s0, -1).norm(dim=1) / math.sqrt(numel)
+        out[s0:s1] = y + (sc[:, None] * nz).reshape(y.shape)
+        s0 = s1
     return out.reshape(-1)
 
 
