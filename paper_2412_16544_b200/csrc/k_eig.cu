@@ -134,6 +134,148 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
 }
 
 // --------------------------------------------------------------------------
+// Large n: the same parallel cyclic Jacobi spread over a cluster of CTAs.
+// A and V live in global memory (L2); every CTA computes the round's
+// rotations itself (bit-identical: same inputs, same code), applies its
+// share of the 2x2 blocks A[{p,q}_P, {p,q}_Q] <- J_P^T A J_Q and of V's
+// column pairs in ONE pass, and the round ends with a single cluster
+// barrier (release/acquire orders the global-memory updates).
+// --------------------------------------------------------------------------
+constexpr int kClusterCTAs = 8;
+constexpr int kClusterThreads = 1024;
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kClusterThreads)
+    jacobi_cluster_kernel(const double* __restrict__ G, int n, double* __restrict__ lambda, double* __restrict__ Vout,
+                          double* A, double* V) {
+    __shared__ int pos[1024];
+    __shared__ double cs[512], sn[512];
+    __shared__ int prs[512], qrs[512];
+    __shared__ int rotated;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int crank = static_cast<int>(cluster_rank());
+    const int gtid = crank * nt + tid, gnt = kClusterCTAs * nt;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    for (int64_t i = gtid; i < nn; i += gnt) {
+        const int64_t r = i % n, c = i / n;
+        A[i] = 0.5 * (G[r + n * c] + G[c + n * r]);
+        V[i] = r == c ? 1.0 : 0.0;
+    }
+    const int m = n + (n & 1);
+    const int half = m / 2;
+    for (int i = tid; i < m; i += nt) pos[i] = i;
+    cluster_sync_all();
+
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        if (tid == 0) rotated = 0;
+        __syncthreads();
+        for (int round = 0; round < m - 1; ++round) {
+            for (int i = tid; i < half; i += nt) {
+                int p = pos[i], q = pos[m - 1 - i];
+                if (p > q) { const int t = p; p = q; q = t; }
+                double c = 1.0, s = 0.0;
+                if (q < n) {
+                    const double app = A[p + static_cast<int64_t>(n) * p];
+                    const double aqq = A[q + static_cast<int64_t>(n) * q];
+                    const double apq = A[p + static_cast<int64_t>(n) * q];
+                    if (fabs(apq) > 1e-300 && fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
+                        const double tau = (aqq - app) / (2.0 * apq);
+                        double t;
+                        if (fabs(tau) > 1e150) t = 0.5 / tau;
+                        else t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                        rotated = 1;
+                    }
+                }
+                cs[i] = c; sn[i] = s; prs[i] = p; qrs[i] = q;
+            }
+            __syncthreads();
+            // every CTA finished reading A for the rotations before anyone writes
+            cluster_sync_all();
+            // 2x2 blocks (P, Q): A' = J_P^T A J_Q over rows {p_P, q_P}, cols {p_Q, q_Q}
+            const int64_t blocks = static_cast<int64_t>(half) * half;
+            for (int64_t b = gtid; b < blocks; b += gnt) {
+                const int P = static_cast<int>(b / half), Q = static_cast<int>(b % half);
+                const int pP = prs[P], qP = qrs[P], pQ = prs[Q], qQ = qrs[Q];
+                if (qP >= n && qQ >= n) continue;
+                const double cP = cs[P], sP = sn[P], cQ = cs[Q], sQ = sn[Q];
+                if (sP == 0.0 && sQ == 0.0) continue;
+                if (qP >= n) {  // row pair padded: only the column rotation of row pP
+                    double* r0 = A + pP;
+                    const double x = r0[static_cast<int64_t>(n) * pQ], y = r0[static_cast<int64_t>(n) * qQ];
+                    r0[static_cast<int64_t>(n) * pQ] = cQ * x - sQ * y;
+                    r0[static_cast<int64_t>(n) * qQ] = sQ * x + cQ * y;
+                    continue;
+                }
+                if (qQ >= n) {  // column pair padded: only the row rotation of column pQ
+                    double* col = A + static_cast<int64_t>(n) * pQ;
+                    const double x = col[pP], y = col[qP];
+                    col[pP] = cP * x - sP * y;
+                    col[qP] = sP * x + cP * y;
+                    continue;
+                }
+                double* a_pp = A + pP + static_cast<int64_t>(n) * pQ;
+                double* a_pq = A + pP + static_cast<int64_t>(n) * qQ;
+                double* a_qp = A + qP + static_cast<int64_t>(n) * pQ;
+                double* a_qq = A + qP + static_cast<int64_t>(n) * qQ;
+                const double x00 = *a_pp, x01 = *a_pq, x10 = *a_qp, x11 = *a_qq;
+                // rows: J_P^T
+                const double y00 = cP * x00 - sP * x10, y01 = cP * x01 - sP * x11;
+                const double y10 = sP * x00 + cP * x10, y11 = sP * x01 + cP * x11;
+                // columns: J_Q
+                double z00 = cQ * y00 - sQ * y01, z01 = sQ * y00 + cQ * y01;
+                double z10 = cQ * y10 - sQ * y11, z11 = sQ * y10 + cQ * y11;
+                if (P == Q && sP != 0.0) { z01 = 0.0; z10 = 0.0; }  // annihilated pair
+                *a_pp = z00; *a_pq = z01; *a_qp = z10; *a_qq = z11;
+            }
+            // V <- V J (column pairs)
+            const int64_t vitems = static_cast<int64_t>(half) * n;
+            for (int64_t it = gtid; it < vitems; it += gnt) {
+                const int Q = static_cast<int>(it / n), r = static_cast<int>(it % n);
+                const double s = sn[Q];
+                if (s == 0.0) continue;
+                const double c = cs[Q];
+                double* vp = V + static_cast<int64_t>(n) * prs[Q] + r;
+                double* vq = V + static_cast<int64_t>(n) * qrs[Q] + r;
+                const double x = *vp, y = *vq;
+                *vp = c * x - s * y;
+                *vq = s * x + c * y;
+            }
+            if (tid == 0) {
+                const int last = pos[m - 1];
+                for (int k = m - 1; k > 1; --k) pos[k] = pos[k - 1];
+                pos[1] = last;
+            }
+            cluster_sync_all();
+        }
+        __syncthreads();
+        if (!rotated) break;  // identical decision in every CTA
+        __syncthreads();
+    }
+    // sort eigenpairs by descending eigenvalue (stable on index)
+    for (int i = gtid; i < n; i += gnt) {
+        const double li = A[i + static_cast<int64_t>(n) * i];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+            const double lj = A[j + static_cast<int64_t>(n) * j];
+            rank += (lj > li) || (lj == li && j < i);
+        }
+        lambda[rank] = li;
+        for (int r = 0; r < n; ++r) Vout[r + static_cast<int64_t>(n) * rank] = V[r + static_cast<int64_t>(n) * i];
+    }
+}
+
+// --------------------------------------------------------------------------
 // Re-orthonormalisation of new directions (expand_core, ht_rise.hpp:53-79):
 // W <- (I - U U^T) W twice, then CholeskyQR2. One CTA; all sizes small.
 // --------------------------------------------------------------------------
@@ -229,6 +371,12 @@ __global__ void __launch_bounds__(512) orthonormalize_kernel(const double* U, in
 
 void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, double* work, cudaStream_t s,
                        int64_t* launches) {
+    if (n > kSmemMaxN) {
+        jacobi_cluster_kernel<<<kClusterCTAs, kClusterThreads, 0, s>>>(G, static_cast<int>(n), lambda, V, work,
+                                                                       work + n * n);
+        ++*launches;
+        return;
+    }
     const bool in_smem = n <= kSmemMaxN;
     const size_t smem = in_smem ? 2 * sizeof(double) * static_cast<size_t>(n * n) : 0;
     if (smem > 48 * 1024) {
