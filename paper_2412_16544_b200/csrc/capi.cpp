@@ -423,8 +423,7 @@ htr_status htr_truncated_svd(htr_context* ctx, const double* m, int32_t m_on_dev
         bool bad = false;
         htr::norm_sq(c, mt.data(), mt.size(), &s2, &bad, false);
         if (bad) htr::raise(HTR_ERR_INVALID_ARGUMENT, "truncated_svd: non-finite entries");
-        DT G = htr::gram(c, mt, 0, false);
-        htr::Truncation t = htr::truncate_gram(c, G, rows, cols, eps_abs, min_rank, htr::unfolding_refiner(c, mt, 0));
+        htr::Truncation t = htr::truncate_mode(c, mt, 0, nullptr, eps_abs, min_rank, cols, false);
         if (rank) *rank = t.rank;
         if (discarded_norm) *discarded_norm = t.discarded;
         if (sigma)

@@ -157,9 +157,9 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kClusterThreads)
     jacobi_cluster_kernel(const double* __restrict__ G, int n, double* __restrict__ lambda, double* __restrict__ Vout,
                           double* A, double* V) {
-    __shared__ int pos[1024];
-    __shared__ double cs[512], sn[512];
-    __shared__ int prs[512], qrs[512];
+    __shared__ int pos[kJacobiMaxN];
+    __shared__ double cs[kJacobiMaxN / 2], sn[kJacobiMaxN / 2];
+    __shared__ int prs[kJacobiMaxN / 2], qrs[kJacobiMaxN / 2];
     __shared__ int rotated;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int crank = static_cast<int>(cluster_rank());

@@ -157,6 +157,20 @@ __global__ void take_columns_kernel(const double* V, int64_t n, int64_t r, doubl
     }
 }
 
+// X[a + ext * (i + inner * o)] = T[i + inner * (a + ext * o)]: the mode
+// unfolding of T (viewed [inner, ext, outer]) as a contiguous ext-row matrix.
+__global__ void unfold_kernel(const double* __restrict__ src, int64_t inner, int64_t ext, int64_t outer,
+                              double* __restrict__ dst) {
+    const int64_t total = inner * ext * outer;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx % inner;  // reads coalesced along the inner axis
+        const int64_t rest = idx / inner;
+        const int64_t a = rest % ext, o = rest / ext;
+        dst[a + ext * (i + inner * o)] = src[idx];
+    }
+}
+
 __global__ void pad_axis_kernel(const double* src, int64_t inner, int64_t ext, int64_t outer, int64_t extra,
                                 double* dst) {
     const int64_t next = ext + extra;
@@ -313,6 +327,14 @@ void launch_pad_axis(const double* src, int64_t inner, int64_t ext, int64_t oute
     const int64_t total = inner * (ext + extra) * outer;
     if (total == 0) return;
     pad_axis_kernel<<<blocks_for(total), 256, 0, s>>>(src, inner, ext, outer, extra, dst);
+    ++*launches;
+}
+
+void launch_unfold(const double* src, int64_t inner, int64_t ext, int64_t outer, double* dst, cudaStream_t s,
+                   int64_t* launches) {
+    const int64_t total = inner * ext * outer;
+    if (total == 0) return;
+    unfold_kernel<<<blocks_for(total), 256, 0, s>>>(src, inner, ext, outer, dst);
     ++*launches;
 }
 

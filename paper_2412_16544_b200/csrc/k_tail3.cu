@@ -6,9 +6,21 @@
 //   ||latent_s||^2
 //
 // on the FP64 tensor cores, with Z_s kept in shared memory between the two
-// contractions. W is the per-slab output of fused3_kernel (L2-resident),
-// B the transfer node's basis matrix (r1 r2 x rt), streamed from L2.
-// Replaces two generic GEMM launches and the latent norm pass; deterministic.
+// contractions. W is the per-slab output of fused3_kernel, B the transfer
+// node's basis matrix (r1 r2 x rt), streamed from L2.
+//
+// Work split (every DMMA issued is a useful tile; no predicated padding):
+//   phase A  M = r0 r1 (m-tiles dealt round-robin to warps, processed in
+//            groups of 4/2/1 sharing the W fragments), N = r2 (NT <= 3
+//            tiles, compile time), K = n2, operands prefetched two k-steps
+//            ahead;
+//   phase B  M = r0 (MT <= 3 tiles, compile time), N = rt, K = r1 r2 split
+//            into kparts ranges so all warps work, B fragments loaded in
+//            chunks of 8 k-steps one chunk ahead (L2 latency), partial tiles
+//            summed in a fixed order through shared memory (deterministic).
+// The last CTA to finish (ticket counter) also reduces ||y||^2 (fused3's
+// per-CTA partials) and ||latent||^2 in a fixed order. Replaces two generic
+// GEMM launches, the latent norm pass and two scalar reductions.
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -18,8 +30,9 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int kGroup = 4;    // tiles per warp per pass
-constexpr int kU2Pitch = 28; // doubles: conflict-free B-fragment reads (<= 24 columns)
+constexpr int kU2Pitch = 28;  // doubles: conflict-free B-fragment reads (<= 24 columns)
+constexpr int kChunk = 8;     // phase-B k-steps per prefetch chunk
+constexpr int kRedDoubles = kWarps * 3 * 64;
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -27,13 +40,63 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
         : "d"(a), "d"(b));
 }
 
+// Z tiles for G m-tiles (mt0, mt0 + 8, ...) x NT n-tiles.
+template <int G, int NT>
+__device__ __forceinline__ void phase_a_group(const double* __restrict__ W, const double* U2s, double* Zs,
+                                              int R01, int r2, int n2, int mt0, int g4, int t4) {
+    double acc[G][NT][2];
+#pragma unroll
+    for (int i = 0; i < G; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    auto load = [&](int k, double (&av)[G]) {
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            const int p = 8 * (mt0 + kWarps * i) + g4;
+            av[i] = (p < R01 && k < n2) ? __ldg(W + static_cast<int64_t>(k) * R01 + p) : 0.0;
+        }
+    };
+    double cur[G], nxt[G];
+    load(t4, cur);
+    load(t4 + 4, nxt);
+    for (int k0 = 0; k0 < n2; k0 += 4) {
+        double fut[G];
+        load(k0 + 8 + t4, fut);
+        const int k = k0 + t4;
+        double b[NT];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) b[j] = (k < n2) ? U2s[k * kU2Pitch + 8 * j + g4] : 0.0;
+#pragma unroll
+        for (int i = 0; i < G; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma(acc[i][j], cur[i], b[j]);
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            cur[i] = nxt[i];
+            nxt[i] = fut[i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const int p = 8 * (mt0 + kWarps * i) + g4;
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int a2 = 8 * j + 2 * t4 + h;
+                if (p < R01 && a2 < r2) Zs[p + R01 * a2] = acc[i][j][h];
+            }
+    }
+}
+
+template <int NT, int MT>
 __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     extern __shared__ __align__(16) double sm[];
     const int r0 = a.r0, r1 = a.r1, r2 = a.r2, rt = a.rt;
     const int R01 = r0 * r1, R12 = r1 * r2;
     const int n2 = static_cast<int>(a.n2);
-    double* U2s = sm;                               // [n2][kU2Pitch]
-    double* Zs = U2s + n2 * kU2Pitch;               // [a0 + r0 (a1 + r1 a2)]
+    double* U2s = sm;  // [n2][kU2Pitch], later the phase-B reduction buffer
+    double* Zs = U2s + max(n2 * kU2Pitch, kRedDoubles);  // [a0 + r0 (a1 + r1 a2)]
     __shared__ double red[kWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -47,118 +110,162 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     __syncthreads();
 
     // ---- phase A: Z_s(p, a2), M = R01 (p), N = r2, K = n2 ----
-    const double* W = a.wslab + s * n2 * static_cast<int64_t>(R01);
-    const int mtA = (R01 + 7) / 8, ntA = (r2 + 7) / 8;
-    for (int base = warp; base < mtA; base += kWarps * kGroup) {
-        double acc[kGroup][3][2];
-#pragma unroll
-        for (int i = 0; i < kGroup; ++i)
-#pragma unroll
-            for (int j = 0; j < 3; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        auto loadA = [&](int k, double (&av)[kGroup]) {
-#pragma unroll
-            for (int i = 0; i < kGroup; ++i) {
-                const int mt = base + kWarps * i;
-                const int p = 8 * mt + g4;
-                av[i] = (mt < mtA && p < R01 && k < n2) ? __ldg(W + static_cast<int64_t>(k) * R01 + p) : 0.0;
-            }
-        };
-        double anext[kGroup];
-        loadA(t4, anext);
-#pragma unroll 2
-        for (int k0 = 0; k0 < n2; k0 += 4) {
-            const int k = k0 + t4;
-            double av[kGroup];
-#pragma unroll
-            for (int i = 0; i < kGroup; ++i) av[i] = anext[i];
-            loadA(k + 4, anext);  // next step's operands in flight during the MMAs
-            double b[3];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) b[j] = (k < n2) ? U2s[k * kU2Pitch + 8 * j + g4] : 0.0;
-#pragma unroll
-            for (int i = 0; i < kGroup; ++i)
-#pragma unroll
-                for (int j = 0; j < 3; ++j)
-                    if (j < ntA) dmma(acc[i][j], av[i], b[j]);
+    {
+        const double* W = a.wslab + s * n2 * static_cast<int64_t>(R01);
+        const int mtA = (R01 + 7) / 8;
+        const int cnt = warp < mtA ? (mtA - warp + kWarps - 1) / kWarps : 0;
+        int t = 0;
+        for (; cnt - t >= 4; t += 4) phase_a_group<4, NT>(W, U2s, Zs, R01, r2, n2, warp + kWarps * t, g4, t4);
+        if (cnt - t >= 2) {
+            phase_a_group<2, NT>(W, U2s, Zs, R01, r2, n2, warp + kWarps * t, g4, t4);
+            t += 2;
         }
-#pragma unroll
-        for (int i = 0; i < kGroup; ++i) {
-            const int mt = base + kWarps * i;
-            if (mt >= mtA) continue;
-            const int p = 8 * mt + g4;
-#pragma unroll
-            for (int j = 0; j < 3; ++j)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int a2 = 8 * j + 2 * t4 + h;
-                    if (p < R01 && a2 < r2) Zs[p + R01 * a2] = acc[i][j][h];
-                }
-        }
+        if (cnt - t >= 1) phase_a_group<1, NT>(W, U2s, Zs, R01, r2, n2, warp + kWarps * t, g4, t4);
     }
     __syncthreads();
 
     // ---- phase B: latent_s(a0, b) = Z_s(a0, j) B(j, b), M = r0, N = rt, K = R12 ----
-    const int mtB = (r0 + 7) / 8, ntB = (rt + 7) / 8;
-    double lsq = 0.0;
+    const int ntB = (rt + 7) / 8;
+    const int kparts = ntB >= kWarps ? 1 : kWarps / ntB;
+    const int KS = (R12 + 3) / 4;
+    const int sp = (KS + kparts - 1) / kparts;
     double* out = a.latent + s * static_cast<int64_t>(r0) * rt;
-    for (int base = warp; base < ntB; base += kWarps * kGroup) {
-        double acc[3][kGroup][2];
+    double* redbuf = U2s;
+    double lsq = 0.0;
+    for (int item = warp; item < ntB * kparts; item += kWarps) {
+        const int nt = item % ntB, q = item / ntB;
+        const int ks0 = q * sp, ks1 = min(KS, ks0 + sp);
+        const int bcol = 8 * nt + g4;
+        const double* Bcol = a.B + static_cast<int64_t>(R12) * bcol;
+        const int kend = min(R12, 4 * ks1);
+        auto load = [&](int ks, double (&bv)[kChunk]) {
 #pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int j = 0; j < kGroup; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        auto loadB = [&](int k, double (&bv)[kGroup]) {
-#pragma unroll
-            for (int j = 0; j < kGroup; ++j) {
-                const int nt = base + kWarps * j;
-                const int bcol = 8 * nt + g4;
-                bv[j] = (nt < ntB && bcol < rt && k < R12) ? __ldg(a.B + k + static_cast<int64_t>(R12) * bcol) : 0.0;
+            for (int c = 0; c < kChunk; ++c) {
+                const int k = 4 * (ks + c) + t4;
+                bv[c] = (bcol < rt && k < kend) ? __ldg(Bcol + k) : 0.0;
             }
         };
-        double bnext[kGroup];
-        loadB(t4, bnext);
-#pragma unroll 2
-        for (int k0 = 0; k0 < R12; k0 += 4) {
-            const int k = k0 + t4;
-            double bv[kGroup];
+        double acc[MT][2];
 #pragma unroll
-            for (int j = 0; j < kGroup; ++j) bv[j] = bnext[j];
-            loadB(k + 4, bnext);  // next step's operands in flight during the MMAs
-            double av[3];
+        for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
+        double bc[kChunk];
+        load(ks0, bc);
+        for (int ks = ks0; ks < ks1; ks += kChunk) {
+            double bn[kChunk];
+            load(ks + kChunk, bn);
 #pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const int a0 = 8 * i + g4;
-                av[i] = (i < mtB && a0 < r0 && k < R12) ? Zs[a0 + r0 * k] : 0.0;
+            for (int c = 0; c < kChunk; ++c) {
+                if (ks + c < ks1) {  // warp-uniform
+                    const int k = 4 * (ks + c) + t4;
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) {
+                        const int a0 = 8 * i + g4;
+                        const double av = (a0 < r0 && k < R12) ? Zs[a0 + r0 * k] : 0.0;
+                        dmma(acc[i], av, bc[c]);
+                    }
+                }
             }
 #pragma unroll
-            for (int j = 0; j < kGroup; ++j)
-#pragma unroll
-                for (int i = 0; i < 3; ++i)
-                    if (i < mtB) dmma(acc[i][j], av[i], bv[j]);
+            for (int c = 0; c < kChunk; ++c) bc[c] = bn[c];
         }
+        if (kparts == 1) {
 #pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int j = 0; j < kGroup; ++j)
+            for (int i = 0; i < MT; ++i)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int nt = base + kWarps * j;
-                    const int a0 = 8 * i + g4, bcol = 8 * nt + 2 * t4 + h;
-                    if (i < mtB && nt < ntB && a0 < r0 && bcol < rt) {
-                        const double v = acc[i][j][h];
-                        out[a0 + static_cast<int64_t>(r0) * bcol] = v;
+                    const int a0 = 8 * i + g4, b = 8 * nt + 2 * t4 + h;
+                    if (a0 < r0 && b < rt) {
+                        const double v = acc[i][h];
+                        out[a0 + static_cast<int64_t>(r0) * b] = v;
                         lsq = fma(v, v, lsq);
                     }
                 }
+        } else {
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+                double* dst = redbuf + ((q * ntB + nt) * MT + i) * 64 + 2 * lane;
+                dst[0] = acc[i][0];
+                dst[1] = acc[i][1];
+            }
+        }
+    }
+    if (kparts > 1) {
+        __syncthreads();
+        for (int e = tid; e < ntB * MT * 64; e += kThreads) {
+            const int nt = e / (MT * 64), i = (e / 64) % MT, ln = (e & 63) >> 1, h = e & 1;
+            const int a0 = 8 * i + (ln >> 2), b = 8 * nt + 2 * (ln & 3) + h;
+            if (a0 >= r0 || b >= rt) continue;
+            double v = 0.0;
+            for (int q = 0; q < kparts; ++q) v += redbuf[q * ntB * MT * 64 + e];
+            out[a0 + static_cast<int64_t>(r0) * b] = v;
+            lsq = fma(v, v, lsq);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lsq += __shfl_xor_sync(0xffffffffu, lsq, o);
     if (lane == 0) red[warp] = lsq;
     __syncthreads();
+    __shared__ bool last;
     if (tid == 0) {
         double t = 0.0;
         for (int w = 0; w < kWarps; ++w) t += red[w];
         a.latsq[s] = t;
+        __threadfence();
+        last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    // last CTA: both scalar reductions in a fixed order (deterministic no
+    // matter which CTA finishes last)
+    __threadfence();
+    double ys = 0.0, ls = 0.0;
+    for (int64_t i = tid; i < a.n_ysq; i += kThreads) ys += __ldcg(a.ysq_partials + i);
+    for (int64_t i = tid; i < a.S; i += kThreads) ls += __ldcg(a.latsq + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ys += __shfl_xor_sync(0xffffffffu, ys, o);
+        ls += __shfl_xor_sync(0xffffffffu, ls, o);
+    }
+    __shared__ double red2[2][kWarps];
+    if (lane == 0) {
+        red2[0][warp] = ys;
+        red2[1][warp] = ls;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int w = 0; w < kWarps; ++w) {
+            t0 += red2[0][w];
+            t1 += red2[1][w];
+        }
+        a.out[0] = t0;
+        a.out[2] = t1;
+        *a.ticket = 0u;
+    }
+}
+
+size_t tail3_smem(int64_t n2, int r0, int r1, int r2) {
+    return sizeof(double) * (std::max<size_t>(static_cast<size_t>(n2) * kU2Pitch, kRedDoubles) +
+                             static_cast<size_t>(r0) * r1 * r2);
+}
+
+template <int NT, int MT>
+void launch_t(const Tail3Args& a, size_t smem, cudaStream_t s) {
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(tail3_kernel<NT, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        configured = smem;
+    }
+    tail3_kernel<NT, MT><<<static_cast<unsigned>(a.S), kThreads, smem, s>>>(a);
+}
+
+template <int NT>
+void launch_nt(const Tail3Args& a, size_t smem, cudaStream_t s) {
+    switch ((a.r0 + 7) / 8) {
+        case 1: return launch_t<NT, 1>(a, smem, s);
+        case 2: return launch_t<NT, 2>(a, smem, s);
+        default: return launch_t<NT, 3>(a, smem, s);
     }
 }
 
@@ -166,19 +273,16 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
 
 bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2) {
     if (r0 < 1 || r1 < 1 || r2 < 1 || rt < 1 || r0 > 24 || r2 > 24) return false;
-    const size_t smem = sizeof(double) * (static_cast<size_t>(n2) * kU2Pitch + static_cast<size_t>(r0) * r1 * r2);
-    return smem <= 200 * 1024;
+    return tail3_smem(n2, r0, r1, r2) <= 200 * 1024;
 }
 
 void launch_tail3(const Tail3Args& a, cudaStream_t s, int64_t* launches) {
-    const size_t smem =
-        sizeof(double) * (static_cast<size_t>(a.n2) * kU2Pitch + static_cast<size_t>(a.r0) * a.r1 * a.r2);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(tail3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = smem;
+    const size_t smem = tail3_smem(a.n2, a.r0, a.r1, a.r2);
+    switch ((a.r2 + 7) / 8) {
+        case 1: launch_nt<1>(a, smem, s); break;
+        case 2: launch_nt<2>(a, smem, s); break;
+        default: launch_nt<3>(a, smem, s); break;
     }
-    tail3_kernel<<<static_cast<unsigned>(a.S), kThreads, smem, s>>>(a);
     ++*launches;
 }
 

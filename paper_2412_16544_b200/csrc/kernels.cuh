@@ -56,6 +56,7 @@ void launch_sumsq(const double* x, int64_t n, double* partials, double* out, cud
 // out[0] = sum of n partials in index order (deterministic).
 void launch_sum_partials(const double* partials, int64_t n, double* out, cudaStream_t s, int64_t* launches);
 
+constexpr int64_t kJacobiMaxN = 2048;  // largest Gram the device eigensolver takes
 // Symmetric eigen-decomposition of an n x n column-major matrix G by
 // parallel cyclic Jacobi in one CTA. Writes eigenvalues (descending) to
 // lambda and the matching eigenvectors as columns of V (n x n, col-major).
@@ -78,6 +79,11 @@ void launch_take_columns(const double* V, int64_t n, int64_t r, double* U, const
 // src viewed as [inner, ext, outer] -> dst [inner, ext+extra, outer].
 void launch_pad_axis(const double* src, int64_t inner, int64_t ext, int64_t outer, int64_t extra, double* dst,
                      cudaStream_t s, int64_t* launches);
+
+// dst (ext x inner*outer, col-major) <- the unfolding of src viewed as
+// [inner, ext, outer] along its middle axis.
+void launch_unfold(const double* src, int64_t inner, int64_t ext, int64_t outer, double* dst, cudaStream_t s,
+                   int64_t* launches);
 
 // Orthogonalise W (alpha x q) against U (alpha x r) twice, then CholeskyQR2,
 // in one CTA (ht_rise.hpp:53-79 expand_core with SURVEY §7.3 item 4). Writes
@@ -129,6 +135,12 @@ struct Tail3Args {
     int64_t n2 = 0, S = 0;
     double* latent = nullptr;
     double* latsq = nullptr;  // S entries
+    // final reductions, done by the last CTA to finish (fixed order):
+    // out[0] = sum(ysq_partials[0..n_ysq)), out[2] = sum(latsq[0..S))
+    const double* ysq_partials = nullptr;
+    int64_t n_ysq = 0;
+    double* out = nullptr;
+    unsigned int* ticket = nullptr;  // zero on entry, left zero on exit
 };
 bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2);
 void launch_tail3(const Tail3Args& a, cudaStream_t s, int64_t* launches);

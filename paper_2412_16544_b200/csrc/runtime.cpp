@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "runtime.hpp"
@@ -17,8 +19,17 @@ namespace htr {
 
 void raise(htr_status code, const std::string& msg) { throw Error{code, msg}; }
 
-void cuda_check(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) raise(HTR_ERR_CUDA, std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what);
+void cuda_check(cudaError_t e, const char* what, int line) {
+    // HTR_DEBUG_SYNC=1: synchronise after every checked call so a faulting
+    // kernel is reported at the launch site that queued it
+    static const bool debug_sync = [] {
+        const char* v = std::getenv("HTR_DEBUG_SYNC");
+        return v && v[0] == '1';
+    }();
+    if (e == cudaSuccess && debug_sync) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess)
+        raise(HTR_ERR_CUDA, std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what + " (line " +
+                                std::to_string(line) + ")");
 }
 
 Stream::Stream(int dev) : device(dev) {
@@ -96,11 +107,10 @@ void comm_unique_id(uint8_t out[128]) {
 }
 
 void comm_init(Context& c, const uint8_t uid[128], int nranks, int rank) {
-    if (nranks <= 1) {
-        c.nranks = 1;
-        c.rank = 0;
-        return;
-    }
+    // An explicit call always builds a communicator, a single-rank one
+    // included: every reduction then goes through NCCL exactly as at N > 1.
+    if (nranks < 1 || rank < 0 || rank >= nranks) raise(HTR_ERR_INVALID_ARGUMENT, "bad nranks/rank for init_comm");
+    if (c.nccl_comm) raise(HTR_ERR_INVALID_ARGUMENT, "context already has a communicator");
     ncclUniqueId id;
     std::memcpy(&id, uid, 128);
     ncclComm_t comm;
@@ -125,6 +135,8 @@ Context::Context(int dev) : device(dev) {
     HTR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     HTR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_sc), 1024 * sizeof(double)));
     d_sc = alloc(1024);
+    HTR_CUDA(cudaMalloc(reinterpret_cast<void**>(&d_ticket), sizeof(unsigned int)));
+    HTR_CUDA(cudaMemset(d_ticket, 0, sizeof(unsigned int)));
     for (auto& e : ev) HTR_CUDA(cudaEventCreate(&e));
 }
 
@@ -134,10 +146,11 @@ Context::~Context() {
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
     if (h_sc) cudaFreeHost(h_sc);
+    if (d_ticket) cudaFree(d_ticket);
 }
 
 void Context::allreduce(double* d, int64_t n) {
-    if (nranks <= 1 || n == 0) return;
+    if (!nccl_comm || n == 0) return;
     nccl_check(nccl().allReduce(d, d, static_cast<size_t>(n), ncclDouble, ncclSum,
                                 static_cast<ncclComm_t>(nccl_comm), s),
                "ncclAllReduce");
@@ -276,9 +289,12 @@ void norm_sq(Context& c, const double* x, int64_t n, double* ysq, bool* nonfinit
 ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode);
 
 Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
-                         const ProjectedGram& refine) {
+                         const ProjectedGram& refine, double noise_scale) {
     const int64_t n = rows;
     const int64_t k = std::min(rows, cols);
+    if (n > kJacobiMaxN)
+        raise(HTR_ERR_RUNTIME, "truncation of a " + std::to_string(n) + "-row unfolding exceeds the device eigensolver's " +
+                                   std::to_string(kJacobiMaxN) + "-row limit");
     BufPtr lam = c.alloc(n);
     BufPtr V = c.alloc(n * n);
     BufPtr work = c.alloc(2 * n * n);
@@ -288,7 +304,7 @@ Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, do
     if (refine) {
         std::vector<double> lh(static_cast<size_t>(n));
         c.fetch(lam->p, n, lh.data());
-        const double lmax = std::max(lh[0], 0.0);
+        const double lmax = std::max({lh[0], noise_scale, 0.0});
         if (lmax > 0.0 && eps_abs * eps_abs < 1e-7 * lmax) {
             int64_t s0 = 0;
             while (s0 < n && lh[static_cast<size_t>(s0)] >= 1e-6 * lmax) ++s0;
@@ -336,11 +352,11 @@ Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, do
     return t;
 }
 
-ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode) {
-    return [&c, t, mode](const double* W, int64_t q) {
+ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode, bool reduce) {
+    return [&c, t, mode, reduce](const double* W, int64_t q) {
         const int64_t n = t.shape[static_cast<size_t>(mode)];
         DT B = mode_mul(c, t, mode, W, q, n, 1);  // W^T along `mode`
-        return gram(c, B, mode);
+        return gram(c, B, mode, reduce);
     };
 }
 
@@ -435,11 +451,6 @@ Index svds_below(const DimensionTree& t, Index l) {
     return n;
 }
 
-/// Basis matrix view (alpha x r) of a non-root core (bht.hpp:81-86).
-struct Basis {
-    const double* p;
-    int64_t alpha, r;
-};
 Basis basis_of(const Rep& h, NodeId id) {
     const DT& c = h.core(id);
     if (h.tree.node(id).kind == NodeKind::Leaf) return {c.data(), c.shape[0], c.shape[1]};
@@ -459,6 +470,202 @@ Shape layer_extents(const Rep& h, Index l, const RankMap& ranks, int64_t batch, 
     ext.push_back(batch);
     return ext;
 }
+
+namespace {
+
+/// G_R = (I - U U^T) G (I - U U^T): the Gram of the residual
+/// compute_residual(U, C) (ht_rise.hpp:31-38) without forming it.
+void residual_gram(Context& c, DT& G, const Basis& U) {
+    const int64_t a = U.alpha, r = U.r;
+    DT X1 = c.tensor({r, a});
+    {
+        GemmDesc d;  // X1 = U^T G
+        d.M = r; d.N1 = a; d.K1 = a;
+        d.A = U.p; d.sam = a; d.sak1 = 1;
+        d.B = G.data(); d.sbk1 = 1; d.sbn1 = a;
+        d.C = X1.data(); d.scm = 1; d.scn1 = r;
+        run_gemm(c, d);
+    }
+    {
+        GemmDesc d;  // G -= U X1
+        d.M = a; d.N1 = a; d.K1 = r;
+        d.A = U.p; d.sam = 1; d.sak1 = a;
+        d.B = X1.data(); d.sbk1 = 1; d.sbn1 = r;
+        d.C = G.data(); d.scm = 1; d.scn1 = a;
+        d.alpha = -1.0; d.beta = 1.0;
+        run_gemm(c, d);
+    }
+    DT X2 = c.tensor({a, r});
+    {
+        GemmDesc d;  // X2 = G U
+        d.M = a; d.N1 = r; d.K1 = a;
+        d.A = G.data(); d.sam = 1; d.sak1 = a;
+        d.B = U.p; d.sbk1 = 1; d.sbn1 = a;
+        d.C = X2.data(); d.scm = 1; d.scn1 = a;
+        run_gemm(c, d);
+    }
+    {
+        GemmDesc d;  // G -= X2 U^T
+        d.M = a; d.N1 = a; d.K1 = r;
+        d.A = X2.data(); d.sam = 1; d.sak1 = a;
+        d.B = U.p; d.sbk1 = a; d.sbn1 = 1;
+        d.C = G.data(); d.scm = 1; d.scn1 = a;
+        d.alpha = -1.0; d.beta = 1.0;
+        run_gemm(c, d);
+    }
+}
+
+}  // namespace
+
+namespace {
+
+/// K = X^T X (n x n) of a rows x n column-major matrix.
+DT cols_gram(Context& c, const double* X, int64_t rows, int64_t n) {
+    DT K = c.tensor({n, n});
+    GemmDesc d;
+    d.M = n; d.N1 = n; d.K1 = rows;
+    d.A = X; d.sam = rows; d.sak1 = 1;
+    d.B = X; d.sbk1 = 1; d.sbn1 = rows;
+    d.C = K.data(); d.scm = 1; d.scn1 = n;
+    run_gemm(c, d);
+    return K;
+}
+
+/// Truncation of a rows x cols matrix X (rows > cols) through its column-side
+/// Gram X^T X: the same singular values and rank rule (truncated_svd.hpp:
+/// 53-100), left vectors U = X V_r Sigma_r^{-1}, re-orthonormalised by
+/// CholeskyQR2. Small eigenvalues are re-measured through (X W)^T (X W).
+Truncation truncate_cols_side(Context& c, const DT& X, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank) {
+    DT K = cols_gram(c, X.data(), rows, cols);
+    ProjectedGram refine = [&c, X, rows, cols](const double* W, int64_t q) {
+        DT Y = c.tensor({rows, q});
+        GemmDesc d;  // Y = X W
+        d.M = rows; d.N1 = q; d.K1 = cols;
+        d.A = X.data(); d.sam = 1; d.sak1 = rows;
+        d.B = W; d.sbk1 = 1; d.sbn1 = cols;
+        d.C = Y.data(); d.scm = 1; d.scn1 = rows;
+        run_gemm(c, d);
+        return cols_gram(c, Y.data(), rows, q);
+    };
+    const Truncation tv = truncate_gram(c, K, cols, rows, eps_abs, min_rank, refine);
+    Truncation t;
+    t.rank = tv.rank;
+    t.discarded = tv.discarded;
+    t.sigma = tv.sigma;
+    t.u = c.tensor({rows, t.rank});
+    if (t.rank == 0) return t;
+    const size_t r = static_cast<size_t>(t.rank);
+    if (std::all_of(t.sigma.begin(), t.sigma.end(), [](double v) { return v == 0.0; })) {
+        // zero matrix: the reference SVD's leading identity columns
+        std::vector<double> e(static_cast<size_t>(rows) * r, 0.0);
+        for (size_t i = 0; i < r; ++i) e[i + static_cast<size_t>(rows) * i] = 1.0;
+        HTR_CUDA(cudaMemcpyAsync(t.u.data(), e.data(), sizeof(double) * e.size(), cudaMemcpyHostToDevice, c.s));
+        HTR_CUDA(cudaStreamSynchronize(c.s));
+        return t;
+    }
+    std::vector<double> v(static_cast<size_t>(cols) * r);
+    c.fetch(tv.u.data(), static_cast<int64_t>(v.size()), v.data());
+    for (size_t j = 0; j < r; ++j) {
+        const double inv = t.sigma[j] > 0.0 ? 1.0 / t.sigma[j] : 0.0;
+        for (int64_t i = 0; i < cols; ++i) v[static_cast<size_t>(i) + static_cast<size_t>(cols) * j] *= inv;
+    }
+    DT Vs = c.tensor({cols, t.rank});
+    HTR_CUDA(cudaMemcpyAsync(Vs.data(), v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, c.s));
+    {
+        GemmDesc d;  // U = X V_r Sigma_r^{-1}
+        d.M = rows; d.N1 = t.rank; d.K1 = cols;
+        d.A = X.data(); d.sam = 1; d.sak1 = rows;
+        d.B = Vs.data(); d.sbk1 = 1; d.sbn1 = cols;
+        d.C = t.u.data(); d.scm = 1; d.scn1 = rows;
+        run_gemm(c, d);
+    }
+    BufPtr info = c.alloc(4);
+    BufPtr work = c.alloc(t.rank * t.rank + 16);
+    launch_orthonormalize_new(nullptr, rows, 0, t.u.data(), t.rank, info->p, work->p, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+    HTR_CUDA(cudaStreamSynchronize(c.s));  // v is pageable host memory
+    return t;
+}
+
+}  // namespace
+
+}  // namespace
+
+Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, double eps_abs, int64_t min_rank,
+                         int64_t cols_global, bool sharded) {
+    const int64_t rows = t.shape[static_cast<size_t>(mode)];
+    const int64_t cols_local = t.size() / rows;
+    const bool reduce = sharded && c.nccl_comm;
+    if (!reduce && rows > kColumnSideRows && cols_local < rows) {
+        // tall unfolding on one rank: decompose the smaller, column-side Gram
+        int64_t inner = 1, outer = 1;
+        for (int k = 0; k < mode; ++k) inner *= t.shape[static_cast<size_t>(k)];
+        for (size_t k = static_cast<size_t>(mode) + 1; k < t.shape.size(); ++k) outer *= t.shape[k];
+        DT X = c.tensor({rows, cols_local});
+        launch_unfold(t.data(), inner, rows, outer, X.data(), c.s, &c.launches);
+        HTR_CUDA(cudaGetLastError());
+        if (old && old->r > 0) {
+            // explicit residual X <- (I - U U^T) X (compute_residual, ht_rise.hpp:31-38)
+            DT T = c.tensor({old->r, cols_local});
+            GemmDesc d;  // T = U^T X
+            d.M = old->r; d.N1 = cols_local; d.K1 = rows;
+            d.A = old->p; d.sam = rows; d.sak1 = 1;
+            d.B = X.data(); d.sbk1 = 1; d.sbn1 = rows;
+            d.C = T.data(); d.scm = 1; d.scn1 = old->r;
+            run_gemm(c, d);
+            GemmDesc e;  // X -= U T
+            e.M = rows; e.N1 = cols_local; e.K1 = old->r;
+            e.A = old->p; e.sam = 1; e.sak1 = rows;
+            e.B = T.data(); e.sbk1 = 1; e.sbn1 = old->r;
+            e.C = X.data(); e.scm = 1; e.scn1 = rows;
+            e.alpha = -1.0; e.beta = 1.0;
+            run_gemm(c, e);
+        }
+        return truncate_cols_side(c, X, rows, cols_local, eps_abs, min_rank);
+    }
+    DT G = gram(c, t, mode, reduce);
+    if (!old) return truncate_gram(c, G, rows, cols_global, eps_abs, min_rank, unfolding_refiner(c, t, mode, reduce));
+    // the residual Gram is formed by subtraction: its eigenvalues carry
+    // rounding noise on the scale of the unprojected Gram (its trace)
+    std::vector<double> diag(static_cast<size_t>(rows));
+    HTR_CUDA(cudaMemcpy2DAsync(diag.data(), sizeof(double), G.data(), sizeof(double) * static_cast<size_t>(rows + 1),
+                               sizeof(double), static_cast<size_t>(rows), cudaMemcpyDeviceToHost, c.s));
+    const Basis U = *old;
+    residual_gram(c, G, U);
+    HTR_CUDA(cudaStreamSynchronize(c.s));
+    double gtrace = 0.0;
+    for (double v : diag) gtrace += v;
+    // refinement measures the residual R = (I - U U^T) C directly:
+    // W^T R = ((I - U U^T) W)^T C
+    ProjectedGram refine = [&c, t, mode, U, reduce](const double* W, int64_t q) {
+        DT T = c.tensor({U.r, q});
+        {
+            GemmDesc d;  // T = U^T W
+            d.M = U.r; d.N1 = q; d.K1 = U.alpha;
+            d.A = U.p; d.sam = U.alpha; d.sak1 = 1;
+            d.B = W; d.sbk1 = 1; d.sbn1 = U.alpha;
+            d.C = T.data(); d.scm = 1; d.scn1 = U.r;
+            run_gemm(c, d);
+        }
+        DT Wp = c.tensor({U.alpha, q});
+        HTR_CUDA(cudaMemcpyAsync(Wp.data(), W, sizeof(double) * static_cast<size_t>(U.alpha * q),
+                                 cudaMemcpyDeviceToDevice, c.s));
+        {
+            GemmDesc d;  // Wp -= U T
+            d.M = U.alpha; d.N1 = q; d.K1 = U.r;
+            d.A = U.p; d.sam = 1; d.sak1 = U.alpha;
+            d.B = T.data(); d.sbk1 = 1; d.sbn1 = U.r;
+            d.C = Wp.data(); d.scm = 1; d.scn1 = U.alpha;
+            d.alpha = -1.0; d.beta = 1.0;
+            run_gemm(c, d);
+        }
+        DT B = mode_mul(c, t, mode, Wp.data(), q, U.alpha, 1);
+        return gram(c, B, mode, reduce);
+    };
+    return truncate_gram(c, G, rows, cols_global, eps_abs, min_rank, refine, gtrace);
+}
+
+namespace {
 
 DT project(Context& c, const DT& t, int mode, const Basis& b, double* energy_slot) {
     if (b.alpha != t.shape[static_cast<size_t>(mode)])
@@ -484,7 +691,7 @@ DT project(Context& c, const DT& t, int mode, const Basis& b, double* energy_slo
 }
 
 int64_t global_batch(Context& c, int64_t local) {
-    if (c.nranks <= 1) return local;
+    if (!c.nccl_comm) return local;
     c.h_sc[0] = static_cast<double>(local);
     HTR_CUDA(cudaMemcpyAsync(c.d_sc->p + 8, c.h_sc, sizeof(double), cudaMemcpyHostToDevice, c.s));
     c.allreduce(c.d_sc->p + 8, 1);
@@ -562,9 +769,8 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
     // deepest layer: plain HOSVD of y over all leaves, then sequential projections
     std::vector<Truncation> bases;
     for (const TreeNode& n : tree.layer(p)) {
-        DT G = gram(c, cur, static_cast<int>(n.leaf_dim));
-        bases.push_back(truncate_gram(c, G, G.shape[0], cols_of(cur, static_cast<int>(n.leaf_dim)), eps_nw, 1,
-                                      unfolding_refiner(c, cur, static_cast<int>(n.leaf_dim))));
+        const int mode = static_cast<int>(n.leaf_dim);
+        bases.push_back(truncate_mode(c, cur, mode, nullptr, eps_nw, 1, cols_of(cur, mode)));
     }
     RankMap ranks;
     for (size_t i = 0; i < bases.size(); ++i) {
@@ -589,9 +795,7 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
         cur.shape = layer_extents(*h, l, ranks, batch, false);
         std::vector<Truncation> lb;
         for (Index j = 0; j < tree.layer_size(l); ++j) {
-            DT G = gram(c, cur, static_cast<int>(j));
-            lb.push_back(truncate_gram(c, G, G.shape[0], cols_of(cur, static_cast<int>(j)), eps_nw, 1,
-                                       unfolding_refiner(c, cur, static_cast<int>(j))));
+            lb.push_back(truncate_mode(c, cur, static_cast<int>(j), nullptr, eps_nw, 1, cols_of(cur, static_cast<int>(j))));
         }
         for (Index j = 0; j < tree.layer_size(l); ++j) {
             const TreeNode& n = tree.layer(l)[static_cast<size_t>(j)];
@@ -625,7 +829,7 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
 // encode (bht.hpp:373-401)
 // ---------------------------------------------------------------------------
 
-EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
+EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* latent_target) {
     const DimensionTree& tree = h.tree;
     const Index d = tree.dims(), p = tree.depth();
     const int64_t batch = y.shape[static_cast<size_t>(d)];
@@ -634,7 +838,13 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
     const RankMap ranks = h.ranks();
     double* sc = c.d_sc->p;  // [0] ysq, [1] nonfinite, [2] latent^2, [16..] step energies
     int nslots = 0;
-    HTR_CUDA(cudaMemsetAsync(sc, 0, 512 * sizeof(double), c.s));
+    // the generic kernels accumulate into the scalar slots; the fused
+    // leaf+tail path assigns sc[0] and sc[2] and needs no clearing
+    bool zeroed = false;
+    auto zero_scalars = [&] {
+        if (!zeroed) HTR_CUDA(cudaMemsetAsync(sc, 0, 512 * sizeof(double), c.s));
+        zeroed = true;
+    };
 
     DT cur = y;
     bool leaves_done = false;
@@ -651,7 +861,9 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
                               tree.layer(1)[1].kind == NodeKind::Transfer;
         const int rt = tree_123 ? static_cast<int>(ranks.at(NodeId{1, 1})) : 0;
         const bool use_tail = tree_123 && tail3_supported(r0, r1, r2, rt, y.shape[2]);
-        if (fused3_supported(y.shape[0], y.shape[1], y.shape[2], r0, r1, r2)) {
+        const bool fused_ok = fused3_supported(y.shape[0], y.shape[1], y.shape[2], r0, r1, r2);
+        if (!(fused_ok && use_tail)) zero_scalars();
+        if (fused_ok) {
             Fused3Args fa;
             fa.Y = y.data();
             fa.n2 = y.shape[2];
@@ -677,7 +889,7 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
             if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[1], c.s));
             HTR_CUDA(cudaGetLastError());
             if (grid > 0) {  // else (no tensor map for this pointer): generic kernels below
-                launch_sum_partials(fa.ysq_partials, grid, sc + 0, c.s, &c.launches);
+                if (!use_tail) launch_sum_partials(fa.ysq_partials, grid, sc + 0, c.s, &c.launches);
                 leaves_done = true;
                 out.fused = true;
                 if (use_tail) {
@@ -691,13 +903,21 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
                     ta.rt = rt;
                     ta.n2 = fa.n2;
                     ta.S = batch;
-                    DT lat = c.tensor({r0, rt, batch});
+                    DT lat;
+                    if (latent_target && latent_target->shape == Shape{r0, rt, batch}) {
+                        lat = *latent_target;
+                    } else {
+                        lat = c.tensor({r0, rt, batch});
+                    }
                     ta.latent = lat.data();
                     BufPtr lsq = c.alloc(batch);
                     ta.latsq = lsq->p;
+                    ta.ysq_partials = fa.ysq_partials;
+                    ta.n_ysq = grid;
+                    ta.out = sc;
+                    ta.ticket = c.d_ticket;
                     launch_tail3(ta, c.s, &c.launches);
                     HTR_CUDA(cudaGetLastError());
-                    launch_sum_partials(lsq->p, batch, sc + 2, c.s, &c.launches);
                     cur = lat;
                     tail_done = true;
                 } else {
@@ -707,6 +927,7 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact) {
         }
     }
     if (!leaves_done) {
+        zero_scalars();
         for (const TreeNode& n : tree.layer(p))
             cur = project(c, cur, static_cast<int>(n.leaf_dim), basis_of(h, n.id), exact ? sc + 16 + nslots++ : nullptr);
     }
@@ -767,8 +988,10 @@ void append_root(Context& c, Rep& out, const Rep& in, const DT& latent) {
     const std::shared_ptr<RootStore>& rs = in.root;
     const int64_t slice = r11 * r12;
     if (rs && rs->r11 == r11 && rs->r12 == r12 && rs->committed == in.acc && in.acc + n <= rs->cap) {
-        // tip of the shared store: append in place, O(batch)
-        HTR_CUDA(cudaMemcpyAsync(rs->buf->p + slice * in.acc, latent.data(), sizeof(double) * static_cast<size_t>(slice * n),
+        // tip of the shared store: append in place, O(batch); nothing to
+        // copy when the encoder already wrote the latent into the slot
+        if (latent.buf != rs->buf || latent.offset != slice * in.acc)
+            HTR_CUDA(cudaMemcpyAsync(rs->buf->p + slice * in.acc, latent.data(), sizeof(double) * static_cast<size_t>(slice * n),
                                  cudaMemcpyDeviceToDevice, c.s));
         rs->committed = in.acc + n;
         out.root = rs;
@@ -792,51 +1015,6 @@ void append_root(Context& c, Rep& out, const Rep& in, const DT& latent) {
 // HT-RISE update (ht_rise.hpp:99-186)
 // ---------------------------------------------------------------------------
 
-namespace {
-
-/// G_R = (I - U U^T) G (I - U U^T): the Gram of the residual
-/// compute_residual(U, C) (ht_rise.hpp:31-38) without forming it.
-void residual_gram(Context& c, DT& G, const Basis& U) {
-    const int64_t a = U.alpha, r = U.r;
-    DT X1 = c.tensor({r, a});
-    {
-        GemmDesc d;  // X1 = U^T G
-        d.M = r; d.N1 = a; d.K1 = a;
-        d.A = U.p; d.sam = a; d.sak1 = 1;
-        d.B = G.data(); d.sbk1 = 1; d.sbn1 = a;
-        d.C = X1.data(); d.scm = 1; d.scn1 = r;
-        run_gemm(c, d);
-    }
-    {
-        GemmDesc d;  // G -= U X1
-        d.M = a; d.N1 = a; d.K1 = r;
-        d.A = U.p; d.sam = 1; d.sak1 = a;
-        d.B = X1.data(); d.sbk1 = 1; d.sbn1 = r;
-        d.C = G.data(); d.scm = 1; d.scn1 = a;
-        d.alpha = -1.0; d.beta = 1.0;
-        run_gemm(c, d);
-    }
-    DT X2 = c.tensor({a, r});
-    {
-        GemmDesc d;  // X2 = G U
-        d.M = a; d.N1 = r; d.K1 = a;
-        d.A = G.data(); d.sam = 1; d.sak1 = a;
-        d.B = U.p; d.sbk1 = 1; d.sbn1 = a;
-        d.C = X2.data(); d.scm = 1; d.scn1 = a;
-        run_gemm(c, d);
-    }
-    {
-        GemmDesc d;  // G -= X2 U^T
-        d.M = a; d.N1 = a; d.K1 = r;
-        d.A = X2.data(); d.sam = 1; d.sak1 = a;
-        d.B = U.p; d.sbk1 = a; d.sbn1 = 1;
-        d.C = G.data(); d.scm = 1; d.scn1 = a;
-        d.alpha = -1.0; d.beta = 1.0;
-        run_gemm(c, d);
-    }
-}
-
-}  // namespace
 
 UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_override, bool adaptive) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -851,7 +1029,17 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
     std::memset(&res.report, 0, sizeof(res.report));
     htr_update_report& rep = res.report;
 
-    EncodeOut enc = encode(c, h, y, c.exact_loss);
+    // the latent of a skipped batch lands in the root store's next slices:
+    // written there speculatively when this value is the store's tip
+    DT slot;
+    const DT* target = nullptr;
+    if (const auto& rs = h.root; rs && rs->committed == h.acc && h.acc + batch <= rs->cap) {
+        slot.buf = rs->buf;
+        slot.shape = {rs->r11, rs->r12, batch};
+        slot.offset = rs->r11 * rs->r12 * h.acc;
+        target = &slot;
+    }
+    EncodeOut enc = encode(c, h, y, c.exact_loss, target);
     if (enc.nonfinite) raise(HTR_ERR_INVALID_ARGUMENT, "ht_rise_update: non-finite input");
     double norm_y = std::sqrt(enc.ysq);
     rep.eps_des = eps_rel * norm_y;
@@ -909,38 +1097,9 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
 
     auto expand_node = [&](const TreeNode& n, const DT& cur, int mode) {
         const Basis U = basis_of(*out, n.id);
-        DT G = gram(c, cur, mode);
-        residual_gram(c, G, U);
         const int64_t cols = static_cast<int64_t>(
             std::llround(static_cast<double>(cur.size() / cur.shape[static_cast<size_t>(mode)]) * col_scale));
-        // refinement measures the residual R = (I - U U^T) C directly:
-        // W^T R = ((I - U U^T) W)^T C
-        ProjectedGram refine = [&c, &cur, mode, U](const double* W, int64_t q) {
-            DT T = c.tensor({U.r, q});
-            {
-                GemmDesc d;  // T = U^T W
-                d.M = U.r; d.N1 = q; d.K1 = U.alpha;
-                d.A = U.p; d.sam = U.alpha; d.sak1 = 1;
-                d.B = W; d.sbk1 = 1; d.sbn1 = U.alpha;
-                d.C = T.data(); d.scm = 1; d.scn1 = U.r;
-                run_gemm(c, d);
-            }
-            DT Wp = c.tensor({U.alpha, q});
-            HTR_CUDA(cudaMemcpyAsync(Wp.data(), W, sizeof(double) * static_cast<size_t>(U.alpha * q),
-                                     cudaMemcpyDeviceToDevice, c.s));
-            {
-                GemmDesc d;  // Wp -= U T
-                d.M = U.alpha; d.N1 = q; d.K1 = U.r;
-                d.A = U.p; d.sam = 1; d.sak1 = U.alpha;
-                d.B = T.data(); d.sbk1 = 1; d.sbn1 = U.r;
-                d.C = Wp.data(); d.scm = 1; d.scn1 = U.alpha;
-                d.alpha = -1.0; d.beta = 1.0;
-                run_gemm(c, d);
-            }
-            DT B = mode_mul(c, cur, mode, Wp.data(), q, U.alpha, 1);
-            return gram(c, B, mode);
-        };
-        Truncation tb = truncate_gram(c, G, U.alpha, cols, eps_nw, 0, refine);
+        Truncation tb = truncate_mode(c, cur, mode, &U, eps_nw, 0, cols);
         if (tb.rank == 0) return;
         // re-orthonormalise the new directions against the old basis and
         // append (expand_core, ht_rise.hpp:53-79)

@@ -29,8 +29,8 @@ struct Error {
     std::string msg;
 };
 [[noreturn]] void raise(htr_status code, const std::string& msg);
-void cuda_check(cudaError_t e, const char* what);
-#define HTR_CUDA(x) ::htr::cuda_check((x), #x)
+void cuda_check(cudaError_t e, const char* what, int line);
+#define HTR_CUDA(x) ::htr::cuda_check((x), #x, __LINE__)
 
 /// Owns the context's CUDA stream; shared by every buffer allocated on it so
 /// stream-ordered frees stay valid after the context handle is destroyed.
@@ -103,6 +103,7 @@ struct Context {
     bool profile = false;
     double* h_sc = nullptr;  // pinned scalars
     BufPtr d_sc;             // device scalars
+    unsigned int* d_ticket = nullptr;  // last-CTA ticket of the fused tail (kept zero between launches)
     // timing of the fused encode kernel and of the generic GEMMs
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     double fused_ms = 0.0, gemm_ms = 0.0;
@@ -150,15 +151,33 @@ struct Truncation {
 /// truncation re-measure a subspace against the matrix M itself.
 using ProjectedGram = std::function<DT(const double* W, int64_t q)>;
 /// Error-truncated basis of a symmetric Gram (truncated_svd.hpp:53-100 on the
-/// matrix whose Gram this is). k = min(rows, cols). When the tolerance sits
-/// near the Gram's rounding floor (eps^2 < 1e-7 lambda_max) the eigenvalues
-/// below 1e-6 lambda_max are re-measured through `refine` (a second Gram of
-/// the projection of M onto that subspace), which resolves singular values
-/// down to ~u sigma_max like the reference's direct SVD.
+/// matrix whose Gram this is). k = min(rows, cols). The Gram's eigenvalues
+/// carry an absolute rounding error ~u * Lambda, Lambda = max(lambda_max,
+/// `noise_scale`); `noise_scale` is the norm of the Gram this one was derived
+/// from by subtraction (the unprojected Gram of a residual Gram), 0 for a
+/// plain Gram. When the tolerance sits near that floor (eps^2 < 1e-7 Lambda)
+/// the eigenvalues below 1e-6 Lambda are re-measured through `refine` (a
+/// second Gram of the projection of M onto that subspace), which resolves
+/// singular values down to ~u sigma_max like the reference's direct SVD.
 Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
-                         const ProjectedGram& refine = nullptr);
+                         const ProjectedGram& refine = nullptr, double noise_scale = 0.0);
 /// Refiner for a plain unfolding of `t` along `mode`.
-ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode);
+ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode, bool reduce = true);
+
+/// Basis matrix view (alpha x r) of a non-root core (bht.hpp:81-86).
+struct Basis {
+    const double* p;
+    int64_t alpha, r;
+};
+/// Unfoldings taller than this (rows > cols, one rank) are truncated through
+/// their column-side Gram.
+constexpr int64_t kColumnSideRows = 1024;
+/// Error-truncated basis of the mode-`mode` unfolding of t, or with `old`
+/// of its residual (I - U U^T) t_(mode) (compute_residual, ht_rise.hpp:31-38).
+/// cols_global = the unfolding's column count over all ranks; `sharded`
+/// false for a rank-local matrix (no all-reduce).
+Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, double eps_abs, int64_t min_rank,
+                         int64_t cols_global, bool sharded = true);
 
 // ---- algorithms --------------------------------------------------------------
 struct BuildOut {
@@ -175,7 +194,10 @@ struct EncodeOut {
     bool exact = false;
     bool nonfinite = false;
 };
-EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact);
+/// `latent_target`, when given, is where the fused tail writes the latent if
+/// it runs (a view of the root store's next free slices): a skip decision
+/// then only commits it.
+EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* latent_target = nullptr);
 
 struct UpdateOut {
     std::shared_ptr<Rep> rep;

@@ -271,7 +271,7 @@ class DeviceTensor:
                 raise ValueError("DeviceTensor: float64 storage required")
             if not d.is_contiguous():
                 raise ValueError("DeviceTensor: contiguous storage required")
-            if d.numel() != int(np.prod(self.shape)):
+            if d.numel() != math.prod(self.shape):
                 raise ValueError("DeviceTensor: element count does not match shape")
             return int(d.data_ptr())
         return int(d)
@@ -290,15 +290,23 @@ def _shape_arr(shape):
     return (C.c_int64 * len(shape))(*[int(s) for s in shape])
 
 
+def _torch_stream(t) -> int:
+    """Raw handle of torch's current stream on t's device."""
+    import torch
+
+    idx = t.device.index
+    try:
+        return int(torch._C._cuda_getCurrentRawStream(idx))
+    except AttributeError:  # private API moved: public (slower) path
+        return int(torch.cuda.current_stream(t.device).cuda_stream)
+
+
 def _tensor_arg(y, ctx: Optional["Context"] = None):
     """-> (pointer, on_device, shape, keepalive). Device inputs produced on
     torch's current stream are ordered before the library's stream."""
     if isinstance(y, DeviceTensor):
         if ctx is not None and hasattr(y.data, "data_ptr"):
-            import torch
-
-            s = torch.cuda.current_stream(y.data.device).cuda_stream
-            ctx.check(lib().htr_context_wait_stream(ctx.handle, C.c_void_p(s)))
+            ctx.check(lib().htr_context_wait_stream(ctx.handle, C.c_void_p(_torch_stream(y.data))))
         return C.cast(C.c_void_p(y.ptr()), _D), 1, tuple(int(s) for s in y.shape), y
     a = _as_host(y)
     if a.ndim == 0:
