@@ -33,6 +33,10 @@ METRIC = "HT-RISE update GB/s of streamed tensor data"
 UNIT = "GB/s"
 
 
+HBM_NOMINAL_GBS = 8000.0
+FP64_DMMA_TFLOPS = 37.18  # profiles/r1_microbench_fp64.txt (best DMMA.8x8x4 line)
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -266,7 +270,25 @@ def run_ours(args):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "fused3_kernel (leaf projections + ||Y||^2, DMMA f64)",
                 "kernel_ms": avg, "share_of_step": avg / ms, "peak_kind": peak_kind,
-                "algorithmic_bytes_per_launch": local_bytes}
+                "algorithmic_bytes_per_launch": local_bytes,
+                "frac_of_nominal_8000": achieved / HBM_NOMINAL_GBS}
+        # the same kernel against the FP64 tensor pipe (c5 sits
+        # at the FP64/HBM ridge): per slab (s, i2) it contracts n0 x n1 with
+        # U1 (n1 x r1) and then U0^T (r0 x n0); DMMA tiles pad r to 8
+        rk = rep.ranks()
+        if len(w.dims) == 3 and (1, 0) in rk and (2, 0) in rk:
+            n0, n1, n2 = w.dims
+            r0, r1 = rk[(1, 0)], rk[(2, 0)]
+            pad = lambda r: -(-r // 8) * 8  # noqa: E731
+            slabs = n_local * n2
+            flops = 2.0 * slabs * (n0 * n1 * r1 + r0 * n0 * r1)
+            flops_issued = 2.0 * slabs * (n0 * n1 * pad(r1) + pad(r0) * n0 * pad(r1))
+            tf = flops / (avg * 1e-3) / 1e12
+            roof["fp64_pipe"] = {"achieved": tf, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
+                                 "frac": tf / FP64_DMMA_TFLOPS,
+                                 "issued_frac": flops_issued / (avg * 1e-3) / 1e12 / FP64_DMMA_TFLOPS,
+                                 "algorithmic_flops_per_launch": flops, "issued_flops_per_launch": flops_issued,
+                                 "peak_kind": "measured: DMMA.8x8x4 microbenchmark, profiles/r1_microbench_fp64.txt"}
 
     if rank == 0:
         cb = None

@@ -1,16 +1,148 @@
-// htrise-b200 drop-in: compression metrics (reference
-// /root/reference/proj/include/htrise/metrics.hpp: compression_ratio 200-207,
-// reduction_ratio 210-214, relative_test_error 218-237). Per-field
-// normalisation (metrics.hpp:93-197) is outside the accelerated path; see
-// DESIGN.md "Out of scope".
+// htrise-b200 drop-in: compression metrics and the per-field normalisation
+// ledger (reference /root/reference/proj/include/htrise/metrics.hpp:
+// NormalizationMethod 15-33, NormalizationParams 38-46, normalize 93-171,
+// denormalize 174-197, compression_ratio 200-207, reduction_ratio 210-214,
+// relative_test_error 218-237). normalize/denormalize run on the host: they
+// belong to the CLI ingest step above the accelerated path and are here so
+// the HTRS ledger (io.hpp) round-trips the reference's records.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
+#include <optional>
 #include <stdexcept>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "htrise/bht.hpp"
 
 namespace htrise {
+
+enum class NormalizationMethod { None, MaxAbs, UnitVec, ZScore };
+
+inline std::string to_string(NormalizationMethod m) {
+    switch (m) {
+        case NormalizationMethod::MaxAbs: return "maxabs";
+        case NormalizationMethod::UnitVec: return "unitvec";
+        case NormalizationMethod::ZScore: return "zscore";
+        case NormalizationMethod::None: break;
+    }
+    return "none";
+}
+
+inline NormalizationMethod normalization_from_string(const std::string& s) {
+    static const std::pair<const char*, NormalizationMethod> names[] = {
+        {"none", NormalizationMethod::None},
+        {"maxabs", NormalizationMethod::MaxAbs},
+        {"unitvec", NormalizationMethod::UnitVec},
+        {"zscore", NormalizationMethod::ZScore}};
+    for (const auto& [n, m] : names)
+        if (s == n) return m;
+    throw std::invalid_argument("unknown normalization method: " + s);
+}
+
+/// Per-field scalars that undo a normalisation (one entry without a field
+/// axis, else one per slice along it); zero scales are floored to 1.
+struct NormalizationParams {
+    NormalizationMethod method = NormalizationMethod::None;
+    std::optional<Index> field_axis;
+    std::vector<double> scale;
+    std::vector<double> offset;
+    std::vector<bool> floored;
+
+    bool operator==(const NormalizationParams&) const = default;
+};
+
+namespace detail {
+
+/// Calls fn(field, run pointer, run length) over the contiguous runs of t in
+/// storage order (outer index slowest): the reference's accumulation order,
+/// which keeps the recorded parameters bit-identical.
+template <typename T, typename Fn>
+void field_runs(T* data, const Shape& shape, std::optional<Index> axis, Fn&& fn) {
+    const Index total = shape_product(shape);
+    if (!axis) {
+        fn(Index{0}, data, total);
+        return;
+    }
+    require_mode(static_cast<Index>(shape.size()), *axis, "normalize");
+    const ModeSplit sp = split_at(shape, *axis);
+    for (Index o = 0; o < sp.outer; ++o)
+        for (Index f = 0; f < sp.extent; ++f) fn(f, data + sp.inner * (f + sp.extent * o), sp.inner);
+}
+
+}  // namespace detail
+
+/// Scale (z-score: also centre) y, per field slice along `field_axis` when
+/// given; population standard deviation for z-score.
+inline std::pair<DenseTensor, NormalizationParams> normalize(const DenseTensor& y, NormalizationMethod method,
+                                                             std::optional<Index> field_axis = std::nullopt) {
+    NormalizationParams p;
+    p.method = method;
+    p.field_axis = field_axis;
+    if (field_axis) detail::require_mode(y.order(), *field_axis, "normalize");
+    const std::size_t fields = field_axis ? static_cast<std::size_t>(y.extent(*field_axis)) : 1;
+    p.scale.assign(fields, method == NormalizationMethod::None ? 1.0 : 0.0);
+    p.offset.assign(fields, 0.0);
+    p.floored.assign(fields, false);
+    if (method == NormalizationMethod::None) return {y, p};
+
+    auto at = [](std::vector<double>& v, Index f) -> double& { return v[static_cast<std::size_t>(f)]; };
+    if (method == NormalizationMethod::MaxAbs) {
+        detail::field_runs(y.data(), y.shape(), field_axis, [&](Index f, const double* v, Index n) {
+            double& m = at(p.scale, f);
+            for (Index i = 0; i < n; ++i) m = std::max(m, std::abs(v[i]));
+        });
+    } else if (method == NormalizationMethod::UnitVec) {
+        detail::field_runs(y.data(), y.shape(), field_axis, [&](Index f, const double* v, Index n) {
+            double& m = at(p.scale, f);
+            for (Index i = 0; i < n; ++i) m += v[i] * v[i];
+        });
+        for (double& m : p.scale) m = std::sqrt(m);
+    } else {
+        std::vector<Index> count(fields, 0);
+        detail::field_runs(y.data(), y.shape(), field_axis, [&](Index f, const double* v, Index n) {
+            double& mu = at(p.offset, f);
+            for (Index i = 0; i < n; ++i) mu += v[i];
+            count[static_cast<std::size_t>(f)] += n;
+        });
+        for (std::size_t f = 0; f < fields; ++f) p.offset[f] /= static_cast<double>(count[f]);
+        detail::field_runs(y.data(), y.shape(), field_axis, [&](Index f, const double* v, Index n) {
+            double& ss = at(p.scale, f);
+            const double mu = at(p.offset, f);
+            for (Index i = 0; i < n; ++i) ss += (v[i] - mu) * (v[i] - mu);
+        });
+        for (std::size_t f = 0; f < fields; ++f) p.scale[f] = std::sqrt(p.scale[f] / static_cast<double>(count[f]));
+    }
+    for (std::size_t f = 0; f < fields; ++f)
+        if (p.scale[f] == 0.0) {
+            p.scale[f] = 1.0;
+            p.floored[f] = true;
+        }
+    DenseTensor out = y;
+    const bool centre = method == NormalizationMethod::ZScore;
+    detail::field_runs(out.data(), out.shape(), field_axis, [&](Index f, double* v, Index n) {
+        const double mu = centre ? at(p.offset, f) : 0.0, sc = at(p.scale, f);
+        for (Index i = 0; i < n; ++i) v[i] = (v[i] - mu) / sc;
+    });
+    return {std::move(out), std::move(p)};
+}
+
+/// Inverse of normalize for recorded parameters.
+inline DenseTensor denormalize(const DenseTensor& y, const NormalizationParams& p) {
+    const std::size_t fields = p.field_axis ? static_cast<std::size_t>(y.extent(*p.field_axis)) : 1;
+    if (fields != p.scale.size()) throw std::invalid_argument("denormalize: parameter count mismatch");
+    if (p.method == NormalizationMethod::None) return y;
+    DenseTensor out = y;
+    const bool centre = p.method == NormalizationMethod::ZScore;
+    detail::field_runs(out.data(), out.shape(), p.field_axis, [&](Index f, double* v, Index n) {
+        const std::size_t fi = static_cast<std::size_t>(f);
+        const double mu = centre ? p.offset[fi] : 0.0, sc = p.scale[fi];
+        for (Index i = 0; i < n; ++i) v[i] = v[i] * sc + mu;
+    });
+    return out;
+}
 
 inline double compression_ratio(const HTRepresentation& h) {
     if (h.accumulated < 1) throw std::invalid_argument("compression_ratio: empty accumulation");

@@ -80,6 +80,36 @@ def build_dropin_test() -> str:
     return DROPIN_BIN
 
 
+IO_SRC = os.path.join(ROOT, "tests", "cpp", "test_io.cpp")
+IO_BIN = os.path.join(ROOT, "tests", "cpp", "build", "test_io")
+PIN_SRC = os.path.join(ROOT, "tests", "cpp", "json_pin.cpp")
+PIN_BIN = os.path.join(ROOT, "tests", "cpp", "build", "json_pin")
+# the reference serialises container headers with nlohmann::json; the copy
+# shipped in this image is the format checker of json_pin (test only)
+NLOHMANN_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty"
+
+
+def build_io_test() -> str:
+    """Compile the container test program (tests/cpp/test_io.cpp)."""
+    os.makedirs(os.path.dirname(IO_BIN), exist_ok=True)
+    cmd = [CXX, "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", CUDA_INC, IO_SRC,
+           "-L", PKG, "-lhtrise_cuda", "-Wl,-rpath,$ORIGIN/../../../paper_2412_16544_b200", "-o", IO_BIN]
+    subprocess.run(cmd, check=True)
+    return IO_BIN
+
+
+def build_json_pin():
+    """Compile json_pin against the image's nlohmann::json, if present."""
+    if not os.path.exists(os.path.join(NLOHMANN_INC, "nlohmann", "json.hpp")):
+        return None
+    os.makedirs(os.path.dirname(PIN_BIN), exist_ok=True)
+    subprocess.run([CXX, "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-I", NLOHMANN_INC, PIN_SRC,
+                    "-o", PIN_BIN], check=True)
+    return PIN_BIN
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
     print(build_dropin_test())
+    print(build_io_test())
+    print(build_json_pin())

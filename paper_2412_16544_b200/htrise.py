@@ -581,6 +581,28 @@ class HTRepresentation:
     def reserve(self, samples: int):
         self.ctx.check(lib().htr_rep_reserve(self.ctx.handle, self._h, int(samples)))
 
+    @staticmethod
+    def from_cores(tree: DimensionTree, dims, cores, accumulated: int, epsilon_rel: float,
+                   ctx: Optional[Context] = None) -> "HTRepresentation":
+        """Device value from host cores (`cores[(layer, pos)]`, canonical
+        layout, root included): uploads them bit for bit (htr_rep_import)."""
+        ctx = ctx or default_context()
+        nodes, nn = tree.c_nodes()
+        arrays, shapes = [], []
+        for i in range(nn):
+            nid = (nodes[i].layer, nodes[i].pos)
+            a = np.asfortranarray(np.asarray(cores[nid], dtype=np.float64))
+            arrays.append(a)
+            s = list(a.shape) + [1] * (3 - a.ndim)
+            shapes.extend(int(x) for x in s[:3])
+        ptrs = (_D * nn)(*[_ptr(a) for a in arrays])
+        shp = (C.c_int64 * len(shapes))(*shapes)
+        out = _P()
+        ctx.check(lib().htr_rep_import(ctx.handle, nodes, nn, _shape_arr(dims), len(dims), ptrs, shp,
+                                       int(accumulated), float(epsilon_rel), C.byref(out)))
+        del arrays
+        return HTRepresentation(out, ctx, tree, list(dims), int(accumulated), float(epsilon_rel))
+
 
 # ---------------------------------------------------------------------------
 # algorithms

@@ -8,7 +8,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADERS = ["tensor.hpp", "dimension_tree.hpp", "truncated_svd.hpp", "bht.hpp", "ht_rise.hpp", "metrics.hpp",
-           "htrise.hpp", "device.hpp"]
+           "htrise.hpp", "device.hpp", "json.hpp", "io.hpp"]
 
 
 @pytest.mark.parametrize("header", HEADERS)
