@@ -182,7 +182,8 @@ HTR_API htr_status htr_rep_reserve(htr_context* ctx, htr_rep* rep, int64_t sampl
 HTR_API htr_status htr_truncated_svd(htr_context* ctx, const double* m, int32_t m_on_device, int64_t rows,
                              int64_t cols, double eps_abs, int64_t min_rank, double* u, double* sigma,
                              int64_t* rank, double* discarded_norm);
-/* mode_multiply (tensor.hpp:300-312): out = t x_mode M, M is q x extent. */
+/* mode_multiply (tensor.hpp:300-312): out = t x_mode M, M is q x extent
+ * (column-major) and lives where t lives (t_on_device). */
 HTR_API htr_status htr_mode_multiply(htr_context* ctx, const double* t, int32_t t_on_device, const int64_t* shape,
                              int32_t order, int32_t mode, const double* m, int64_t q, double* out,
                              int32_t out_on_device);

@@ -223,9 +223,10 @@ __device__ __forceinline__ void small_fibre(const double (&x)[JM], const double*
 template <int JM, int QM, bool MODE0>
 __global__ void __launch_bounds__(256) mode_small_kernel(const double* __restrict__ t, int64_t I, int J, int64_t O,
                                                           const double* __restrict__ M, int Q, int64_t smq, int64_t smj,
-                                                          double* __restrict__ out, double* energy) {
+                                                          double* __restrict__ out, double* energy, double* ysq) {
     __shared__ double Ms[QM * JM];  // zero-padded to QM x JM
     __shared__ double red[8];
+    __shared__ double red_y[8];
     // MODE0 (I == 1): per-warp staging of 32 consecutive fibres (coalesced)
     __shared__ double stage[MODE0 ? 4 : 1][MODE0 ? 32 * (JM > QM ? JM : QM) + 32 : 1];  // 4 warps in MODE0
     for (int e = threadIdx.x; e < QM * JM; e += blockDim.x) {
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(256) mode_small_kernel(const double* __restric
         Ms[e] = (q < Q && j < J) ? M[q * smq + j * smj] : 0.0;
     }
     __syncthreads();
-    double en = 0.0;
+    double en = 0.0, ys = 0.0;  // residual energy, ||t||^2 (the input read once for both)
     double* enp = energy ? &en : nullptr;
     if constexpr (MODE0) {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -251,6 +252,9 @@ __global__ void __launch_bounds__(256) mode_small_kernel(const double* __restric
             double x[JM], y[QM];
 #pragma unroll
             for (int j = 0; j < JM; ++j) x[j] = (lane < nf && j < J) ? st[lane * (JM + 1) + j] : 0.0;
+            if (ysq)
+#pragma unroll
+                for (int j = 0; j < JM; ++j) ys = fma(x[j], x[j], ys);
             small_fibre<JM, QM>(x, Ms, J, y, lane < nf ? enp : nullptr);
             __syncwarp();
 #pragma unroll
@@ -273,6 +277,9 @@ __global__ void __launch_bounds__(256) mode_small_kernel(const double* __restric
             double x[JM], y[QM];
 #pragma unroll
             for (int j = 0; j < JM; ++j) x[j] = j < J ? __ldg(src + I * j) : 0.0;
+            if (ysq)
+#pragma unroll
+                for (int j = 0; j < JM; ++j) ys = fma(x[j], x[j], ys);
             small_fibre<JM, QM>(x, Ms, J, y, enp);
             double* dst = out + i + I * static_cast<int64_t>(Q) * o;
 #pragma unroll
@@ -280,15 +287,25 @@ __global__ void __launch_bounds__(256) mode_small_kernel(const double* __restric
                 if (q < Q) dst[I * q] = y[q];
         }
     }
-    if (energy) {
+    if (energy || ysq) {
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) en += __shfl_xor_sync(0xffffffffu, en, off);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = en;
+        for (int off = 16; off > 0; off >>= 1) {
+            en += __shfl_xor_sync(0xffffffffu, en, off);
+            ys += __shfl_xor_sync(0xffffffffu, ys, off);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            red[threadIdx.x >> 5] = en;
+            red_y[threadIdx.x >> 5] = ys;
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
-            double tot = 0.0;
-            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += red[w];
-            energy[blockIdx.x] = tot;
+            double tot = 0.0, toty = 0.0;
+            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+                tot += red[w];
+                toty += red_y[w];
+            }
+            if (energy) energy[blockIdx.x] = tot;
+            if (ysq) ysq[blockIdx.x] = toty;
         }
     }
 }
@@ -339,7 +356,8 @@ void launch_unfold(const double* src, int64_t inner, int64_t ext, int64_t outer,
 }
 
 int launch_mode_small(const double* t, int64_t I, int64_t J, int64_t O, const double* M, int64_t Q, int64_t smq,
-                      int64_t smj, double* out, double* energy, int num_sms, cudaStream_t s, int64_t* launches) {
+                      int64_t smj, double* out, double* energy, double* ysq, int num_sms, cudaStream_t s,
+                      int64_t* launches) {
     if (J > 32 || Q > 32) return -1;
     const bool mode0 = I == 1;
     const int64_t units = mode0 ? (O + 31) / 32 * 32 : I * O;
@@ -352,10 +370,10 @@ int launch_mode_small(const double* t, int64_t I, int64_t J, int64_t O, const do
     if (jm == JJ && qm == QQ) {                                                                                 \
         if (mode0)                                                                                              \
             mode_small_kernel<JJ, QQ, true><<<blocks, 128, 0, s>>>(t, I, static_cast<int>(J), O, M,              \
-                                                                    static_cast<int>(Q), smq, smj, out, energy); \
+                                                                    static_cast<int>(Q), smq, smj, out, energy, ysq); \
         else                                                                                                    \
             mode_small_kernel<JJ, QQ, false><<<blocks, 256, 0, s>>>(t, I, static_cast<int>(J), O, M,             \
-                                                                     static_cast<int>(Q), smq, smj, out, energy); \
+                                                                     static_cast<int>(Q), smq, smj, out, energy, ysq); \
         ++*launches;                                                                                            \
         return blocks;                                                                                          \
     }

@@ -14,9 +14,11 @@
 //            groups of 4/2/1 sharing the W fragments), N = r2 (NT <= 3
 //            tiles, compile time), K = n2, operands prefetched two k-steps
 //            ahead;
-//   phase B  M = r0 (MT <= 3 tiles, compile time), N = rt, K = r1 r2 split
-//            into kparts ranges so all warps work, B fragments loaded in
-//            chunks of 8 k-steps one chunk ahead (L2 latency), partial tiles
+//   phase B  M = r0 (MT <= 3 tiles, compile time), N = rt in pairs of
+//            n-tiles per warp (each Z fragment feeds two DMMAs), whole pairs
+//            in full rounds over the warps and the remainder split over
+//            K = r1 r2 so all warps carry equal work; B fragments loaded in
+//            chunks of 8 k-steps one chunk ahead (L2 latency); partial tiles
 //            summed in a fixed order through shared memory (deterministic).
 // The last CTA to finish (ticket counter) also reduces ||y||^2 (fused3's
 // per-CTA partials) and ||latent||^2 in a fixed order. Replaces two generic
@@ -32,7 +34,7 @@ constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kU2Pitch = 28;  // doubles: conflict-free B-fragment reads (<= 24 columns)
 constexpr int kChunk = 8;     // phase-B k-steps per prefetch chunk
-constexpr int kRedDoubles = kWarps * 3 * 64;
+constexpr int kRedDoubles = kWarps * 3 * 2 * 64;  // phase-B partial tiles (K split)
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -125,78 +127,111 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     __syncthreads();
 
     // ---- phase B: latent_s(a0, b) = Z_s(a0, j) B(j, b), M = r0, N = rt, K = R12 ----
+    // work item = a pair of n-tiles over a K range: per k-step 3 Z and 2 B
+    // fragment loads feed 2 MT DMMAs. Whole pairs are dealt to the warps in
+    // full rounds; the remaining npairs % kWarps pairs are split over K so
+    // every warp gets the same share, and their partial tiles are summed in
+    // a fixed order through shared memory (deterministic).
     const int ntB = (rt + 7) / 8;
-    const int kparts = ntB >= kWarps ? 1 : kWarps / ntB;
+    const int npairs = (ntB + 1) / 2;
+    const int full = npairs / kWarps * kWarps;
+    const int rem = npairs - full;
+    const int kparts = rem ? kWarps / rem : 1;
     const int KS = (R12 + 3) / 4;
     const int sp = (KS + kparts - 1) / kparts;
     double* out = a.latent + s * static_cast<int64_t>(r0) * rt;
     double* redbuf = U2s;
     double lsq = 0.0;
-    for (int item = warp; item < ntB * kparts; item += kWarps) {
-        const int nt = item % ntB, q = item / ntB;
-        const int ks0 = q * sp, ks1 = min(KS, ks0 + sp);
-        const int bcol = 8 * nt + g4;
-        const double* Bcol = a.B + static_cast<int64_t>(R12) * bcol;
+    auto pair_tiles = [&](int pr, int ks0, int ks1, double (&acc)[MT][2][2]) {
         const int kend = min(R12, 4 * ks1);
-        auto load = [&](int ks, double (&bv)[kChunk]) {
+        const double* Bc[2];
+        bool colok[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int bcol = 8 * (2 * pr + j) + g4;
+            colok[j] = bcol < rt;
+            Bc[j] = a.B + static_cast<int64_t>(R12) * (colok[j] ? bcol : 0);
+        }
+        auto load = [&](int ks, double (&bv)[kChunk][2]) {
 #pragma unroll
             for (int c = 0; c < kChunk; ++c) {
                 const int k = 4 * (ks + c) + t4;
-                bv[c] = (bcol < rt && k < kend) ? __ldg(Bcol + k) : 0.0;
+#pragma unroll
+                for (int j = 0; j < 2; ++j) bv[c][j] = (colok[j] && k < kend) ? __ldg(Bc[j] + k) : 0.0;
             }
         };
-        double acc[MT][2];
 #pragma unroll
-        for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
-        double bc[kChunk];
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        double bc[kChunk][2];
         load(ks0, bc);
         for (int ks = ks0; ks < ks1; ks += kChunk) {
-            double bn[kChunk];
+            double bn[kChunk][2];
             load(ks + kChunk, bn);
 #pragma unroll
             for (int c = 0; c < kChunk; ++c) {
                 if (ks + c < ks1) {  // warp-uniform
                     const int k = 4 * (ks + c) + t4;
+                    double av[MT];
 #pragma unroll
                     for (int i = 0; i < MT; ++i) {
                         const int a0 = 8 * i + g4;
-                        const double av = (a0 < r0 && k < R12) ? Zs[a0 + r0 * k] : 0.0;
-                        dmma(acc[i], av, bc[c]);
+                        av[i] = (a0 < r0 && k < R12) ? Zs[a0 + r0 * k] : 0.0;
                     }
+#pragma unroll
+                    for (int i = 0; i < MT; ++i)
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) dmma(acc[i][j], av[i], bc[c][j]);
                 }
             }
 #pragma unroll
-            for (int c = 0; c < kChunk; ++c) bc[c] = bn[c];
+            for (int c = 0; c < kChunk; ++c) {
+                bc[c][0] = bn[c][0];
+                bc[c][1] = bn[c][1];
+            }
         }
-        if (kparts == 1) {
+    };
+    for (int pr = warp; pr < full; pr += kWarps) {
+        double acc[MT][2][2];
+        pair_tiles(pr, 0, KS, acc);
 #pragma unroll
-            for (int i = 0; i < MT; ++i)
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int a0 = 8 * i + g4, b = 8 * nt + 2 * t4 + h;
+                    const int a0 = 8 * i + g4, b = 8 * (2 * pr + j) + 2 * t4 + h;
                     if (a0 < r0 && b < rt) {
-                        const double v = acc[i][h];
+                        const double v = acc[i][j][h];
                         out[a0 + static_cast<int64_t>(r0) * b] = v;
                         lsq = fma(v, v, lsq);
                     }
                 }
-        } else {
-#pragma unroll
-            for (int i = 0; i < MT; ++i) {
-                double* dst = redbuf + ((q * ntB + nt) * MT + i) * 64 + 2 * lane;
-                dst[0] = acc[i][0];
-                dst[1] = acc[i][1];
-            }
-        }
     }
-    if (kparts > 1) {
+    if (rem) {
+        if (warp < rem * kparts) {
+            const int pr = full + warp % rem, q = warp / rem;
+            double acc[MT][2][2];
+            pair_tiles(pr, q * sp, min(KS, (q + 1) * sp), acc);
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    double* dst = redbuf + (((q * rem + warp % rem) * MT + i) * 2 + j) * 64 + 2 * lane;
+                    dst[0] = acc[i][j][0];
+                    dst[1] = acc[i][j][1];
+                }
+        }
         __syncthreads();
-        for (int e = tid; e < ntB * MT * 64; e += kThreads) {
-            const int nt = e / (MT * 64), i = (e / 64) % MT, ln = (e & 63) >> 1, h = e & 1;
-            const int a0 = 8 * i + (ln >> 2), b = 8 * nt + 2 * (ln & 3) + h;
+        const int per_part = rem * MT * 2 * 64;
+        for (int e = tid; e < per_part; e += kThreads) {
+            const int tile = e / 64, ln = (e & 63) >> 1, h = e & 1;
+            const int j = tile % 2, i = (tile / 2) % MT, pr = full + tile / (2 * MT);
+            const int a0 = 8 * i + (ln >> 2), b = 8 * (2 * pr + j) + 2 * (ln & 3) + h;
             if (a0 >= r0 || b >= rt) continue;
             double v = 0.0;
-            for (int q = 0; q < kparts; ++q) v += redbuf[q * ntB * MT * 64 + e];
+            for (int q = 0; q < kparts; ++q) v += redbuf[q * per_part + e];
             out[a0 + static_cast<int64_t>(r0) * b] = v;
             lsq = fma(v, v, lsq);
         }

@@ -94,10 +94,13 @@ void launch_orthonormalize_new(const double* U, int64_t alpha, int64_t r, double
 
 // out[i, q, o] = sum_j M(q, j) t[i, j, o] with M(q, j) = M[q*smq + j*smj],
 // J, Q <= 32 (streaming, one thread per fibre). When energy != nullptr the
-// kernel also writes per-CTA partials of sum ||t_fibre - M^T (M t_fibre)||^2.
-// Returns the CTA count, or -1 when the extents are too large.
+// kernel also writes per-CTA partials of sum ||t_fibre - M^T (M t_fibre)||^2,
+// and with ysq != nullptr per-CTA partials of ||t||^2 (the input is read once
+// for all three). Both partial arrays need 8 * num_sms entries. Returns the
+// CTA count, or -1 when the extents are too large.
 int launch_mode_small(const double* t, int64_t I, int64_t J, int64_t O, const double* M, int64_t Q, int64_t smq,
-                      int64_t smj, double* out, double* energy, int num_sms, cudaStream_t s, int64_t* launches);
+                      int64_t smj, double* out, double* energy, double* ysq, int num_sms, cudaStream_t s,
+                      int64_t* launches);
 
 // Fill dst[i] = value for n entries.
 void launch_fill(double* dst, int64_t n, double value, cudaStream_t s, int64_t* launches);

@@ -195,8 +195,8 @@ DT mode_mul(Context& c, const DT& t, int mode, const double* Mp, int64_t Q, int6
     DT out = c.tensor(os);
     if (sp.J <= 16 && Q <= 16 && sp.I * sp.O >= 4096) {
         // tiny extents: streaming kernel (the MMA tiles would be mostly padding)
-        if (launch_mode_small(t.data(), sp.I, sp.J, sp.O, Mp, Q, smq, smj, out.data(), nullptr, c.num_sms, c.s,
-                              &c.launches) > 0) {
+        if (launch_mode_small(t.data(), sp.I, sp.J, sp.O, Mp, Q, smq, smj, out.data(), nullptr, nullptr, c.num_sms,
+                              c.s, &c.launches) > 0) {
             HTR_CUDA(cudaGetLastError());
             return out;
         }
@@ -667,21 +667,31 @@ Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, do
 
 namespace {
 
-DT project(Context& c, const DT& t, int mode, const Basis& b, double* energy_slot) {
+/// t x_mode U^T. With energy_slot the explicit residual energy of the step
+/// is added there; with ysq_slot ||t||^2 is written there when the streaming
+/// kernel runs (*ysq_done reports whether it did).
+DT project(Context& c, const DT& t, int mode, const Basis& b, double* energy_slot, double* ysq_slot = nullptr,
+           bool* ysq_done = nullptr) {
     if (b.alpha != t.shape[static_cast<size_t>(mode)])
         raise(HTR_ERR_INVALID_ARGUMENT, "mode_multiply: factor/extent mismatch");
     const Split sp = split_at(t.shape, mode);
-    if (energy_slot && sp.J <= 16 && b.r <= 16 && sp.I * sp.O >= 4096) {
-        // streaming projection with the explicit residual energy fused in
+    if (ysq_done) *ysq_done = false;
+    if ((energy_slot || ysq_slot) && sp.J <= 16 && b.r <= 16 && sp.I * sp.O >= 4096) {
+        // streaming projection with the explicit residual energy and/or the
+        // input's squared norm fused in
         Shape os = t.shape;
         os[static_cast<size_t>(mode)] = b.r;
         DT coeff = c.tensor(os);
-        BufPtr parts = c.alloc(8 * c.num_sms);
-        const int nb = launch_mode_small(t.data(), sp.I, sp.J, sp.O, b.p, b.r, b.alpha, 1, coeff.data(), parts->p,
-                                         c.num_sms, c.s, &c.launches);
+        BufPtr parts = energy_slot ? c.alloc(8 * c.num_sms) : nullptr;
+        BufPtr yparts = ysq_slot ? c.alloc(8 * c.num_sms) : nullptr;
+        const int nb = launch_mode_small(t.data(), sp.I, sp.J, sp.O, b.p, b.r, b.alpha, 1, coeff.data(),
+                                         parts ? parts->p : nullptr, yparts ? yparts->p : nullptr, c.num_sms, c.s,
+                                         &c.launches);
         if (nb > 0) {
-            launch_sum_partials(parts->p, nb, energy_slot, c.s, &c.launches);
+            if (parts) launch_sum_partials(parts->p, nb, energy_slot, c.s, &c.launches);
+            if (yparts) launch_sum_partials(yparts->p, nb, ysq_slot, c.s, &c.launches);
             HTR_CUDA(cudaGetLastError());
+            if (ysq_done) *ysq_done = ysq_slot != nullptr;
             return coeff;
         }
     }
@@ -926,10 +936,17 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
             }
         }
     }
+    bool ysq_fused = false;  // ||y||^2 taken during the first projection (one read of y)
     if (!leaves_done) {
         zero_scalars();
-        for (const TreeNode& n : tree.layer(p))
-            cur = project(c, cur, static_cast<int>(n.leaf_dim), basis_of(h, n.id), exact ? sc + 16 + nslots++ : nullptr);
+        bool first = true;
+        for (const TreeNode& n : tree.layer(p)) {
+            bool done = false;
+            cur = project(c, cur, static_cast<int>(n.leaf_dim), basis_of(h, n.id), exact ? sc + 16 + nslots++ : nullptr,
+                          first ? sc + 0 : nullptr, first ? &done : nullptr);
+            if (first) ysq_fused = done;
+            first = false;
+        }
     }
     for (Index l = p - 1; l >= 1 && !tail_done; --l) {
         cur.shape = layer_extents(h, l, ranks, batch, leaves_done);
@@ -943,7 +960,8 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
 
     // ||y||^2 unless the fused kernel produced it, plus ||latent||^2
     BufPtr parts = c.alloc(kReduceBlocks);
-    if (!leaves_done) {
+    const bool ysq_scanned = !leaves_done && !ysq_fused;  // sumsq also flags non-finite input
+    if (ysq_scanned) {
         launch_sumsq(y.data(), y.size(), parts->p, sc + 0, c.s, &c.launches);
     }
     BufPtr parts2 = c.alloc(kReduceBlocks);
@@ -958,7 +976,7 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
         ++c.fused_calls;
     }
     out.ysq = c.h_sc[0];
-    out.nonfinite = !leaves_done ? c.h_sc[1] != 0.0 : !std::isfinite(out.ysq);
+    out.nonfinite = ysq_scanned ? c.h_sc[1] != 0.0 : !std::isfinite(out.ysq);
     const double latsq = c.h_sc[2];
     if (exact) {
         double loss = 0.0;
@@ -967,8 +985,8 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
     } else {
         out.proj_sq = std::max(0.0, out.ysq - latsq);
     }
-    if (out.nonfinite && leaves_done) {
-        // the fused pass saw inf/nan in ||y||^2: distinguish overflow from
+    if (out.nonfinite && !ysq_scanned) {
+        // a fused pass saw inf/nan in ||y||^2: distinguish overflow from
         // non-finite input with the explicit scan
         double s = 0.0;
         bool bad = false;
