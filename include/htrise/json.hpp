@@ -121,7 +121,15 @@ public:
         write(out);
         return out;
     }
+    /// Pretty form (nlohmann's dump(indent) layout: one member per line,
+    /// "key": value, empty containers inline).
+    std::string dump(int indent) const {
+        std::string out;
+        write_pretty(out, indent, 0);
+        return out;
+    }
     void write(std::string& out) const;
+    void write_pretty(std::string& out, int indent, int level) const;
     static Value parse(const char* first, const char* last);
     static Value parse(const std::string& s) { return parse(s.data(), s.data() + s.size()); }
 
@@ -433,6 +441,36 @@ inline void Value::write(std::string& out) const {
             }
             out += '}';
         }
+    }
+}
+
+inline void Value::write_pretty(std::string& out, int indent, int level) const {
+    const std::string pad(static_cast<std::size_t>(indent * (level + 1)), ' ');
+    const std::string close(static_cast<std::size_t>(indent * level), ' ');
+    if (is_array() && !as_array().empty()) {
+        out += "[\n";
+        bool first = true;
+        for (const Value& x : as_array()) {
+            if (!first) out += ",\n";
+            first = false;
+            out += pad;
+            x.write_pretty(out, indent, level + 1);
+        }
+        out += "\n" + close + "]";
+    } else if (is_object() && !as_object().empty()) {
+        out += "{\n";
+        bool first = true;
+        for (const auto& [k, x] : as_object()) {
+            if (!first) out += ",\n";
+            first = false;
+            out += pad;
+            detail::write_string(out, k);
+            out += ": ";
+            x.write_pretty(out, indent, level + 1);
+        }
+        out += "\n" + close + "}";
+    } else {
+        write(out);
     }
 }
 

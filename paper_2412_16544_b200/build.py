@@ -98,6 +98,19 @@ def build_io_test() -> str:
     return IO_BIN
 
 
+CLI_SRC = os.path.join(PKG, "cli", "htrise_cli.cpp")
+CLI_BIN = os.path.join(PKG, "htrise")
+
+
+def build_cli() -> str:
+    """The `htrise` command-line tool (reference tools/main.cpp) over the
+    drop-in headers, next to the library it links."""
+    cmd = [CXX, "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", CUDA_INC, CLI_SRC,
+           "-L", PKG, "-lhtrise_cuda", "-Wl,-rpath,$ORIGIN", "-o", CLI_BIN]
+    subprocess.run(cmd, check=True)
+    return CLI_BIN
+
+
 def build_json_pin():
     """Compile json_pin against the image's nlohmann::json, if present."""
     if not os.path.exists(os.path.join(NLOHMANN_INC, "nlohmann", "json.hpp")):
@@ -113,3 +126,4 @@ if __name__ == "__main__":
     print(build_dropin_test())
     print(build_io_test())
     print(build_json_pin())
+    print(build_cli())

@@ -218,6 +218,195 @@ __global__ void __launch_bounds__(NT, 3) gemm_kernel(const GemmDesc d, const int
             }
 }
 
+// ---------------------------------------------------------------------------
+// Fast path for plain contractions: single-level k and n maps, one operand
+// dimension contiguous per operand, 16-byte aligned rows. 32x32 warp tiles
+// (8 fragment loads feed 16 DMMAs per k-step), 16-byte cp.async staging into
+// padded shared layouts (conflict-free fragment reads; k-contiguous operands
+// read as 16-byte (k, k+1) pairs), 3 stages of 16 k. Optional
+// per-CTA sum of squares of the stored outputs (sq_partials).
+// ---------------------------------------------------------------------------
+constexpr int FBK = 16;      // k per stage
+constexpr int FSTAGE = 3;
+// pitch of a k-contiguous row in shared memory: 16-byte fragment loads of
+// (k, k+1) pairs from 8 rows x 4 pairs hit 8 distinct 16-byte bank groups
+constexpr int FPK = FBK + 8;
+
+struct FastArgs {
+    int64_t M, N, K;
+    int64_t sam, sak, sbk, sbn;  // single-level operand strides
+    int64_t kchunk, splits;
+    double* partial;             // split-K partials or nullptr
+    double* sq_partials;         // per-CTA sum of squares of C, or nullptr
+};
+
+template <int BM, int BN, bool AK>
+__host__ __device__ constexpr int fast_a_doubles() {
+    return AK ? BM * FPK : FBK * (BM + 4);
+}
+template <int BM, int BN, bool BKF>
+__host__ __device__ constexpr int fast_b_doubles() {
+    return BKF ? BN * FPK : FBK * (BN + 4);
+}
+template <int BM, int BN, bool AK, bool BKF>
+constexpr size_t fast_smem_bytes() {
+    return sizeof(double) * FSTAGE * (fast_a_doubles<BM, BN, AK>() + fast_b_doubles<BM, BN, BKF>());
+}
+
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+
+template <int BM, int BN, bool AK, bool BKF>
+__global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, 2)
+    gemm_fast_kernel(const GemmDesc d, const FastArgs f, const Launch L) {
+    constexpr int WX = BM / 32, NTH = WX * (BN / 32) * 32;
+    constexpr int SA = fast_a_doubles<BM, BN, AK>(), SB = fast_b_doubles<BM, BN, BKF>();
+    constexpr int PAM = BM + 4, PBN = BN + 4;
+    extern __shared__ __align__(16) double fsm[];
+    double* As = fsm;                 // [FSTAGE][SA]
+    double* Bs = fsm + FSTAGE * SA;   // [FSTAGE][SB]
+    __shared__ double red[NTH / 32];
+
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    const int wm = (warp % WX) * 32, wn = (warp / WX) * 32;
+    const int64_t zb = blockIdx.z / f.splits, zs = blockIdx.z - zb * f.splits;
+    const double* A = d.A + zb * d.sab;
+    const double* B = d.B + zb * d.sbb;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
+    const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
+    const int64_t kbeg = zs * f.kchunk;
+    const int64_t kend = min(f.K, kbeg + f.kchunk);
+    const int ntiles = static_cast<int>((kend - kbeg + FBK - 1) / FBK);
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    // stage fill: every operand row / column segment is copied in 16-byte
+    // chunks (the contiguous extent is even, so a chunk is all in or all out)
+    auto issue = [&](int kt, int st) {
+        const int64_t k0 = kbeg + static_cast<int64_t>(kt) * FBK;
+        double* as = As + st * SA;
+        double* bs = Bs + st * SB;
+        if constexpr (AK) {
+#pragma unroll
+            for (int c = t; c < BM * (FBK / 2); c += NTH) {
+                const int m = c / (FBK / 2), kk = 2 * (c % (FBK / 2));
+                const bool ok = m0 + m < f.M && k0 + kk < kend;
+                cp_async16(as + m * FPK + kk, ok ? A + (m0 + m) * f.sam + (k0 + kk) : A, ok);
+            }
+        } else {
+#pragma unroll
+            for (int c = t; c < FBK * (BM / 2); c += NTH) {
+                const int kk = c / (BM / 2), m = 2 * (c % (BM / 2));
+                const bool ok = m0 + m < f.M && k0 + kk < kend;
+                cp_async16(as + kk * PAM + m, ok ? A + (k0 + kk) * f.sak + (m0 + m) : A, ok);
+            }
+        }
+        if constexpr (BKF) {
+#pragma unroll
+            for (int c = t; c < BN * (FBK / 2); c += NTH) {
+                const int n = c / (FBK / 2), kk = 2 * (c % (FBK / 2));
+                const bool ok = n0 + n < f.N && k0 + kk < kend;
+                cp_async16(bs + n * FPK + kk, ok ? B + (n0 + n) * f.sbn + (k0 + kk) : B, ok);
+            }
+        } else {
+#pragma unroll
+            for (int c = t; c < FBK * (BN / 2); c += NTH) {
+                const int kk = c / (BN / 2), n = 2 * (c % (BN / 2));
+                const bool ok = n0 + n < f.N && k0 + kk < kend;
+                cp_async16(bs + kk * PBN + n, ok ? B + (k0 + kk) * f.sbk + (n0 + n) : B, ok);
+            }
+        }
+    };
+
+#pragma unroll
+    for (int st = 0; st < FSTAGE - 1; ++st) {
+        if (st < ntiles) issue(st, st);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int kt = 0; kt < ntiles; ++kt) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(FSTAGE - 2) : "memory");
+        __syncthreads();
+        if (kt + FSTAGE - 1 < ntiles) issue(kt + FSTAGE - 1, (kt + FSTAGE - 1) % FSTAGE);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const double* as = As + (kt % FSTAGE) * SA;
+        const double* bs = Bs + (kt % FSTAGE) * SB;
+        // two k-steps per iteration; lane t4 carries k = ks + 2 t4 in the
+        // first MMA and ks + 2 t4 + 1 in the second (the same split of the k
+        // sum for A and B), so a k-contiguous operand is read as 16-byte pairs
+#pragma unroll
+        for (int ks = 0; ks < FBK; ks += 8) {
+            double a0[4], a1[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if constexpr (AK) {
+                    const double2 v = *reinterpret_cast<const double2*>(as + (wm + 8 * i + g4) * FPK + ks + 2 * t4);
+                    a0[i] = v.x;
+                    a1[i] = v.y;
+                } else {
+                    a0[i] = as[(ks + 2 * t4) * PAM + wm + 8 * i + g4];
+                    a1[i] = as[(ks + 2 * t4 + 1) * PAM + wm + 8 * i + g4];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {  // B pairs loaded per column tile: fewer live registers
+                double b0, b1;
+                if constexpr (BKF) {
+                    const double2 v = *reinterpret_cast<const double2*>(bs + (wn + 8 * j + g4) * FPK + ks + 2 * t4);
+                    b0 = v.x;
+                    b1 = v.y;
+                } else {
+                    b0 = bs[(ks + 2 * t4) * PBN + wn + 8 * j + g4];
+                    b1 = bs[(ks + 2 * t4 + 1) * PBN + wn + 8 * j + g4];
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dmma884(acc[i][j], a0[i], b0);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dmma884(acc[i][j], a1[i], b1);
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+
+    double* C = d.C + zb * d.scb;
+    double sq = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t m = m0 + wm + 8 * i + g4, n = n0 + wn + 8 * j + 2 * t4 + h;
+                if (m < f.M && n < f.N) {
+                    if (f.partial) {
+                        f.partial[(static_cast<int64_t>(blockIdx.z) * f.M + m) * f.N + n] = acc[i][j][h];
+                    } else {
+                        double* c = C + m * d.scm + n_part(L, n, d.scn1, d.scn2, d.N1);
+                        const double v = d.beta == 0.0 ? d.alpha * acc[i][j][h] : fma(d.alpha, acc[i][j][h], d.beta * *c);
+                        *c = v;
+                        sq = fma(v, v, sq);
+                    }
+                }
+            }
+    if (f.sq_partials) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) red[warp] = sq;
+        __syncthreads();
+        if (t == 0) {
+            double s2 = 0.0;
+            for (int w = 0; w < NTH / 32; ++w) s2 += red[w];
+            f.sq_partials[blockIdx.x + static_cast<int64_t>(gridDim.x) * (blockIdx.y + static_cast<int64_t>(gridDim.y) * blockIdx.z)] = s2;
+        }
+    }
+}
+
 __global__ void splitk_reduce_kernel(const GemmDesc d, const double* partial, int64_t splits, const Launch L) {
     const int64_t M = d.M, N = d.N1 * d.N2, MN = M * N, total = MN * d.batch;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -234,13 +423,52 @@ __global__ void splitk_reduce_kernel(const GemmDesc d, const double* partial, in
 struct Plan {
     int bm, bn;
     int64_t tiles_n, tiles_m, splits, kchunk;
+    bool fast = false, ak = false, bkf = false;
+    int64_t sam = 0, sak = 0, sbk = 0, sbn = 0;
 };
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+/// Single-level operand maps with one contiguous, even dimension per operand
+/// and 16-byte aligned rows: eligible for gemm_fast_kernel.
+bool fast_eligible(const GemmDesc& d, Plan& p) {
+    if (d.energy_partials) return false;
+    const int64_t M = d.M, N = d.N1 * d.N2, K = d.K1 * d.K2;
+    if (d.K2 == 1) {
+        p.sak = d.sak1;
+        p.sbk = d.sbk1;
+    } else if (d.K1 == 1) {
+        p.sak = d.sak2;
+        p.sbk = d.sbk2;
+    } else if (d.sak2 == d.K1 * d.sak1 && d.sbk2 == d.K1 * d.sbk1) {
+        p.sak = d.sak1;
+        p.sbk = d.sbk1;
+    } else {
+        return false;
+    }
+    if (d.N2 == 1) p.sbn = d.sbn1;
+    else if (d.N1 == 1) p.sbn = d.sbn2;
+    else if (d.sbn2 == d.N1 * d.sbn1) p.sbn = d.sbn1;
+    else return false;
+    p.sam = d.sam;
+    p.ak = p.sak == 1;
+    p.bkf = p.sbk == 1;
+    if (!p.ak && p.sam != 1) return false;
+    if (!p.bkf && p.sbn != 1) return false;
+    if (!aligned16(d.A) || !aligned16(d.B) || (d.batch > 1 && ((d.sab | d.sbb) & 1))) return false;
+    if (p.ak ? ((K | p.sam) & 1) : ((M | p.sak) & 1)) return false;
+    if (p.bkf ? ((K | p.sbn) & 1) : ((N | p.sbk) & 1)) return false;
+    return M < (int64_t{1} << 31) && N < (int64_t{1} << 31) && K < (int64_t{1} << 31);
+}
 
 Plan plan_for(const GemmDesc& d, int num_sms) {
     Plan p;
     const int64_t N = d.N1 * d.N2, K = d.K1 * d.K2;
-    // tile shape with the least padded area (ties: the square tile)
-    const int shapes[3][2] = {{64, 64}, {64, 32}, {32, 64}};
+    p.fast = fast_eligible(d, p);
+    // tile shape with the least padded area (ties: the first listed)
+    const int slow_shapes[3][2] = {{64, 64}, {64, 32}, {32, 64}};
+    const int fast_shapes[3][2] = {{128, 64}, {64, 128}, {64, 64}};
+    const auto& shapes = p.fast ? fast_shapes : slow_shapes;
     int64_t best = -1;
     for (const auto& sh : shapes) {
         const int64_t area = ((d.M + sh[0] - 1) / sh[0]) * sh[0] * ((N + sh[1] - 1) / sh[1]) * sh[1];
@@ -265,6 +493,33 @@ Plan plan_for(const GemmDesc& d, int num_sms) {
     return p;
 }
 
+template <int BM, int BN, bool AK, bool BKF>
+void launch_fast_t(const GemmDesc& d, const FastArgs& f, const Launch& L, dim3 grid, cudaStream_t s) {
+    constexpr size_t smem = fast_smem_bytes<BM, BN, AK, BKF>();
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(gemm_fast_kernel<BM, BN, AK, BKF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        configured = true;
+    }
+    gemm_fast_kernel<BM, BN, AK, BKF><<<grid, (BM / 32) * (BN / 32) * 32, smem, s>>>(d, f, L);
+}
+
+template <int BM, int BN>
+void launch_fast_tile(const Plan& p, const GemmDesc& d, const FastArgs& f, const Launch& L, dim3 grid,
+                      cudaStream_t s) {
+    if (p.ak && p.bkf) launch_fast_t<BM, BN, true, true>(d, f, L, grid, s);
+    else if (p.ak) launch_fast_t<BM, BN, true, false>(d, f, L, grid, s);
+    else if (p.bkf) launch_fast_t<BM, BN, false, true>(d, f, L, grid, s);
+    else launch_fast_t<BM, BN, false, false>(d, f, L, grid, s);
+}
+
+void launch_fast(const Plan& p, const GemmDesc& d, const FastArgs& f, const Launch& L, dim3 grid, cudaStream_t s) {
+    if (p.bm == 128) launch_fast_tile<128, 64>(p, d, f, L, grid, s);
+    else if (p.bn == 128) launch_fast_tile<64, 128>(p, d, f, L, grid, s);
+    else launch_fast_tile<64, 64>(p, d, f, L, grid, s);
+}
+
 }  // namespace
 
 int64_t gemm_workspace_doubles(const GemmDesc& d, int num_sms) {
@@ -272,12 +527,15 @@ int64_t gemm_workspace_doubles(const GemmDesc& d, int num_sms) {
     return p.splits > 1 ? p.splits * d.batch * d.M * d.N1 * d.N2 : 0;
 }
 
+bool gemm_is_fast(const GemmDesc& d, int num_sms) { return plan_for(d, num_sms).fast && plan_for(d, num_sms).splits == 1; }
+
 int64_t gemm_energy_partials(const GemmDesc& d, int num_sms) {
     const Plan p = plan_for(d, num_sms);
     return p.tiles_n * p.tiles_m * d.batch;
 }
 
-int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t s, int64_t* launches) {
+int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t s, int64_t* launches,
+                double* sq_partials) {
     const int64_t N = d.N1 * d.N2, K = d.K1 * d.K2;
     if (d.M <= 0 || N <= 0 || d.batch <= 0) return 0;
     if (K <= 0) return 0;  // extents are >= 1 by construction
@@ -306,6 +564,18 @@ int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t 
     const dim3 grid(static_cast<unsigned>(p.tiles_n), static_cast<unsigned>(p.tiles_m),
                     static_cast<unsigned>(p.splits * d.batch));
     double* partial = p.splits > 1 ? workspace : nullptr;
+    if (p.fast) {
+        FastArgs f{d.M, N, K, p.sam, p.sak, p.sbk, p.sbn, p.kchunk, p.splits, partial, sq_partials};
+        launch_fast(p, d, f, L, grid, s);
+        ++*launches;
+        if (p.splits > 1) {
+            const int64_t total = d.M * N * d.batch;
+            const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * num_sms));
+            splitk_reduce_kernel<<<blocks, 256, 0, s>>>(d, partial, p.splits, L);
+            ++*launches;
+        }
+        return 0;
+    }
     if (p.bm == 64 && p.bn == 64) gemm_kernel<64, 64><<<grid, NT, gemm_smem_bytes<64, 64>(), s>>>(d, p.kchunk, partial, L);
     else if (p.bm == 64) gemm_kernel<64, 32><<<grid, NT, gemm_smem_bytes<64, 32>(), s>>>(d, p.kchunk, partial, L);
     else gemm_kernel<32, 64><<<grid, NT, gemm_smem_bytes<32, 64>(), s>>>(d, p.kchunk, partial, L);

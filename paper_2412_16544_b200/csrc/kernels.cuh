@@ -45,7 +45,12 @@ struct GemmDesc {
 int64_t gemm_workspace_doubles(const GemmDesc& d, int num_sms);
 // Number of per-CTA partials the residual-energy epilogue writes.
 int64_t gemm_energy_partials(const GemmDesc& d, int num_sms);
-int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t s, int64_t* launches);
+// With sq_partials (plain-store GEMMs on the fast path only) every CTA also
+// writes the sum of squares of the outputs it stored; gemm_energy_partials()
+// entries. Callers check gemm_is_fast() first.
+int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t s, int64_t* launches,
+                double* sq_partials = nullptr);
+bool gemm_is_fast(const GemmDesc& d, int num_sms);
 
 // Sum of squares of n doubles -> out[0] (deterministic two-pass). partials
 // needs kReduceBlocks doubles. Also writes out[1] = 1.0 if any entry is

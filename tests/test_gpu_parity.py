@@ -373,6 +373,32 @@ def test_fused_skip_writes_root_slot_with_value_semantics(ht):
     assert a.accumulated == 40
 
 
+@pytest.mark.parametrize("tree_kind", ["balanced4", "1_23"])
+def test_adaptive_budget_stream_vs_oracle(ht, tree_kind):
+    """Appendix-C adaptive budget (bht.hpp:227-245, 305-310; ht_rise.hpp:
+    166-171) on the device path: per-layer budgets from the achieved error,
+    identical ranks and reconstructions to the oracle after every batch."""
+    rng = np.random.default_rng(4242 if tree_kind == "balanced4" else 4343)
+    if tree_kind == "balanced4":
+        dims, eps = [5, 6, 5, 4], 0.3
+        tree_g, tree_o = ht.DimensionTree.balanced(4), ho.DimensionTree.balanced(4)
+        batches = [ro.random_tensor(dims + [3], rng) for _ in range(5)]
+    else:
+        dims, eps = [64, 64, 24], 0.05
+        tree_g, tree_o = ht.tree_1_23(), ho.custom_tree_1_23()
+        bases = [ro.random_orthonormal(n, 5, rng) for n in dims]
+        batches = [ro.tucker_family_batch(bases, 4, rng) + 0.01 * rng.standard_normal(dims + [4]) for _ in range(4)]
+    gpu, _ = ht.bht_l2r(batches[0], tree_g, eps, adaptive_budget=True)
+    ref, _ = ho.bht_l2r(batches[0], tree_o, eps, adaptive=True)
+    compare_reps(ht, gpu, ref)
+    for b in batches[1:]:
+        gpu, ug = ht.ht_rise_update(gpu, b, adaptive_budget=True)
+        ref, ur = ho.ht_rise_update(ref, b, adaptive=True)
+        assert ug.skipped == ur.skipped
+        assert gpu.ranks() == ref.ranks()
+    compare_reps(ht, gpu, ref)
+
+
 # ---- the BASELINE configs ------------------------------------------------------
 
 def _host(t, shape):
