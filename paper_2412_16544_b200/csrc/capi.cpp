@@ -264,8 +264,14 @@ htr_status htr_decode(htr_context* ctx, const htr_rep* rep, const double* latent
         const htr::Rep& h = R(rep);
         Shape s = to_shape(latent_shape, 3);
         DT lt = input(c, latent, latent_on_device != 0, s);
+        if (out_on_device) {  // straight into the caller's buffer
+            if (!out) htr::raise(HTR_ERR_INVALID_ARGUMENT, "null output pointer");
+            htr::decode(c, h, lt, out);
+            HTR_CUDA(cudaStreamSynchronize(c.s));
+            return;
+        }
         DT full = htr::decode(c, h, lt);
-        output(c, full.data(), full.size(), out, out_on_device != 0);
+        output(c, full.data(), full.size(), out, false);
     });
 }
 
@@ -280,8 +286,14 @@ htr_status htr_reconstruct_slice(htr_context* ctx, const htr_rep* rep, int64_t m
         lt.buf = h.root->buf;
         lt.offset = h.root->r11 * h.root->r12 * (m - 1);
         lt.shape = {h.root->r11, h.root->r12, 1};
+        if (out_on_device) {
+            if (!out) htr::raise(HTR_ERR_INVALID_ARGUMENT, "null output pointer");
+            htr::decode(c, h, lt, out);
+            HTR_CUDA(cudaStreamSynchronize(c.s));
+            return;
+        }
         DT full = htr::decode(c, h, lt);
-        output(c, full.data(), full.size(), out, out_on_device != 0);
+        output(c, full.data(), full.size(), out, false);
     });
 }
 

@@ -238,6 +238,7 @@ struct FastArgs {
     int64_t kchunk, splits;
     double* partial;             // split-K partials or nullptr
     double* sq_partials;         // per-CTA sum of squares of C, or nullptr
+    int staged;                  // C is n-contiguous, rows 16-byte aligned: coalesced epilogue
 };
 
 template <int BM, int BN, bool AK>
@@ -340,8 +341,10 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, 2)
         // two k-steps per iteration; lane t4 carries k = ks + 2 t4 in the
         // first MMA and ks + 2 t4 + 1 in the second (the same split of the k
         // sum for A and B), so a k-contiguous operand is read as 16-byte pairs
+        const int64_t kleft = kend - (kbeg + static_cast<int64_t>(kt) * FBK);  // valid k in this tile
 #pragma unroll
         for (int ks = 0; ks < FBK; ks += 8) {
+            if (ks >= kleft) break;  // warp-uniform: the zero-filled tail of the last tile
             double a0[4], a1[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -376,6 +379,48 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, 2)
 
     double* C = d.C + zb * d.scb;
     double sq = 0.0;
+    if (f.staged && !f.partial) {
+        // C rows are contiguous in n and 16-byte aligned: stage the tile in
+        // shared memory and write it back in full 16-byte pairs (the direct
+        // fragment layout leaves half of every 32-byte sector unwritten)
+        constexpr int PC = BN + 2;
+        double* cs = fsm;
+        __syncthreads();  // every warp is done with the operand stages
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                double2 v;
+                v.x = acc[i][j][0];
+                v.y = acc[i][j][1];
+                *reinterpret_cast<double2*>(cs + (wm + 8 * i + g4) * PC + wn + 8 * j + 2 * t4) = v;
+            }
+        __syncthreads();
+#pragma unroll 4
+        for (int e = t; e < BM * (BN / 2); e += NTH) {
+            const int ml = e / (BN / 2), nl = 2 * (e % (BN / 2));
+            const int64_t m = m0 + ml, n = n0 + nl;
+            if (m >= f.M || n >= f.N) continue;
+            double2 v = *reinterpret_cast<const double2*>(cs + ml * PC + nl);
+            double* c = C + m * d.scm + n;
+            if (n + 1 < f.N) {
+                if (d.beta != 0.0) {
+                    const double2 o = *reinterpret_cast<const double2*>(c);
+                    v.x = fma(d.alpha, v.x, d.beta * o.x);
+                    v.y = fma(d.alpha, v.y, d.beta * o.y);
+                } else {
+                    v.x *= d.alpha;
+                    v.y *= d.alpha;
+                }
+                *reinterpret_cast<double2*>(c) = v;
+                sq = fma(v.x, v.x, fma(v.y, v.y, sq));
+            } else {
+                const double x = d.beta == 0.0 ? d.alpha * v.x : fma(d.alpha, v.x, d.beta * *c);
+                *c = x;
+                sq = fma(x, x, sq);
+            }
+        }
+    } else {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -394,6 +439,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, 2)
                     }
                 }
             }
+    }
     if (f.sq_partials) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
@@ -496,6 +542,7 @@ Plan plan_for(const GemmDesc& d, int num_sms) {
 template <int BM, int BN, bool AK, bool BKF>
 void launch_fast_t(const GemmDesc& d, const FastArgs& f, const Launch& L, dim3 grid, cudaStream_t s) {
     constexpr size_t smem = fast_smem_bytes<BM, BN, AK, BKF>();
+    static_assert(sizeof(double) * BM * (BN + 2) <= smem, "C staging tile must fit the operand stages");
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(gemm_fast_kernel<BM, BN, AK, BKF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -565,7 +612,12 @@ int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t 
                     static_cast<unsigned>(p.splits * d.batch));
     double* partial = p.splits > 1 ? workspace : nullptr;
     if (p.fast) {
-        FastArgs f{d.M, N, K, p.sam, p.sak, p.sbk, p.sbn, p.kchunk, p.splits, partial, sq_partials};
+        // coalesced epilogue: C single-level and contiguous in n, 16-byte rows
+        const bool c_flat = d.N2 == 1 || d.N1 == 1 ? true : d.scn2 == d.N1 * d.scn1;
+        const int64_t c_sn = d.N2 == 1 ? d.scn1 : (d.N1 == 1 ? d.scn2 : d.scn1);
+        const int staged = c_flat && c_sn == 1 && aligned16(d.C) && (d.scm % 2 == 0) &&
+                           (d.batch == 1 || d.scb % 2 == 0);
+        FastArgs f{d.M, N, K, p.sam, p.sak, p.sbk, p.sbn, p.kchunk, p.splits, partial, sq_partials, staged};
         launch_fast(p, d, f, L, grid, s);
         ++*launches;
         if (p.splits > 1) {

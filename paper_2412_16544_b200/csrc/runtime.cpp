@@ -188,11 +188,30 @@ Split split_at(const Shape& s, int mode) {
 }
 }  // namespace
 
-DT mode_mul(Context& c, const DT& t, int mode, const double* Mp, int64_t Q, int64_t smq, int64_t smj) {
+DT mode_mul(Context& c, const DT& t, int mode, const double* Mp, int64_t Q, int64_t smq, int64_t smj, double* dst) {
     const Split sp = split_at(t.shape, mode);
     Shape os = t.shape;
     os[static_cast<size_t>(mode)] = Q;
-    DT out = c.tensor(os);
+    DT out;
+    if (dst) {
+        out.shape = os;
+        out.buf = std::make_shared<Buf>(c.st, dst, htrise::shape_product(os));
+    } else {
+        out = c.tensor(os);
+    }
+    if (sp.I > 1 && sp.O > 1 && sp.O <= 65535) {
+        // an interior mode: one plain GEMM per outer index (the (i, o) column
+        // map is not a single stride), eligible for the fast kernel
+        GemmDesc b;
+        b.M = Q; b.N1 = sp.I; b.K1 = sp.J; b.batch = sp.O;
+        b.A = Mp; b.sam = smq; b.sak1 = smj;
+        b.B = t.data(); b.sbk1 = sp.I; b.sbn1 = 1; b.sbb = sp.I * sp.J;
+        b.C = out.data(); b.scm = sp.I; b.scn1 = 1; b.scb = sp.I * Q;
+        if (gemm_is_fast(b, c.num_sms)) {
+            run_gemm(c, b);
+            return out;
+        }
+    }
     if (sp.J <= 16 && Q <= 16 && sp.I * sp.O >= 4096) {
         // tiny extents: streaming kernel (the MMA tiles would be mostly padding)
         if (launch_mode_small(t.data(), sp.I, sp.J, sp.O, Mp, Q, smq, smj, out.data(), nullptr, nullptr, c.num_sms,
@@ -1204,48 +1223,53 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
 // decode (bht.hpp:406-456)
 // ---------------------------------------------------------------------------
 
-DT decode(Context& c, const Rep& h, const DT& latent) {
+DT decode(Context& c, const Rep& h, const DT& latent, double* dst) {
     const int64_t r11 = h.root->r11, r12 = h.root->r12;
     if (latent.shape.size() != 3 || latent.shape[0] != r11 || latent.shape[1] != r12)
         raise(HTR_ERR_INVALID_ARGUMENT, "decode: latent ranks " + htrise::shape_to_string(latent.shape) +
                                             " do not match root [" + std::to_string(r11) + "x" + std::to_string(r12) + "]");
-    struct Tag {
-        NodeId node;
-        bool open;
-        Index dim;
-    };
-    const TreeNode& rootn = h.tree.node({0, 0});
-    std::vector<Tag> tags = {{rootn.successors[0], true, -1}, {rootn.successors[1], true, -1}};
+    // The mode products of bht.hpp:406-456 act on distinct modes and commute.
+    // Transfer nodes (which do not grow the tensor) are expanded top-down
+    // first; the leaf factors, each growing its mode from r to n, follow in
+    // order of increasing growth, so every product runs on the smallest
+    // tensor it can. The last product writes into dst.
+    std::vector<NodeId> modes = {h.tree.node({0, 0}).successors[0], h.tree.node({0, 0}).successors[1]};
     DT cur = latent;
-    for (Index l = 1; l <= h.tree.depth(); ++l) {
-        for (size_t pos = 0; pos < tags.size(); ++pos) {
-            Tag& tg = tags[pos];
-            if (!tg.open || tg.node.layer != l) continue;
-            const TreeNode& n = h.tree.node(tg.node);
+    for (bool split = true; split;) {
+        split = false;
+        for (size_t pos = 0; pos < modes.size(); ++pos) {
+            const TreeNode& n = h.tree.node(modes[pos]);
+            if (n.kind != NodeKind::Transfer) continue;
             const Basis b = basis_of(h, n.id);
             // multiply mode `pos` by the basis (alpha x r): M(q, j) = B[q + alpha j]
             DT next = mode_mul(c, cur, static_cast<int>(pos), b.p, b.alpha, 1, b.alpha);
-            if (n.kind == NodeKind::Leaf) {
-                tg.open = false;
-                tg.dim = n.leaf_dim;
-                cur = next;
-            } else {
-                const Shape& cs = h.core(n.id).shape;
-                Shape split = next.shape;
-                split[pos] = cs[0];
-                split.insert(split.begin() + static_cast<std::ptrdiff_t>(pos) + 1, cs[1]);
-                next.shape = split;
-                cur = next;
-                const NodeId s0 = n.successors[0], s1 = n.successors[1];
-                tags[pos] = {s0, true, -1};
-                tags.insert(tags.begin() + static_cast<std::ptrdiff_t>(pos) + 1, Tag{s1, true, -1});
-                ++pos;
-            }
+            const Shape& cs = h.core(n.id).shape;
+            Shape sh = next.shape;
+            sh[pos] = cs[0];
+            sh.insert(sh.begin() + static_cast<std::ptrdiff_t>(pos) + 1, cs[1]);
+            next.shape = sh;
+            cur = next;
+            modes[pos] = n.successors[0];
+            modes.insert(modes.begin() + static_cast<std::ptrdiff_t>(pos) + 1, n.successors[1]);
+            split = true;
+            break;
         }
     }
-    // validate() forces in-order spans, so the modes already carry dims in order
-    for (size_t k = 0; k < tags.size(); ++k)
-        if (tags[k].dim != static_cast<Index>(k)) raise(HTR_ERR_RUNTIME, "decode: unexpected mode order");
+    // validate() forces in-order spans: mode k now carries leaf dimension k
+    for (size_t k = 0; k < modes.size(); ++k)
+        if (h.tree.node(modes[k]).leaf_dim != static_cast<Index>(k)) raise(HTR_ERR_RUNTIME, "decode: unexpected mode order");
+    std::vector<size_t> order(modes.size());
+    for (size_t k = 0; k < order.size(); ++k) order[k] = k;
+    auto growth = [&](size_t k) {
+        const Basis b = basis_of(h, modes[k]);
+        return static_cast<double>(b.alpha) / static_cast<double>(std::max<int64_t>(b.r, 1));
+    };
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return growth(a) < growth(b); });
+    for (size_t i = 0; i < order.size(); ++i) {
+        const size_t k = order[i];
+        const Basis b = basis_of(h, modes[k]);
+        cur = mode_mul(c, cur, static_cast<int>(k), b.p, b.alpha, 1, b.alpha, i + 1 == order.size() ? dst : nullptr);
+    }
     return cur;
 }
 

@@ -130,8 +130,10 @@ struct Context {
 
 // ---- building blocks -------------------------------------------------------
 void run_gemm(Context& c, const GemmDesc& d);
-/// out = t x_mode M with M(q, j) = Mp[q*smq + j*smj] (q < Q).
-DT mode_mul(Context& c, const DT& t, int mode, const double* Mp, int64_t Q, int64_t smq, int64_t smj);
+/// out = t x_mode M with M(q, j) = Mp[q*smq + j*smj] (q < Q); written to
+/// `dst` (caller memory, out.size() doubles) when given.
+DT mode_mul(Context& c, const DT& t, int mode, const double* Mp, int64_t Q, int64_t smq, int64_t smj,
+            double* dst = nullptr);
 /// Sum over the fibres of (t - U (U^T t)) along `mode`, given coeff = U^T t;
 /// result added into the device scalar `slot`.
 void residual_energy(Context& c, const DT& t, int mode, const double* U, int64_t r, const DT& coeff,
@@ -205,7 +207,8 @@ struct UpdateOut {
 };
 UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_override, bool adaptive);
 
-DT decode(Context& c, const Rep& h, const DT& latent);
+/// bht.hpp:406-456; the result lands in `dst` (caller device memory) when given.
+DT decode(Context& c, const Rep& h, const DT& latent, double* dst = nullptr);
 
 /// Append latent slices [r11, r12, N] to a representation's root (value
 /// semantics: returns the new root view).
