@@ -199,9 +199,11 @@ DT mode_mul(Context& c, const DT& t, int mode, const double* Mp, int64_t Q, int6
     } else {
         out = c.tensor(os);
     }
-    if (sp.I > 1 && sp.O > 1 && sp.O <= 65535) {
-        // an interior mode: one plain GEMM per outer index (the (i, o) column
-        // map is not a single stride), eligible for the fast kernel
+    const bool small = sp.J <= 16 && Q <= 16 && sp.I * sp.O >= 4096;
+    if (!small && Q >= 32 && sp.I > 1 && sp.O > 1 && sp.O <= 65535) {
+        // an interior mode producing >= 32 rows (decode's leaf expansions):
+        // one plain GEMM per outer index (the (i, o) column map is not a
+        // single stride), eligible for the fast kernel
         GemmDesc b;
         b.M = Q; b.N1 = sp.I; b.K1 = sp.J; b.batch = sp.O;
         b.A = Mp; b.sam = smq; b.sak1 = smj;
@@ -212,7 +214,7 @@ DT mode_mul(Context& c, const DT& t, int mode, const double* Mp, int64_t Q, int6
             return out;
         }
     }
-    if (sp.J <= 16 && Q <= 16 && sp.I * sp.O >= 4096) {
+    if (small) {
         // tiny extents: streaming kernel (the MMA tiles would be mostly padding)
         if (launch_mode_small(t.data(), sp.I, sp.J, sp.O, Mp, Q, smq, smj, out.data(), nullptr, nullptr, c.num_sms,
                               c.s, &c.launches) > 0) {
