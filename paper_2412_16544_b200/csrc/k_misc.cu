@@ -310,6 +310,185 @@ __global__ void __launch_bounds__(256) mode_small_kernel(const double* __restric
     }
 }
 
+// Two adjacent modes at once: out[i, q0, q1, o] = sum_{j0, j1} U0[j0, q0]
+// t[i, j0, j1, o] U1[j1, q1], one thread per (i, o) plane of J0 x J1
+// elements (read once, contracted in registers), plus per-CTA ||t||^2
+// partials. Extents are templated upper bounds, zero-padded in shared memory.
+template <int JM0, int JM1, int QM0, int QM1>
+__global__ void __launch_bounds__(256) pair_project_kernel(const double* __restrict__ t, int64_t I, int J0, int J1,
+                                                           int64_t O, const double* __restrict__ U0, int Q0,
+                                                           const double* __restrict__ U1, int Q1,
+                                                           double* __restrict__ out, double* ysq) {
+    __shared__ double U0s[JM0 * QM0], U1s[JM1 * QM1];  // [j][q]
+    __shared__ double red[8];
+    for (int e = threadIdx.x; e < JM0 * QM0; e += blockDim.x) {
+        const int j = e / QM0, q = e % QM0;
+        U0s[e] = (j < J0 && q < Q0) ? U0[j + static_cast<int64_t>(J0) * q] : 0.0;
+    }
+    for (int e = threadIdx.x; e < JM1 * QM1; e += blockDim.x) {
+        const int j = e / QM1, q = e % QM1;
+        U1s[e] = (j < J1 && q < Q1) ? U1[j + static_cast<int64_t>(J1) * q] : 0.0;
+    }
+    __syncthreads();
+    double ys = 0.0;
+    const int64_t planes = I * O;
+    for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; f < planes;
+         f += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t o = f / I, i = f - o * I;
+        const double* src = t + i + I * static_cast<int64_t>(J0) * J1 * o;
+        double acc[QM0][QM1];
+#pragma unroll
+        for (int a = 0; a < QM0; ++a)
+#pragma unroll
+            for (int b = 0; b < QM1; ++b) acc[a][b] = 0.0;
+#pragma unroll
+        for (int j1 = 0; j1 < JM1; ++j1) {
+            if (j1 >= J1) break;
+            double x[JM0];
+#pragma unroll
+            for (int j0 = 0; j0 < JM0; ++j0) x[j0] = j0 < J0 ? __ldg(src + I * (j0 + static_cast<int64_t>(J0) * j1)) : 0.0;
+            double tq[QM0];
+#pragma unroll
+            for (int a = 0; a < QM0; ++a) {
+                double v = 0.0;
+#pragma unroll
+                for (int j0 = 0; j0 < JM0; ++j0) v = fma(U0s[j0 * QM0 + a], x[j0], v);
+                tq[a] = v;
+            }
+#pragma unroll
+            for (int j0 = 0; j0 < JM0; ++j0) ys = fma(x[j0], x[j0], ys);
+#pragma unroll
+            for (int a = 0; a < QM0; ++a)
+#pragma unroll
+                for (int b = 0; b < QM1; ++b) acc[a][b] = fma(tq[a], U1s[j1 * QM1 + b], acc[a][b]);
+        }
+        double* dst = out + i + I * static_cast<int64_t>(Q0) * Q1 * o;
+#pragma unroll
+        for (int b = 0; b < QM1; ++b)
+#pragma unroll
+            for (int a = 0; a < QM0; ++a)
+                if (a < Q0 && b < Q1) dst[I * (a + static_cast<int64_t>(Q0) * b)] = acc[a][b];
+    }
+    if (ysq) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) ys += __shfl_xor_sync(0xffffffffu, ys, off);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ys;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += red[w];
+            ysq[blockIdx.x] = tot;
+        }
+    }
+}
+
+// pair_project for contiguous planes (I == 1): 8 lanes per plane, lane j1
+// reads column j1 (J0 contiguous doubles), so a warp streams 4 whole planes
+// (2 KB contiguous for 8x8); the column contributions are summed across the
+// 8 lanes with xor shuffles and written as one contiguous Q0*Q1 block.
+__global__ void __launch_bounds__(256) pair_project_contig_kernel(const double* __restrict__ t, int J0, int J1,
+                                                                  int64_t O, const double* __restrict__ U0, int Q0,
+                                                                  const double* __restrict__ U1, int Q1,
+                                                                  double* __restrict__ out, double* ysq) {
+    constexpr int JM = 8, QM = 4;
+    __shared__ double U0s[JM * QM], U1s[JM * QM];  // [j][q]
+    __shared__ double red[8];
+    for (int e = threadIdx.x; e < JM * QM; e += blockDim.x) {
+        const int j = e / QM, q = e % QM;
+        U0s[e] = (j < J0 && q < Q0) ? U0[j + static_cast<int64_t>(J0) * q] : 0.0;
+        U1s[e] = (j < J1 && q < Q1) ? U1[j + static_cast<int64_t>(J1) * q] : 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, j1 = lane & 7, sub = lane >> 3;
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    const int64_t wid = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t plane = static_cast<int64_t>(J0) * J1, QQ = static_cast<int64_t>(Q0) * Q1;
+    double ys = 0.0;
+    for (int64_t base = wid * 4; base < O; base += warps * 4) {
+        const int64_t f = base + sub;
+        const bool live = f < O && j1 < J1;
+        const double* src = t + f * plane + static_cast<int64_t>(J0) * j1;
+        double x[JM];
+        if (live && J0 == JM && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
+#pragma unroll
+            for (int v = 0; v < JM / 2; ++v) {
+                const double2 p2 = __ldg(reinterpret_cast<const double2*>(src) + v);
+                x[2 * v] = p2.x;
+                x[2 * v + 1] = p2.y;
+            }
+        } else {
+#pragma unroll
+            for (int j0 = 0; j0 < JM; ++j0) x[j0] = (live && j0 < J0) ? __ldg(src + j0) : 0.0;
+        }
+        double tq[QM];
+#pragma unroll
+        for (int a = 0; a < QM; ++a) {
+            double v = 0.0;
+#pragma unroll
+            for (int j0 = 0; j0 < JM; ++j0) v = fma(U0s[j0 * QM + a], x[j0], v);
+            tq[a] = v;
+        }
+#pragma unroll
+        for (int j0 = 0; j0 < JM; ++j0) ys = fma(x[j0], x[j0], ys);
+        double acc[QM * QM];
+#pragma unroll
+        for (int a = 0; a < QM; ++a)
+#pragma unroll
+            for (int b = 0; b < QM; ++b) acc[a + QM * b] = tq[a] * U1s[j1 * QM + b];
+        // butterfly reduce-scatter over the plane's 8 lanes: each step keeps
+        // half of the entries and adds the partner's copy of that half; lane
+        // j1 ends with acc entries 2*j1 and 2*j1 + 1 (8 + 4 + 2 shuffles)
+        double h8[8], h4[4], h2[2];
+        {
+            const bool up = (j1 & 4) != 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double other = __shfl_xor_sync(0xffffffffu, up ? acc[i] : acc[i + 8], 4);
+                h8[i] = (up ? acc[i + 8] : acc[i]) + other;
+            }
+        }
+        {
+            const bool up = (j1 & 2) != 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double other = __shfl_xor_sync(0xffffffffu, up ? h8[i] : h8[i + 4], 2);
+                h4[i] = (up ? h8[i + 4] : h8[i]) + other;
+            }
+        }
+        {
+            const bool up = (j1 & 1) != 0;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const double other = __shfl_xor_sync(0xffffffffu, up ? h4[i] : h4[i + 2], 1);
+                h2[i] = (up ? h4[i + 2] : h4[i]) + other;
+            }
+        }
+        if (f < O) {
+            double* dst = out + f * QQ;
+            if (Q0 == QM && Q1 == QM) {  // compact block == acc layout: one 16-byte store
+                *reinterpret_cast<double2*>(dst + 2 * j1) = make_double2(h2[0], h2[1]);
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int kk = 2 * j1 + h, a = kk % QM, b = kk / QM;
+                    if (a < Q0 && b < Q1) dst[a + Q0 * b] = h2[h];
+                }
+            }
+        }
+    }
+    if (ysq) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) ys += __shfl_xor_sync(0xffffffffu, ys, off);
+        if (lane == 0) red[threadIdx.x >> 5] = ys;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += red[w];
+            ysq[blockIdx.x] = tot;
+        }
+    }
+}
+
 int blocks_for(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4096))); }
 
 }  // namespace
@@ -383,6 +562,25 @@ int launch_mode_small(const double* t, int64_t I, int64_t J, int64_t O, const do
     HTR_SMALL(32, 4) HTR_SMALL(32, 8) HTR_SMALL(32, 16) HTR_SMALL(32, 32)
 #undef HTR_SMALL
     return -1;
+}
+
+int launch_pair_project(const double* t, int64_t I, int64_t J0, int64_t J1, int64_t O, const double* U0, int64_t Q0,
+                        const double* U1, int64_t Q1, double* out, double* ysq, int num_sms, cudaStream_t s,
+                        int64_t* launches) {
+    if (J0 > 8 || J1 > 8 || Q0 > 4 || Q1 > 4) return -1;
+    if (I == 1) {
+        const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((O + 31) / 32, 8 * num_sms)));
+        pair_project_contig_kernel<<<blocks, 256, 0, s>>>(t, static_cast<int>(J0), static_cast<int>(J1), O, U0,
+                                                          static_cast<int>(Q0), U1, static_cast<int>(Q1), out, ysq);
+        ++*launches;
+        return blocks;
+    }
+    const int64_t planes = I * O;
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((planes + 255) / 256, 8 * num_sms)));
+    pair_project_kernel<8, 8, 4, 4><<<blocks, 256, 0, s>>>(t, I, static_cast<int>(J0), static_cast<int>(J1), O, U0,
+                                                           static_cast<int>(Q0), U1, static_cast<int>(Q1), out, ysq);
+    ++*launches;
+    return blocks;
 }
 
 void launch_fill(double* dst, int64_t n, double value, cudaStream_t s, int64_t* launches) {

@@ -107,6 +107,14 @@ int launch_mode_small(const double* t, int64_t I, int64_t J, int64_t O, const do
                       int64_t smj, double* out, double* energy, double* ysq, int num_sms, cudaStream_t s,
                       int64_t* launches);
 
+// Two adjacent modes at once (t viewed as [I, J0, J1, O] -> out [I, Q0, Q1, O]):
+// out = t x_0 U0^T x_1 U1^T with U0 J0 x Q0, U1 J1 x Q1 (column-major bases),
+// J <= 8, Q <= 4; per-CTA ||t||^2 partials in ysq (8 * num_sms entries) when
+// given. Returns the CTA count, or -1 when the extents are out of range.
+int launch_pair_project(const double* t, int64_t I, int64_t J0, int64_t J1, int64_t O, const double* U0, int64_t Q0,
+                        const double* U1, int64_t Q1, double* out, double* ysq, int num_sms, cudaStream_t s,
+                        int64_t* launches);
+
 // Fill dst[i] = value for n entries.
 void launch_fill(double* dst, int64_t n, double value, cudaStream_t s, int64_t* launches);
 

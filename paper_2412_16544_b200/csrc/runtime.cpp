@@ -960,13 +960,44 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
     bool ysq_fused = false;  // ||y||^2 taken during the first projection (one read of y)
     if (!leaves_done) {
         zero_scalars();
-        bool first = true;
-        for (const TreeNode& n : tree.layer(p)) {
+        const std::vector<TreeNode>& lay = tree.layer(p);
+        for (size_t q = 0; q < lay.size();) {
+            const TreeNode& n = lay[q];
+            const int mode = static_cast<int>(n.leaf_dim);
+            const bool first = q == 0;
+            if (!exact && c.fused && q + 1 < lay.size() && lay[q + 1].kind == NodeKind::Leaf &&
+                lay[q + 1].leaf_dim == n.leaf_dim + 1) {
+                // two adjacent small leaves in one pass over the tensor
+                const Basis b0 = basis_of(h, n.id), b1 = basis_of(h, lay[q + 1].id);
+                int64_t I = 1, O = 1;
+                for (int k = 0; k < mode; ++k) I *= cur.shape[static_cast<size_t>(k)];
+                for (size_t k = static_cast<size_t>(mode) + 2; k < cur.shape.size(); ++k) O *= cur.shape[k];
+                const int64_t J0 = cur.shape[static_cast<size_t>(mode)], J1 = cur.shape[static_cast<size_t>(mode) + 1];
+                if (J0 <= 8 && J1 <= 8 && b0.r <= 4 && b1.r <= 4 && I * O >= 4096) {
+                    Shape os = cur.shape;
+                    os[static_cast<size_t>(mode)] = b0.r;
+                    os[static_cast<size_t>(mode) + 1] = b1.r;
+                    DT out = c.tensor(os);
+                    BufPtr yp = first ? c.alloc(8 * c.num_sms) : nullptr;
+                    const int nb = launch_pair_project(cur.data(), I, J0, J1, O, b0.p, b0.r, b1.p, b1.r, out.data(),
+                                                       yp ? yp->p : nullptr, c.num_sms, c.s, &c.launches);
+                    if (nb > 0) {
+                        HTR_CUDA(cudaGetLastError());
+                        if (yp) {
+                            launch_sum_partials(yp->p, nb, sc + 0, c.s, &c.launches);
+                            ysq_fused = true;
+                        }
+                        cur = out;
+                        q += 2;
+                        continue;
+                    }
+                }
+            }
             bool done = false;
-            cur = project(c, cur, static_cast<int>(n.leaf_dim), basis_of(h, n.id), exact ? sc + 16 + nslots++ : nullptr,
+            cur = project(c, cur, mode, basis_of(h, n.id), exact ? sc + 16 + nslots++ : nullptr,
                           first ? sc + 0 : nullptr, first ? &done : nullptr);
             if (first) ysq_fused = done;
-            first = false;
+            ++q;
         }
     }
     for (Index l = p - 1; l >= 1 && !tail_done; --l) {

@@ -399,6 +399,33 @@ def test_adaptive_budget_stream_vs_oracle(ht, tree_kind):
     compare_reps(ht, gpu, ref)
 
 
+@pytest.mark.parametrize("dims,ranks", [([8, 8, 8, 8], [3, 4, 2, 4]), ([7, 8, 5, 6, 8, 8, 4, 8], [2, 4, 3, 1, 4, 2, 3, 4])])
+def test_pair_projection_matches_generic(ht, dims, ranks):
+    """The fast encode projects adjacent small leaves pairwise in one pass
+    (with ||y||^2 fused into the first); it must agree with the per-mode
+    path and with the oracle's decisions."""
+    rng = np.random.default_rng(len(dims) * 100 + sum(ranks))
+    bases = [ro.random_orthonormal(n, r, rng) for n, r in zip(dims, ranks)]
+    y0 = ro.tucker_family_batch(bases, 3, rng)
+    tree = ht.DimensionTree.balanced(len(dims))
+    rep, _ = ht.bht_l2r(y0, tree, 1e-6)
+    ref, _ = ho.bht_l2r(y0, ho.DimensionTree.balanced(len(dims)), 1e-6)
+    assert rep.ranks() == ref.ranks()
+    y1 = ro.tucker_family_batch(bases, 4, rng) + 1e-3 * rng.standard_normal(dims + [4])
+    ctx = rep.ctx
+    la, pa = ht.encode(rep, y1)
+    ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+    try:
+        lb, pb = ht.encode(rep, y1)
+    finally:
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    assert np.linalg.norm(la - lb) <= 1e-12 * np.linalg.norm(lb)
+    assert abs(pa ** 2 - pb ** 2) <= 1e-12 * np.linalg.norm(y1) ** 2
+    _, ug = ht.ht_rise_update(rep, y1)
+    _, ur = ho.ht_rise_update(ref, y1)
+    assert ug.skipped == ur.skipped
+
+
 # ---- the BASELINE configs ------------------------------------------------------
 
 def _host(t, shape):
