@@ -141,13 +141,15 @@ def run_reference(args):
     world, rank, local = _dist_env()
     if rank != 0:
         return 0
+    from paper_2412_16544_b200.workloads import CONFIGS
     cb = cpu_baseline(seconds_budget=max(5.0, 4.0 * max(1, args.steps)))
     steps_ms = 8.0 * 128 ** 3 * 256 / (cb["value"] * 1e9) * 1e3
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": steps_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c5: HT-RISE skip-path update, 128^3 x 256 f64, tree (1,(2,3)), eps 1e-3",
-                       "sample": "bounded CPU sample"},
+            "config": {"workload": f"c5: {CONFIGS['c5'].description}", "batch_bytes": 8 * 128 ** 3 * 256,
+                       "samples_per_gpu": 256, "parallelism": "host threads (numpy/OpenBLAS)",
+                       "sample": "bounded CPU sample of the same workload (see cpu_baseline.sample)"},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
