@@ -379,8 +379,14 @@ void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, do
     }
     const bool in_smem = n <= kSmemMaxN;
     const size_t smem = in_smem ? 2 * sizeof(double) * static_cast<size_t>(n * n) : 0;
-    if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    // static + dynamic shared memory above 48 KB needs the opt-in (the
+    // kernel's static arrays take ~17 KB): raise the limit once to the
+    // largest in-smem problem
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(2 * sizeof(double) * kSmemMaxN * kSmemMaxN));
+        configured = true;
     }
     const int threads = n <= 32 ? 128 : (n <= 64 ? 256 : kJacobiThreads);
     jacobi_kernel<<<1, threads, smem, s>>>(G, static_cast<int>(n), lambda, V, work, in_smem ? 1 : 0);

@@ -453,6 +453,110 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, 2)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent small-K expansion: out[i + I (q + Q o)] = sum_j M(q, j)
+// t[i + I (j + J o)] with J <= 32, Q <= 128 (decode's leaf expansions,
+// r -> n). M stays resident in shared memory; each CTA walks (o, 64-wide
+// i-tile) items, double-buffering the t tiles (16-byte cp.async), computes
+// the 128 x 64 tile on DMMA (32 x 32 warp tiles, (k, k+1) pair loads of M)
+// and stores it from the fragments as 16-byte pairs (whole sectors). Two
+// CTAs per SM overlap one tile's stores with the other's MMAs.
+// ---------------------------------------------------------------------------
+constexpr int XQ = 128, XN = 64, XJ = 32, XT = 256;
+constexpr int XPA = XJ + 8;   // M row pitch ([q][j], pair loads conflict-free)
+constexpr int XPB = XN + 4;   // t tile pitch ([j][i])
+constexpr size_t expand_smem_bytes() { return sizeof(double) * (XQ * XPA + 2 * XJ * XPB); }
+
+__global__ void __launch_bounds__(XT, 2) expand_kernel(const double* __restrict__ t, int64_t I, int J, int64_t O,
+                                                       const double* __restrict__ Mp, int Q, int64_t smq,
+                                                       int64_t smj, double* __restrict__ out) {
+    extern __shared__ __align__(16) double xsm[];
+    double* As = xsm;                      // [XQ][XPA]
+    double* Bs = As + XQ * XPA;            // [2][XJ][XPB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+    const int JP = (J + 7) / 8 * 8;  // k processed in pairs of k-steps
+    for (int e = tid; e < XQ * XJ; e += XT) {
+        const int q = e / XJ, j = e % XJ;
+        As[q * XPA + j] = (q < Q && j < J) ? Mp[q * smq + j * smj] : 0.0;
+    }
+    const int64_t tiles_i = (I + XN - 1) / XN;
+    const int64_t items = tiles_i * O;
+    // zero-filled k rows beyond J stay zero in both buffers
+    for (int e = tid; e < 2 * XJ * XPB; e += XT) Bs[e] = 0.0;
+    __syncthreads();
+
+    auto issue = [&](int64_t item, int buf) {
+        const int64_t o = item / tiles_i, i0 = (item - o * tiles_i) * XN;
+        double* bs = Bs + buf * XJ * XPB;
+        const double* src = t + I * static_cast<int64_t>(J) * o + i0;
+        for (int c = tid; c < J * (XN / 2); c += XT) {
+            const int j = c / (XN / 2), ii = 2 * (c % (XN / 2));
+            const bool ok = i0 + ii < I;
+            const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(bs + j * XPB + ii));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d),
+                         "l"(ok ? src + I * j + ii : t), "r"(ok ? 16 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    int64_t item = blockIdx.x;
+    int buf = 0;
+    if (item < items) issue(item, 0);
+    for (; item < items; item += gridDim.x, buf ^= 1) {
+        const int64_t next = item + gridDim.x;
+        if (next < items) {
+            issue(next, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const double* bs = Bs + buf * XJ * XPB;
+        double acc[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int ks = 0; ks < JP; ks += 8) {
+            double a0[4], a1[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double2 v = *reinterpret_cast<const double2*>(As + (wm + 8 * i + g4) * XPA + ks + 2 * t4);
+                a0[i] = v.x;
+                a1[i] = v.y;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double b0 = bs[(ks + 2 * t4) * XPB + wn + 8 * j + g4];
+                const double b1 = bs[(ks + 2 * t4 + 1) * XPB + wn + 8 * j + g4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dmma884(acc[i][j], a0[i], b0);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dmma884(acc[i][j], a1[i], b1);
+            }
+        }
+        // 16-byte stores straight from the fragments: the 4 lanes of a row
+        // write 64 contiguous bytes (whole sectors)
+        const int64_t o = item / tiles_i, i0 = (item - o * tiles_i) * XN;
+        double* dst = out + I * static_cast<int64_t>(Q) * o + i0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int q = wm + 8 * i + g4;
+            if (q >= Q) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int ii = wn + 8 * j + 2 * t4;
+                if (i0 + ii < I)
+                    *reinterpret_cast<double2*>(dst + I * q + ii) = make_double2(acc[i][j][0], acc[i][j][1]);
+            }
+        }
+        __syncthreads();  // this B buffer is refilled next-but-one item
+    }
+}
+
 __global__ void splitk_reduce_kernel(const GemmDesc d, const double* partial, int64_t splits, const Launch L) {
     const int64_t M = d.M, N = d.N1 * d.N2, MN = M * N, total = MN * d.batch;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -579,6 +683,24 @@ bool gemm_is_fast(const GemmDesc& d, int num_sms) { return plan_for(d, num_sms).
 int64_t gemm_energy_partials(const GemmDesc& d, int num_sms) {
     const Plan p = plan_for(d, num_sms);
     return p.tiles_n * p.tiles_m * d.batch;
+}
+
+int launch_expand(const double* t, int64_t I, int64_t J, int64_t O, const double* M, int64_t Q, int64_t smq,
+                  int64_t smj, double* out, int num_sms, cudaStream_t s, int64_t* launches) {
+    // 16-byte rows: I even, aligned bases; J, Q within the resident tile
+    if (J > XJ || Q > XQ || Q < 1 || J < 1 || (I & 1) || !aligned16(t) || !aligned16(out)) return -1;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(expand_smem_bytes()));
+        configured = true;
+    }
+    const int64_t items = (I + XN - 1) / XN * O;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(items, 2 * num_sms)));
+    expand_kernel<<<grid, XT, expand_smem_bytes(), s>>>(t, I, static_cast<int>(J), O, M, static_cast<int>(Q), smq, smj,
+                                                        out);
+    ++*launches;
+    return grid;
 }
 
 int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t s, int64_t* launches,

@@ -51,6 +51,12 @@ int64_t gemm_energy_partials(const GemmDesc& d, int num_sms);
 int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t s, int64_t* launches,
                 double* sq_partials = nullptr);
 bool gemm_is_fast(const GemmDesc& d, int num_sms);
+// out[i + I (q + Q o)] = sum_j M(q, j) t[i + I (j + J o)], M(q, j) =
+// M[q*smq + j*smj]: the r -> n expansions of decode (J <= 32, Q <= 128, I
+// even, 16-byte aligned t and out). Persistent DMMA kernel with M resident
+// in shared memory. Returns the CTA count, or -1 when not applicable.
+int launch_expand(const double* t, int64_t I, int64_t J, int64_t O, const double* M, int64_t Q, int64_t smq,
+                  int64_t smj, double* out, int num_sms, cudaStream_t s, int64_t* launches);
 
 // Sum of squares of n doubles -> out[0] (deterministic two-pass). partials
 // needs kReduceBlocks doubles. Also writes out[1] = 1.0 if any entry is

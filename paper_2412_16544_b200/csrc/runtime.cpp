@@ -200,6 +200,13 @@ DT mode_mul(Context& c, const DT& t, int mode, const double* Mp, int64_t Q, int6
         out = c.tensor(os);
     }
     const bool small = sp.J <= 16 && Q <= 16 && sp.I * sp.O >= 4096;
+    if (!small && Q >= 32 && Q <= 128 && sp.J <= 32 && sp.I >= 64) {
+        // an r -> n expansion (decode): persistent kernel, factor resident
+        if (launch_expand(t.data(), sp.I, sp.J, sp.O, Mp, Q, smq, smj, out.data(), c.num_sms, c.s, &c.launches) > 0) {
+            HTR_CUDA(cudaGetLastError());
+            return out;
+        }
+    }
     if (!small && Q >= 32 && sp.I > 1 && sp.O > 1 && sp.O <= 65535) {
         // an interior mode producing >= 32 rows (decode's leaf expansions):
         // one plain GEMM per outer index (the (i, o) column map is not a
