@@ -166,23 +166,39 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
             for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
         double bc[kChunk][2];
         load(ks0, bc);
+        bool rowok[MT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) rowok[i] = 8 * i + g4 < r0;
         for (int ks = ks0; ks < ks1; ks += kChunk) {
             double bn[kChunk][2];
             load(ks + kChunk, bn);
+            if (ks + kChunk <= ks1 && 4 * (ks + kChunk) <= R12) {
+                // whole chunk in range: no per-step branch, so the Z loads of
+                // later steps can be issued ahead of earlier steps' MMAs
 #pragma unroll
-            for (int c = 0; c < kChunk; ++c) {
-                if (ks + c < ks1) {  // warp-uniform
+                for (int c = 0; c < kChunk; ++c) {
                     const int k = 4 * (ks + c) + t4;
                     double av[MT];
 #pragma unroll
-                    for (int i = 0; i < MT; ++i) {
-                        const int a0 = 8 * i + g4;
-                        av[i] = (a0 < r0 && k < R12) ? Zs[a0 + r0 * k] : 0.0;
-                    }
+                    for (int i = 0; i < MT; ++i) av[i] = rowok[i] ? Zs[8 * i + g4 + r0 * k] : 0.0;
 #pragma unroll
                     for (int i = 0; i < MT; ++i)
 #pragma unroll
                         for (int j = 0; j < 2; ++j) dmma(acc[i][j], av[i], bc[c][j]);
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < kChunk; ++c) {
+                    if (ks + c < ks1) {  // warp-uniform
+                        const int k = 4 * (ks + c) + t4;
+                        double av[MT];
+#pragma unroll
+                        for (int i = 0; i < MT; ++i) av[i] = (rowok[i] && k < R12) ? Zs[8 * i + g4 + r0 * k] : 0.0;
+#pragma unroll
+                        for (int i = 0; i < MT; ++i)
+#pragma unroll
+                            for (int j = 0; j < 2; ++j) dmma(acc[i][j], av[i], bc[c][j]);
+                    }
                 }
             }
 #pragma unroll
