@@ -137,6 +137,18 @@ def library_path() -> str:
     return _LIB_PATH
 
 
+class _Fns:
+    """Bound foreign functions of the hot calls (attribute lookups cached)."""
+
+    def __getattr__(self, name):
+        f = getattr(lib(), "htr_" + name)
+        setattr(self, name, f)
+        return f
+
+
+_fn = _Fns()
+
+
 def lib():
     """Load libhtrise_cuda.so (fails loudly: there is no fallback path)."""
     global _lib_handle
@@ -181,6 +193,7 @@ class Context:
             _raise(code, msg)
         self.device = device
         self.world = 1
+        self._update_report = _UpdateReport()
 
     def check(self, code: int):
         if code != OK:
@@ -267,7 +280,7 @@ class DeviceTensor:
     def ptr(self) -> int:
         d = self.data
         if hasattr(d, "data_ptr"):
-            if str(getattr(d, "dtype", "")) != "torch.float64":
+            if d.dtype is not _torch_f64():
                 raise ValueError("DeviceTensor: float64 storage required")
             if not d.is_contiguous():
                 raise ValueError("DeviceTensor: contiguous storage required")
@@ -290,15 +303,27 @@ def _shape_arr(shape):
     return (C.c_int64 * len(shape))(*[int(s) for s in shape])
 
 
+_torch_cache = {}
+
+
+def _torch_f64():
+    f = _torch_cache.get("f64")
+    if f is None:
+        import torch
+
+        f = _torch_cache["f64"] = torch.float64
+    return f
+
+
 def _torch_stream(t) -> int:
     """Raw handle of torch's current stream on t's device."""
-    import torch
+    raw = _torch_cache.get("raw")
+    if raw is None:
+        import torch
 
-    idx = t.device.index
-    try:
-        return int(torch._C._cuda_getCurrentRawStream(idx))
-    except AttributeError:  # private API moved: public (slower) path
-        return int(torch.cuda.current_stream(t.device).cuda_stream)
+        raw = _torch_cache["raw"] = getattr(torch._C, "_cuda_getCurrentRawStream", None) or (
+            lambda idx: torch.cuda.current_stream(idx).cuda_stream)
+    return int(raw(t.get_device()))
 
 
 def _tensor_arg(y, ctx: Optional["Context"] = None):
@@ -306,8 +331,10 @@ def _tensor_arg(y, ctx: Optional["Context"] = None):
     torch's current stream are ordered before the library's stream."""
     if isinstance(y, DeviceTensor):
         if ctx is not None and hasattr(y.data, "data_ptr"):
-            ctx.check(lib().htr_context_wait_stream(ctx.handle, C.c_void_p(_torch_stream(y.data))))
-        return C.cast(C.c_void_p(y.ptr()), _D), 1, tuple(int(s) for s in y.shape), y
+            code = _fn.context_wait_stream(ctx._h, _torch_stream(y.data))
+            if code:
+                ctx.check(code)
+        return C.cast(y.ptr(), _D), 1, tuple(map(int, y.shape)), y
     a = _as_host(y)
     if a.ndim == 0:
         a = a.reshape(1)
@@ -630,18 +657,20 @@ def ht_rise_update(h: HTRepresentation, y, epsilon_rel: Optional[float] = None, 
     ctx = h.ctx
     p, on_dev, shape, keep = _tensor_arg(y, ctx)
     out = _P()
-    rep = _UpdateReport()
+    rep = ctx._update_report  # reused: the C side overwrites every field it reports
     eps = -1.0 if epsilon_rel is None else float(epsilon_rel)
-    ctx.check(lib().htr_ht_rise_update(ctx.handle, h.handle, p, on_dev, _shape_arr(shape), len(shape), eps,
-                                       int(bool(adaptive_budget)), C.byref(out), C.byref(rep)))
+    code = _fn.ht_rise_update(ctx._h, h.handle, p, on_dev, _shape_arr(shape), len(shape), eps,
+                              1 if adaptive_budget else 0, C.byref(out), C.byref(rep))
+    if code:
+        ctx.check(code)
     del keep
-    ids = [(rep.node_layer[i], rep.node_pos[i]) for i in range(rep.n_nodes)]
-    acc = None if h._acc is None else h._acc + shape[-1] * getattr(ctx, "world", 1)
+    n = rep.n_nodes
+    ids = list(zip(rep.node_layer[:n], rep.node_pos[:n]))
+    acc = None if h._acc is None else h._acc + shape[-1] * ctx.world
     return HTRepresentation(out, ctx, h._tree, h._dims, acc, h._eps), UpdateReport(
-        bool(rep.skipped), rep.proj_error, rep.eps_des,
-        {ids[i]: int(rep.added_ranks[i]) for i in range(rep.n_nodes)},
-        {ids[i]: int(rep.new_ranks[i]) for i in range(rep.n_nodes)},
-        rep.seconds, bool(rep.used_fused_path), bool(rep.used_exact_loss), int(rep.kernel_launches))
+        bool(rep.skipped), rep.proj_error, rep.eps_des, dict(zip(ids, rep.added_ranks[:n])),
+        dict(zip(ids, rep.new_ranks[:n])), rep.seconds, bool(rep.used_fused_path), bool(rep.used_exact_loss),
+        int(rep.kernel_launches))
 
 
 def _latent_shape(h: HTRepresentation, batch: int):
