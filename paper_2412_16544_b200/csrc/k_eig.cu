@@ -14,6 +14,15 @@ namespace htr {
 namespace {
 
 constexpr int kJacobiThreads = 1024;
+
+/// Round-robin tournament (circle method): after `round` rounds player 0
+/// stays at position 0 and positions 1..m-1 have rotated right by `round`.
+__device__ __forceinline__ int tour_pos(int i, int round, int m) {
+    if (i == 0) return 0;
+    int k = (i - 1 - round) % (m - 1);
+    if (k < 0) k += m - 1;
+    return 1 + k;
+}
 constexpr int64_t kSmemMaxN = 112;  // 2 * 112^2 * 8 B = 196 KB of shared memory
 
 __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __restrict__ G, int n,
@@ -21,7 +30,6 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
                                                                 double* __restrict__ Vout, double* gwork,
                                                                 int in_smem) {
     extern __shared__ double smem[];
-    __shared__ int pos[1024];
     __shared__ double cs[512], sn[512];
     __shared__ int prs[512], qrs[512];
     __shared__ int rotated;
@@ -37,7 +45,6 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
         V[i] = r == c ? 1.0 : 0.0;
     }
     const int m = n + (n & 1);
-    for (int i = tid; i < m; i += nt) pos[i] = i;
     __syncthreads();
 
     const int half = m / 2;
@@ -47,7 +54,7 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
         for (int round = 0; round < m - 1; ++round) {
             // phase 1: rotations for the disjoint pairs of this round
             for (int i = tid; i < half; i += nt) {
-                int p = pos[i], q = pos[m - 1 - i];
+                int p = tour_pos(i, round, m), q = tour_pos(m - 1 - i, round, m);
                 if (p > q) { const int t = p; p = q; q = t; }
                 double c = 1.0, s = 0.0;
                 if (q < n) {
@@ -107,12 +114,6 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
                     A[q + static_cast<int64_t>(n) * p] = 0.0;
                 }
             }
-            // rotate the tournament positions (pos[0] fixed)
-            if (tid == 0) {
-                const int last = pos[m - 1];
-                for (int k = m - 1; k > 1; --k) pos[k] = pos[k - 1];
-                pos[1] = last;
-            }
             __syncthreads();
         }
         __syncthreads();
@@ -157,7 +158,6 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kClusterThreads)
     jacobi_cluster_kernel(const double* __restrict__ G, int n, double* __restrict__ lambda, double* __restrict__ Vout,
                           double* A, double* V) {
-    __shared__ int pos[kJacobiMaxN];
     __shared__ double cs[kJacobiMaxN / 2], sn[kJacobiMaxN / 2];
     __shared__ int prs[kJacobiMaxN / 2], qrs[kJacobiMaxN / 2];
     __shared__ int rotated;
@@ -172,7 +172,6 @@ __global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kClusterT
     }
     const int m = n + (n & 1);
     const int half = m / 2;
-    for (int i = tid; i < m; i += nt) pos[i] = i;
     cluster_sync_all();
 
     for (int sweep = 0; sweep < 40; ++sweep) {
@@ -180,7 +179,7 @@ __global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kClusterT
         __syncthreads();
         for (int round = 0; round < m - 1; ++round) {
             for (int i = tid; i < half; i += nt) {
-                int p = pos[i], q = pos[m - 1 - i];
+                int p = tour_pos(i, round, m), q = tour_pos(m - 1 - i, round, m);
                 if (p > q) { const int t = p; p = q; q = t; }
                 double c = 1.0, s = 0.0;
                 if (q < n) {
@@ -250,11 +249,6 @@ __global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kClusterT
                 const double x = *vp, y = *vq;
                 *vp = c * x - s * y;
                 *vq = s * x + c * y;
-            }
-            if (tid == 0) {
-                const int last = pos[m - 1];
-                for (int k = m - 1; k > 1; --k) pos[k] = pos[k - 1];
-                pos[1] = last;
             }
             cluster_sync_all();
         }
