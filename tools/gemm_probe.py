@@ -1,3 +1,5 @@
+"""Timing of the DMMA GEMM engine on mode-0 products (through htr_mode_multiply
+with device operands) against numpy; prints TF/s and the kernel chosen."""
 import os, sys, ctypes as C
 sys.path.insert(0, "/root/repo")
 import numpy as np, torch
@@ -12,7 +14,6 @@ for (J, O, Q) in [(400, 5120, 400), (128, 32768, 20), (400, 20480, 400)]:
     shape = (C.c_int64 * 2)(J, O)
     call = lambda: ctx.check(ht.lib().htr_mode_multiply(ctx.handle, dp(X), 1, shape, 2, 0, dp(Mt), Q, dp(out), 1))
     call(); ctx.synchronize()
-    ref = (Mt.T.reshape(Q, J) if False else None)
     # check: out(q, o) = sum_j M(q, j) X(j, o); M(q,j) = Mt_storage[q + Q j]
     Mq = Mt.reshape(-1)[: Q * J].reshape(J, Q).T          # (Q, J)
     want = (Mq @ X.T).T                                     # (O, Q) storage == canonical (Q, O)
