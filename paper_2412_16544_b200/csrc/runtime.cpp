@@ -1026,8 +1026,14 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
     BufPtr parts2 = c.alloc(kReduceBlocks);
     if (!tail_done) launch_sumsq(cur.data(), cur.size(), parts2->p, sc + 2, c.s, &c.launches);  // sc[2], sc[3]
     HTR_CUDA(cudaGetLastError());
+    if (c.nccl_comm) {
+        // the global batch count rides on the same all-reduce (slot 8)
+        c.h_sc[8] = static_cast<double>(batch);
+        HTR_CUDA(cudaMemcpyAsync(sc + 8, c.h_sc + 8, sizeof(double), cudaMemcpyHostToDevice, c.s));
+    }
     c.allreduce(sc, 16 + nslots);
     c.fetch(sc, 16 + nslots, c.h_sc);
+    out.gbatch = c.nccl_comm ? static_cast<int64_t>(std::llround(c.h_sc[8])) : batch;
     if (c.profile && leaves_done) {
         float ms = 0.f;
         HTR_CUDA(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
@@ -1133,7 +1139,7 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
     rep.proj_error = std::sqrt(enc.proj_sq);
     rep.used_fused_path = enc.fused ? 1 : 0;
     rep.used_exact_loss = enc.exact ? 1 : 0;
-    const int64_t gbatch = global_batch(c, batch);
+    const int64_t gbatch = enc.gbatch;
 
     auto finish = [&](std::shared_ptr<Rep> out) {
         RankMap nr = out->ranks();

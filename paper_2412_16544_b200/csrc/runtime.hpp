@@ -195,6 +195,7 @@ struct EncodeOut {
     bool fused = false;
     bool exact = false;
     bool nonfinite = false;
+    int64_t gbatch = 0;     // samples of this batch over all ranks (same all-reduce)
 };
 /// `latent_target`, when given, is where the fused tail writes the latent if
 /// it runs (a view of the root store's next free slices): a skip decision
