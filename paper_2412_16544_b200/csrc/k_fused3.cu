@@ -355,12 +355,12 @@ int launch_impl(const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launc
     return static_cast<int>(B);
 }
 
-template <int N>
+template <int N0, int N1>
 int dispatch_mt(int mt, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {
     switch (mt) {
-        case 1: return launch_impl<N, N, 1, 1>(a, num_sms, s, launches);
-        case 2: return launch_impl<N, N, 2, 2>(a, num_sms, s, launches);
-        case 3: return launch_impl<N, N, 3, 3>(a, num_sms, s, launches);
+        case 1: return launch_impl<N0, N1, 1, 1>(a, num_sms, s, launches);
+        case 2: return launch_impl<N0, N1, 2, 2>(a, num_sms, s, launches);
+        case 3: return launch_impl<N0, N1, 3, 3>(a, num_sms, s, launches);
         default: return -1;
     }
 }
@@ -369,7 +369,7 @@ int dispatch_mt(int mt, const Fused3Args& a, int num_sms, cudaStream_t s, int64_
 
 bool fused3_supported(int64_t n0, int64_t n1, int64_t n2, int r0, int r1, int r2) {
     (void)n2;
-    if (n0 != n1 || (n0 != 64 && n0 != 128)) return false;
+    if ((n0 != 64 && n0 != 128) || (n1 != 64 && n1 != 128)) return false;
     if (r0 < 1 || r1 < 1 || r2 < 1 || r0 > 24 || r1 > 24) return false;
     return true;
 }
@@ -385,10 +385,11 @@ int64_t fused3_workspace_doubles(int64_t n0, int64_t n1, int64_t n2, int64_t S, 
 }
 
 int launch_fused3(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {
-    (void)n1;
     const int mt = (std::max(a.r0, a.r1) + 7) / 8;
-    if (n0 == 128) return dispatch_mt<128>(mt, a, num_sms, s, launches);
-    if (n0 == 64) return dispatch_mt<64>(mt, a, num_sms, s, launches);
+    if (n0 == 128 && n1 == 128) return dispatch_mt<128, 128>(mt, a, num_sms, s, launches);
+    if (n0 == 64 && n1 == 64) return dispatch_mt<64, 64>(mt, a, num_sms, s, launches);
+    if (n0 == 128 && n1 == 64) return dispatch_mt<128, 64>(mt, a, num_sms, s, launches);
+    if (n0 == 64 && n1 == 128) return dispatch_mt<64, 128>(mt, a, num_sms, s, launches);
     return -1;
 }
 

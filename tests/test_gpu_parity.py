@@ -304,18 +304,20 @@ def test_fused_path_matches_generic(ht):
         assert upd.used_fused_path
 
 
-@pytest.mark.parametrize("ranks,n2,nsamp", [
-    ((3, 5, 7), 64, 4),      # one tile everywhere, rt = 12: two column tiles, K split in 4
-    ((9, 9, 2), 37, 12),     # ragged n2, NT = 1
-    ((17, 6, 24), 64, 3),    # MT = 3, NT = 3
-    ((24, 12, 9), 50, 10),   # rt > 64: no K split
-    ((20, 20, 20), 64, 6),   # the c5 shape
+@pytest.mark.parametrize("ranks,n2,nsamp,n01", [
+    ((3, 5, 7), 64, 4, (64, 64)),      # one tile everywhere, rt = 12: two column tiles, K split in 4
+    ((9, 9, 2), 37, 12, (64, 64)),     # ragged n2, NT = 1
+    ((17, 6, 24), 64, 3, (64, 64)),    # MT = 3, NT = 3
+    ((24, 12, 9), 50, 10, (64, 64)),   # rt > 64: no K split
+    ((20, 20, 20), 64, 6, (64, 64)),   # the c5 shape
+    ((7, 11, 5), 24, 5, (128, 64)),    # mixed slab extents
+    ((12, 4, 9), 33, 6, (64, 128)),
 ])
-def test_fused_tail_tile_cases(ht, ranks, n2, nsamp):
+def test_fused_tail_tile_cases(ht, ranks, n2, nsamp, n01):
     """fused3 + tail3 (skip-path encode) against the generic GEMM chain across
     the tail kernel's compile-time tile counts and its K-split reduction."""
     rng = np.random.default_rng(sum(ranks) * 1000 + n2)
-    bases = [ro.random_orthonormal(n, r, rng) for n, r in zip((64, 64, n2), ranks)]
+    bases = [ro.random_orthonormal(n, r, rng) for n, r in zip((n01[0], n01[1], n2), ranks)]
     y0 = ro.tucker_family_batch(bases, nsamp, rng)
     rep, _ = ht.bht_l2r(y0, ht.tree_1_23(), 1e-9)
     ref, _ = ho.bht_l2r(y0, ho.custom_tree_1_23(), 1e-9)
@@ -343,6 +345,7 @@ def test_fused_tail_tile_cases(ht, ranks, n2, nsamp):
     r2, ur = ho.ht_rise_update(ref, y1)
     assert upd.skipped == ur.skipped
     assert upd.skipped == upd.used_exact_loss
+    assert upd.used_exact_loss or upd.used_fused_path  # the fused kernels ran
     assert g2.ranks() == r2.ranks()
 
 
