@@ -429,6 +429,25 @@ def test_pair_projection_matches_generic(ht, dims, ranks):
     assert ug.skipped == ur.skipped
 
 
+def test_fused_path_rejects_non_finite_input(ht):
+    """A NaN / Inf in the batch shows up in the fused kernel's ||y||^2; the
+    runtime re-scans and raises like the reference (bht.hpp:189-211)."""
+    rng = np.random.default_rng(8)
+    bases = [ro.random_orthonormal(64, 4, rng) for _ in range(3)]
+    rep, _ = ht.bht_l2r(ro.tucker_family_batch(bases, 3, rng), ht.tree_1_23(), 1e-3)
+    for bad in (np.nan, np.inf):
+        y = ro.tucker_family_batch(bases, 3, rng)
+        y[5, 7, 9, 1] = bad
+        with pytest.raises(ValueError):
+            ht.ht_rise_update(rep, y)
+        with pytest.raises(ValueError):
+            ht.bht_l2r(y, ht.tree_1_23(), 1e-3)
+    # a huge but finite batch (||y||^2 overflows) is accepted
+    y = ro.tucker_family_batch(bases, 3, rng) * 1e160
+    _, upd = ht.ht_rise_update(rep, y)
+    assert np.isfinite(upd.eps_des) or upd.eps_des == np.inf
+
+
 # ---- the BASELINE configs ------------------------------------------------------
 
 def _host(t, shape):
