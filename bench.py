@@ -2,11 +2,14 @@
 """HT-RISE update throughput on B200 (BASELINE.json metric: GB/s of streamed
 tensor data, with the fused kernel's HBM roofline fraction).
 
-One step = one ht_rise_update of a config-5 batch (128^3 x 256 f64 = 4.295 GB,
+One step = one HT-RISE update of a config-5 batch (128^3 x 256 f64 = 4.295 GB,
 tree (1,(2,3)), eps 1e-3) through libhtrise_cuda.so. The stream is first
 seeded with BHT-l2r on batch 0 (untimed, like the reference's CLI); steps then
 cycle through distinct pre-generated batches that are resident in HBM (each
-4.3 GB >> the 126 MB L2, so no flush is needed).
+4.3 GB >> the 126 MB L2, so no flush is needed). The headline times the K
+steps as one stream (ht_rise_update_many: the reference CLI's loop over
+batches, with batch i+1's encode queued before batch i's decision is read
+back); "per_call" times the same K steps as K ht_rise_update calls.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -194,7 +197,7 @@ def run_ours(args):
     pool_n = max(2, min(args.pool, args.steps + args.warmup))
     pool = [w.make_batch(1 + i, "cuda", batch=n_local, sample_offset=off) for i in range(pool_n)]
     torch.cuda.synchronize()
-    rep.reserve((2 + args.steps * 2 + args.warmup + 4) * n_local)
+    rep.reserve((2 + args.steps * 3 + args.warmup * 2 + 4) * n_local)
 
     def barrier():
         if dist is not None:
@@ -224,15 +227,44 @@ def run_ours(args):
         e1.synchronize()
     torch.cuda.synchronize()
     barrier()
+    call_launches = ctx.launch_count() - launches0
+    call_ms = e0.elapsed_time(e1) / args.steps
+    ctx.set_option(ht.OPT_PROFILE_EVENTS, 0)
+
+    # the same K batches as one stream (ht_rise_update_many: batch i+1's
+    # encode is queued before batch i's skip decision is read back, so the
+    # device does not idle across the host round trip of each decision)
+    def batches(k0, k):
+        return [ht.DeviceTensor(pool[(k0 + i) % pool_n], shape) for i in range(k)]
+
+    vals, _ = ht.ht_rise_update_many(rep, batches(0, args.warmup))
+    rep = vals[-1]
+    ctx.synchronize()
+    ctx.set_option(ht.OPT_PROFILE_EVENTS, 1)
+    ctx.reset_timing()
+    launches0 = ctx.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks2:
+        e0.record(stream)
+        vals, reports = ht.ht_rise_update_many(rep, batches(args.warmup, args.steps))
+        e1.record(stream)
+        e1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    rep = vals[-1]
+    stream_skipped = sum(int(u.skipped) for u in reports)
+    stream_fused = sum(int(u.used_fused_path) for u in reports)
     launches = ctx.launch_count() - launches0
     ms = e0.elapsed_time(e1) / args.steps
     fused_ms, fused_calls, _, _ = ctx.kernel_timing()
     ctx.set_option(ht.OPT_PROFILE_EVENTS, 0)
     if dist is not None:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms, call_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms, call_ms = float(t[0].item()), float(t[1].item())
     value = global_bytes / (ms * 1e-3) / 1e9
+    call_value = global_bytes / (call_ms * 1e-3) / 1e9
 
     # end to end through the public API: pinned host batch -> H2D -> update
     e2e = None
@@ -314,9 +346,13 @@ def run_ours(args):
                 "config": {"workload": f"{args.config}: {w.description}", "batch_bytes": global_bytes,
                            "samples_per_gpu": n_local, "parallelism": f"batch-shard x{world}",
                            "l2": "inputs 4.3 GB/step >> 126 MB L2 (no flush needed)",
-                           "distinct_batches": pool_n, "skipped_updates": skipped, "fused_path_updates": fused_used},
+                           "distinct_batches": pool_n, "api": "ht_rise_update_many (K batches, one stream)",
+                           "skipped_updates": stream_skipped, "fused_path_updates": stream_fused},
+                "per_call": {"api": "ht_rise_update, one call per batch (host round trip per decision)",
+                             "value": call_value, "ms_per_step": call_ms, "skipped_updates": skipped,
+                             "fused_path_updates": fused_used, "gpu_launches": int(call_launches)},
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clocks.summary()}
+                "clocks": clocks2.summary(), "clocks_per_call": clocks.summary()}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

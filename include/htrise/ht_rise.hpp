@@ -13,6 +13,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "htrise/bht.hpp"
 #include "htrise/device.hpp"
@@ -94,6 +95,46 @@ inline std::pair<HTRepresentation, UpdateReport> ht_rise_update(const HTRepresen
         r.new_ranks[id] = rep.new_ranks[i];
     }
     return {HTRepresentation::from_device(device::wrap(out)), std::move(r)};
+}
+
+/// Extension (not in the reference): ht_rise_update over a sequence of
+/// batches, each applied to the previous result, as the reference's CLI loop
+/// does (tools/main.cpp:225-243). Results are identical to the loop; the
+/// library queues batch i+1's skip-path encode before batch i's decision is
+/// read back. Returns the value and report after each batch.
+inline std::vector<std::pair<HTRepresentation, UpdateReport>> ht_rise_update_many(
+    const HTRepresentation& h, const std::vector<DenseTensor>& ys, const UpdateOptions& opts = {}) {
+    std::vector<std::pair<HTRepresentation, UpdateReport>> res;
+    if (ys.empty()) return res;
+    const int32_t order = static_cast<int32_t>(ys.front().order());
+    std::vector<const double*> ptrs;
+    std::vector<int64_t> shapes;
+    for (const DenseTensor& y : ys) {
+        if (static_cast<int32_t>(y.order()) != order)
+            throw std::invalid_argument("ht_rise_update_many: batches of different tensor order");
+        ptrs.push_back(y.data());
+        shapes.insert(shapes.end(), y.shape().begin(), y.shape().end());
+    }
+    std::vector<htr_rep*> outs(ys.size(), nullptr);
+    std::vector<htr_update_report> reps(ys.size());
+    device::check(htr_ht_rise_update_many(device::ctx(), h.device_handle(), static_cast<int64_t>(ys.size()),
+                                          ptrs.data(), 0, shapes.data(), order, opts.epsilon_rel.value_or(-1.0),
+                                          opts.adaptive_budget ? 1 : 0, outs.data(), reps.data()));
+    for (size_t i = 0; i < ys.size(); ++i) {
+        const htr_update_report& rep = reps[i];
+        UpdateReport r;
+        r.skipped = rep.skipped != 0;
+        r.proj_error = rep.proj_error;
+        r.eps_des = rep.eps_des;
+        r.seconds = rep.seconds;
+        for (int k = 0; k < rep.n_nodes; ++k) {
+            const NodeId id{rep.node_layer[k], rep.node_pos[k]};
+            r.added_ranks[id] = rep.added_ranks[k];
+            r.new_ranks[id] = rep.new_ranks[k];
+        }
+        res.emplace_back(HTRepresentation::from_device(device::wrap(outs[i])), std::move(r));
+    }
+    return res;
 }
 
 }  // namespace htrise

@@ -144,6 +144,21 @@ HTR_API htr_status htr_ht_rise_update(htr_context* ctx, const htr_rep* in, const
                               const int64_t* shape, int32_t order, double eps_rel_override,
                               int32_t adaptive_budget, htr_rep** out, htr_update_report* report);
 
+/* A stream of n updates (extension; the reference's caller loops
+ * ht_rise_update over batches, tools/main.cpp:225-243): identical to n
+ * htr_ht_rise_update calls each applied to the previous result, with the
+ * skip-path encode of batch i+1 queued on the device before batch i's skip
+ * decision is read back (a skip leaves the bases unchanged; after an
+ * expansion the speculative work is discarded and batch i+1 re-runs).
+ * ys[i] is batch i (all on the device or all on the host), shapes holds
+ * n * order extents. On success outs[i] / reports[i] hold the value and the
+ * report after batch i (free each value with htr_rep_free); on failure no
+ * output is set. */
+HTR_API htr_status htr_ht_rise_update_many(htr_context* ctx, const htr_rep* in, int64_t n, const double* const* ys,
+                                   int32_t y_on_device, const int64_t* shapes, int32_t order,
+                                   double eps_rel_override, int32_t adaptive_budget, htr_rep** outs,
+                                   htr_update_report* reports);
+
 /* ---- encode / decode / reconstruct (bht.hpp:373-479) ----------------- */
 /* latent is r11 x r12 x N (canonical). */
 HTR_API htr_status htr_encode(htr_context* ctx, const htr_rep* rep, const double* y, int32_t y_on_device,

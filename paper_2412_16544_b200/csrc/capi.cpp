@@ -241,6 +241,27 @@ htr_status htr_ht_rise_update(htr_context* ctx, const htr_rep* in, const double*
     });
 }
 
+htr_status htr_ht_rise_update_many(htr_context* ctx, const htr_rep* in, int64_t n, const double* const* ys,
+                                   int32_t y_on_device, const int64_t* shapes, int32_t order, double eps_rel_override,
+                                   int32_t adaptive_budget, htr_rep** outs, htr_update_report* reports) {
+    return guarded(ctx, [&] {
+        htr::Context& c = C(ctx);
+        if (n < 0) htr::raise(HTR_ERR_INVALID_ARGUMENT, "ht_rise_update_many: negative batch count");
+        if (n > 0 && (!ys || !shapes || !outs)) htr::raise(HTR_ERR_INVALID_ARGUMENT, "ht_rise_update_many: null argument");
+        auto batch_of = [&](int64_t i) {
+            Shape s = to_shape(shapes + i * order, order);
+            return input(c, ys[i], y_on_device != 0, s);
+        };
+        (void)R(in);
+        std::vector<htr::UpdateOut> us =
+            htr::ht_rise_update_many(c, in->rep, n, batch_of, eps_rel_override, adaptive_budget != 0);
+        for (int64_t i = 0; i < n; ++i) {
+            if (reports) reports[i] = us[static_cast<size_t>(i)].report;
+            outs[i] = new htr_rep{us[static_cast<size_t>(i)].rep};
+        }
+    });
+}
+
 htr_status htr_encode(htr_context* ctx, const htr_rep* rep, const double* y, int32_t y_on_device, const int64_t* shape,
                       int32_t order, double* latent, int32_t latent_on_device, double* proj_error) {
     return guarded(ctx, [&] {

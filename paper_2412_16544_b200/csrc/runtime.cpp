@@ -867,6 +867,88 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
 // encode (bht.hpp:373-401)
 // ---------------------------------------------------------------------------
 
+namespace {
+
+struct Tree3 {
+    NodeId leaf_of[3];
+    int r0 = 0, r1 = 0, r2 = 0, rt = 0;
+    bool tree_123 = false;  // (1,(2,3)): layer 1 = [leaf d0, transfer(d1,d2)]
+};
+
+Tree3 tree3_ranks(const Rep& h, const RankMap& ranks) {
+    const DimensionTree& tree = h.tree;
+    Tree3 t;
+    for (Index l = 1; l <= tree.depth(); ++l)
+        for (const TreeNode& n : tree.layer(l))
+            if (n.kind == NodeKind::Leaf) t.leaf_of[n.leaf_dim] = n.id;
+    t.r0 = static_cast<int>(ranks.at(t.leaf_of[0]));
+    t.r1 = static_cast<int>(ranks.at(t.leaf_of[1]));
+    t.r2 = static_cast<int>(ranks.at(t.leaf_of[2]));
+    t.tree_123 = tree.depth() == 2 && tree.layer(1)[0].kind == NodeKind::Leaf &&
+                 tree.layer(1)[1].kind == NodeKind::Transfer;
+    t.rt = t.tree_123 ? static_cast<int>(ranks.at(NodeId{1, 1})) : 0;
+    return t;
+}
+
+}  // namespace
+
+bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc, DT* latent,
+                         cudaEvent_t ev0, cudaEvent_t ev1) {
+    if (h.tree.dims() != 3 || h.tree.depth() != 2) return false;
+    const Tree3 t = tree3_ranks(h, h.ranks());
+    const int64_t batch = y.shape[3];
+    if (!t.tree_123 || !tail3_supported(t.r0, t.r1, t.r2, t.rt, y.shape[2]) ||
+        !fused3_supported(y.shape[0], y.shape[1], y.shape[2], t.r0, t.r1, t.r2))
+        return false;
+    Fused3Args fa;
+    fa.Y = y.data();
+    fa.n2 = y.shape[2];
+    fa.S = batch;
+    fa.U0 = h.core(t.leaf_of[0]).data();
+    fa.U1 = h.core(t.leaf_of[1]).data();
+    fa.U2 = h.core(t.leaf_of[2]).data();
+    fa.r0 = t.r0;
+    fa.r1 = t.r1;
+    fa.r2 = t.r2;
+    fa.slab_gemm = false;
+    const int64_t ws = fused3_workspace_doubles(y.shape[0], y.shape[1], fa.n2, batch, t.r0, t.r1, t.r2, c.num_sms);
+    BufPtr w = c.alloc(ws);  // freed stream-ordered after the kernels below
+    fa.wslab = w->p;
+    fa.ysq_partials = w->p + fa.n2 * batch * static_cast<int64_t>(t.r0) * t.r1;
+    if (ev0) HTR_CUDA(cudaEventRecord(ev0, c.s));
+    const int grid = launch_fused3(y.shape[0], y.shape[1], fa, c.num_sms, c.s, &c.launches);
+    if (ev1) HTR_CUDA(cudaEventRecord(ev1, c.s));
+    HTR_CUDA(cudaGetLastError());
+    if (grid <= 0) return false;  // no tensor map for this pointer: nothing was launched
+    Tail3Args ta;
+    ta.wslab = fa.wslab;
+    ta.U2 = fa.U2;
+    ta.B = h.core(NodeId{1, 1}).data();
+    ta.r0 = t.r0;
+    ta.r1 = t.r1;
+    ta.r2 = t.r2;
+    ta.rt = t.rt;
+    ta.n2 = fa.n2;
+    ta.S = batch;
+    DT lat;
+    if (latent_target && latent_target->shape == Shape{t.r0, t.rt, batch}) {
+        lat = *latent_target;
+    } else {
+        lat = c.tensor({t.r0, t.rt, batch});
+    }
+    ta.latent = lat.data();
+    BufPtr lsq = c.alloc(batch);
+    ta.latsq = lsq->p;
+    ta.ysq_partials = fa.ysq_partials;
+    ta.n_ysq = grid;
+    ta.out = sc;
+    ta.ticket = c.d_ticket;
+    launch_tail3(ta, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+    *latent = lat;
+    return true;
+}
+
 EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* latent_target) {
     const DimensionTree& tree = h.tree;
     const Index d = tree.dims(), p = tree.depth();
@@ -888,77 +970,43 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
     bool leaves_done = false;
     bool tail_done = false;  // latent and ||latent||^2 already produced
     if (!exact && c.fused && d == 3) {
-        NodeId leaf_of[3];
-        for (Index l = 1; l <= p; ++l)
-            for (const TreeNode& n : tree.layer(l))
-                if (n.kind == NodeKind::Leaf) leaf_of[n.leaf_dim] = n.id;
-        const int r0 = static_cast<int>(ranks.at(leaf_of[0])), r1 = static_cast<int>(ranks.at(leaf_of[1])),
-                  r2 = static_cast<int>(ranks.at(leaf_of[2]));
-        // (1,(2,3)) tree: layer 1 = [leaf d0, transfer(d1,d2)], layer 2 = [leaf d1, leaf d2]
-        const bool tree_123 = p == 2 && tree.layer(1)[0].kind == NodeKind::Leaf &&
-                              tree.layer(1)[1].kind == NodeKind::Transfer;
-        const int rt = tree_123 ? static_cast<int>(ranks.at(NodeId{1, 1})) : 0;
-        const bool use_tail = tree_123 && tail3_supported(r0, r1, r2, rt, y.shape[2]);
-        const bool fused_ok = fused3_supported(y.shape[0], y.shape[1], y.shape[2], r0, r1, r2);
-        if (!(fused_ok && use_tail)) zero_scalars();
-        if (fused_ok) {
-            Fused3Args fa;
-            fa.Y = y.data();
-            fa.n2 = y.shape[2];
-            fa.S = batch;
-            fa.U0 = h.core(leaf_of[0]).data();
-            fa.U1 = h.core(leaf_of[1]).data();
-            fa.U2 = h.core(leaf_of[2]).data();
-            fa.r0 = r0;
-            fa.r1 = r1;
-            fa.r2 = r2;
-            DT Z;
-            if (!use_tail) {
-                Z = c.tensor({r0, r1, r2, batch});
+        DT lat;
+        if (launch_skip_encode3(c, h, y, latent_target, sc, &lat, c.profile ? c.ev[0] : nullptr,
+                                c.profile ? c.ev[1] : nullptr)) {
+            // fused leaves + tail: ((1,(2,3)) trees)
+            leaves_done = tail_done = out.fused = true;
+            cur = lat;
+        } else {
+            const Tree3 t = tree3_ranks(h, ranks);
+            zero_scalars();
+            if (fused3_supported(y.shape[0], y.shape[1], y.shape[2], t.r0, t.r1, t.r2)) {
+                // fused leaves, slab-axis GEMM, then the generic interior projections
+                Fused3Args fa;
+                fa.Y = y.data();
+                fa.n2 = y.shape[2];
+                fa.S = batch;
+                fa.U0 = h.core(t.leaf_of[0]).data();
+                fa.U1 = h.core(t.leaf_of[1]).data();
+                fa.U2 = h.core(t.leaf_of[2]).data();
+                fa.r0 = t.r0;
+                fa.r1 = t.r1;
+                fa.r2 = t.r2;
+                DT Z = c.tensor({t.r0, t.r1, t.r2, batch});
                 fa.Z = Z.data();
-            }
-            fa.slab_gemm = !use_tail;
-            const int64_t ws = fused3_workspace_doubles(y.shape[0], y.shape[1], fa.n2, batch, r0, r1, r2, c.num_sms);
-            BufPtr w = c.alloc(ws);
-            fa.wslab = w->p;
-            fa.ysq_partials = w->p + fa.n2 * batch * static_cast<int64_t>(r0) * r1;
-            if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[0], c.s));
-            const int grid = launch_fused3(y.shape[0], y.shape[1], fa, c.num_sms, c.s, &c.launches);
-            if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[1], c.s));
-            HTR_CUDA(cudaGetLastError());
-            if (grid > 0) {  // else (no tensor map for this pointer): generic kernels below
-                if (!use_tail) launch_sum_partials(fa.ysq_partials, grid, sc + 0, c.s, &c.launches);
-                leaves_done = true;
-                out.fused = true;
-                if (use_tail) {
-                    Tail3Args ta;
-                    ta.wslab = fa.wslab;
-                    ta.U2 = fa.U2;
-                    ta.B = h.core(NodeId{1, 1}).data();
-                    ta.r0 = r0;
-                    ta.r1 = r1;
-                    ta.r2 = r2;
-                    ta.rt = rt;
-                    ta.n2 = fa.n2;
-                    ta.S = batch;
-                    DT lat;
-                    if (latent_target && latent_target->shape == Shape{r0, rt, batch}) {
-                        lat = *latent_target;
-                    } else {
-                        lat = c.tensor({r0, rt, batch});
-                    }
-                    ta.latent = lat.data();
-                    BufPtr lsq = c.alloc(batch);
-                    ta.latsq = lsq->p;
-                    ta.ysq_partials = fa.ysq_partials;
-                    ta.n_ysq = grid;
-                    ta.out = sc;
-                    ta.ticket = c.d_ticket;
-                    launch_tail3(ta, c.s, &c.launches);
-                    HTR_CUDA(cudaGetLastError());
-                    cur = lat;
-                    tail_done = true;
-                } else {
+                fa.slab_gemm = true;
+                const int64_t ws =
+                    fused3_workspace_doubles(y.shape[0], y.shape[1], fa.n2, batch, t.r0, t.r1, t.r2, c.num_sms);
+                BufPtr w = c.alloc(ws);
+                fa.wslab = w->p;
+                fa.ysq_partials = w->p + fa.n2 * batch * static_cast<int64_t>(t.r0) * t.r1;
+                if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[0], c.s));
+                const int grid = launch_fused3(y.shape[0], y.shape[1], fa, c.num_sms, c.s, &c.launches);
+                if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[1], c.s));
+                HTR_CUDA(cudaGetLastError());
+                if (grid > 0) {  // else (no tensor map for this pointer): generic kernels below
+                    launch_sum_partials(fa.ysq_partials, grid, sc + 0, c.s, &c.launches);
+                    leaves_done = true;
+                    out.fused = true;
                     cur = Z;
                 }
             }
@@ -1264,6 +1312,173 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
     }
     return finish(out);
 }
+
+// ---------------------------------------------------------------------------
+// stream of updates (extension; the reference's CLI loops ht_rise_update over
+// batches, main.cpp:225-243): skip-path encodes pipelined one batch ahead
+// ---------------------------------------------------------------------------
+
+std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep>& h0, int64_t n,
+                                           const std::function<DT(int64_t)>& batch_of, double eps_override,
+                                           bool adaptive) {
+    std::vector<UpdateOut> res;
+    res.reserve(static_cast<size_t>(std::max<int64_t>(n, 0)));
+    std::shared_ptr<Rep> cur = h0;
+    const Index d = h0->tree.dims();
+    // one launched-but-undecided skip-path encode
+    struct Slot {
+        int64_t index = -1;
+        DT y, latent;
+        BufPtr dsc;       // [0] ||y||^2, [1] batch count (sharded), [2] ||latent||^2
+        double* host = nullptr;  // pinned copy of dsc[0..2]
+        cudaEvent_t done = nullptr, t0 = nullptr, t1 = nullptr;
+        int64_t launches = 0;
+        std::chrono::steady_clock::time_point started;
+    };
+    Slot slots[2];
+    for (int k = 0; k < 2; ++k) {
+        slots[k].host = c.h_sc + 960 + 16 * k;
+        HTR_CUDA(cudaEventCreateWithFlags(&slots[k].done, cudaEventDisableTiming));
+        HTR_CUDA(cudaEventCreate(&slots[k].t0));
+        HTR_CUDA(cudaEventCreate(&slots[k].t1));
+    }
+    struct EventGuard {
+        Slot* s;
+        ~EventGuard() {
+            for (int k = 0; k < 2; ++k) {
+                cudaEventDestroy(s[k].done);
+                cudaEventDestroy(s[k].t0);
+                cudaEventDestroy(s[k].t1);
+            }
+        }
+    } guard{slots};
+
+    // batches are fetched once each, in order; at most two are held
+    DT held[2];
+    int64_t held_idx[2] = {-1, -1};
+    auto batch = [&](int64_t i) -> DT {
+        for (int k = 0; k < 2; ++k)
+            if (held_idx[k] == i) return held[k];
+        const int k = held_idx[0] < held_idx[1] ? 0 : 1;  // evict the older
+        held[k] = batch_of(i);
+        held_idx[k] = i;
+        check_batch_input(held[k].shape, cur->tree, &cur->dims, "ht_rise_update");
+        return held[k];
+    };
+
+    // launch batch i against h's bases with its latent at root slice `at`
+    auto launch = [&](Slot& sl, const Rep& h, int64_t i, int64_t at) -> bool {
+        sl.index = -1;
+        if (!c.fused || c.exact_loss || d != 3) return false;
+        sl.y = batch(i);
+        const int64_t nb = sl.y.shape[3];
+        DT slot;
+        const DT* target = nullptr;
+        if (const auto& rs = h.root; rs && rs->committed == h.acc && at + nb <= rs->cap) {
+            slot.buf = rs->buf;
+            slot.shape = {rs->r11, rs->r12, nb};
+            slot.offset = rs->r11 * rs->r12 * at;
+            target = &slot;
+        }
+        const int64_t l0 = c.launches;
+        sl.started = std::chrono::steady_clock::now();
+        sl.dsc = c.alloc(4);
+        if (!launch_skip_encode3(c, h, sl.y, target, sl.dsc->p, &sl.latent, c.profile ? sl.t0 : nullptr,
+                                 c.profile ? sl.t1 : nullptr))
+            return false;
+        if (c.nccl_comm) {
+            // the global batch count rides on the skip test's all-reduce
+            sl.host[8] = static_cast<double>(nb);
+            HTR_CUDA(cudaMemcpyAsync(sl.dsc->p + 1, sl.host + 8, sizeof(double), cudaMemcpyHostToDevice, c.s));
+            c.allreduce(sl.dsc->p, 3);
+        }
+        HTR_CUDA(cudaMemcpyAsync(sl.host, sl.dsc->p, 3 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        HTR_CUDA(cudaEventRecord(sl.done, c.s));
+        sl.launches = c.launches - l0;
+        sl.index = i;
+        return true;
+    };
+
+    // the skip decision of a launched batch (ht_rise_update's, bit for bit);
+    // null when the batch needs the full update (expansion, guard band,
+    // non-finite input)
+    auto decide = [&](Slot& sl, const Rep& h) -> std::shared_ptr<Rep> {
+        HTR_CUDA(cudaEventSynchronize(sl.done));
+        const int64_t nb = sl.y.shape[3];
+        const double ysq = sl.host[0], latsq = sl.host[2];
+        const int64_t gbatch = c.nccl_comm ? static_cast<int64_t>(std::llround(sl.host[1])) : nb;
+        if (c.profile) {
+            float ms = 0.f;
+            HTR_CUDA(cudaEventElapsedTime(&ms, sl.t0, sl.t1));
+            c.fused_ms += ms;
+            ++c.fused_calls;
+        }
+        if (!std::isfinite(ysq)) return nullptr;
+        const double eps_rel = effective_eps_rel(eps_override >= 0 ? eps_override : h.eps_rel);
+        const double eps_des = eps_rel * std::sqrt(ysq);
+        const double proj_sq = std::max(0.0, ysq - latsq);
+        if (std::abs(proj_sq - eps_des * eps_des) <= 1e-12 * ysq) return nullptr;
+        const double proj_error = std::sqrt(proj_sq);
+        if (!(proj_error <= eps_des)) return nullptr;
+        auto out = std::make_shared<Rep>(h);
+        append_root(c, *out, h, sl.latent);
+        out->acc_global = h.acc_global + gbatch;
+        UpdateOut u;
+        std::memset(&u.report, 0, sizeof(u.report));
+        htr_update_report& r = u.report;
+        r.skipped = 1;
+        r.proj_error = proj_error;
+        r.eps_des = eps_des;
+        r.used_fused_path = 1;
+        int k = 0;
+        for (const auto& [id, rk] : out->ranks()) {
+            if (k >= HTR_MAX_NODES) break;
+            r.node_layer[k] = static_cast<int32_t>(id.layer);
+            r.node_pos[k] = static_cast<int32_t>(id.pos);
+            r.new_ranks[k] = rk;
+            r.added_ranks[k] = 0;
+            ++k;
+        }
+        r.n_nodes = k;
+        r.kernel_launches = sl.launches;
+        r.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - sl.started).count();
+        u.rep = out;
+        res.push_back(std::move(u));
+        return out;
+    };
+
+    int cs = 0;          // slot of batch i when `pending`
+    bool pending = false;
+    for (int64_t i = 0; i < n; ++i) {
+        if (!pending) pending = launch(slots[cs], *cur, i, cur->acc);
+        if (!pending) {
+            UpdateOut u = ht_rise_update(c, *cur, batch(i), eps_override, adaptive);
+            cur = u.rep;
+            res.push_back(std::move(u));
+            continue;
+        }
+        // batch i+1 against the same bases, its latent right after batch i's
+        const bool ahead =
+            i + 1 < n && launch(slots[cs ^ 1], *cur, i + 1, cur->acc + slots[cs].y.shape[3]);
+        if (auto next = decide(slots[cs], *cur)) {
+            cur = next;
+            cs ^= 1;
+            pending = ahead;
+        } else {
+            // expansion (or a decision inside the guard band): the full
+            // update; a speculative batch i+1 is discarded (its latent went to
+            // slices beyond the committed ones) and re-runs on the new bases
+            UpdateOut u = ht_rise_update(c, *cur, slots[cs].y, eps_override, adaptive);
+            cur = u.rep;
+            res.push_back(std::move(u));
+            pending = false;
+        }
+        slots[cs ^ 1].dsc.reset();
+    }
+    HTR_CUDA(cudaStreamSynchronize(c.s));
+    return res;
+}
+
 
 // ---------------------------------------------------------------------------
 // decode (bht.hpp:406-456)

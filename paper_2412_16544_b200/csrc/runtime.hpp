@@ -208,6 +208,23 @@ struct UpdateOut {
 };
 UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_override, bool adaptive);
 
+/// The skip-path encode of a 3-way (1,(2,3)) batch as two launches (fused3 +
+/// tail3), ||y||^2 -> sc[0] and ||latent||^2 -> sc[2]. false (nothing
+/// launched) outside the fused kernels' shapes and ranks.
+bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc, DT* latent,
+                         cudaEvent_t ev0, cudaEvent_t ev1);
+
+/// A stream of updates h -> h1 -> ... -> hn, identical to n ht_rise_update
+/// calls (extension: the reference's caller loops over batches, main.cpp).
+/// While batch i's skip decision is read back, batch i+1's skip-path encode
+/// is already queued against the same bases (a skip leaves them unchanged);
+/// when batch i expands, that speculative work is discarded and batch i+1
+/// re-runs against the new bases. batch_of(i) supplies batch i (called once
+/// per batch, in order).
+std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep>& h, int64_t n,
+                                           const std::function<DT(int64_t)>& batch_of, double eps_override,
+                                           bool adaptive);
+
 /// bht.hpp:406-456; the result lands in `dst` (caller device memory) when given.
 DT decode(Context& c, const Rep& h, const DT& latent, double* dst = nullptr);
 

@@ -110,6 +110,8 @@ _SIGNATURES = {
                                 C.c_int32, C.POINTER(_P), C.POINTER(_BuildReport)]),
     "htr_ht_rise_update": (C.c_int32, [_P, _P, _D, C.c_int32, _I64, C.c_int32, C.c_double, C.c_int32,
                                        C.POINTER(_P), C.POINTER(_UpdateReport)]),
+    "htr_ht_rise_update_many": (C.c_int32, [_P, _P, C.c_int64, C.POINTER(_D), C.c_int32, _I64, C.c_int32,
+                                            C.c_double, C.c_int32, C.POINTER(_P), C.POINTER(_UpdateReport)]),
     "htr_encode": (C.c_int32, [_P, _P, _D, C.c_int32, _I64, C.c_int32, _D, C.c_int32, _D]),
     "htr_decode": (C.c_int32, [_P, _P, _D, C.c_int32, _I64, _D, C.c_int32]),
     "htr_reconstruct_slice": (C.c_int32, [_P, _P, C.c_int64, _D, C.c_int32]),
@@ -671,6 +673,55 @@ def ht_rise_update(h: HTRepresentation, y, epsilon_rel: Optional[float] = None, 
         bool(rep.skipped), rep.proj_error, rep.eps_des, dict(zip(ids, rep.added_ranks[:n])),
         dict(zip(ids, rep.new_ranks[:n])), rep.seconds, bool(rep.used_fused_path), bool(rep.used_exact_loss),
         int(rep.kernel_launches))
+
+
+def _update_report(rep) -> "UpdateReport":
+    n = rep.n_nodes
+    ids = list(zip(rep.node_layer[:n], rep.node_pos[:n]))
+    return UpdateReport(
+        bool(rep.skipped), rep.proj_error, rep.eps_des, dict(zip(ids, rep.added_ranks[:n])),
+        dict(zip(ids, rep.new_ranks[:n])), rep.seconds, bool(rep.used_fused_path), bool(rep.used_exact_loss),
+        int(rep.kernel_launches))
+
+
+def ht_rise_update_many(h: HTRepresentation, batches, epsilon_rel: Optional[float] = None,
+                        adaptive_budget: bool = False):
+    """A stream of updates (extension; the reference's caller loops
+    ht_rise_update over batches, tools/main.cpp:225-243). Identical to
+    calling ht_rise_update on each batch in turn, each on the previous
+    result; the library queues batch i+1's skip-path encode before batch i's
+    skip decision is read back. Returns ([value after each batch], [report
+    of each batch])."""
+    ctx = h.ctx
+    batches = list(batches)
+    n = len(batches)
+    if n == 0:
+        return [], []
+    args = [_tensor_arg(y, ctx) for y in batches]
+    on_dev = {a[1] for a in args}
+    if len(on_dev) != 1:
+        raise ValueError("ht_rise_update_many: batches must be all on the device or all on the host")
+    order = len(args[0][2])
+    if any(len(a[2]) != order for a in args):
+        raise ValueError("ht_rise_update_many: batches of different tensor order")
+    ptrs = (_D * n)(*[a[0] for a in args])
+    shapes = (C.c_int64 * (n * order))(*[int(e) for a in args for e in a[2]])
+    outs = (_P * n)()
+    reps = (_UpdateReport * n)()
+    eps = -1.0 if epsilon_rel is None else float(epsilon_rel)
+    code = _fn.ht_rise_update_many(ctx._h, h.handle, n, ptrs, on_dev.pop(), shapes, order, eps,
+                                   1 if adaptive_budget else 0, outs, reps)
+    if code:
+        ctx.check(code)
+    del args
+    values, reports = [], []
+    acc = h._acc
+    for i in range(n):
+        if acc is not None:
+            acc += int(shapes[i * order + order - 1]) * ctx.world
+        values.append(HTRepresentation(_P(outs[i]), ctx, h._tree, h._dims, acc, h._eps))
+        reports.append(_update_report(reps[i]))
+    return values, reports
 
 
 def _latent_shape(h: HTRepresentation, batch: int):

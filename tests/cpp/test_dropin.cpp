@@ -227,6 +227,47 @@ int main() {
             offset += n;
         }
     }
+    {  // extension: ht_rise_update_many == the per-batch loop (random batches
+       // expand every step; a (1,(2,3)) family stream skips on the fused path)
+        std::mt19937_64 r6(8080);
+        std::uniform_int_distribution<Index> nb(1, 4);
+        std::vector<DenseTensor> batches;
+        for (int k = 0; k < 6; ++k) batches.push_back(random_tensor({3, 4, 3, nb(r6)}, r6));
+        auto [rep0, report] = bht_l2r(batches[0], DimensionTree::balanced(3), 0.25);
+        std::vector<DenseTensor> rest(batches.begin() + 1, batches.end());
+        auto many = ht_rise_update_many(rep0, rest);
+        CHECK(many.size() == rest.size());
+        HTRepresentation rep = rep0;
+        for (std::size_t k = 0; k < rest.size(); ++k) {
+            auto [next, update] = ht_rise_update(rep, rest[k]);
+            rep = std::move(next);
+            CHECK(update.skipped == many[k].second.skipped);
+            CHECK(update.proj_error == many[k].second.proj_error);
+            CHECK(update.new_ranks == many[k].second.new_ranks);
+            CHECK(rep.accumulated == many[k].first.accumulated);
+        }
+        for (Index m = 1; m <= rep.accumulated; ++m)
+            CHECK(reconstruct_slice(rep, m) == reconstruct_slice(many.back().first, m));
+
+        std::vector<Matrix> bases;
+        for (Index n : {64, 64, 16}) bases.push_back(random_orthonormal(n, 3, r6));
+        DimensionTree t123 = DimensionTree::from_layers(
+            {{TreeNode{{0, 0}, NodeKind::Root, {{1, 0}, {1, 1}}}},
+             {TreeNode{{1, 0}, NodeKind::Leaf, {}, {0, 0}, 0}, TreeNode{{1, 1}, NodeKind::Transfer, {{2, 0}, {2, 1}}}},
+             {TreeNode{{2, 0}, NodeKind::Leaf, {}, {0, 0}, 1}, TreeNode{{2, 1}, NodeKind::Leaf, {}, {0, 0}, 2}}});
+        auto [f0, frep] = bht_l2r(tucker_family_batch(bases, 3, r6), t123, 1e-6);
+        std::vector<DenseTensor> fam;
+        for (int k = 0; k < 5; ++k) fam.push_back(tucker_family_batch(bases, 2, r6));
+        auto fm = ht_rise_update_many(f0, fam);
+        HTRepresentation fr = f0;
+        for (std::size_t k = 0; k < fam.size(); ++k) {
+            auto [next, update] = ht_rise_update(fr, fam[k]);
+            fr = std::move(next);
+            CHECK(update.skipped && fm[k].second.skipped);
+            CHECK(update.proj_error == fm[k].second.proj_error);
+        }
+        CHECK(fm.back().first.root() == fr.root());
+    }
     {  // test_metrics.cpp:89-98 / acceptance C5 counting identities
         std::mt19937_64 r5(555555);
         std::vector<Matrix> bases;

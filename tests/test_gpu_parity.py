@@ -312,6 +312,10 @@ def test_fused_path_matches_generic(ht):
     ((20, 20, 20), 64, 6, (64, 64)),   # the c5 shape
     ((7, 11, 5), 24, 5, (128, 64)),    # mixed slab extents
     ((12, 4, 9), 33, 6, (64, 128)),
+    # rank remainders on DFMA rows (r0 = 8 m + 1..4)
+    ((18, 5, 7), 40, 5, (128, 128)),   # m = 2, 2 remainder rows, r1 in one tile
+    ((10, 20, 3), 64, 4, (64, 128)),   # m = 1, 2 remainder rows, r1 in three tiles
+    ((19, 13, 4), 29, 3, (128, 64)),   # m = 2, 3 remainder rows
 ])
 def test_fused_tail_tile_cases(ht, ranks, n2, nsamp, n01):
     """fused3 + tail3 (skip-path encode) against the generic GEMM chain across

@@ -67,6 +67,50 @@ __global__ void dmma16816_kernel(double* out, int iters) {
   if (s == 12345.678) out[threadIdx.x] = s;
 }
 
+// DMMA and DFMA interleaved in one warp: do they share the FP64 pipe?
+// NF DFMAs per thread ride along each group of 4 DMMAs (NF=0: DMMA only).
+template <int NF>
+__global__ void mixed_kernel(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c[4][2];
+  double f[NF > 0 ? NF : 1];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { c[i][0] = i; c[i][1] = -i; }
+#pragma unroll
+  for (int i = 0; i < (NF > 0 ? NF : 1); ++i) f[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+#pragma unroll
+      for (int j = i; j < NF; j += 4) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(f[j]) : "d"(a), "d"(b));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s += c[i][0] + c[i][1];
+#pragma unroll
+  for (int i = 0; i < NF; ++i) s += f[i];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+template <int NF>
+void run_mixed(int sms, double* out, int iters, cudaEvent_t e0, cudaEvent_t e1) {
+  for (int threads : {256, 512}) {
+    const int blocks = sms * 2;
+    float ms;
+    mixed_kernel<NF><<<blocks, threads>>>(out, 100);
+    cudaEventRecord(e0);
+    mixed_kernel<NF><<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
+    const double dmma_fl = 2.0 * 256 * 4 * (double)iters * blocks * (threads / 32);
+    const double dfma_fl = 2.0 * NF * (double)iters * blocks * threads;
+    printf("MIXED dfma/thread per 4 dmma=%d thr=%d : %.3f ms  dmma %.2f TF + dfma %.2f TF = %.2f TF\n", NF, threads,
+           ms, dmma_fl / ms / 1e9, dfma_fl / ms / 1e9, (dmma_fl + dfma_fl) / ms / 1e9);
+  }
+}
+
 __global__ void read_kernel(const double2* __restrict__ p, size_t n2, double* out) {
   double s0 = 0, s1 = 0;
   size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -126,6 +170,11 @@ int main() {
       printf("DMMA16816 ch=2 blocks=%d thr=%d : %.2f TFLOP/s\n", blocks, threads, fl / ms / 1e9);
     }
   }
+  run_mixed<0>(sms, out, iters, e0, e1);
+  run_mixed<4>(sms, out, iters, e0, e1);
+  run_mixed<8>(sms, out, iters, e0, e1);
+  run_mixed<16>(sms, out, iters, e0, e1);
+  run_mixed<32>(sms, out, iters, e0, e1);
   size_t bytes = (size_t)4 << 30;
   double2* buf; CK(cudaMalloc(&buf, bytes));
   CK(cudaMemset(buf, 0, bytes));
