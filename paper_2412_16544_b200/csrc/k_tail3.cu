@@ -291,6 +291,10 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
         }
         a.out[0] = t0;
         a.out[2] = t1;
+        if (a.host_out) {
+            a.host_out[0] = t0;
+            a.host_out[2] = t1;
+        }
         *a.ticket = 0u;
     }
 }

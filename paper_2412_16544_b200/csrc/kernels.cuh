@@ -162,6 +162,9 @@ struct Tail3Args {
     const double* ysq_partials = nullptr;
     int64_t n_ysq = 0;
     double* out = nullptr;
+    // optional copy of out[0] / out[2] in mapped pinned host memory (the host
+    // reads it after the stream or an event completes: no D2H copy)
+    double* host_out = nullptr;
     unsigned int* ticket = nullptr;  // zero on entry, left zero on exit
 };
 bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2);

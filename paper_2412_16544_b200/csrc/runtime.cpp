@@ -134,6 +134,8 @@ Context::Context(int dev) : device(dev) {
     uint64_t thr = UINT64_MAX;
     HTR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     HTR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_sc), 1024 * sizeof(double)));
+    HTR_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_map), 64 * sizeof(double), cudaHostAllocMapped));
+    HTR_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_map), h_map, 0));
     d_sc = alloc(1024);
     HTR_CUDA(cudaMalloc(reinterpret_cast<void**>(&d_ticket), sizeof(unsigned int)));
     HTR_CUDA(cudaMemset(d_ticket, 0, sizeof(unsigned int)));
@@ -146,6 +148,7 @@ Context::~Context() {
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
     if (h_sc) cudaFreeHost(h_sc);
+    if (h_map) cudaFreeHost(h_map);
     if (d_ticket) cudaFree(d_ticket);
 }
 
@@ -893,7 +896,7 @@ Tree3 tree3_ranks(const Rep& h, const RankMap& ranks) {
 }  // namespace
 
 bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc, DT* latent,
-                         cudaEvent_t ev0, cudaEvent_t ev1) {
+                         cudaEvent_t ev0, cudaEvent_t ev1, double* host_out) {
     if (h.tree.dims() != 3 || h.tree.depth() != 2) return false;
     const Tree3 t = tree3_ranks(h, h.ranks());
     const int64_t batch = y.shape[3];
@@ -942,6 +945,7 @@ bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent
     ta.ysq_partials = fa.ysq_partials;
     ta.n_ysq = grid;
     ta.out = sc;
+    ta.host_out = host_out;
     ta.ticket = c.d_ticket;
     launch_tail3(ta, c.s, &c.launches);
     HTR_CUDA(cudaGetLastError());
@@ -972,7 +976,7 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
     if (!exact && c.fused && d == 3) {
         DT lat;
         if (launch_skip_encode3(c, h, y, latent_target, sc, &lat, c.profile ? c.ev[0] : nullptr,
-                                c.profile ? c.ev[1] : nullptr)) {
+                                c.profile ? c.ev[1] : nullptr, c.nccl_comm ? nullptr : c.d_map)) {
             // fused leaves + tail: ((1,(2,3)) trees)
             leaves_done = tail_done = out.fused = true;
             cur = lat;
@@ -1079,8 +1083,15 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
         c.h_sc[8] = static_cast<double>(batch);
         HTR_CUDA(cudaMemcpyAsync(sc + 8, c.h_sc + 8, sizeof(double), cudaMemcpyHostToDevice, c.s));
     }
-    c.allreduce(sc, 16 + nslots);
-    c.fetch(sc, 16 + nslots, c.h_sc);
+    if (tail_done && !c.nccl_comm) {
+        // the fused tail wrote both norms to mapped host memory
+        HTR_CUDA(cudaStreamSynchronize(c.s));
+        c.h_sc[0] = c.h_map[0];
+        c.h_sc[2] = c.h_map[2];
+    } else {
+        c.allreduce(sc, 16 + nslots);
+        c.fetch(sc, 16 + nslots, c.h_sc);
+    }
     out.gbatch = c.nccl_comm ? static_cast<int64_t>(std::llround(c.h_sc[8])) : batch;
     if (c.profile && leaves_done) {
         float ms = 0.f;
@@ -1331,6 +1342,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         DT y, latent;
         BufPtr dsc;       // [0] ||y||^2, [1] batch count (sharded), [2] ||latent||^2
         double* host = nullptr;  // pinned copy of dsc[0..2]
+        double* mapped = nullptr;  // mapped host block the tail writes dsc[0], dsc[2] to
         cudaEvent_t done = nullptr, t0 = nullptr, t1 = nullptr;
         int64_t launches = 0;
         std::chrono::steady_clock::time_point started;
@@ -1338,6 +1350,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
     Slot slots[2];
     for (int k = 0; k < 2; ++k) {
         slots[k].host = c.h_sc + 960 + 16 * k;
+        slots[k].mapped = c.h_map + 16 + 16 * k;
         HTR_CUDA(cudaEventCreateWithFlags(&slots[k].done, cudaEventDisableTiming));
         HTR_CUDA(cudaEventCreate(&slots[k].t0));
         HTR_CUDA(cudaEventCreate(&slots[k].t1));
@@ -1383,16 +1396,17 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         const int64_t l0 = c.launches;
         sl.started = std::chrono::steady_clock::now();
         sl.dsc = c.alloc(4);
+        double* mapped_dev = c.d_map + (sl.mapped - c.h_map);
         if (!launch_skip_encode3(c, h, sl.y, target, sl.dsc->p, &sl.latent, c.profile ? sl.t0 : nullptr,
-                                 c.profile ? sl.t1 : nullptr))
+                                 c.profile ? sl.t1 : nullptr, c.nccl_comm ? nullptr : mapped_dev))
             return false;
         if (c.nccl_comm) {
             // the global batch count rides on the skip test's all-reduce
             sl.host[8] = static_cast<double>(nb);
             HTR_CUDA(cudaMemcpyAsync(sl.dsc->p + 1, sl.host + 8, sizeof(double), cudaMemcpyHostToDevice, c.s));
             c.allreduce(sl.dsc->p, 3);
+            HTR_CUDA(cudaMemcpyAsync(sl.host, sl.dsc->p, 3 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
         }
-        HTR_CUDA(cudaMemcpyAsync(sl.host, sl.dsc->p, 3 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
         HTR_CUDA(cudaEventRecord(sl.done, c.s));
         sl.launches = c.launches - l0;
         sl.index = i;
@@ -1405,7 +1419,8 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
     auto decide = [&](Slot& sl, const Rep& h) -> std::shared_ptr<Rep> {
         HTR_CUDA(cudaEventSynchronize(sl.done));
         const int64_t nb = sl.y.shape[3];
-        const double ysq = sl.host[0], latsq = sl.host[2];
+        const double* v = c.nccl_comm ? sl.host : sl.mapped;
+        const double ysq = v[0], latsq = v[2];
         const int64_t gbatch = c.nccl_comm ? static_cast<int64_t>(std::llround(sl.host[1])) : nb;
         if (c.profile) {
             float ms = 0.f;

@@ -102,6 +102,8 @@ struct Context {
     bool fused = true;
     bool profile = false;
     double* h_sc = nullptr;  // pinned scalars
+    double* h_map = nullptr; // mapped pinned scalars written by kernels (64 doubles)
+    double* d_map = nullptr; // its device address
     BufPtr d_sc;             // device scalars
     unsigned int* d_ticket = nullptr;  // last-CTA ticket of the fused tail (kept zero between launches)
     // timing of the fused encode kernel and of the generic GEMMs
@@ -211,8 +213,10 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
 /// The skip-path encode of a 3-way (1,(2,3)) batch as two launches (fused3 +
 /// tail3), ||y||^2 -> sc[0] and ||latent||^2 -> sc[2]. false (nothing
 /// launched) outside the fused kernels' shapes and ranks.
+/// host_out (device address of mapped host memory, or null) receives the
+/// same two scalars.
 bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc, DT* latent,
-                         cudaEvent_t ev0, cudaEvent_t ev1);
+                         cudaEvent_t ev0, cudaEvent_t ev1, double* host_out = nullptr);
 
 /// A stream of updates h -> h1 -> ... -> hn, identical to n ht_rise_update
 /// calls (extension: the reference's caller loops over batches, main.cpp).

@@ -697,7 +697,14 @@ def ht_rise_update_many(h: HTRepresentation, batches, epsilon_rel: Optional[floa
     n = len(batches)
     if n == 0:
         return [], []
-    args = [_tensor_arg(y, ctx) for y in batches]
+    # order the library's stream after each distinct producing stream once
+    streams = {_torch_stream(y.data) for y in batches
+               if isinstance(y, DeviceTensor) and hasattr(y.data, "data_ptr")}
+    for st in streams:
+        code = _fn.context_wait_stream(ctx._h, st)
+        if code:
+            ctx.check(code)
+    args = [_tensor_arg(y) for y in batches]
     on_dev = {a[1] for a in args}
     if len(on_dev) != 1:
         raise ValueError("ht_rise_update_many: batches must be all on the device or all on the host")
