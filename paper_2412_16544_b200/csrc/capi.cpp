@@ -160,6 +160,10 @@ htr_status htr_context_set_option(htr_context* ctx, int32_t option, double value
             case HTR_OPT_EXACT_LOSS: c.exact_loss = value != 0.0; break;
             case HTR_OPT_FUSED_ENCODE: c.fused = value != 0.0; break;
             case HTR_OPT_PROFILE_EVENTS: c.profile = value != 0.0; break;
+            case HTR_OPT_TAIL_KERNEL:
+                if (value < 0 || value > 2) htr::raise(HTR_ERR_INVALID_ARGUMENT, "tail kernel option: 0, 1 or 2");
+                c.tail_kernel = static_cast<int>(value);
+                break;
             default: htr::raise(HTR_ERR_INVALID_ARGUMENT, "unknown option " + std::to_string(option));
         }
     });

@@ -23,9 +23,13 @@
 // The last CTA to finish (ticket counter) also reduces ||y||^2 (fused3's
 // per-CTA partials) and ||latent||^2 in a fixed order. Replaces two generic
 // GEMM launches, the latent norm pass and two scalar reductions.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace htr {
 namespace {
@@ -42,10 +46,13 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
         : "d"(a), "d"(b));
 }
 
-// Z tiles for G m-tiles (mt0, mt0 + 8, ...) x NT n-tiles.
-template <int G, int NT>
+// Z tiles for G m-tiles (mt0, mt0 + stride, ...) x NT n-tiles, stored into
+// this CTA's Zs and (cluster split) into every peer CTA's copy.
+template <int G, int NT, bool CL>
 __device__ __forceinline__ void phase_a_group(const double* __restrict__ W, const double* U2s, double* Zs,
-                                              int R01, int r2, int n2, int mt0, int g4, int t4) {
+                                              int R01, int r2, int n2, int mt0, int stride_rt, int g4, int t4,
+                                              int csize) {
+    const int stride = CL ? stride_rt : kWarps;
     double acc[G][NT][2];
 #pragma unroll
     for (int i = 0; i < G; ++i)
@@ -54,7 +61,7 @@ __device__ __forceinline__ void phase_a_group(const double* __restrict__ W, cons
     auto load = [&](int k, double (&av)[G]) {
 #pragma unroll
         for (int i = 0; i < G; ++i) {
-            const int p = 8 * (mt0 + kWarps * i) + g4;
+            const int p = 8 * (mt0 + stride * i) + g4;
             av[i] = (p < R01 && k < n2) ? __ldg(W + static_cast<int64_t>(k) * R01 + p) : 0.0;
         }
     };
@@ -78,20 +85,30 @@ __device__ __forceinline__ void phase_a_group(const double* __restrict__ W, cons
             nxt[i] = fut[i];
         }
     }
+    cg::cluster_group cluster = cg::this_cluster();
 #pragma unroll
     for (int i = 0; i < G; ++i) {
-        const int p = 8 * (mt0 + kWarps * i) + g4;
+        const int p = 8 * (mt0 + stride * i) + g4;
 #pragma unroll
         for (int j = 0; j < NT; ++j)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int a2 = 8 * j + 2 * t4 + h;
-                if (p < R01 && a2 < r2) Zs[p + R01 * a2] = acc[i][j][h];
+                if (p < R01 && a2 < r2) {
+                    const int idx = p + R01 * a2;
+                    Zs[idx] = acc[i][j][h];
+                    if constexpr (CL) {
+                        for (int q = 1; q < csize; ++q) {  // distributed shared memory of the peers
+                            const unsigned peer = (cluster.block_rank() + q) % csize;
+                            cluster.map_shared_rank(Zs, peer)[idx] = acc[i][j][h];
+                        }
+                    }
+                }
             }
     }
 }
 
-template <int NT, int MT>
+template <int NT, int MT, bool CL>
 __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     extern __shared__ __align__(16) double sm[];
     const int r0 = a.r0, r1 = a.r1, r2 = a.r2, rt = a.rt;
@@ -103,7 +120,12 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g4 = lane >> 2, t4 = lane & 3;
-    const int64_t s = blockIdx.x;
+    // cluster split (small batches): the csize CTAs of a cluster share one
+    // sample; each computes 1/csize of Z (all-gathered into every CTA's
+    // shared memory) and 1/csize of the latent's column pairs
+    const int C = CL ? a.csize : 1;
+    const int crank = CL ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+    const int64_t s = blockIdx.x / C;
 
     for (int e = tid; e < n2 * kU2Pitch; e += kThreads) {
         const int i2 = e / kU2Pitch, c = e - i2 * kU2Pitch;
@@ -115,16 +137,21 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     {
         const double* W = a.wslab + s * n2 * static_cast<int64_t>(R01);
         const int mtA = (R01 + 7) / 8;
-        const int cnt = warp < mtA ? (mtA - warp + kWarps - 1) / kWarps : 0;
+        const int gw = crank * kWarps + warp, stride = C * kWarps;
+        const int cnt = gw < mtA ? (mtA - gw + stride - 1) / stride : 0;
         int t = 0;
-        for (; cnt - t >= 4; t += 4) phase_a_group<4, NT>(W, U2s, Zs, R01, r2, n2, warp + kWarps * t, g4, t4);
+        for (; cnt - t >= 4; t += 4)
+            phase_a_group<4, NT, CL>(W, U2s, Zs, R01, r2, n2, gw + stride * t, stride, g4, t4, C);
         if (cnt - t >= 2) {
-            phase_a_group<2, NT>(W, U2s, Zs, R01, r2, n2, warp + kWarps * t, g4, t4);
+            phase_a_group<2, NT, CL>(W, U2s, Zs, R01, r2, n2, gw + stride * t, stride, g4, t4, C);
             t += 2;
         }
-        if (cnt - t >= 1) phase_a_group<1, NT>(W, U2s, Zs, R01, r2, n2, warp + kWarps * t, g4, t4);
+        if (cnt - t >= 1) phase_a_group<1, NT, CL>(W, U2s, Zs, R01, r2, n2, gw + stride * t, stride, g4, t4, C);
     }
-    __syncthreads();
+    if constexpr (CL)
+        cg::this_cluster().sync();  // every CTA's Z complete (no DSMEM access after this)
+    else
+        __syncthreads();
 
     // ---- phase B: latent_s(a0, b) = Z_s(a0, j) B(j, b), M = r0, N = rt, K = R12 ----
     // work item = a pair of n-tiles over a K range: per k-step 3 Z and 2 B
@@ -133,7 +160,10 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     // every warp gets the same share, and their partial tiles are summed in
     // a fixed order through shared memory (deterministic).
     const int ntB = (rt + 7) / 8;
-    const int npairs = (ntB + 1) / 2;
+    const int npairs_all = (ntB + 1) / 2;
+    // this CTA's contiguous range of column pairs [pb0, pb0 + npairs)
+    const int pb0 = static_cast<int>(static_cast<int64_t>(npairs_all) * crank / C);
+    const int npairs = static_cast<int>(static_cast<int64_t>(npairs_all) * (crank + 1) / C) - pb0;
     const int full = npairs / kWarps * kWarps;
     const int rem = npairs - full;
     const int kparts = rem ? kWarps / rem : 1;
@@ -143,6 +173,7 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     double* redbuf = U2s;
     double lsq = 0.0;
     auto pair_tiles = [&](int pr, int ks0, int ks1, double (&acc)[MT][2][2]) {
+        pr += pb0;
         const int kend = min(R12, 4 * ks1);
         const double* Bc[2];
         bool colok[2];
@@ -217,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
             for (int j = 0; j < 2; ++j)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int a0 = 8 * i + g4, b = 8 * (2 * pr + j) + 2 * t4 + h;
+                    const int a0 = 8 * i + g4, b = 8 * (2 * (pb0 + pr) + j) + 2 * t4 + h;
                     if (a0 < r0 && b < rt) {
                         const double v = acc[i][j][h];
                         out[a0 + static_cast<int64_t>(r0) * b] = v;
@@ -243,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
         const int per_part = rem * MT * 2 * 64;
         for (int e = tid; e < per_part; e += kThreads) {
             const int tile = e / 64, ln = (e & 63) >> 1, h = e & 1;
-            const int j = tile % 2, i = (tile / 2) % MT, pr = full + tile / (2 * MT);
+            const int j = tile % 2, i = (tile / 2) % MT, pr = pb0 + full + tile / (2 * MT);
             const int a0 = 8 * i + (ln >> 2), b = 8 * (2 * pr + j) + 2 * (ln & 3) + h;
             if (a0 >= r0 || b >= rt) continue;
             double v = 0.0;
@@ -260,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     if (tid == 0) {
         double t = 0.0;
         for (int w = 0; w < kWarps; ++w) t += red[w];
-        a.latsq[s] = t;
+        a.latsq[s * C + crank] = t;
         __threadfence();
         last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
     }
@@ -271,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     __threadfence();
     double ys = 0.0, ls = 0.0;
     for (int64_t i = tid; i < a.n_ysq; i += kThreads) ys += __ldcg(a.ysq_partials + i);
-    for (int64_t i = tid; i < a.S; i += kThreads) ls += __ldcg(a.latsq + i);
+    for (int64_t i = tid; i < a.S * C; i += kThreads) ls += __ldcg(a.latsq + i);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         ys += __shfl_xor_sync(0xffffffffu, ys, o);
@@ -299,6 +330,254 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     }
 }
 
+// ---- sample-pair variant --------------------------------------------------
+// One CTA per pair of samples (s0, s0 + 1), 10 warps:
+//   phase A  Z_s = W_s U2 for both samples (as above), written transposed
+//            into one shared-memory operand Z^T[j, n] with n = a0 + r0 * (s - s0);
+//   phase B  latent^T[b, n] = sum_j B[j, b] Z^T[j, n]: M = rt (transfer basis
+//            columns, streamed from L2 as the A operand), N = 2 r0 (c5: 40 = 5
+//            whole n-tiles, so no MMA row is padding), K = r1 r2; each warp
+//            owns groups of 5 m-tiles x all n-tiles (25 DMMAs per k-step on 5 A
+//            and 5 B fragment loads), A prefetched two k-steps ahead.
+// c5 per pair: phase A 2 x 4800 + phase B 25000 DMMAs (vs 2 x 19800 one
+// sample per CTA, whose M = r0 = 20 pads to 24), in 128 CTAs.
+constexpr int kPairWarps = 10;
+constexpr int kPairThreads = kPairWarps * 32;
+constexpr int kGroup = 5;  // phase-B m-tiles per warp work item
+
+__host__ __device__ __forceinline__ int pair_pitch(int nb) { return (nb % 16 == 8) ? nb : nb + 8; }
+
+// Z^T tiles of one sample for G m-tiles (mt0, mt0 + kPairWarps, ...) x NT n-tiles
+template <int G, int NT>
+__device__ __forceinline__ void phase_a_pair(const double* __restrict__ W, const double* U2s, double* Zt, int pitch,
+                                             int r0, int r1, int r2, int n2, int sl, int mt0, int g4, int t4) {
+    const int R01 = r0 * r1;
+    double acc[G][NT][2];
+#pragma unroll
+    for (int i = 0; i < G; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    auto load = [&](int k, double (&av)[G]) {
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            const int p = 8 * (mt0 + kPairWarps * i) + g4;
+            av[i] = (p < R01 && k < n2) ? __ldg(W + static_cast<int64_t>(k) * R01 + p) : 0.0;
+        }
+    };
+    double cur[G], nxt[G];
+    load(t4, cur);
+    load(t4 + 4, nxt);
+    for (int k0 = 0; k0 < n2; k0 += 4) {
+        double fut[G];
+        load(k0 + 8 + t4, fut);
+        const int k = k0 + t4;
+        double b[NT];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) b[j] = (k < n2) ? U2s[k * kU2Pitch + 8 * j + g4] : 0.0;
+#pragma unroll
+        for (int i = 0; i < G; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma(acc[i][j], cur[i], b[j]);
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            cur[i] = nxt[i];
+            nxt[i] = fut[i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const int p = 8 * (mt0 + kPairWarps * i) + g4;
+        const int a0 = p % r0, a1 = p / r0;
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int a2 = 8 * j + 2 * t4 + h;
+                if (p < R01 && a2 < r2) Zt[(a0 + r0 * sl) + pitch * (a1 + r1 * a2)] = acc[i][j][h];
+            }
+    }
+}
+
+template <int NT, int NTB>
+__global__ void __launch_bounds__(kPairThreads) tail3_pair_kernel(const Tail3Args a) {
+    extern __shared__ __align__(16) double sm[];
+    constexpr int NB = 8 * NTB;
+    const int r0 = a.r0, r1 = a.r1, r2 = a.r2, rt = a.rt;
+    const int R01 = r0 * r1, R12 = r1 * r2;
+    const int n2 = static_cast<int>(a.n2);
+    const int pitch = pair_pitch(NB);
+    const int KS = (R12 + 3) / 4;
+    double* U2s = sm;                   // [n2][kU2Pitch]
+    double* Zt = U2s + n2 * kU2Pitch;   // [4 KS][pitch]
+    __shared__ double red[kPairWarps][2];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    const int64_t s0 = 2 * static_cast<int64_t>(blockIdx.x);
+    const int ns = static_cast<int>(min(static_cast<int64_t>(2), a.S - s0));
+
+    for (int e = tid; e < n2 * kU2Pitch; e += kPairThreads) {
+        const int i2 = e / kU2Pitch, c = e - i2 * kU2Pitch;
+        U2s[e] = c < r2 ? a.U2[i2 + static_cast<int64_t>(n2) * c] : 0.0;
+    }
+    for (int e = tid; e < 4 * KS * pitch; e += kPairThreads) Zt[e] = 0.0;
+    __syncthreads();
+
+    // ---- phase A: both samples' Z into Z^T ----
+    const int mtA = (R01 + 7) / 8;
+    const int cnt = warp < mtA ? (mtA - warp + kPairWarps - 1) / kPairWarps : 0;
+    for (int sl = 0; sl < ns; ++sl) {
+        const double* W = a.wslab + (s0 + sl) * n2 * static_cast<int64_t>(R01);
+        int t = 0;
+        for (; cnt - t >= 4; t += 4)
+            phase_a_pair<4, NT>(W, U2s, Zt, pitch, r0, r1, r2, n2, sl, warp + kPairWarps * t, g4, t4);
+        if (cnt - t >= 2) {
+            phase_a_pair<2, NT>(W, U2s, Zt, pitch, r0, r1, r2, n2, sl, warp + kPairWarps * t, g4, t4);
+            t += 2;
+        }
+        if (cnt - t >= 1) phase_a_pair<1, NT>(W, U2s, Zt, pitch, r0, r1, r2, n2, sl, warp + kPairWarps * t, g4, t4);
+    }
+    __syncthreads();
+
+    // ---- phase B: latent^T = B^T Z^T ----
+    const int MTB = (rt + 7) / 8;
+    const int ngroups = (MTB + kGroup - 1) / kGroup;
+    double lsq[2] = {0.0, 0.0};
+    for (int g = warp; g < ngroups; g += kPairWarps) {
+        const int mt0 = g * kGroup;
+        double acc[kGroup][NTB][2];
+#pragma unroll
+        for (int i = 0; i < kGroup; ++i)
+#pragma unroll
+            for (int j = 0; j < NTB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        const double* Bc[kGroup];
+        bool ok[kGroup];
+#pragma unroll
+        for (int i = 0; i < kGroup; ++i) {
+            const int bcol = 8 * (mt0 + i) + g4;
+            ok[i] = bcol < rt;
+            Bc[i] = a.B + static_cast<int64_t>(R12) * (ok[i] ? bcol : 0);
+        }
+        auto loadA = [&](int ks, double (&v)[kGroup]) {
+            const int k = 4 * ks + t4;
+#pragma unroll
+            for (int i = 0; i < kGroup; ++i) v[i] = (ok[i] && k < R12) ? __ldg(Bc[i] + k) : 0.0;
+        };
+        double cur[kGroup];
+        loadA(0, cur);
+        for (int ks = 0; ks < KS; ++ks) {
+            double nxt[kGroup];
+            loadA(ks + 1, nxt);
+            const double* zr = Zt + pitch * (4 * ks + t4) + g4;
+            double bv[NTB];
+#pragma unroll
+            for (int j = 0; j < NTB; ++j) bv[j] = zr[8 * j];
+#pragma unroll
+            for (int i = 0; i < kGroup; ++i)
+#pragma unroll
+                for (int j = 0; j < NTB; ++j) dmma(acc[i][j], cur[i], bv[j]);
+#pragma unroll
+            for (int i = 0; i < kGroup; ++i) cur[i] = nxt[i];
+        }
+#pragma unroll
+        for (int i = 0; i < kGroup; ++i)
+#pragma unroll
+            for (int j = 0; j < NTB; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int b = 8 * (mt0 + i) + g4, n = 8 * j + 2 * t4 + h;
+                    const int sl = n >= r0 ? 1 : 0, a0 = n - r0 * sl;
+                    if (b < rt && n < r0 * ns) {
+                        const double v = acc[i][j][h];
+                        a.latent[a0 + static_cast<int64_t>(r0) * b + static_cast<int64_t>(r0) * rt * (s0 + sl)] = v;
+                        if (sl) lsq[1] = fma(v, v, lsq[1]);
+                        else lsq[0] = fma(v, v, lsq[0]);
+                    }
+                }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lsq[q] += __shfl_xor_sync(0xffffffffu, lsq[q], o);
+    if (lane == 0) {
+        red[warp][0] = lsq[0];
+        red[warp][1] = lsq[1];
+    }
+    __syncthreads();
+    __shared__ bool last;
+    if (tid == 0) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int w = 0; w < kPairWarps; ++w) {
+            t0 += red[w][0];
+            t1 += red[w][1];
+        }
+        a.latsq[s0] = t0;
+        if (ns == 2) a.latsq[s0 + 1] = t1;
+        __threadfence();
+        last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double ys = 0.0, ls = 0.0;
+    for (int64_t i = tid; i < a.n_ysq; i += kPairThreads) ys += __ldcg(a.ysq_partials + i);
+    for (int64_t i = tid; i < a.S; i += kPairThreads) ls += __ldcg(a.latsq + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ys += __shfl_xor_sync(0xffffffffu, ys, o);
+        ls += __shfl_xor_sync(0xffffffffu, ls, o);
+    }
+    __shared__ double red2[2][kPairWarps];
+    if (lane == 0) {
+        red2[0][warp] = ys;
+        red2[1][warp] = ls;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int w = 0; w < kPairWarps; ++w) {
+            t0 += red2[0][w];
+            t1 += red2[1][w];
+        }
+        a.out[0] = t0;
+        a.out[2] = t1;
+        if (a.host_out) {
+            a.host_out[0] = t0;
+            a.host_out[2] = t1;
+        }
+        *a.ticket = 0u;
+    }
+}
+
+size_t tail3_pair_smem(int64_t n2, int r0, int r1, int r2) {
+    const int nb = 8 * ((2 * r0 + 7) / 8);
+    const int64_t ks = (static_cast<int64_t>(r1) * r2 + 3) / 4;
+    return sizeof(double) * (static_cast<size_t>(n2) * kU2Pitch + static_cast<size_t>(4 * ks * pair_pitch(nb)));
+}
+
+template <int NT, int NTB>
+void launch_pair_t(const Tail3Args& a, size_t smem, cudaStream_t s) {
+    static size_t configured = 0;
+    if (smem > 46 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(tail3_pair_kernel<NT, NTB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        configured = smem;
+    }
+    tail3_pair_kernel<NT, NTB><<<static_cast<unsigned>((a.S + 1) / 2), kPairThreads, smem, s>>>(a);
+}
+
+template <int NT>
+void launch_pair_nt(const Tail3Args& a, size_t smem, cudaStream_t s) {
+    switch ((2 * a.r0 + 7) / 8) {
+        case 1: return launch_pair_t<NT, 1>(a, smem, s);
+        case 2: return launch_pair_t<NT, 2>(a, smem, s);
+        case 3: return launch_pair_t<NT, 3>(a, smem, s);
+        case 4: return launch_pair_t<NT, 4>(a, smem, s);
+        case 5: return launch_pair_t<NT, 5>(a, smem, s);
+        default: return launch_pair_t<NT, 6>(a, smem, s);
+    }
+}
+
 size_t tail3_smem(int64_t n2, int r0, int r1, int r2) {
     return sizeof(double) * (std::max<size_t>(static_cast<size_t>(n2) * kU2Pitch, kRedDoubles) +
                              static_cast<size_t>(r0) * r1 * r2);
@@ -306,13 +585,30 @@ size_t tail3_smem(int64_t n2, int r0, int r1, int r2) {
 
 template <int NT, int MT>
 void launch_t(const Tail3Args& a, size_t smem, cudaStream_t s) {
-    static size_t configured = 0;
-    if (smem > 46 * 1024 && smem > configured) {  // margin for the static arrays
-        cudaFuncSetAttribute(tail3_kernel<NT, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        configured = smem;
+    static size_t configured[2] = {0, 0};
+    const int cl = a.csize > 1 ? 1 : 0;
+    if (smem > 46 * 1024 && smem > configured[cl]) {  // margin for the static arrays
+        cudaFuncSetAttribute(cl ? tail3_kernel<NT, MT, true> : tail3_kernel<NT, MT, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        configured[cl] = smem;
     }
-    tail3_kernel<NT, MT><<<static_cast<unsigned>(a.S), kThreads, smem, s>>>(a);
+    if (!cl) {
+        tail3_kernel<NT, MT, false><<<static_cast<unsigned>(a.S), kThreads, smem, s>>>(a);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(a.S * a.csize));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(a.csize);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, tail3_kernel<NT, MT, true>, a);
 }
 
 template <int NT>
@@ -332,11 +628,35 @@ bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2) {
 }
 
 void launch_tail3(const Tail3Args& a, cudaStream_t s, int64_t* launches) {
+    if (a.variant == 2) {
+        const size_t psmem = tail3_pair_smem(a.n2, a.r0, a.r1, a.r2);
+        if (psmem <= 220 * 1024) {
+            switch ((a.r2 + 7) / 8) {
+                case 1: launch_pair_nt<1>(a, psmem, s); break;
+                case 2: launch_pair_nt<2>(a, psmem, s); break;
+                default: launch_pair_nt<3>(a, psmem, s); break;
+            }
+            ++*launches;
+            return;
+        }
+    }
     const size_t smem = tail3_smem(a.n2, a.r0, a.r1, a.r2);
+    // small batches (per-rank shards of a multi-GPU run): when fewer than
+    // half the SMs would hold a sample, split each sample over a cluster of up
+    // to 8 CTAs (grid up to 2 CTAs per SM). Measured on c5 shards
+    // (tools/shard_probe.py): S = 128 is fastest unsplit (the split adds the
+    // all-gather and per-CTA staging without freeing pipe time), S = 64 with
+    // 4-CTA and S = 32 with 4- or 8-CTA clusters (tail 69 -> 38 us at S = 32)
+    Tail3Args b = a;
+    b.csize = 1;
+    if (a.variant != 1 && 2 * a.S <= static_cast<int64_t>(a.num_sms))
+        while (b.csize < 8 && a.S * b.csize * 2 <= 2 * static_cast<int64_t>(a.num_sms) &&
+               b.csize * 2 <= (a.rt + 15) / 16)  // at least one column pair per CTA
+            b.csize *= 2;
     switch ((a.r2 + 7) / 8) {
-        case 1: launch_nt<1>(a, smem, s); break;
-        case 2: launch_nt<2>(a, smem, s); break;
-        default: launch_nt<3>(a, smem, s); break;
+        case 1: launch_nt<1>(b, smem, s); break;
+        case 2: launch_nt<2>(b, smem, s); break;
+        default: launch_nt<3>(b, smem, s); break;
     }
     ++*launches;
 }

@@ -166,6 +166,9 @@ struct Tail3Args {
     // reads it after the stream or an event completes: no D2H copy)
     double* host_out = nullptr;
     unsigned int* ticket = nullptr;  // zero on entry, left zero on exit
+    int variant = 0;  // 0 auto, 1 one sample per CTA, 2 sample pairs (falls back to 1 when it does not fit)
+    int num_sms = kNumSMs;
+    int csize = 1;    // CTAs per sample (a thread-block cluster), set by the launcher
 };
 bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2);
 void launch_tail3(const Tail3Args& a, cudaStream_t s, int64_t* launches);

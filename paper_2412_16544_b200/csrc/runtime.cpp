@@ -940,13 +940,15 @@ bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent
         lat = c.tensor({t.r0, t.rt, batch});
     }
     ta.latent = lat.data();
-    BufPtr lsq = c.alloc(batch);
+    BufPtr lsq = c.alloc(8 * batch);  // per-CTA partials (up to 8 CTAs per sample)
     ta.latsq = lsq->p;
     ta.ysq_partials = fa.ysq_partials;
     ta.n_ysq = grid;
     ta.out = sc;
     ta.host_out = host_out;
     ta.ticket = c.d_ticket;
+    ta.variant = c.tail_kernel;
+    ta.num_sms = c.num_sms;
     launch_tail3(ta, c.s, &c.launches);
     HTR_CUDA(cudaGetLastError());
     *latent = lat;

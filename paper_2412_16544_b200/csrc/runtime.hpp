@@ -101,6 +101,7 @@ struct Context {
     bool exact_loss = false;
     bool fused = true;
     bool profile = false;
+    int tail_kernel = 0;  // HTR_OPT_TAIL_KERNEL
     double* h_sc = nullptr;  // pinned scalars
     double* h_map = nullptr; // mapped pinned scalars written by kernels (64 doubles)
     double* d_map = nullptr; // its device address

@@ -316,6 +316,10 @@ def test_fused_path_matches_generic(ht):
     ((18, 5, 7), 40, 5, (128, 128)),   # m = 2, 2 remainder rows, r1 in one tile
     ((10, 20, 3), 64, 4, (64, 128)),   # m = 1, 2 remainder rows, r1 in three tiles
     ((19, 13, 4), 29, 3, (128, 64)),   # m = 2, 3 remainder rows
+    ((24, 24, 24), 16, 5, (64, 64)),   # the widest ranks: the pair tail does not fit, one sample per CTA
+    ((3, 2, 2), 8, 1, (64, 64)),       # one sample (an unpaired CTA)
+    ((20, 20, 20), 128, 2, (128, 128)),  # c5 ranks, 2 samples: 8-CTA clusters, 3-4 column pairs each
+    ((16, 8, 16), 48, 5, (128, 64)),   # rt = 128: 8 pairs over 8-CTA clusters
 ])
 def test_fused_tail_tile_cases(ht, ranks, n2, nsamp, n01):
     """fused3 + tail3 (skip-path encode) against the generic GEMM chain across
@@ -334,9 +338,21 @@ def test_fused_tail_tile_cases(ht, ranks, n2, nsamp, n01):
         lb, pb = ht.encode(rep, y1)
     finally:
         ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    # every tail kernel: the default (a sample split over a CTA cluster when
+    # the batch is small), one CTA per sample, sample pairs
+    lv = []
+    for v in (1, 2):
+        ctx.set_option(ht.OPT_TAIL_KERNEL, v)
+        try:
+            lv.append(ht.encode(rep, y1)[0])
+        finally:
+            ctx.set_option(ht.OPT_TAIL_KERNEL, 0)
     lr, _ = ho.encode(ref, y1)
     assert la.shape == lr.shape
     assert np.linalg.norm(la - lb) <= 1e-12 * np.linalg.norm(lb)
+    for l1 in lv:
+        assert l1.shape == la.shape
+        assert np.linalg.norm(l1 - lb) <= 1e-12 * np.linalg.norm(lb)
     # against the oracle: latents agree up to the sign/rotation of the bases,
     # so compare norms per sample and the decoded tensors
     assert np.allclose(np.linalg.norm(la, axis=(0, 1)), np.linalg.norm(lr, axis=(0, 1)), rtol=1e-10, atol=0)

@@ -12,15 +12,17 @@ from paper_2412_16544_b200.workloads import CONFIGS
 
 w = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c5"]
 per_call = len(sys.argv) > 2 and sys.argv[2] == "call"
+nb = int(sys.argv[3]) if len(sys.argv) > 3 else w.batch  # samples per batch (a rank's shard)
 ctx = ht.Context(0)
 ht.set_default_context(ctx)
-y0 = w.make_batch(0, "cuda")
-rep, _ = ht.bht_l2r(ht.DeviceTensor(y0, w.shape), w.tree(), w.eps)
+shape = tuple(w.dims) + (nb,)
+y0 = w.make_batch(0, "cuda", batch=nb)
+rep, _ = ht.bht_l2r(ht.DeviceTensor(y0, shape), w.tree(), w.eps)
 del y0
-pool = [w.make_batch(1 + i, "cuda") for i in range(2)]
+pool = [w.make_batch(1 + i, "cuda", batch=nb) for i in range(2)]
 torch.cuda.synchronize()
-rep.reserve(64 * w.batch)
-bs = [ht.DeviceTensor(pool[i % 2], w.shape) for i in range(8)]
+rep.reserve(64 * nb)
+bs = [ht.DeviceTensor(pool[i % 2], shape) for i in range(8)]
 vals, _ = ht.ht_rise_update_many(rep, bs[:3])
 rep = vals[-1]
 ctx.synchronize()
