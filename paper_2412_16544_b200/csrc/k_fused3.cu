@@ -12,9 +12,15 @@
 // ((1,(2,3)) and ((1,2),3)); the interior transfer projection then runs on
 // the r0 r1 r2 / (N0 N1 n2)-size Z.
 //
-// Structure (one CTA per SM, no CTA barriers in the main loop). Each of 8
-// warps owns every 8th slab X = Y[:, :, i2, s] (N0 x N1, contiguous) of its
-// CTA's slab range and walks it in steps of 16 columns x 32 rows; each step
+// Structure (one CTA per SM, no CTA barriers in the main loop). A CTA owns a
+// contiguous range of slabs X = Y[:, :, i2, s] (N0 x N1, contiguous). Its 12
+// warps take whole slabs in rounds (warp w: slabs w, w + 12, ...); the last
+// partial round (fewer than 12 slabs) is split evenly over all warps at
+// column-pair granularity (16 columns), so no warp has more than 1/8 slab
+// more work than another at any batch size (c5 per-rank shards at 8 GPUs:
+// 27-28 slabs per CTA). A slab split between warps has its partial W pieces
+// summed in warp order at the end of the kernel (deterministic).
+// Each warp walks its slabs in steps of 16 columns x 32 rows; each step
 // arrives by two TMA tensor copies (cp.async.bulk.tensor.3d over a
 // [N0, N1, slabs] tensor map, 16x16 boxes, 128-byte swizzle) into the warp's
 // own 4-deep shared-memory ring, issued by one lane three steps ahead and
@@ -125,11 +131,65 @@ __global__ void __launch_bounds__(kThreads, 1)
     double2* U1f = U0f + NC * MT0 * 32;                                              // [N1/8][MT1][32]
     uint64_t* full = reinterpret_cast<uint64_t*>(U1f + (N1 / 8) * MT1 * 32);  // [warp][stage]
     __shared__ double red[kWarps];
+    __shared__ int64_t piece_slab[kWarps][2];  // slab of a warp's partial head / tail piece, or -1
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g4 = lane >> 2, t4 = lane & 3;
     const int R01 = a.r0 * a.r1;
 
+    if (tid < 2 * kWarps) piece_slab[tid >> 1][tid & 1] = -1;
+
+    const int64_t B = gridDim.x, b = blockIdx.x;
+    const int64_t tb = cta_begin(ri.T, b, B), te = cta_begin(ri.T, b + 1, B);
+    // whole-slab rounds, then this warp's share [u0, u1) of the last partial
+    // round's (slab, column pair) units
+    // (slab indices fit in 32 bits: make_batch_map rejects T >= 2^31)
+    const int tb32 = static_cast<int>(tb);
+    const int rounds = static_cast<int>(te - tb) / kWarps;
+    const int tr = tb32 + rounds * kWarps;  // first slab of the partial round
+    const int units = (static_cast<int>(te) - tr) * NP;
+    const int u0 = units * warp / kWarps, u1 = units * (warp + 1) / kWarps;
+    const int whole = rounds * IPS;         // steps in whole slabs
+    const int total = whole + (u1 - u0) * NQ;
+    // step i -> slab, column pair, row quarter; unit index u (partial round only)
+    auto coords = [&](int i, int& t, int& pair, int& q, int& u) {
+        if (i < whole) {
+            const int j = i / IPS;
+            const int rem = i - j * IPS;
+            pair = rem / NQ;
+            q = rem - pair * NQ;
+            t = tb32 + warp + kWarps * j;
+            u = -1;
+        } else {
+            const int k = i - whole;
+            u = u0 + k / NQ;
+            q = k % NQ;
+            pair = u % NP;
+            t = tr + u / NP;
+        }
+    };
+    double* my_stages = stages + warp * kStages * kStageDoubles;
+    uint64_t* my_full = full + warp * kStages;
+    const uint64_t policy = evict_first_policy();
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+
+    auto issue = [&](int i) {  // lane 0 only
+        const int st = i % kStages;
+        int t, u, pair, q;
+        coords(i, t, pair, q, u);
+        mbar_expect_tx(&my_full[st], kStageBytes);
+        double* dst = my_stages + st * kStageDoubles;
+        tma_load_3d(dst, &tmap, kRows * q, kCols * pair, t, &my_full[st], policy);
+        tma_load_3d(dst + kBoxDoubles, &tmap, kRows * q + kBoxRows, kCols * pair, t, &my_full[st], policy);
+    };
+    // lane 0 sets up its warp's ring and starts the stream before the basis
+    // fragments are staged (the first loads' latency overlaps the staging)
+    if (lane == 0) {
+        for (int k = 0; k < kStages; ++k) mbar_init(&my_full[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int k = 0; k < kStages; ++k)
+            if (k < total) issue(k);
+    }
     // ---- stage basis fragments (zero-padded to 8-multiples) ----
     for (int idx = tid; idx < NC * MT0 * 32; idx += kThreads) {
         const int l = idx & 31, mt = (idx >> 5) % MT0, c = idx / (32 * MT0);
@@ -148,37 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         v.y = col < a.r1 ? a.U1[i1y + static_cast<int64_t>(N1) * col] : 0.0;
         U1f[idx] = v;
     }
-    if (tid < kWarps * kStages) mbar_init(&full[tid], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
-
-    const int64_t B = gridDim.x, b = blockIdx.x;
-    const int64_t tb = cta_begin(ri.T, b, B), te = cta_begin(ri.T, b + 1, B);
-    const int64_t slab_elems = static_cast<int64_t>(N0) * N1;
-    auto steps_of = [&](int w) -> int64_t {
-        return (te - tb > w ? (te - tb - w + kWarps - 1) / kWarps : 0) * IPS;
-    };
-
-    const int64_t total = steps_of(warp);
-    double* my_stages = stages + warp * kStages * kStageDoubles;
-    uint64_t* my_full = full + warp * kStages;
-    const uint64_t policy = evict_first_policy();
-    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-
-    auto issue = [&](int64_t i) {  // lane 0 only
-        const int st = static_cast<int>(i % kStages);
-        const int64_t j = i / IPS;
-        const int rem = static_cast<int>(i - j * IPS);
-        const int pair = rem / NQ, q = rem - pair * NQ;
-        const int t = static_cast<int>(tb + warp + kWarps * j);
-        mbar_expect_tx(&my_full[st], kStageBytes);
-        double* dst = my_stages + st * kStageDoubles;
-        tma_load_3d(dst, &tmap, kRows * q, kCols * pair, t, &my_full[st], policy);
-        tma_load_3d(dst + kBoxDoubles, &tmap, kRows * q + kBoxRows, kCols * pair, t, &my_full[st], policy);
-    };
-    if (lane == 0)
-        for (int k = 0; k < kStages; ++k)
-            if (k < total) issue(k);
 
     double ysq0 = 0.0, ysq1 = 0.0, ysq2 = 0.0, ysq3 = 0.0;
     double wacc[MT0][MT1][2];
@@ -188,11 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < MT1; ++j) wacc[i][j][0] = wacc[i][j][1] = 0.0;
 
-    for (int64_t i = 0; i < total; ++i) {
-        const int st = static_cast<int>(i % kStages);
-        const int64_t j = i / IPS;
-        const int rem = static_cast<int>(i - j * IPS);
-        const int pair = rem / NQ, q = rem - pair * NQ;
+    for (int i = 0; i < total; ++i) {
+        const int st = i % kStages;
+        int t, u, pair, q;
+        coords(i, t, pair, q, u);
         if (q == 0) {
 #pragma unroll
             for (int x = 0; x < MT0; ++x)
@@ -251,10 +280,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int ma = 0; ma < MT0; ++ma)
                             dmma(wacc[ma][mb], pacc[ma][nt][h], h ? u[mb].y : u[mb].x);
             }
-            if (pair == NP - 1) {
-                // slab done: publish W (compact a0 + r0 a1) and reset
-                const int64_t t = tb + warp + kWarps * j;
-                double* wdst = a.wslab + t * R01;
+            if (pair == NP - 1 || (u >= 0 && u == u1 - 1)) {
+                // this warp's piece of the slab done: publish W (compact
+                // a0 + r0 a1) and reset; a partial piece (the slab is shared
+                // with a neighbouring warp) goes to the warp's head/tail slot
+                const bool from_start = u < 0 || u - pair >= u0;  // the piece includes column pair 0
+                double* wdst = a.wslab + static_cast<int64_t>(t) * R01;
+                if (!(from_start && pair == NP - 1)) {
+                    const int which = from_start ? 1 : 0;
+                    wdst = a.wpart + ((static_cast<int64_t>(b) * kWarps + warp) * 2 + which) * R01;
+                    if (lane == 0) piece_slab[warp][which] = t;
+                }
 #pragma unroll
                 for (int ma = 0; ma < MT0; ++ma)
 #pragma unroll
@@ -269,6 +305,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
 
+    __syncthreads();
+    // slabs split between warps: W = the pieces summed in warp order
+    __shared__ int64_t split[2 * kWarps];
+    __shared__ int nsplit;
+    if (tid == 0) {
+        int n = 0;
+        for (int k = 0; k < 2 * kWarps; ++k) {
+            const int64_t t = piece_slab[k >> 1][k & 1];
+            bool seen = t < 0;
+            for (int m = 0; m < n && !seen; ++m) seen = split[m] == t;
+            if (!seen) split[n++] = t;
+        }
+        nsplit = n;
+    }
+    __syncthreads();
+    const double* parts = a.wpart + static_cast<int64_t>(b) * kWarps * 2 * R01;
+#pragma unroll 2
+    for (int idx = tid; idx < nsplit * R01; idx += kThreads) {
+        const int m = idx / R01, e = idx - m * R01;
+        const int64_t t = split[m];
+        double v = 0.0;
+        for (int k = 0; k < 2 * kWarps; ++k)
+            if (piece_slab[k >> 1][k & 1] == t) v += __ldcg(parts + static_cast<int64_t>(k) * R01 + e);
+        a.wslab[t * R01 + e] = v;
+    }
     // ||Y||^2 partial of this CTA (fixed shuffle tree, fixed warp order)
     double ys = (ysq0 + ysq1) + (ysq2 + ysq3);
 #pragma unroll
@@ -319,6 +380,8 @@ int launch_impl(const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launc
     const int64_t T = a.n2 * a.S;
     const int64_t B = std::min<int64_t>(num_sms, T);
     RangeInfo ri{T};
+    Fused3Args args = a;
+    args.wpart = a.ysq_partials + B;  // B * kWarps * 2 * r0 r1 doubles (fused3_workspace_doubles)
     alignas(64) CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
     if (!make_batch_map(&map, a.Y, N0, N1, T)) return -1;
@@ -329,7 +392,7 @@ int launch_impl(const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launc
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         configured = true;
     }
-    kfn<<<static_cast<unsigned>(B), kThreads, smem, s>>>(a, ri, map);
+    kfn<<<static_cast<unsigned>(B), kThreads, smem, s>>>(args, ri, map);
     ++*launches;
     if (!a.slab_gemm) return static_cast<int>(B);
     // Z_s[p, a2] = sum_i2 W[(s, i2), p] U2[i2, a2]: the slab-axis (mode 2)
@@ -381,7 +444,8 @@ int64_t fused3_workspace_doubles(int64_t n0, int64_t n1, int64_t n2, int64_t S, 
     (void)r2;
     const int64_t T = n2 * S;
     const int64_t B = std::min<int64_t>(num_sms, T);
-    return T * static_cast<int64_t>(r0) * r1 + B;  // per-slab W + ||Y||^2 partials
+    // per-slab W + ||Y||^2 partials + split-slab pieces (2 per warp)
+    return T * static_cast<int64_t>(r0) * r1 + B + B * kWarps * 2 * static_cast<int64_t>(r0) * r1;
 }
 
 int launch_fused3(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {

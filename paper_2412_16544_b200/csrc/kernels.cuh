@@ -138,6 +138,7 @@ struct Fused3Args {
     double* Z = nullptr;          // r0*r1*r2 x S
     double* wslab = nullptr;      // workspace: per-slab W (r0 r1 per slab)
     double* ysq_partials = nullptr;  // grid entries
+    double* wpart = nullptr;      // split-slab partial W (set by the launcher, after ysq_partials)
     bool slab_gemm = true;        // also enqueue Z = sum_i2 W (x) U2 (else left to tail3)
 };
 // Whether the fused kernel supports this shape; returns the grid size used.
