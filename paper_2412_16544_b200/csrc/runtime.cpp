@@ -140,6 +140,11 @@ Context::Context(int dev) : device(dev) {
     HTR_CUDA(cudaMalloc(reinterpret_cast<void**>(&d_ticket), sizeof(unsigned int)));
     HTR_CUDA(cudaMemset(d_ticket, 0, sizeof(unsigned int)));
     for (auto& e : ev) HTR_CUDA(cudaEventCreate(&e));
+    for (auto& se : slot_ev) {
+        HTR_CUDA(cudaEventCreateWithFlags(&se[0], cudaEventDisableTiming));
+        HTR_CUDA(cudaEventCreate(&se[1]));
+        HTR_CUDA(cudaEventCreate(&se[2]));
+    }
 }
 
 Context::~Context() {
@@ -147,6 +152,9 @@ Context::~Context() {
     if (nccl_comm) nccl().commDestroy(static_cast<ncclComm_t>(nccl_comm));
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
+    for (auto& se : slot_ev)
+        for (auto& e : se)
+            if (e) cudaEventDestroy(e);
     if (h_sc) cudaFreeHost(h_sc);
     if (h_map) cudaFreeHost(h_map);
     if (d_ticket) cudaFree(d_ticket);
@@ -1350,23 +1358,24 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         std::chrono::steady_clock::time_point started;
     };
     Slot slots[2];
+    // HTR_TIMELINE=1: device timeline of the stream (events around each
+    // launch), printed to stderr at the end (diagnostics only)
+    static const bool timeline = std::getenv("HTR_TIMELINE") != nullptr;
+    std::vector<cudaEvent_t> tl;
+    auto mark = [&] {
+        if (!timeline) return;
+        cudaEvent_t e;
+        HTR_CUDA(cudaEventCreate(&e));
+        HTR_CUDA(cudaEventRecord(e, c.s));
+        tl.push_back(e);
+    };
     for (int k = 0; k < 2; ++k) {
         slots[k].host = c.h_sc + 960 + 16 * k;
         slots[k].mapped = c.h_map + 16 + 16 * k;
-        HTR_CUDA(cudaEventCreateWithFlags(&slots[k].done, cudaEventDisableTiming));
-        HTR_CUDA(cudaEventCreate(&slots[k].t0));
-        HTR_CUDA(cudaEventCreate(&slots[k].t1));
+        slots[k].done = c.slot_ev[k][0];
+        slots[k].t0 = c.slot_ev[k][1];
+        slots[k].t1 = c.slot_ev[k][2];
     }
-    struct EventGuard {
-        Slot* s;
-        ~EventGuard() {
-            for (int k = 0; k < 2; ++k) {
-                cudaEventDestroy(s[k].done);
-                cudaEventDestroy(s[k].t0);
-                cudaEventDestroy(s[k].t1);
-            }
-        }
-    } guard{slots};
 
     // batches are fetched once each, in order; at most two are held
     DT held[2];
@@ -1398,6 +1407,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         const int64_t l0 = c.launches;
         sl.started = std::chrono::steady_clock::now();
         sl.dsc = c.alloc(4);
+        mark();
         double* mapped_dev = c.d_map + (sl.mapped - c.h_map);
         if (!launch_skip_encode3(c, h, sl.y, target, sl.dsc->p, &sl.latent, c.profile ? sl.t0 : nullptr,
                                  c.profile ? sl.t1 : nullptr, c.nccl_comm ? nullptr : mapped_dev))
@@ -1410,6 +1420,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
             HTR_CUDA(cudaMemcpyAsync(sl.host, sl.dsc->p, 3 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
         }
         HTR_CUDA(cudaEventRecord(sl.done, c.s));
+        mark();
         sl.launches = c.launches - l0;
         sl.index = i;
         return true;
@@ -1493,6 +1504,15 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         slots[cs ^ 1].dsc.reset();
     }
     HTR_CUDA(cudaStreamSynchronize(c.s));
+    if (timeline && tl.size() >= 2) {
+        for (size_t k = 0; k + 1 < tl.size(); k += 2) {
+            float busy = 0.f, gap = 0.f;
+            HTR_CUDA(cudaEventElapsedTime(&busy, tl[k], tl[k + 1]));
+            if (k + 2 < tl.size()) HTR_CUDA(cudaEventElapsedTime(&gap, tl[k + 1], tl[k + 2]));
+            std::fprintf(stderr, "timeline launch %zu: %.4f ms, then %.4f ms to the next\n", k / 2, busy, gap);
+        }
+        for (cudaEvent_t e : tl) cudaEventDestroy(e);
+    }
     return res;
 }
 

@@ -109,6 +109,8 @@ struct Context {
     unsigned int* d_ticket = nullptr;  // last-CTA ticket of the fused tail (kept zero between launches)
     // timing of the fused encode kernel and of the generic GEMMs
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // the stream API's two in-flight slots: done, fused start, fused end
+    cudaEvent_t slot_ev[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
     double fused_ms = 0.0, gemm_ms = 0.0;
     int64_t fused_calls = 0, gemm_calls = 0;
     // batch-axis sharding over NCCL (dlopen'd)

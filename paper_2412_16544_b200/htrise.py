@@ -34,6 +34,7 @@ import ctypes as C
 import math
 import os
 from dataclasses import dataclass, field
+from collections.abc import Sequence as _SequenceABC
 from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
@@ -722,14 +723,40 @@ def ht_rise_update_many(h: HTRepresentation, batches, epsilon_rel: Optional[floa
     if code:
         ctx.check(code)
     del args
-    values, reports = [], []
+    values = []
     acc = h._acc
     for i in range(n):
         if acc is not None:
             acc += int(shapes[i * order + order - 1]) * ctx.world
         values.append(HTRepresentation(_P(outs[i]), ctx, h._tree, h._dims, acc, h._eps))
-        reports.append(_update_report(reps[i]))
-    return values, reports
+    return values, _Reports(reps)
+
+
+class _Reports(_SequenceABC):
+    """The reports of ht_rise_update_many, decoded from the C structs on first
+    access (the call returns as soon as the device work is done)."""
+
+    def __init__(self, raw):
+        self._raw = raw
+        self._done: Dict[int, UpdateReport] = {}
+
+    def __len__(self):
+        return len(self._raw)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        r = self._done.get(i)
+        if r is None:
+            r = self._done[i] = _update_report(self._raw[i])
+        return r
+
+    def __eq__(self, other):
+        return list(self) == list(other)
 
 
 def _latent_shape(h: HTRepresentation, batch: int):
