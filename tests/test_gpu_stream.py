@@ -149,3 +149,28 @@ def test_stream_empty_and_errors(ht):
     # the input value is untouched by the failed stream
     r, _ = ht.ht_rise_update(rep0, batches[1])
     assert r.accumulated == rep0.accumulated + 2
+
+
+def test_stream_single_rank_nccl_matches_local(ht):
+    """The stream API on the sharded runtime path: with a 1-rank NCCL
+    communicator the skip norms and batch count go through ncclAllReduce and
+    a D2H copy instead of the tail's mapped-memory write; results must equal
+    the plain context's bit for bit (skips, an expansion, root slices)."""
+    rng = np.random.default_rng(1212)
+    plain = ht.Context(0)
+    comm = ht.Context(0)
+    comm.init_comm(ht.comm_unique_id(), 1, 0)
+    batches = _family_stream(7, rng, grow_at=(3,))
+    tree = ht.tree_1_23()
+    outs = []
+    for c in (plain, comm):
+        r0, _ = ht.bht_l2r(batches[0], tree, 1e-3, ctx=c)
+        r0.reserve(64)
+        outs.append(ht.ht_rise_update_many(r0, [_dev(ht, b) for b in batches[1:]]))
+    (va, ua), (vb, ub) = outs
+    for a, b in zip(ua, ub):
+        _same_report(a, b)
+    assert any(not u.skipped for u in ua) and any(u.skipped for u in ua)
+    assert np.array_equal(va[-1].root(), vb[-1].root())
+    plain.close()
+    comm.close()
