@@ -29,11 +29,14 @@ for name in a.configs.split(","):
         fused += upd.used_fused_path
         del yb
     gb = w.bytes_per_batch / 1e9
+    med = sorted(skip_t)[len(skip_t) // 2] if skip_t else None
     row = {"config": name, "batch_GB": round(gb, 4), "bht_l2r_ms": round(1e3 * t_bht, 2),
            "updates": nb - 1, "skips": len(skip_t), "fused_path": fused,
+           "skip_ms_median": round(1e3 * med, 3) if skip_t else None,
            "skip_ms_mean": round(1e3 * sum(skip_t) / len(skip_t), 3) if skip_t else None,
+           "skip_ms_first": round(1e3 * skip_t[0], 3) if skip_t else None,
            "nonskip_ms_mean": round(1e3 * sum(full_t) / len(full_t), 3) if full_t else None,
-           "skip_GBps": round(gb / (sum(skip_t) / len(skip_t)), 1) if skip_t else None,
+           "skip_GBps_median": round(gb / med, 1) if skip_t else None,
            "ranks": {str(k): v for k, v in rep.ranks().items()}}
     rows.append(row)
     print(json.dumps(row), flush=True)
