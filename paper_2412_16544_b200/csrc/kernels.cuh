@@ -172,6 +172,31 @@ struct Tail3Args {
     int csize = 1;    // CTAs per sample (a thread-block cluster), set by the launcher
 };
 bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2);
+
+// Balanced 4-leaf subtree over 4 consecutive modes of extent 8, all ranks 4
+// (config 4): every contiguous 8^4 block o of X (O blocks, 16-byte aligned)
+// -> the subtree root's 4 outputs out[(o % P) + P (c + 4 (o / P))], through
+// the 4 leaf projections and the 3 transfers. The first launch over y writes
+// per-CTA ||y||^2 partials; the finishing launch writes per-CTA ||out||^2
+// partials and its last CTA sc[0] = ||y||^2, sc[2] = ||out||^2.
+struct QuadArgs {
+    const double* X = nullptr;
+    int64_t O = 0, P = 1;
+    const double* U[4] = {nullptr, nullptr, nullptr, nullptr};  // 8 x 4 leaf bases
+    const double* T01 = nullptr;  // 16 x 4 basis of the transfer over leaves 0,1
+    const double* T23 = nullptr;  // leaves 2,3
+    const double* T = nullptr;    // the subtree root (over the two transfers)
+    double* out = nullptr;
+    double* partials = nullptr;   // >= grid entries
+    const double* ysq_partials = nullptr;  // finishing launch: the first launch's partials
+    int64_t n_ysq = 0;
+    double* sc = nullptr;
+    double* host_out = nullptr;
+    unsigned int* ticket = nullptr;
+};
+bool quad_supported(int64_t extent, int64_t rank);
+/// Returns the grid size (number of partials written), -1 for an unaligned X.
+int launch_quad(const QuadArgs& a, bool finish, int num_sms, cudaStream_t s, int64_t* launches);
 void launch_tail3(const Tail3Args& a, cudaStream_t s, int64_t* launches);
 
 }  // namespace htr

@@ -963,6 +963,78 @@ bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent
     return true;
 }
 
+bool launch_skip_encode8(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc, DT* latent,
+                         cudaEvent_t ev0, cudaEvent_t ev1, double* host_out) {
+    const DimensionTree& tree = h.tree;
+    if (tree.dims() != 8 || tree.depth() != 3) return false;
+    for (int k = 0; k < 8; ++k)
+        if (y.shape[static_cast<size_t>(k)] != 8) return false;
+    const RankMap ranks = h.ranks();
+    for (const auto& [id, r] : ranks)
+        if (id.layer > 0 && !quad_supported(8, r)) return false;
+    // the two layer-1 subtrees: transfers over transfers over leaves m..m+3
+    QuadArgs q[2];
+    for (int side = 0; side < 2; ++side) {
+        const TreeNode& root = tree.node(NodeId{1, side});
+        if (root.kind != NodeKind::Transfer) return false;
+        const TreeNode* mid[2];
+        for (int j = 0; j < 2; ++j) {
+            mid[j] = &tree.node(root.successors[static_cast<size_t>(j)]);
+            if (mid[j]->kind != NodeKind::Transfer) return false;
+            for (int k = 0; k < 2; ++k) {
+                const TreeNode& leaf = tree.node(mid[j]->successors[static_cast<size_t>(k)]);
+                if (leaf.kind != NodeKind::Leaf || leaf.leaf_dim != 4 * side + 2 * j + k) return false;
+                q[side].U[2 * j + k] = h.core(leaf.id).data();
+            }
+        }
+        q[side].T01 = h.core(mid[0]->id).data();
+        q[side].T23 = h.core(mid[1]->id).data();
+        q[side].T = h.core(root.id).data();
+    }
+    const int64_t batch = y.shape[8];
+    // first half: modes 0-3 (contiguous 8^4 blocks of y) -> [8^4 (modes 4-7), 4, batch]
+    if ((reinterpret_cast<uintptr_t>(y.data()) & 15u) != 0) return false;
+    DT mid = c.tensor({8, 8, 8, 8, 4, batch});
+    BufPtr yparts = c.alloc(c.num_sms);
+    q[0].X = y.data();
+    q[0].O = 4096 * batch;
+    q[0].P = 4096;
+    q[0].out = mid.data();
+    q[0].partials = yparts->p;
+    if (ev0) HTR_CUDA(cudaEventRecord(ev0, c.s));
+    const int g0 = launch_quad(q[0], false, c.num_sms, c.s, &c.launches);
+    if (ev1) HTR_CUDA(cudaEventRecord(ev1, c.s));
+    HTR_CUDA(cudaGetLastError());
+    // second half: blocks (c, s) of mid over modes 4-7 -> the latent [4, 4, batch]
+    DT lat;
+    if (latent_target && latent_target->shape == Shape{4, 4, batch}) {
+        lat = *latent_target;
+    } else {
+        lat = c.tensor({4, 4, batch});
+    }
+    BufPtr lparts = c.alloc(c.num_sms);
+    q[1].X = mid.data();
+    q[1].O = 4 * batch;
+    q[1].P = 4;
+    q[1].out = lat.data();
+    q[1].partials = lparts->p;
+    q[1].ysq_partials = yparts->p;
+    q[1].n_ysq = g0;
+    q[1].sc = sc;
+    q[1].host_out = host_out;
+    q[1].ticket = c.d_ticket;
+    launch_quad(q[1], true, c.num_sms, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+    *latent = lat;
+    return true;
+}
+
+bool launch_skip_encode_fused(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc,
+                              DT* latent, cudaEvent_t ev0, cudaEvent_t ev1, double* host_out) {
+    return launch_skip_encode3(c, h, y, latent_target, sc, latent, ev0, ev1, host_out) ||
+           launch_skip_encode8(c, h, y, latent_target, sc, latent, ev0, ev1, host_out);
+}
+
 EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* latent_target) {
     const DimensionTree& tree = h.tree;
     const Index d = tree.dims(), p = tree.depth();
@@ -1024,6 +1096,13 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
                     cur = Z;
                 }
             }
+        }
+    } else if (!exact && c.fused && d == 8) {
+        DT lat;
+        if (launch_skip_encode8(c, h, y, latent_target, sc, &lat, c.profile ? c.ev[0] : nullptr,
+                                c.profile ? c.ev[1] : nullptr, c.nccl_comm ? nullptr : c.d_map)) {
+            leaves_done = tail_done = out.fused = true;
+            cur = lat;
         }
     }
     bool ysq_fused = false;  // ||y||^2 taken during the first projection (one read of y)
@@ -1393,9 +1472,9 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
     // launch batch i against h's bases with its latent at root slice `at`
     auto launch = [&](Slot& sl, const Rep& h, int64_t i, int64_t at) -> bool {
         sl.index = -1;
-        if (!c.fused || c.exact_loss || d != 3) return false;
+        if (!c.fused || c.exact_loss || (d != 3 && d != 8)) return false;
         sl.y = batch(i);
-        const int64_t nb = sl.y.shape[3];
+        const int64_t nb = sl.y.shape[static_cast<size_t>(d)];
         DT slot;
         const DT* target = nullptr;
         if (const auto& rs = h.root; rs && rs->committed == h.acc && at + nb <= rs->cap) {
@@ -1409,8 +1488,8 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         sl.dsc = c.alloc(4);
         mark();
         double* mapped_dev = c.d_map + (sl.mapped - c.h_map);
-        if (!launch_skip_encode3(c, h, sl.y, target, sl.dsc->p, &sl.latent, c.profile ? sl.t0 : nullptr,
-                                 c.profile ? sl.t1 : nullptr, c.nccl_comm ? nullptr : mapped_dev))
+        if (!launch_skip_encode_fused(c, h, sl.y, target, sl.dsc->p, &sl.latent, c.profile ? sl.t0 : nullptr,
+                                      c.profile ? sl.t1 : nullptr, c.nccl_comm ? nullptr : mapped_dev))
             return false;
         if (c.nccl_comm) {
             // the global batch count rides on the skip test's all-reduce
@@ -1431,7 +1510,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
     // non-finite input)
     auto decide = [&](Slot& sl, const Rep& h) -> std::shared_ptr<Rep> {
         HTR_CUDA(cudaEventSynchronize(sl.done));
-        const int64_t nb = sl.y.shape[3];
+        const int64_t nb = sl.y.shape[static_cast<size_t>(d)];
         const double* v = c.nccl_comm ? sl.host : sl.mapped;
         const double ysq = v[0], latsq = v[2];
         const int64_t gbatch = c.nccl_comm ? static_cast<int64_t>(std::llround(sl.host[1])) : nb;
@@ -1487,7 +1566,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         }
         // batch i+1 against the same bases, its latent right after batch i's
         const bool ahead =
-            i + 1 < n && launch(slots[cs ^ 1], *cur, i + 1, cur->acc + slots[cs].y.shape[3]);
+            i + 1 < n && launch(slots[cs ^ 1], *cur, i + 1, cur->acc + slots[cs].y.shape[static_cast<size_t>(d)]);
         if (auto next = decide(slots[cs], *cur)) {
             cur = next;
             cs ^= 1;

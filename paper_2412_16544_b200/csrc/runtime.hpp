@@ -220,6 +220,13 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
 /// same two scalars.
 bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc, DT* latent,
                          cudaEvent_t ev0, cudaEvent_t ev1, double* host_out = nullptr);
+/// The same for 8-way balanced trees with extents 8 and ranks 4 (two
+/// 4-leaf subtree launches, config 4).
+bool launch_skip_encode8(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc, DT* latent,
+                         cudaEvent_t ev0, cudaEvent_t ev1, double* host_out = nullptr);
+/// Whichever fused skip-path encode applies (3-way or 8-way); false when none.
+bool launch_skip_encode_fused(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc,
+                              DT* latent, cudaEvent_t ev0, cudaEvent_t ev1, double* host_out = nullptr);
 
 /// A stream of updates h -> h1 -> ... -> hn, identical to n ht_rise_update
 /// calls (extension: the reference's caller loops over batches, main.cpp).

@@ -449,6 +449,46 @@ def test_pair_projection_matches_generic(ht, dims, ranks):
     assert ug.skipped == ur.skipped
 
 
+def test_quad_subtree_fused_matches_generic(ht):
+    """8-way balanced trees with extents 8 and ranks 4 (config 4's shape) take
+    the fused 4-leaf-subtree encode (two launches); its latent and skip test
+    must equal the generic per-mode chain, and the stream must follow the
+    oracle's decisions."""
+    from paper_2412_16544_b200.workloads import CONFIGS
+    import dataclasses
+
+    w = dataclasses.replace(CONFIGS["c4"], batch=3)
+    shape = tuple(w.dims) + (w.batch,)
+    y0 = w.make_batch(0, "cuda")
+    rep, _ = ht.bht_l2r(ht.DeviceTensor(y0, shape), w.tree(), w.eps)
+    assert all(r == 4 for r in rep.ranks().values())
+    y1 = w.make_batch(1, "cuda")
+    ctx = rep.ctx
+    la, pa = ht.encode(rep, ht.DeviceTensor(y1, shape))
+    ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+    try:
+        lb, pb = ht.encode(rep, ht.DeviceTensor(y1, shape))
+    finally:
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    assert la.shape == lb.shape == (4, 4, 3)
+    assert np.linalg.norm(la - lb) <= 1e-12 * np.linalg.norm(lb)
+    assert abs(pa - pb) <= 1e-6 * pb
+    r2, ug = ht.ht_rise_update(rep, ht.DeviceTensor(y1, shape))
+    assert ug.used_fused_path or ug.used_exact_loss
+    ref, _ = ho.bht_l2r(_host(y0, shape), _oracle_tree(w), w.eps)
+    r2o, uo = ho.ht_rise_update(ref, _host(y1, shape))
+    assert ug.skipped == uo.skipped
+    assert r2.ranks() == r2o.ranks()
+    for m in (1, r2.accumulated):
+        a, b = ht.reconstruct_slice(r2, m), ho.reconstruct_slice(r2o, m)
+        assert np.linalg.norm(a - b) <= 1e-9 * np.linalg.norm(b)
+    # a non-finite entry surfaces through the fused ||y||^2
+    bad = y1.clone()
+    bad.view(-1)[12345] = float("nan")
+    with pytest.raises(ValueError, match="non-finite"):
+        ht.ht_rise_update(rep, ht.DeviceTensor(bad, shape))
+
+
 def test_fused_path_rejects_non_finite_input(ht):
     """A NaN / Inf in the batch shows up in the fused kernel's ||y||^2; the
     runtime re-scans and raises like the reference (bht.hpp:189-211)."""
