@@ -174,3 +174,31 @@ def test_stream_single_rank_nccl_matches_local(ht):
     assert np.array_equal(va[-1].root(), vb[-1].root())
     plain.close()
     comm.close()
+
+
+def test_stream_ragged_batches_and_options(ht):
+    """Batches of different sizes (the root slot of a speculative batch moves
+    with the previous batch's size), an explicit epsilon and the adaptive
+    budget: still identical to the per-call loop."""
+    rng = np.random.default_rng(4242)
+    bases = [ro.random_orthonormal(64, 8, rng) for _ in range(3)]
+    sizes = [4, 1, 3, 6, 2, 5, 1]
+    batches = []
+    for k, n in enumerate(sizes):
+        b = [u[:, : (4 if k < 4 else 6)] for u in bases]  # growth at batch 4
+        y = ro.tucker_family_batch(b, n, rng)
+        batches.append(np.asfortranarray(y + 1e-7 * rng.standard_normal(y.shape)))
+    for eps, adaptive in ((None, False), (2e-3, False), (None, True)):
+        rep0, _ = ht.bht_l2r(batches[0], ht.tree_1_23(), 1e-3)
+        rep0.reserve(64)
+        args = [_dev(ht, b) for b in batches[1:]]
+        r, seq = rep0, []
+        for a in args:
+            r, u = ht.ht_rise_update(r, a, epsilon_rel=eps, adaptive_budget=adaptive)
+            seq.append((r, u))
+        many, reports = ht.ht_rise_update_many(rep0, args, epsilon_rel=eps, adaptive_budget=adaptive)
+        for (rs, us), rm, um in zip(seq, many, reports):
+            _same_report(us, um)
+            assert rs.accumulated == rm.accumulated
+        assert np.array_equal(many[-1].root(), seq[-1][0].root())
+        assert any(u.skipped for u in reports) and not all(u.skipped for u in reports)
