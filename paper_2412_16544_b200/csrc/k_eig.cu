@@ -25,6 +25,26 @@ __device__ __forceinline__ int tour_pos(int i, int round, int m) {
 }
 constexpr int64_t kSmemMaxN = 112;  // 2 * 112^2 * 8 B = 196 KB of shared memory
 
+/// Jacobi rotation for the pair (p, q), or (c, s) = (1, 0) when a_pq is
+/// negligible: relative to the diagonal (|a_pq| <= 1e-15 sqrt(|a_pp a_qq|),
+/// the classical test) or absolutely, below 2^-60 of the input's trace. The
+/// Gram the solver receives already carries ~n u tr(G) of rounding error, so
+/// chasing smaller off-diagonal entries (rotations among noise-level
+/// eigenvalues) only burns sweeps; without the absolute floor a Gram with a
+/// noise-level tail never meets the relative test and runs all 40 sweeps.
+__device__ __forceinline__ bool jacobi_rotation(double app, double aqq, double apq, double floor_abs, double* c_out,
+                                                double* s_out) {
+    if (!(fabs(apq) > floor_abs && fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq)))) return false;
+    const double tau = (aqq - app) / (2.0 * apq);
+    double t;
+    if (fabs(tau) > 1e150) t = 0.5 / tau;
+    else t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+    const double c = 1.0 / sqrt(1.0 + t * t);
+    *c_out = c;
+    *s_out = t * c;
+    return true;
+}
+
 __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __restrict__ G, int n,
                                                                 double* __restrict__ lambda,
                                                                 double* __restrict__ Vout, double* gwork,
@@ -48,6 +68,14 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
     __syncthreads();
 
     const int half = m / 2;
+    __shared__ double tr_abs;
+    if (tid == 0) {
+        double t = 0.0;
+        for (int i = 0; i < n; ++i) t += fabs(A[i + static_cast<int64_t>(n) * i]);
+        tr_abs = t;
+    }
+    __syncthreads();
+    const double floor_abs = 0x1p-60 * tr_abs;
     for (int sweep = 0; sweep < 40; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
@@ -57,62 +85,58 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
                 int p = tour_pos(i, round, m), q = tour_pos(m - 1 - i, round, m);
                 if (p > q) { const int t = p; p = q; q = t; }
                 double c = 1.0, s = 0.0;
-                if (q < n) {
-                    const double app = A[p + static_cast<int64_t>(n) * p];
-                    const double aqq = A[q + static_cast<int64_t>(n) * q];
-                    const double apq = A[p + static_cast<int64_t>(n) * q];
-                    if (fabs(apq) > 1e-300 && fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
-                        const double tau = (aqq - app) / (2.0 * apq);
-                        double t;
-                        if (fabs(tau) > 1e150) t = 0.5 / tau;
-                        else t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                        c = 1.0 / sqrt(1.0 + t * t);
-                        s = t * c;
-                        rotated = 1;
-                    }
-                }
+                if (q < n &&
+                    jacobi_rotation(A[p + static_cast<int64_t>(n) * p], A[q + static_cast<int64_t>(n) * q],
+                                    A[p + static_cast<int64_t>(n) * q], floor_abs, &c, &s))
+                    rotated = 1;
                 cs[i] = c; sn[i] = s; prs[i] = p; qrs[i] = q;
             }
             __syncthreads();
-            // phase 2: rows p, q of A  (A <- J^T A)
-            const int64_t items = static_cast<int64_t>(half) * n;
-            for (int64_t it = tid; it < items; it += nt) {
-                const int i = static_cast<int>(it / n), j = static_cast<int>(it % n);
-                const double s = sn[i];
-                if (s == 0.0) continue;
-                const double c = cs[i];
-                const int p = prs[i], q = qrs[i];
-                const double ap = A[p + static_cast<int64_t>(n) * j], aq = A[q + static_cast<int64_t>(n) * j];
-                A[p + static_cast<int64_t>(n) * j] = c * ap - s * aq;
-                A[q + static_cast<int64_t>(n) * j] = s * ap + c * aq;
-            }
-            __syncthreads();
-            // phase 3: columns p, q of A and V  (A <- A J, V <- V J)
-            for (int64_t it = tid; it < items; it += nt) {
-                const int i = static_cast<int>(it / n), j = static_cast<int>(it % n);
-                const double s = sn[i];
-                if (s == 0.0) continue;
-                const double c = cs[i];
-                const int p = prs[i], q = qrs[i];
-                double* cp = A + static_cast<int64_t>(n) * p;
-                double* cq = A + static_cast<int64_t>(n) * q;
-                const double ap = cp[j], aq = cq[j];
-                cp[j] = c * ap - s * aq;
-                cq[j] = s * ap + c * aq;
-                double* vp = V + static_cast<int64_t>(n) * p;
-                double* vq = V + static_cast<int64_t>(n) * q;
-                const double xp = vp[j], xq = vq[j];
-                vp[j] = c * xp - s * xq;
-                vq[j] = s * xp + c * xq;
-            }
-            __syncthreads();
-            // the annihilated pair entries are exactly zero by construction
-            for (int i = tid; i < half; i += nt) {
-                if (sn[i] != 0.0) {
-                    const int p = prs[i], q = qrs[i];
-                    A[p + static_cast<int64_t>(n) * q] = 0.0;
-                    A[q + static_cast<int64_t>(n) * p] = 0.0;
+            // phase 2: 2x2 blocks (P, Q): A' = J_P^T A J_Q over rows {p_P, q_P},
+            // columns {p_Q, q_Q} in one pass, and V's column pairs
+            const int blocks = half * half;
+            for (int b = tid; b < blocks; b += nt) {
+                const int P = b % half, Q = b / half;
+                const int pP = prs[P], qP = qrs[P], pQ = prs[Q], qQ = qrs[Q];
+                const double cP = cs[P], sP = sn[P], cQ = cs[Q], sQ = sn[Q];
+                if ((sP == 0.0 && sQ == 0.0) || (qP >= n && qQ >= n)) continue;
+                if (qP >= n) {  // row pair padded: only the column rotation of row pP
+                    double* r0 = A + pP;
+                    const double x = r0[static_cast<int64_t>(n) * pQ], y = r0[static_cast<int64_t>(n) * qQ];
+                    r0[static_cast<int64_t>(n) * pQ] = cQ * x - sQ * y;
+                    r0[static_cast<int64_t>(n) * qQ] = sQ * x + cQ * y;
+                    continue;
                 }
+                if (qQ >= n) {  // column pair padded: only the row rotation of column pQ
+                    double* col = A + static_cast<int64_t>(n) * pQ;
+                    const double x = col[pP], y = col[qP];
+                    col[pP] = cP * x - sP * y;
+                    col[qP] = sP * x + cP * y;
+                    continue;
+                }
+                double* a_pp = A + pP + static_cast<int64_t>(n) * pQ;
+                double* a_pq = A + pP + static_cast<int64_t>(n) * qQ;
+                double* a_qp = A + qP + static_cast<int64_t>(n) * pQ;
+                double* a_qq = A + qP + static_cast<int64_t>(n) * qQ;
+                const double x00 = *a_pp, x01 = *a_pq, x10 = *a_qp, x11 = *a_qq;
+                const double y00 = cP * x00 - sP * x10, y01 = cP * x01 - sP * x11;
+                const double y10 = sP * x00 + cP * x10, y11 = sP * x01 + cP * x11;
+                double z00 = cQ * y00 - sQ * y01, z01 = sQ * y00 + cQ * y01;
+                double z10 = cQ * y10 - sQ * y11, z11 = sQ * y10 + cQ * y11;
+                if (P == Q && sP != 0.0) { z01 = 0.0; z10 = 0.0; }  // annihilated pair
+                *a_pp = z00; *a_pq = z01; *a_qp = z10; *a_qq = z11;
+            }
+            const int vitems = half * n;
+            for (int it = tid; it < vitems; it += nt) {
+                const int Q = it / n, r = it - Q * n;
+                const double s = sn[Q];
+                if (s == 0.0) continue;
+                const double c = cs[Q];
+                double* vp = V + static_cast<int64_t>(n) * prs[Q] + r;
+                double* vq = V + static_cast<int64_t>(n) * qrs[Q] + r;
+                const double x = *vp, y = *vq;
+                *vp = c * x - s * y;
+                *vq = s * x + c * y;
             }
             __syncthreads();
         }
@@ -173,6 +197,14 @@ __global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kClusterT
     const int m = n + (n & 1);
     const int half = m / 2;
     cluster_sync_all();
+    __shared__ double tr_abs;
+    if (tid == 0) {
+        double t = 0.0;
+        for (int i = 0; i < n; ++i) t += fabs(A[i + static_cast<int64_t>(n) * i]);
+        tr_abs = t;  // identical in every CTA (same inputs, same order)
+    }
+    __syncthreads();
+    const double floor_abs = 0x1p-60 * tr_abs;
 
     for (int sweep = 0; sweep < 40; ++sweep) {
         if (tid == 0) rotated = 0;
@@ -182,20 +214,10 @@ __global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kClusterT
                 int p = tour_pos(i, round, m), q = tour_pos(m - 1 - i, round, m);
                 if (p > q) { const int t = p; p = q; q = t; }
                 double c = 1.0, s = 0.0;
-                if (q < n) {
-                    const double app = A[p + static_cast<int64_t>(n) * p];
-                    const double aqq = A[q + static_cast<int64_t>(n) * q];
-                    const double apq = A[p + static_cast<int64_t>(n) * q];
-                    if (fabs(apq) > 1e-300 && fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
-                        const double tau = (aqq - app) / (2.0 * apq);
-                        double t;
-                        if (fabs(tau) > 1e150) t = 0.5 / tau;
-                        else t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                        c = 1.0 / sqrt(1.0 + t * t);
-                        s = t * c;
-                        rotated = 1;
-                    }
-                }
+                if (q < n &&
+                    jacobi_rotation(A[p + static_cast<int64_t>(n) * p], A[q + static_cast<int64_t>(n) * q],
+                                    A[p + static_cast<int64_t>(n) * q], floor_abs, &c, &s))
+                    rotated = 1;
                 cs[i] = c; sn[i] = s; prs[i] = p; qrs[i] = q;
             }
             __syncthreads();
