@@ -23,15 +23,19 @@ __device__ __forceinline__ int tour_pos(int i, int round, int m) {
     if (k < 0) k += m - 1;
     return 1 + k;
 }
-constexpr int64_t kSmemMaxN = 112;  // 2 * 112^2 * 8 B = 196 KB of shared memory
+constexpr int64_t kSmemMaxN = 112;   // A and V in shared memory: 2 * 112^2 * 8 B = 196 KB
+constexpr int64_t kSmemMaxNA = 160;  // A alone in shared memory (200 KB), V in global memory
 
 /// Jacobi rotation for the pair (p, q), or (c, s) = (1, 0) when a_pq is
 /// negligible: relative to the diagonal (|a_pq| <= 1e-15 sqrt(|a_pp a_qq|),
-/// the classical test) or absolutely, below 2^-60 of the input's trace. The
-/// Gram the solver receives already carries ~n u tr(G) of rounding error, so
-/// chasing smaller off-diagonal entries (rotations among noise-level
-/// eigenvalues) only burns sweeps; without the absolute floor a Gram with a
-/// noise-level tail never meets the relative test and runs all 40 sweeps.
+/// the classical test) or absolutely, below 2^-53 (= u) of the input's
+/// trace. The Gram the solver receives already carries ~n u tr(G) of
+/// rounding error and every rotation leaves ~u max|A| in the entries it
+/// touches, so chasing smaller off-diagonal entries (rotations among
+/// noise-level eigenvalues) only burns sweeps; without the absolute floor a
+/// Gram with a noise-level tail never meets the relative test and runs all
+/// 40 sweeps. (Tight-eps truncations re-measure the small eigenvalues through
+/// a second, projected Gram, whose own trace sets its floor.)
 __device__ __forceinline__ bool jacobi_rotation(double app, double aqq, double apq, double floor_abs, double* c_out,
                                                 double* s_out) {
     if (!(fabs(apq) > floor_abs && fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq)))) return false;
@@ -48,15 +52,17 @@ __device__ __forceinline__ bool jacobi_rotation(double app, double aqq, double a
 __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __restrict__ G, int n,
                                                                 double* __restrict__ lambda,
                                                                 double* __restrict__ Vout, double* gwork,
-                                                                int in_smem) {
+                                                                int a_smem, int v_smem) {
     extern __shared__ double smem[];
     __shared__ double cs[512], sn[512];
     __shared__ int prs[512], qrs[512];
     __shared__ int rotated;
 
     const int tid = threadIdx.x, nt = blockDim.x;
-    double* A = in_smem ? smem : gwork;
-    double* V = in_smem ? smem + static_cast<int64_t>(n) * n : gwork + static_cast<int64_t>(n) * n;
+    // A in shared memory up to n = 160; V too up to n = 112, else in global
+    // memory (touched only by this CTA: bar.sync orders its updates)
+    double* A = a_smem ? smem : gwork;
+    double* V = v_smem ? smem + static_cast<int64_t>(n) * n : gwork + static_cast<int64_t>(n) * n;
     const int64_t nn = static_cast<int64_t>(n) * n;
     for (int64_t i = tid; i < nn; i += nt) {
         const int64_t r = i % n, c = i / n;
@@ -75,7 +81,7 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
         tr_abs = t;
     }
     __syncthreads();
-    const double floor_abs = 0x1p-60 * tr_abs;
+    const double floor_abs = 0x1p-53 * tr_abs;
     for (int sweep = 0; sweep < 40; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
@@ -167,7 +173,7 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
 // barrier (release/acquire orders the global-memory updates).
 // --------------------------------------------------------------------------
 constexpr int kClusterCTAs = 8;
-constexpr int kClusterThreads = 1024;
+constexpr int kClusterThreads = 512;
 
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -204,7 +210,7 @@ __global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kClusterT
         tr_abs = t;  // identical in every CTA (same inputs, same order)
     }
     __syncthreads();
-    const double floor_abs = 0x1p-60 * tr_abs;
+    const double floor_abs = 0x1p-53 * tr_abs;
 
     for (int sweep = 0; sweep < 40; ++sweep) {
         if (tid == 0) rotated = 0;
@@ -223,54 +229,84 @@ __global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kClusterT
             __syncthreads();
             // every CTA finished reading A for the rotations before anyone writes
             cluster_sync_all();
-            // 2x2 blocks (P, Q): A' = J_P^T A J_Q over rows {p_P, q_P}, cols {p_Q, q_Q}
-            const int64_t blocks = static_cast<int64_t>(half) * half;
-            for (int64_t b = gtid; b < blocks; b += gnt) {
-                const int P = static_cast<int>(b / half), Q = static_cast<int>(b % half);
-                const int pP = prs[P], qP = qrs[P], pQ = prs[Q], qQ = qrs[Q];
-                if (qP >= n && qQ >= n) continue;
-                const double cP = cs[P], sP = sn[P], cQ = cs[Q], sQ = sn[Q];
-                if (sP == 0.0 && sQ == 0.0) continue;
-                if (qP >= n) {  // row pair padded: only the column rotation of row pP
-                    double* r0 = A + pP;
-                    const double x = r0[static_cast<int64_t>(n) * pQ], y = r0[static_cast<int64_t>(n) * qQ];
-                    r0[static_cast<int64_t>(n) * pQ] = cQ * x - sQ * y;
-                    r0[static_cast<int64_t>(n) * qQ] = sQ * x + cQ * y;
-                    continue;
+            // 2x2 blocks (P, Q): A' = J_P^T A J_Q over rows {p_P, q_P}, cols
+            // {p_Q, q_Q}, then V's column pairs. Items are disjoint, so each
+            // thread issues the loads of kBatch items before any store (A and
+            // V are in L2: one round trip per batch instead of per item). A
+            // padded pair (q = n, odd n) has s = 0, so its rotation is the
+            // identity and only its in-range entries are touched.
+            constexpr int kBatch = 2;
+            const int blocks = half * half;
+            for (int b0 = gtid; b0 < blocks; b0 += kBatch * gnt) {
+                double x[kBatch][4];
+                int off[kBatch][4];  // n <= 2048: n^2 fits 32 bits
+                bool live[kBatch], okr[kBatch], okc[kBatch];
+                double c_p[kBatch], s_p[kBatch], c_q[kBatch], s_q[kBatch];
+                bool diag[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const int b = b0 + u * gnt;
+                    live[u] = false;
+                    if (b >= blocks) continue;
+                    const int P = b / half, Q = b - P * half;
+                    c_p[u] = cs[P]; s_p[u] = sn[P]; c_q[u] = cs[Q]; s_q[u] = sn[Q];
+                    if (s_p[u] == 0.0 && s_q[u] == 0.0) continue;
+                    const int pP = prs[P], qP = qrs[P], pQ = prs[Q], qQ = qrs[Q];
+                    okr[u] = qP < n;
+                    okc[u] = qQ < n;
+                    diag[u] = P == Q;
+                    live[u] = true;
+                    off[u][0] = pP + n * pQ;
+                    off[u][1] = pP + n * qQ;
+                    off[u][2] = qP + n * pQ;
+                    off[u][3] = qP + n * qQ;
+                    x[u][0] = A[off[u][0]];
+                    x[u][1] = okc[u] ? A[off[u][1]] : 0.0;
+                    x[u][2] = okr[u] ? A[off[u][2]] : 0.0;
+                    x[u][3] = (okr[u] && okc[u]) ? A[off[u][3]] : 0.0;
                 }
-                if (qQ >= n) {  // column pair padded: only the row rotation of column pQ
-                    double* col = A + static_cast<int64_t>(n) * pQ;
-                    const double x = col[pP], y = col[qP];
-                    col[pP] = cP * x - sP * y;
-                    col[qP] = sP * x + cP * y;
-                    continue;
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    if (!live[u]) continue;
+                    const double cP = c_p[u], sP = s_p[u], cQ = c_q[u], sQ = s_q[u];
+                    const double y00 = cP * x[u][0] - sP * x[u][2], y01 = cP * x[u][1] - sP * x[u][3];
+                    const double y10 = sP * x[u][0] + cP * x[u][2], y11 = sP * x[u][1] + cP * x[u][3];
+                    double z00 = cQ * y00 - sQ * y01, z01 = sQ * y00 + cQ * y01;
+                    double z10 = cQ * y10 - sQ * y11, z11 = sQ * y10 + cQ * y11;
+                    if (diag[u] && sP != 0.0) { z01 = 0.0; z10 = 0.0; }  // annihilated pair
+                    A[off[u][0]] = z00;
+                    if (okc[u]) A[off[u][1]] = z01;
+                    if (okr[u]) A[off[u][2]] = z10;
+                    if (okr[u] && okc[u]) A[off[u][3]] = z11;
                 }
-                double* a_pp = A + pP + static_cast<int64_t>(n) * pQ;
-                double* a_pq = A + pP + static_cast<int64_t>(n) * qQ;
-                double* a_qp = A + qP + static_cast<int64_t>(n) * pQ;
-                double* a_qq = A + qP + static_cast<int64_t>(n) * qQ;
-                const double x00 = *a_pp, x01 = *a_pq, x10 = *a_qp, x11 = *a_qq;
-                // rows: J_P^T
-                const double y00 = cP * x00 - sP * x10, y01 = cP * x01 - sP * x11;
-                const double y10 = sP * x00 + cP * x10, y11 = sP * x01 + cP * x11;
-                // columns: J_Q
-                double z00 = cQ * y00 - sQ * y01, z01 = sQ * y00 + cQ * y01;
-                double z10 = cQ * y10 - sQ * y11, z11 = sQ * y10 + cQ * y11;
-                if (P == Q && sP != 0.0) { z01 = 0.0; z10 = 0.0; }  // annihilated pair
-                *a_pp = z00; *a_pq = z01; *a_qp = z10; *a_qq = z11;
             }
-            // V <- V J (column pairs)
-            const int64_t vitems = static_cast<int64_t>(half) * n;
-            for (int64_t it = gtid; it < vitems; it += gnt) {
-                const int Q = static_cast<int>(it / n), r = static_cast<int>(it % n);
-                const double s = sn[Q];
-                if (s == 0.0) continue;
-                const double c = cs[Q];
-                double* vp = V + static_cast<int64_t>(n) * prs[Q] + r;
-                double* vq = V + static_cast<int64_t>(n) * qrs[Q] + r;
-                const double x = *vp, y = *vq;
-                *vp = c * x - s * y;
-                *vq = s * x + c * y;
+            // V <- V J (column pairs), batched the same way
+            const int vitems = half * n;
+            for (int i0 = gtid; i0 < vitems; i0 += kBatch * gnt) {
+                double vx[kBatch], vy[kBatch], vc[kBatch], vs[kBatch];
+                int vpp[kBatch], vqq[kBatch];
+                bool vl[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const int it = i0 + u * gnt;
+                    vl[u] = false;
+                    if (it >= vitems) continue;
+                    const int Q = it / n, r = it - Q * n;
+                    vs[u] = sn[Q];
+                    if (vs[u] == 0.0) continue;
+                    vc[u] = cs[Q];
+                    vpp[u] = n * prs[Q] + r;
+                    vqq[u] = n * qrs[Q] + r;
+                    vx[u] = V[vpp[u]];
+                    vy[u] = V[vqq[u]];
+                    vl[u] = true;
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    if (!vl[u]) continue;
+                    V[vpp[u]] = vc[u] * vx[u] - vs[u] * vy[u];
+                    V[vqq[u]] = vs[u] * vx[u] + vc[u] * vy[u];
+                }
             }
             cluster_sync_all();
         }
@@ -387,25 +423,26 @@ __global__ void __launch_bounds__(512) orthonormalize_kernel(const double* U, in
 
 void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, double* work, cudaStream_t s,
                        int64_t* launches) {
-    if (n > kSmemMaxN) {
+    if (n > kSmemMaxNA) {
         jacobi_cluster_kernel<<<kClusterCTAs, kClusterThreads, 0, s>>>(G, static_cast<int>(n), lambda, V, work,
                                                                        work + n * n);
         ++*launches;
         return;
     }
-    const bool in_smem = n <= kSmemMaxN;
-    const size_t smem = in_smem ? 2 * sizeof(double) * static_cast<size_t>(n * n) : 0;
+    const bool v_smem = n <= kSmemMaxN;
+    const size_t smem = (v_smem ? 2 : 1) * sizeof(double) * static_cast<size_t>(n * n);
     // static + dynamic shared memory above 48 KB needs the opt-in (the
     // kernel's static arrays take ~17 KB): raise the limit once to the
     // largest in-smem problem
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(2 * sizeof(double) * kSmemMaxN * kSmemMaxN));
+                             static_cast<int>(sizeof(double) * std::max(2 * kSmemMaxN * kSmemMaxN,
+                                                                        kSmemMaxNA * kSmemMaxNA)));
         configured = true;
     }
     const int threads = n <= 32 ? 128 : (n <= 64 ? 256 : kJacobiThreads);
-    jacobi_kernel<<<1, threads, smem, s>>>(G, static_cast<int>(n), lambda, V, work, in_smem ? 1 : 0);
+    jacobi_kernel<<<1, threads, smem, s>>>(G, static_cast<int>(n), lambda, V, work, 1, v_smem ? 1 : 0);
     ++*launches;
 }
 
