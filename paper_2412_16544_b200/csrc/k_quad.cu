@@ -38,9 +38,9 @@ constexpr int kQBlock = QN * QN * QN * QN;  // elements per subtree block
 // rows are read with the same rotation). P1 partials are reduced over the 4
 // j-lanes by shuffles, then mode e2 runs per chunk and modes e3 + the
 // transfers per block, as above.
-constexpr int kQ2Warps = 12;
+constexpr int kQ2Warps = 8;
 constexpr int kQ2Threads = kQ2Warps * 32;
-constexpr int kQ2Stages = 2;
+constexpr int kQ2Stages = 3;
 constexpr int kQ2Chunk = 512;                        // doubles (4 KB): one e3 slice of a block
 constexpr int kQ2Scratch = 128 + 512 + 256 + 64 + 16;  // S1 (one chunk), S2, S3, V01, V
 
@@ -100,8 +100,18 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
 
     const int e2 = lane >> 2, j = lane & 3;
     // rotation of the 16-byte parts read (conflict-free: the 8 lanes of a
-    // quarter-warp cover the 8 16-byte slots of a 128-byte window)
+    // quarter-warp cover the 8 16-byte slots of a 128-byte window); the lane's
+    // copy of U0 is held in registers in the same rotated order
     const int rot = ((j >> 1) | ((e2 & 1) << 1)) & 3;
+    double ur[QN / 2][2][QR];  // [step v][e0 parity][q] for part (v + rot) & 3
+#pragma unroll
+    for (int v = 0; v < QN / 2; ++v) {
+        const int part = (v + rot) & 3;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q = 0; q < QR; ++q) ur[v][h][q] = Us[0][(2 * part + h) * QR + q];
+    }
     double ysv[QN / 2] = {0.0, 0.0, 0.0, 0.0};  // independent chains
     for (int64_t g = 0; g < chunks; ++g) {
         const int st = static_cast<int>(g % kQ2Stages);
@@ -126,18 +136,11 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
             for (int v = 0; v < QN / 2; ++v) {
                 const int part = (v + rot) & 3;  // e0 = 2 part, 2 part + 1
                 const double2 x2 = *reinterpret_cast<const double2*>(ch + QN * e1 + 2 * part);
-                const double2 ua = *reinterpret_cast<const double2*>(&Us[0][(2 * part) * QR]);
-                const double2 ub = *reinterpret_cast<const double2*>(&Us[0][(2 * part) * QR + 2]);
-                const double2 uc = *reinterpret_cast<const double2*>(&Us[0][(2 * part + 1) * QR]);
-                const double2 ud = *reinterpret_cast<const double2*>(&Us[0][(2 * part + 1) * QR + 2]);
-                p0[0] = fma(ua.x, x2.x, p0[0]);
-                p0[1] = fma(ua.y, x2.x, p0[1]);
-                p0[2] = fma(ub.x, x2.x, p0[2]);
-                p0[3] = fma(ub.y, x2.x, p0[3]);
-                p0[0] = fma(uc.x, x2.y, p0[0]);
-                p0[1] = fma(uc.y, x2.y, p0[1]);
-                p0[2] = fma(ud.x, x2.y, p0[2]);
-                p0[3] = fma(ud.y, x2.y, p0[3]);
+#pragma unroll
+                for (int q = 0; q < QR; ++q) {
+                    p0[q] = fma(ur[v][0][q], x2.x, p0[q]);
+                    p0[q] = fma(ur[v][1][q], x2.y, p0[q]);
+                }
                 if constexpr (!FINISH) {
                     ysv[v] = fma(x2.x, x2.x, ysv[v]);
                     ysv[v] = fma(x2.y, x2.y, ysv[v]);
@@ -158,23 +161,25 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             if (g + kQ2Stages < chunks) issue(g + kQ2Stages);
         }
-        // reduce P1 over the 4 j-lanes of this e2 (fixed butterfly order)
+        // reduce-scatter P1 over the 4 j-lanes of this e2 (fixed order): lane
+        // j ends with the sums of row x0 = j, which is what it stores.
+        // Level 1 (partner j ^ 1): keep rows with x0 & 1 == j & 1.
+        const bool odd = (j & 1) != 0, up = (j & 2) != 0;
+        double h[2][QR];  // rows x0 = (j & 1) and (j & 1) + 2
 #pragma unroll
-        for (int x0 = 0; x0 < QR; ++x0)
+        for (int t = 0; t < 2; ++t)
 #pragma unroll
             for (int x1 = 0; x1 < QR; ++x1) {
-                double v = p1[x0][x1];
-                v += __shfl_xor_sync(0xffffffffu, v, 1);
-                v += __shfl_xor_sync(0xffffffffu, v, 2);
-                p1[x0][x1] = v;
+                const double keep = odd ? p1[2 * t + 1][x1] : p1[2 * t][x1];
+                const double send = odd ? p1[2 * t][x1] : p1[2 * t + 1][x1];
+                h[t][x1] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
             }
-        // lane j stores 4 of the 16 values: S1[k16 + 16 e2], k16 = x0 + 4 x1
+        // level 2 (partner j ^ 2): keep row x0 = j
 #pragma unroll
         for (int x1 = 0; x1 < QR; ++x1) {
-            double v = 0.0;
-#pragma unroll
-            for (int x0 = 0; x0 < QR; ++x0) v = (x0 == j) ? p1[x0][x1] : v;
-            S1[(j + QR * x1) + 16 * e2] = v;
+            const double keep = up ? h[1][x1] : h[0][x1];
+            const double send = up ? h[0][x1] : h[1][x1];
+            S1[(j + QR * x1) + 16 * e2] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
         }
         __syncwarp();
         // mode e2 for this e3: S2[k16 + 16 (a2 + 4 e3)] (64 outputs, 2 per lane)
