@@ -113,10 +113,12 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
             for (int q = 0; q < QR; ++q) ur[v][h][q] = Us[0][(2 * part + h) * QR + q];
     }
     double ysv[QN / 2] = {0.0, 0.0, 0.0, 0.0};  // independent chains
+    // ring slot / phase and the chunk's e3 advance incrementally (no 64-bit
+    // division per chunk)
+    int st = 0, k3 = 0;
+    uint32_t parity = 0;
+    int64_t o = gw;  // block of the current chunk
     for (int64_t g = 0; g < chunks; ++g) {
-        const int st = static_cast<int>(g % kQ2Stages);
-        const int k3 = static_cast<int>(g % QN);  // e3 of this chunk
-        const uint32_t parity = static_cast<uint32_t>((g / kQ2Stages) & 1);
         asm volatile(
             "{\n\t.reg .pred p;\nWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n}\n" ::"r"(
                 q_smem(&bar[st])),
@@ -198,9 +200,17 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
             }
         }
         __syncwarp();
-        if (k3 != QN - 1) continue;
+        const bool block_done = k3 == QN - 1;
+        if (++st == kQ2Stages) {
+            st = 0;
+            parity ^= 1u;
+        }
+        if (!block_done) {
+            ++k3;
+            continue;
+        }
+        k3 = 0;
         // ---- block complete: mode e3, then the transfers ----
-        const int64_t o = gw + (g / QN) * nw;
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
             const int jj = lane + 32 * t;
@@ -243,6 +253,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
             if constexpr (FINISH) ysv[0] = fma(v, v, ysv[0]);
         }
         __syncwarp();
+        o += nw;
     }
     // FINISH: the partials are of ||out||^2 (ysv[0] of lanes 0-3)
     double ys = (ysv[0] + ysv[1]) + (ysv[2] + ysv[3]);
