@@ -432,7 +432,8 @@ int dispatch_mt(int mt, const Fused3Args& a, int num_sms, cudaStream_t s, int64_
 
 bool fused3_supported(int64_t n0, int64_t n1, int64_t n2, int r0, int r1, int r2) {
     (void)n2;
-    if ((n0 != 64 && n0 != 128) || (n1 != 64 && n1 != 128)) return false;
+    const bool sq32 = n0 == 32 && n1 == 32;  // leading 32 x 32 slabs (config 3's modes 0, 1)
+    if (!sq32 && ((n0 != 64 && n0 != 128) || (n1 != 64 && n1 != 128))) return false;
     if (r0 < 1 || r1 < 1 || r2 < 1 || r0 > 24 || r1 > 24) return false;
     return true;
 }
@@ -454,6 +455,7 @@ int launch_fused3(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cuda
     if (n0 == 64 && n1 == 64) return dispatch_mt<64, 64>(mt, a, num_sms, s, launches);
     if (n0 == 128 && n1 == 64) return dispatch_mt<128, 64>(mt, a, num_sms, s, launches);
     if (n0 == 64 && n1 == 128) return dispatch_mt<64, 128>(mt, a, num_sms, s, launches);
+    if (n0 == 32 && n1 == 32) return dispatch_mt<32, 32>(mt, a, num_sms, s, launches);
     return -1;
 }
 

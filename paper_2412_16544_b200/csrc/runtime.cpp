@@ -1113,6 +1113,48 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
             const TreeNode& n = lay[q];
             const int mode = static_cast<int>(n.leaf_dim);
             const bool first = q == 0;
+            if (!exact && c.fused && first && mode == 0 && q + 1 < lay.size() && lay[q + 1].kind == NodeKind::Leaf &&
+                lay[q + 1].leaf_dim == 1) {
+                // leaves of modes 0 and 1 in one pass on the FP64 tensor cores:
+                // fused3 over [n0, n1, rest] slabs writes the projected tensor
+                // (r0 x r1 per slab, canonical) and ||y||^2 (config 3)
+                const Basis b0 = basis_of(h, n.id), b1 = basis_of(h, lay[q + 1].id);
+                const int64_t J0 = cur.shape[0], J1 = cur.shape[1];
+                const int64_t rest = cur.size() / (J0 * J1);
+                if (fused3_supported(J0, J1, rest, static_cast<int>(b0.r), static_cast<int>(b1.r), 1) &&
+                    (reinterpret_cast<uintptr_t>(cur.data()) & 15u) == 0) {
+                    Shape os = cur.shape;
+                    os[0] = b0.r;
+                    os[1] = b1.r;
+                    DT lo = c.tensor(os);
+                    Fused3Args fa;
+                    fa.Y = cur.data();
+                    fa.n2 = rest;
+                    fa.S = 1;
+                    fa.U0 = b0.p;
+                    fa.U1 = b1.p;
+                    fa.r0 = static_cast<int>(b0.r);
+                    fa.r1 = static_cast<int>(b1.r);
+                    fa.r2 = 1;
+                    fa.slab_gemm = false;
+                    fa.wslab = lo.data();
+                    const int64_t R01 = b0.r * b1.r;
+                    BufPtr parts = c.alloc(c.num_sms + static_cast<int64_t>(c.num_sms) * 24 * R01);
+                    fa.ysq_partials = parts->p;
+                    if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[0], c.s));
+                    const int grid = launch_fused3(J0, J1, fa, c.num_sms, c.s, &c.launches);
+                    if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[1], c.s));
+                    HTR_CUDA(cudaGetLastError());
+                    if (grid > 0) {
+                        launch_sum_partials(parts->p, grid, sc + 0, c.s, &c.launches);
+                        ysq_fused = true;
+                        out.fused = true;
+                        cur = lo;
+                        q += 2;
+                        continue;
+                    }
+                }
+            }
             if (!exact && c.fused && q + 1 < lay.size() && lay[q + 1].kind == NodeKind::Leaf &&
                 lay[q + 1].leaf_dim == n.leaf_dim + 1) {
                 // two adjacent small leaves in one pass over the tensor

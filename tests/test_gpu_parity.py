@@ -489,6 +489,30 @@ def test_quad_subtree_fused_matches_generic(ht):
         ht.ht_rise_update(rep, ht.DeviceTensor(bad, shape))
 
 
+def test_leading_modes_fused_matches_generic(ht):
+    """Trees whose deepest layer starts with the leaves of modes 0 and 1
+    (config 3's balanced(4) over 32 x 32 x 32 x 8) project both in one fused
+    pass over 32 x 32 slabs; latents and the skip test must equal the
+    generic per-mode chain, before and after rank growth."""
+    from paper_2412_16544_b200.workloads import CONFIGS
+
+    w = CONFIGS["c3"]
+    rep, _ = ht.bht_l2r(ht.DeviceTensor(w.make_batch(0, "cuda"), w.shape), w.tree(), w.eps)
+    ctx = rep.ctx
+    for b in (1, 24):
+        yb = w.make_batch(b, "cuda")
+        la, pa = ht.encode(rep, ht.DeviceTensor(yb, w.shape))
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+        try:
+            lb, pb = ht.encode(rep, ht.DeviceTensor(yb, w.shape))
+        finally:
+            ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+        assert np.linalg.norm(la - lb) <= 1e-12 * np.linalg.norm(lb)
+        assert abs(pa - pb) <= 1e-6 * pb
+        rep, u = ht.ht_rise_update(rep, ht.DeviceTensor(yb, w.shape))
+    assert not u.skipped  # batch 24: the six new components switch on
+
+
 def test_fused_path_rejects_non_finite_input(ht):
     """A NaN / Inf in the batch shows up in the fused kernel's ||y||^2; the
     runtime re-scans and raises like the reference (bht.hpp:189-211)."""
