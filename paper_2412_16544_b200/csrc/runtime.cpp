@@ -710,7 +710,7 @@ namespace {
 /// is added there; with ysq_slot ||t||^2 is written there when the streaming
 /// kernel runs (*ysq_done reports whether it did).
 DT project(Context& c, const DT& t, int mode, const Basis& b, double* energy_slot, double* ysq_slot = nullptr,
-           bool* ysq_done = nullptr) {
+           bool* ysq_done = nullptr, const DT* dst = nullptr) {
     if (b.alpha != t.shape[static_cast<size_t>(mode)])
         raise(HTR_ERR_INVALID_ARGUMENT, "mode_multiply: factor/extent mismatch");
     const Split sp = split_at(t.shape, mode);
@@ -732,6 +732,17 @@ DT project(Context& c, const DT& t, int mode, const Basis& b, double* energy_slo
             HTR_CUDA(cudaGetLastError());
             if (ysq_done) *ysq_done = ysq_slot != nullptr;
             return coeff;
+        }
+    }
+    if (dst && !energy_slot) {
+        // straight into caller memory (a skip's latent into the root store's
+        // next slices): the returned view is the caller's, so a later root
+        // append sees it in place
+        Shape os = t.shape;
+        os[static_cast<size_t>(mode)] = b.r;
+        if (dst->shape == os) {
+            mode_mul(c, t, mode, b.p, b.r, b.alpha, 1, dst->data());
+            return *dst;
         }
     }
     DT coeff = mode_mul(c, t, mode, b.p, b.r, b.alpha, 1);  // U^T
@@ -1192,10 +1203,17 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
     }
     for (Index l = p - 1; l >= 1 && !tail_done; --l) {
         cur.shape = layer_extents(h, l, ranks, batch, leaves_done);
+        // the last projection of layer 1 yields the latent: written into the
+        // root store's next slices when the caller provides them
+        Index last = -1;
+        for (Index j = 0; j < tree.layer_size(l); ++j)
+            if (!(leaves_done && tree.layer(l)[static_cast<size_t>(j)].kind == NodeKind::Leaf)) last = j;
         for (Index j = 0; j < tree.layer_size(l); ++j) {
             const TreeNode& n = tree.layer(l)[static_cast<size_t>(j)];
             if (leaves_done && n.kind == NodeKind::Leaf) continue;
-            cur = project(c, cur, static_cast<int>(j), basis_of(h, n.id), exact ? sc + 16 + nslots++ : nullptr);
+            const DT* dst = (l == 1 && j == last && !exact) ? latent_target : nullptr;
+            cur = project(c, cur, static_cast<int>(j), basis_of(h, n.id), exact ? sc + 16 + nslots++ : nullptr,
+                          nullptr, nullptr, dst);
         }
     }
     out.latent = cur;
