@@ -1046,20 +1046,25 @@ bool launch_skip_encode_fused(Context& c, const Rep& h, const DT& y, const DT* l
            launch_skip_encode8(c, h, y, latent_target, sc, latent, ev0, ev1, host_out);
 }
 
-EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* latent_target) {
+EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* latent_target, double* sc_deferred) {
     const DimensionTree& tree = h.tree;
     const Index d = tree.dims(), p = tree.depth();
     const int64_t batch = y.shape[static_cast<size_t>(d)];
     EncodeOut out;
     out.exact = exact;
     const RankMap ranks = h.ranks();
-    double* sc = c.d_sc->p;  // [0] ysq, [1] nonfinite, [2] latent^2, [16..] step energies
+    // [0] ysq, [1] nonfinite, [2] latent^2, [16..] step energies
+    double* sc = sc_deferred ? sc_deferred : c.d_sc->p;
     int nslots = 0;
+    // (the context's events and mapped block are not per call: a deferred
+    // encode uses neither)
+    const bool prof = c.profile && !sc_deferred;
+    double* host_out = (c.nccl_comm || sc_deferred) ? nullptr : c.d_map;
     // the generic kernels accumulate into the scalar slots; the fused
     // leaf+tail path assigns sc[0] and sc[2] and needs no clearing
     bool zeroed = false;
     auto zero_scalars = [&] {
-        if (!zeroed) HTR_CUDA(cudaMemsetAsync(sc, 0, 512 * sizeof(double), c.s));
+        if (!zeroed) HTR_CUDA(cudaMemsetAsync(sc, 0, (sc_deferred ? 16 : 512) * sizeof(double), c.s));
         zeroed = true;
     };
 
@@ -1068,8 +1073,8 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
     bool tail_done = false;  // latent and ||latent||^2 already produced
     if (!exact && c.fused && d == 3) {
         DT lat;
-        if (launch_skip_encode3(c, h, y, latent_target, sc, &lat, c.profile ? c.ev[0] : nullptr,
-                                c.profile ? c.ev[1] : nullptr, c.nccl_comm ? nullptr : c.d_map)) {
+        if (launch_skip_encode3(c, h, y, latent_target, sc, &lat, prof ? c.ev[0] : nullptr,
+                                prof ? c.ev[1] : nullptr, host_out)) {
             // fused leaves + tail: ((1,(2,3)) trees)
             leaves_done = tail_done = out.fused = true;
             cur = lat;
@@ -1096,9 +1101,9 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
                 BufPtr w = c.alloc(ws);
                 fa.wslab = w->p;
                 fa.ysq_partials = w->p + fa.n2 * batch * static_cast<int64_t>(t.r0) * t.r1;
-                if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[0], c.s));
+                if (prof) HTR_CUDA(cudaEventRecord(c.ev[0], c.s));
                 const int grid = launch_fused3(y.shape[0], y.shape[1], fa, c.num_sms, c.s, &c.launches);
-                if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[1], c.s));
+                if (prof) HTR_CUDA(cudaEventRecord(c.ev[1], c.s));
                 HTR_CUDA(cudaGetLastError());
                 if (grid > 0) {  // else (no tensor map for this pointer): generic kernels below
                     launch_sum_partials(fa.ysq_partials, grid, sc + 0, c.s, &c.launches);
@@ -1110,8 +1115,8 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
         }
     } else if (!exact && c.fused && d == 8) {
         DT lat;
-        if (launch_skip_encode8(c, h, y, latent_target, sc, &lat, c.profile ? c.ev[0] : nullptr,
-                                c.profile ? c.ev[1] : nullptr, c.nccl_comm ? nullptr : c.d_map)) {
+        if (launch_skip_encode8(c, h, y, latent_target, sc, &lat, prof ? c.ev[0] : nullptr,
+                                prof ? c.ev[1] : nullptr, host_out)) {
             leaves_done = tail_done = out.fused = true;
             cur = lat;
         }
@@ -1152,9 +1157,9 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
                     const int64_t R01 = b0.r * b1.r;
                     BufPtr parts = c.alloc(c.num_sms + static_cast<int64_t>(c.num_sms) * 24 * R01);
                     fa.ysq_partials = parts->p;
-                    if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[0], c.s));
+                    if (prof) HTR_CUDA(cudaEventRecord(c.ev[0], c.s));
                     const int grid = launch_fused3(J0, J1, fa, c.num_sms, c.s, &c.launches);
-                    if (c.profile) HTR_CUDA(cudaEventRecord(c.ev[1], c.s));
+                    if (prof) HTR_CUDA(cudaEventRecord(c.ev[1], c.s));
                     HTR_CUDA(cudaGetLastError());
                     if (grid > 0) {
                         launch_sum_partials(parts->p, grid, sc + 0, c.s, &c.launches);
@@ -1227,6 +1232,10 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
     BufPtr parts2 = c.alloc(kReduceBlocks);
     if (!tail_done) launch_sumsq(cur.data(), cur.size(), parts2->p, sc + 2, c.s, &c.launches);  // sc[2], sc[3]
     HTR_CUDA(cudaGetLastError());
+    if (sc_deferred) {
+        out.scan_valid = ysq_scanned;
+        return out;
+    }
     if (c.nccl_comm) {
         // the global batch count rides on the same all-reduce (slot 8)
         c.h_sc[8] = static_cast<double>(batch);
@@ -1242,7 +1251,7 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
         c.fetch(sc, 16 + nslots, c.h_sc);
     }
     out.gbatch = c.nccl_comm ? static_cast<int64_t>(std::llround(c.h_sc[8])) : batch;
-    if (c.profile && leaves_done) {
+    if (prof && leaves_done) {
         float ms = 0.f;
         HTR_CUDA(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
         c.fused_ms += ms;
@@ -1492,6 +1501,9 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         BufPtr dsc;       // [0] ||y||^2, [1] batch count (sharded), [2] ||latent||^2
         double* host = nullptr;  // pinned copy of dsc[0..2]
         double* mapped = nullptr;  // mapped host block the tail writes dsc[0], dsc[2] to
+        bool fused = false;        // launched through the fused skip-path kernels
+        bool used_fused = false;   // (report) any fused kernel in the encode
+        bool scan_valid = false;   // dsc[1] is the non-finite flag of a full scan
         cudaEvent_t done = nullptr, t0 = nullptr, t1 = nullptr;
         int64_t launches = 0;
         std::chrono::steady_clock::time_point started;
@@ -1532,7 +1544,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
     // launch batch i against h's bases with its latent at root slice `at`
     auto launch = [&](Slot& sl, const Rep& h, int64_t i, int64_t at) -> bool {
         sl.index = -1;
-        if (!c.fused || c.exact_loss || (d != 3 && d != 8)) return false;
+        if (c.exact_loss) return false;  // per-step energies: the per-call path
         sl.y = batch(i);
         const int64_t nb = sl.y.shape[static_cast<size_t>(d)];
         DT slot;
@@ -1545,19 +1557,30 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         }
         const int64_t l0 = c.launches;
         sl.started = std::chrono::steady_clock::now();
-        sl.dsc = c.alloc(4);
+        sl.dsc = c.alloc(16);  // [0] ||y||^2, [1] non-finite flag, [2] ||latent||^2, [8] batch count
         mark();
         double* mapped_dev = c.d_map + (sl.mapped - c.h_map);
-        if (!launch_skip_encode_fused(c, h, sl.y, target, sl.dsc->p, &sl.latent, c.profile ? sl.t0 : nullptr,
-                                      c.profile ? sl.t1 : nullptr, c.nccl_comm ? nullptr : mapped_dev))
-            return false;
+        sl.fused = c.fused && launch_skip_encode_fused(c, h, sl.y, target, sl.dsc->p, &sl.latent,
+                                                       c.profile ? sl.t0 : nullptr, c.profile ? sl.t1 : nullptr,
+                                                       c.nccl_comm ? nullptr : mapped_dev);
+        sl.used_fused = sl.fused;
+        sl.scan_valid = false;
+        if (!sl.fused) {
+            // any other tree: the per-call encode, enqueued only (its scalars
+            // land in the slot's block and are read back below)
+            EncodeOut e = encode(c, h, sl.y, false, target, sl.dsc->p);
+            sl.latent = e.latent;
+            sl.used_fused = e.fused;
+            sl.scan_valid = e.scan_valid;
+        }
         if (c.nccl_comm) {
             // the global batch count rides on the skip test's all-reduce
             sl.host[8] = static_cast<double>(nb);
-            HTR_CUDA(cudaMemcpyAsync(sl.dsc->p + 1, sl.host + 8, sizeof(double), cudaMemcpyHostToDevice, c.s));
-            c.allreduce(sl.dsc->p, 3);
-            HTR_CUDA(cudaMemcpyAsync(sl.host, sl.dsc->p, 3 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+            HTR_CUDA(cudaMemcpyAsync(sl.dsc->p + 8, sl.host + 8, sizeof(double), cudaMemcpyHostToDevice, c.s));
+            c.allreduce(sl.dsc->p, 9);
         }
+        if (c.nccl_comm || !sl.fused)
+            HTR_CUDA(cudaMemcpyAsync(sl.host, sl.dsc->p, 9 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
         HTR_CUDA(cudaEventRecord(sl.done, c.s));
         mark();
         sl.launches = c.launches - l0;
@@ -1571,10 +1594,11 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
     auto decide = [&](Slot& sl, const Rep& h) -> std::shared_ptr<Rep> {
         HTR_CUDA(cudaEventSynchronize(sl.done));
         const int64_t nb = sl.y.shape[static_cast<size_t>(d)];
-        const double* v = c.nccl_comm ? sl.host : sl.mapped;
+        const double* v = (c.nccl_comm || !sl.fused) ? sl.host : sl.mapped;
         const double ysq = v[0], latsq = v[2];
-        const int64_t gbatch = c.nccl_comm ? static_cast<int64_t>(std::llround(sl.host[1])) : nb;
-        if (c.profile) {
+        const int64_t gbatch = c.nccl_comm ? static_cast<int64_t>(std::llround(v[8])) : nb;
+        if (sl.scan_valid && v[1] != 0.0) return nullptr;  // non-finite input: the per-call path raises
+        if (c.profile && sl.fused) {
             float ms = 0.f;
             HTR_CUDA(cudaEventElapsedTime(&ms, sl.t0, sl.t1));
             c.fused_ms += ms;
@@ -1596,7 +1620,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         r.skipped = 1;
         r.proj_error = proj_error;
         r.eps_des = eps_des;
-        r.used_fused_path = 1;
+        r.used_fused_path = sl.used_fused ? 1 : 0;
         int k = 0;
         for (const auto& [id, rk] : out->ranks()) {
             if (k >= HTR_MAX_NODES) break;

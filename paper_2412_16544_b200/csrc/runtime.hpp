@@ -201,11 +201,17 @@ struct EncodeOut {
     bool exact = false;
     bool nonfinite = false;
     int64_t gbatch = 0;     // samples of this batch over all ranks (same all-reduce)
+    bool scan_valid = false;  // deferred: sc[1] carries the non-finite flag of a full ||y||^2 scan
 };
 /// `latent_target`, when given, is where the fused tail writes the latent if
 /// it runs (a view of the root store's next free slices): a skip decision
 /// then only commits it.
-EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* latent_target = nullptr);
+/// With `sc_deferred` (16 device doubles) the encode only enqueues its work:
+/// ||y||^2 -> sc[0], the non-finite flag -> sc[1] (when scan_valid),
+/// ||latent||^2 -> sc[2]; the caller all-reduces and reads them back (the
+/// stream API's pipelining). EncodeOut then carries the latent only.
+EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* latent_target = nullptr,
+                 double* sc_deferred = nullptr);
 
 struct UpdateOut {
     std::shared_ptr<Rep> rep;

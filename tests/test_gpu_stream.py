@@ -124,14 +124,22 @@ def test_stream_consecutive_expansions(ht):
     assert sum(not u.skipped for u in reports) >= 2
 
 
-def test_stream_generic_tree_falls_back(ht):
-    # a 4-way balanced tree is outside the fused kernels: every batch takes
-    # the per-call path and the results are still identical
+def test_stream_generic_tree(ht):
+    # a 4-way balanced tree of extent 10 is outside the fused kernels: the
+    # stream enqueues the generic encode (deferred scalars) one batch ahead;
+    # the results are still identical to the per-call loop
     rng = np.random.default_rng(31)
     bases = [ro.random_orthonormal(10, 3, rng) for _ in range(4)]
     batches = [np.asfortranarray(ro.tucker_family_batch(bases, 3, rng)) for _ in range(5)]
     rep0, _ = ht.bht_l2r(batches[0], ht.DimensionTree.balanced(4), 1e-6)
-    _check_stream(ht, rep0, batches[1:], True)
+    _, reports = _check_stream(ht, rep0, batches[1:], True)
+    assert all(u.skipped for u in reports)
+    # a non-finite entry: the deferred encode's scan flags it, the per-call
+    # path raises
+    bad = batches[2].copy()
+    bad[1, 2, 3, 1] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        ht.ht_rise_update_many(rep0, [_dev(ht, batches[1]), _dev(ht, bad)])
 
 
 def test_stream_empty_and_errors(ht):

@@ -12,7 +12,7 @@ from paper_2412_16544_b200 import htrise as ht
 from paper_2412_16544_b200.workloads import CONFIGS
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-w = CONFIGS["c5"]
+w = CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "c5"]
 ctx = ht.Context(0)
 ht.set_default_context(ctx)
 y0 = w.make_batch(0, "cuda")
