@@ -46,8 +46,11 @@ constexpr int kQ2Scratch = 128 + 512 + 256 + 64 + 16;  // S1 (one chunk), S2, S3
 
 __device__ __forceinline__ uint32_t q_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
-template <bool FINISH>
+template <bool FINISH, bool SPLIT>
 __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadArgs a) {
+    // SPLIT (few blocks: the finishing launch): one CTA per block, warp w
+    // takes chunk w (e3 = w); warp 0 finishes the block after a CTA barrier
+    static_assert(!SPLIT || kQ2Warps == QN, "one chunk per warp");
     __shared__ double Us[4][QN * QR];
     __shared__ double Ts[3][QR * QR * QR];
     __shared__ double red[kQ2Warps];
@@ -66,7 +69,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
     }
     double* ring = dyn + warp * kQ2Stages * kQ2Chunk;
     double* S1 = dyn + kQ2Warps * kQ2Stages * kQ2Chunk + warp * kQ2Scratch;  // [k16][e2]
-    double* S2 = S1 + 128;   // [k16][a2][e3]
+    double* S2 = (SPLIT ? dyn + kQ2Warps * kQ2Stages * kQ2Chunk : S1) + 128;  // [k16][a2][e3] (CTA-shared in SPLIT)
     double* S3 = S2 + 512;   // [(a0,a1,a2)][a3]
     double* V01 = S3 + 256;
     double* V = V01 + 64;
@@ -76,11 +79,11 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
     const int64_t gw = static_cast<int64_t>(blockIdx.x) * kQ2Warps + warp;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kQ2Warps;
     const int64_t my_units = gw < units ? (units - gw + nw - 1) / nw : 0;
-    const int64_t chunks = my_units * QN;
+    const int64_t chunks = SPLIT ? (blockIdx.x < units ? 1 : 0) : my_units * QN;
     auto issue = [&](int64_t g) {  // lane 0: chunk g of this warp's sequence
         const int st = static_cast<int>(g % kQ2Stages);
-        const int64_t o = gw + (g / QN) * nw;
-        const double* src = a.X + kQBlock * o + kQ2Chunk * (g % QN);
+        const int64_t o = SPLIT ? static_cast<int64_t>(blockIdx.x) : gw + (g / QN) * nw;
+        const double* src = a.X + kQBlock * o + kQ2Chunk * (SPLIT ? warp : static_cast<int>(g % QN));
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(q_smem(&bar[st])),
                      "r"(kQ2Chunk * 8)
                      : "memory");
@@ -113,11 +116,57 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
             for (int q = 0; q < QR; ++q) ur[v][h][q] = Us[0][(2 * part + h) * QR + q];
     }
     double ysv[QN / 2] = {0.0, 0.0, 0.0, 0.0};  // independent chains
+    // modes e3 and the three transfers of a completed block (one warp)
+    auto finish_block = [&](int64_t ob) {
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int jj = lane + 32 * t;
+            double acc[QR] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int e3 = 0; e3 < QN; ++e3) {
+                const double v = S2[jj + 64 * e3];
+#pragma unroll
+                for (int q = 0; q < QR; ++q) acc[q] = fma(Us[3][e3 * QR + q], v, acc[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < QR; ++q) S3[jj + 64 * q] = acc[q];
+        }
+        __syncwarp();
+        {
+            const int b = lane & 3, m0 = lane >> 2;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int m = m0 + 8 * t;
+                double v = 0.0;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) v = fma(Ts[0][k * QR + b], S3[k + 16 * m], v);
+                V01[b + QR * m] = v;
+            }
+        }
+        __syncwarp();
+        if (lane < 16) {
+            const int b01 = lane & 3, b23 = lane >> 2;
+            double v = 0.0;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) v = fma(Ts[1][m * QR + b23], V01[b01 + QR * m], v);
+            V[b01 + QR * b23] = v;
+        }
+        __syncwarp();
+        if (lane < QR) {
+            double v = 0.0;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v = fma(Ts[2][k * QR + lane], V[k], v);
+            a.out[(ob % a.P) + a.P * (lane + QR * (ob / a.P))] = v;
+            if constexpr (FINISH) ysv[0] = fma(v, v, ysv[0]);
+        }
+        __syncwarp();
+    };
+
     // ring slot / phase and the chunk's e3 advance incrementally (no 64-bit
     // division per chunk)
-    int st = 0, k3 = 0;
+    int st = 0, k3 = SPLIT ? warp : 0;
     uint32_t parity = 0;
-    int64_t o = gw;  // block of the current chunk
+    int64_t o = SPLIT ? static_cast<int64_t>(blockIdx.x) : gw;  // block of the current chunk
     for (int64_t g = 0; g < chunks; ++g) {
         asm volatile(
             "{\n\t.reg .pred p;\nWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n}\n" ::"r"(
@@ -200,6 +249,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
             }
         }
         __syncwarp();
+        if constexpr (SPLIT) continue;  // the block is finished after the loop
         const bool block_done = k3 == QN - 1;
         if (++st == kQ2Stages) {
             st = 0;
@@ -210,50 +260,12 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
             continue;
         }
         k3 = 0;
-        // ---- block complete: mode e3, then the transfers ----
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int jj = lane + 32 * t;
-            double acc[QR] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int e3 = 0; e3 < QN; ++e3) {
-                const double v = S2[jj + 64 * e3];
-#pragma unroll
-                for (int q = 0; q < QR; ++q) acc[q] = fma(Us[3][e3 * QR + q], v, acc[q]);
-            }
-#pragma unroll
-            for (int q = 0; q < QR; ++q) S3[jj + 64 * q] = acc[q];
-        }
-        __syncwarp();
-        {
-            const int b = lane & 3, m0 = lane >> 2;
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const int m = m0 + 8 * t;
-                double v = 0.0;
-#pragma unroll
-                for (int k = 0; k < 16; ++k) v = fma(Ts[0][k * QR + b], S3[k + 16 * m], v);
-                V01[b + QR * m] = v;
-            }
-        }
-        __syncwarp();
-        if (lane < 16) {
-            const int b01 = lane & 3, b23 = lane >> 2;
-            double v = 0.0;
-#pragma unroll
-            for (int m = 0; m < 16; ++m) v = fma(Ts[1][m * QR + b23], V01[b01 + QR * m], v);
-            V[b01 + QR * b23] = v;
-        }
-        __syncwarp();
-        if (lane < QR) {
-            double v = 0.0;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) v = fma(Ts[2][k * QR + lane], V[k], v);
-            a.out[(o % a.P) + a.P * (lane + QR * (o / a.P))] = v;
-            if constexpr (FINISH) ysv[0] = fma(v, v, ysv[0]);
-        }
-        __syncwarp();
+        finish_block(o);
         o += nw;
+    }
+    if constexpr (SPLIT) {
+        __syncthreads();  // every warp's e3 slice of S2 is in place
+        if (warp == 0 && blockIdx.x < units) finish_block(static_cast<int64_t>(blockIdx.x));
     }
     // FINISH: the partials are of ||out||^2 (ysv[0] of lanes 0-3)
     double ys = (ysv[0] + ysv[1]) + (ysv[2] + ysv[3]);
@@ -298,14 +310,19 @@ bool quad_supported(int64_t extent, int64_t rank) { return extent == QN && rank 
 
 int launch_quad(const QuadArgs& a, bool finish, int num_sms, cudaStream_t s, int64_t* launches) {
     if ((reinterpret_cast<uintptr_t>(a.X) & 15u) != 0) return -1;  // TMA bulk copies need 16-byte alignment
-    const int grid = static_cast<int>(
-        std::max<int64_t>(1, std::min<int64_t>(num_sms, (a.O + kQ2Warps - 1) / kQ2Warps)));
+    // few blocks (the finishing launch): one CTA per block, a chunk per warp
+    const bool split = finish && a.O <= num_sms;
+    const int grid = split ? static_cast<int>(a.O)
+                           : static_cast<int>(std::max<int64_t>(
+                                 1, std::min<int64_t>(num_sms, (a.O + kQ2Warps - 1) / kQ2Warps)));
     const size_t smem = sizeof(double) * kQ2Warps * (kQ2Stages * kQ2Chunk + kQ2Scratch);
-    auto kfn = finish ? quad_stream_kernel<true> : quad_stream_kernel<false>;
-    static bool configured[2] = {false, false};
-    if (!configured[finish ? 1 : 0]) {
+    auto kfn = split ? quad_stream_kernel<true, true>
+                     : (finish ? quad_stream_kernel<true, false> : quad_stream_kernel<false, false>);
+    static bool configured[3] = {false, false, false};
+    const int slot = split ? 2 : (finish ? 1 : 0);
+    if (!configured[slot]) {
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured[finish ? 1 : 0] = true;
+        configured[slot] = true;
     }
     kfn<<<grid, kQ2Threads, smem, s>>>(a);
     ++*launches;
