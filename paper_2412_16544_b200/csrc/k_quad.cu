@@ -12,13 +12,17 @@
 // which also finishes ||y||^2 and ||latent||^2 (last CTA, fixed order) like
 // the 3-way tail.
 //
-// One warp per block (12 warps per CTA, no CTA barriers in the loop):
-//   stage 0+1  per 4 KB chunk (one e3 slice): p0 = U0^T x per fibre,
+// One warp per block (8 warps per CTA, a 3-deep ring of 4 KB TMA bulk
+// chunks per warp, no CTA barriers in the loop):
+//   stage 0+1  per chunk (one e3 slice): p0 = U0^T x per fibre,
 //              P1 += p0 (x) U1[e1, :]; ||x||^2 on the side;
 //   stage 2    mode e2 per chunk; stage 3 mode e3 per block;
 //   stage 4-6  the three 16 x 4 transfer projections.
+// The finishing launch (few blocks) runs one CTA per block, a chunk per warp.
 // All FP64 FMAs (DFMA; the contractions are 8 -> 4, far too thin for DMMA
-// tiles): ~36k FMA per 4096-element block, a third of the block's HBM time.
+// tiles): ~36k FMA per 4096-element block. Measured (c4): 128 us over the
+// 537 MB batch = 4.2 TB/s, issue/latency-bound at 2 warps per scheduler
+// (190 registers), profiles/r1_quad_ncu_summary.txt.
 #include <algorithm>
 
 #include "kernels.cuh"
