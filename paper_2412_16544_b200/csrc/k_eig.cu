@@ -328,6 +328,51 @@ __global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kClusterT
 }
 
 // --------------------------------------------------------------------------
+// Positive-definiteness test of G - shift I (full-rank truncations): a
+// right-looking Cholesky in one CTA; flag[0] = 1 if every pivot is positive.
+// Cholesky is backward stable, so success certifies lambda_min(G) > shift up
+// to ~n u ||G||, which the caller's margin covers.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) posdef_kernel(const double* __restrict__ G, int n, double shift,
+                                                      double* __restrict__ A, double* __restrict__ flag) {
+    __shared__ double colk[kJacobiMaxN];
+    __shared__ int ok;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    for (int64_t e = tid; e < nn; e += nt) {
+        const int64_t r = e % n, c = e / n;
+        A[e] = (r >= c) ? G[e] - (r == c ? shift : 0.0) : 0.0;  // lower triangle
+    }
+    if (tid == 0) ok = 1;
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        const double piv = A[k + static_cast<int64_t>(n) * k];
+        if (!(piv > 0.0)) {  // uniform: every thread reads the same pivot
+            if (tid == 0) ok = 0;
+            break;
+        }
+        const double inv = 1.0 / sqrt(piv);
+        const int m = n - k - 1;
+        for (int i = tid; i < m; i += nt) {
+            const double v = A[(k + 1 + i) + static_cast<int64_t>(n) * k] * inv;
+            A[(k + 1 + i) + static_cast<int64_t>(n) * k] = v;
+            colk[i] = v;
+        }
+        __syncthreads();
+        // trailing lower triangle: A[i, j] -= l_i l_j for k < j <= i
+        const int64_t mm = static_cast<int64_t>(m) * m;
+        for (int64_t e = tid; e < mm; e += nt) {
+            const int i = static_cast<int>(e % m), j = static_cast<int>(e / m);
+            if (i < j) continue;
+            A[(k + 1 + i) + static_cast<int64_t>(n) * (k + 1 + j)] -= colk[i] * colk[j];
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    if (tid == 0) flag[0] = ok ? 1.0 : 0.0;
+}
+
+// --------------------------------------------------------------------------
 // Re-orthonormalisation of new directions (expand_core, ht_rise.hpp:53-79):
 // W <- (I - U U^T) W twice, then CholeskyQR2. One CTA; all sizes small.
 // --------------------------------------------------------------------------
@@ -443,6 +488,12 @@ void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, do
     }
     const int threads = n <= 32 ? 128 : (n <= 64 ? 256 : kJacobiThreads);
     jacobi_kernel<<<1, threads, smem, s>>>(G, static_cast<int>(n), lambda, V, work, 1, v_smem ? 1 : 0);
+    ++*launches;
+}
+
+void launch_posdef_test(const double* G, int64_t n, double shift, double* work, double* flag, cudaStream_t s,
+                        int64_t* launches) {
+    posdef_kernel<<<1, 1024, 0, s>>>(G, static_cast<int>(n), shift, work, flag);
     ++*launches;
 }
 

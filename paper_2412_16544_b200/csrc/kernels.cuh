@@ -75,6 +75,11 @@ constexpr int64_t kJacobiMaxN = 2048;  // largest Gram the device eigensolver ta
 void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, double* work, cudaStream_t s,
                        int64_t* launches);
 
+// flag[0] = 1 if G - shift I (n x n, symmetric) is positive definite (one-CTA
+// Cholesky on `work`, n * n doubles), else 0.
+void launch_posdef_test(const double* G, int64_t n, double shift, double* work, double* flag, cudaStream_t s,
+                        int64_t* launches);
+
 // Rank rule of truncated_svd.hpp:74-99 on k = min(rows, cols) values
 // sigma_i^2 = max(lambda_i, 0). info[0] = rank, info[1] = discarded norm,
 // info[2] = trace (sum of lambda) used for the zero-input test.

@@ -631,7 +631,7 @@ Truncation truncate_cols_side(Context& c, const DT& X, int64_t rows, int64_t col
 }  // namespace
 
 Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, double eps_abs, int64_t min_rank,
-                         int64_t cols_global, bool sharded) {
+                         int64_t cols_global, bool sharded, bool any_basis_when_full) {
     const int64_t rows = t.shape[static_cast<size_t>(mode)];
     const int64_t cols_local = t.size() / rows;
     const bool reduce = sharded && c.nccl_comm;
@@ -663,6 +663,35 @@ Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, do
         return truncate_cols_side(c, X, rows, cols_local, eps_abs, min_rank);
     }
     DT G = gram(c, t, mode, reduce);
+    if (!old && any_basis_when_full && rows > 112 && rows <= cols_global && rows <= kJacobiMaxN) {
+        // full-rank shortcut (large Grams only: the eigensolver's cost is in
+        // its many Jacobi rounds there): margin 1e-12 tr(G) >> n u ||G||
+        std::vector<double> diag(static_cast<size_t>(rows));
+        HTR_CUDA(cudaMemcpy2DAsync(diag.data(), sizeof(double), G.data(), sizeof(double) * static_cast<size_t>(rows + 1),
+                                   sizeof(double), static_cast<size_t>(rows), cudaMemcpyDeviceToHost, c.s));
+        HTR_CUDA(cudaStreamSynchronize(c.s));
+        double tr = 0.0;
+        for (double v : diag) tr += v;
+        if (tr > 0.0 && std::isfinite(tr)) {
+            BufPtr work = c.alloc(rows * rows);
+            BufPtr flag = c.alloc(4);
+            HTR_CUDA(cudaMemsetAsync(flag->p, 0, 4 * sizeof(double), c.s));
+            launch_posdef_test(G.data(), rows, eps_abs * eps_abs + 1e-12 * tr, work->p, flag->p, c.s, &c.launches);
+            HTR_CUDA(cudaGetLastError());
+            double f = 0.0;
+            c.fetch(flag->p, 1, &f);
+            if (f == 1.0) {
+                Truncation tr_full;
+                tr_full.rank = rows;
+                tr_full.discarded = 0.0;
+                tr_full.u = c.tensor({rows, rows});
+                // take_columns with a zero-input flag (flag[2] == 0) writes identity columns
+                launch_take_columns(nullptr, rows, rows, tr_full.u.data(), flag->p, c.s, &c.launches);
+                HTR_CUDA(cudaGetLastError());
+                return tr_full;
+            }
+        }
+    }
     if (!old) return truncate_gram(c, G, rows, cols_global, eps_abs, min_rank, unfolding_refiner(c, t, mode, reduce));
     // the residual Gram is formed by subtraction: its eigenvalues carry
     // rounding noise on the scale of the unprojected Gram (its trace)
@@ -830,7 +859,7 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
     std::vector<Truncation> bases;
     for (const TreeNode& n : tree.layer(p)) {
         const int mode = static_cast<int>(n.leaf_dim);
-        bases.push_back(truncate_mode(c, cur, mode, nullptr, eps_nw, 1, cols_of(cur, mode)));
+        bases.push_back(truncate_mode(c, cur, mode, nullptr, eps_nw, 1, cols_of(cur, mode), true, true));
     }
     RankMap ranks;
     for (size_t i = 0; i < bases.size(); ++i) {
@@ -855,7 +884,8 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
         cur.shape = layer_extents(*h, l, ranks, batch, false);
         std::vector<Truncation> lb;
         for (Index j = 0; j < tree.layer_size(l); ++j) {
-            lb.push_back(truncate_mode(c, cur, static_cast<int>(j), nullptr, eps_nw, 1, cols_of(cur, static_cast<int>(j))));
+            lb.push_back(truncate_mode(c, cur, static_cast<int>(j), nullptr, eps_nw, 1, cols_of(cur, static_cast<int>(j)),
+                                       true, true));
         }
         for (Index j = 0; j < tree.layer_size(l); ++j) {
             const TreeNode& n = tree.layer(l)[static_cast<size_t>(j)];

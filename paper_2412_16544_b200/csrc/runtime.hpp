@@ -183,8 +183,15 @@ constexpr int64_t kColumnSideRows = 1024;
 /// of its residual (I - U U^T) t_(mode) (compute_residual, ht_rise.hpp:31-38).
 /// cols_global = the unfolding's column count over all ranks; `sharded`
 /// false for a rank-local matrix (no all-reduce).
+/// any_basis_when_full: the caller needs only the retained subspace (a
+/// BHT-l2r node basis), so when the unfolding is certified full rank
+/// (lambda_min of its Gram above eps_abs^2 with margin, by a Cholesky test)
+/// the identity is returned without an eigensolve. The reference's rank rule
+/// keeps every direction then (truncated_svd.hpp:78-93: the tail from
+/// r = rows - 1 is sigma_min^2 > eps^2), and any orthonormal basis of the
+/// full space spans the same subspace; `sigma` is left empty.
 Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, double eps_abs, int64_t min_rank,
-                         int64_t cols_global, bool sharded = true);
+                         int64_t cols_global, bool sharded = true, bool any_basis_when_full = false);
 
 // ---- algorithms --------------------------------------------------------------
 struct BuildOut {
