@@ -205,6 +205,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         U1f[idx] = v;
     }
     __syncthreads();
+    // the skip-path tail is launched as a programmatic dependent: it may be
+    // scheduled as this grid's CTAs retire and stages its bases before
+    // waiting for this grid's results (griddepcontrol.wait in tail3)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     double ysq0 = 0.0, ysq1 = 0.0, ysq2 = 0.0, ysq3 = 0.0;
     double wacc[MT0][MT1][2];

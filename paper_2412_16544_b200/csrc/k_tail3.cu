@@ -132,6 +132,10 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
         U2s[e] = c < r2 ? a.U2[i2 + static_cast<int64_t>(n2) * c] : 0.0;
     }
     __syncthreads();
+    // launched as a programmatic dependent of the fused leaf kernel: its W
+    // and ||y||^2 partials are complete and visible after this (a no-op for a
+    // plain launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // ---- phase A: Z_s(p, a2), M = R01 (p), N = r2, K = n2 ----
     {
@@ -592,23 +596,26 @@ void launch_t(const Tail3Args& a, size_t smem, cudaStream_t s) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         configured[cl] = smem;
     }
-    if (!cl) {
-        tail3_kernel<NT, MT, false><<<static_cast<unsigned>(a.S), kThreads, smem, s>>>(a);
-        return;
-    }
+    // programmatic dependent launch after the fused leaf kernel (see
+    // griddepcontrol.wait in the kernel)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(a.S * a.csize));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = static_cast<unsigned>(a.csize);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = static_cast<unsigned>(a.csize);
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, tail3_kernel<NT, MT, true>, a);
+    cfg.numAttrs = cl ? 2 : 1;
+    if (cl)
+        cudaLaunchKernelEx(&cfg, tail3_kernel<NT, MT, true>, a);
+    else
+        cudaLaunchKernelEx(&cfg, tail3_kernel<NT, MT, false>, a);
 }
 
 template <int NT>
