@@ -112,7 +112,7 @@ _SIGNATURES = {
                                 C.c_int32, C.POINTER(_P), C.POINTER(_BuildReport)]),
     "htr_ht_rise_update": (C.c_int32, [_P, _P, _D, C.c_int32, _I64, C.c_int32, C.c_double, C.c_int32,
                                        C.POINTER(_P), C.POINTER(_UpdateReport)]),
-    "htr_ht_rise_update_many": (C.c_int32, [_P, _P, C.c_int64, C.POINTER(_D), C.c_int32, _I64, C.c_int32,
+    "htr_ht_rise_update_many": (C.c_int32, [_P, _P, C.c_int64, C.POINTER(_P), C.c_int32, _I64, C.c_int32,
                                             C.c_double, C.c_int32, C.POINTER(_P), C.POINTER(_UpdateReport)]),
     "htr_encode": (C.c_int32, [_P, _P, _D, C.c_int32, _I64, C.c_int32, _D, C.c_int32, _D]),
     "htr_decode": (C.c_int32, [_P, _P, _D, C.c_int32, _I64, _D, C.c_int32]),
@@ -699,26 +699,41 @@ def ht_rise_update_many(h: HTRepresentation, batches, epsilon_rel: Optional[floa
     n = len(batches)
     if n == 0:
         return [], []
-    # order the library's stream after each distinct producing stream once
-    streams = {_torch_stream(y.data) for y in batches
-               if isinstance(y, DeviceTensor) and hasattr(y.data, "data_ptr")}
-    for st in streams:
-        code = _fn.context_wait_stream(ctx._h, st)
-        if code:
-            ctx.check(code)
-    args = [_tensor_arg(y) for y in batches]
-    on_dev = {a[1] for a in args}
-    if len(on_dev) != 1:
+    dev = [isinstance(y, DeviceTensor) for y in batches]
+    if any(dev) and not all(dev):
         raise ValueError("ht_rise_update_many: batches must be all on the device or all on the host")
-    order = len(args[0][2])
-    if any(len(a[2]) != order for a in args):
+    if dev[0]:
+        # device batches: validate each distinct buffer once, and order the
+        # library's stream after each distinct producing stream once
+        ptr_of, streams = {}, set()
+        for y in batches:
+            key = id(y.data)
+            if key not in ptr_of:
+                ptr_of[key] = y.ptr()
+                if hasattr(y.data, "data_ptr"):
+                    streams.add(_torch_stream(y.data))
+        for st in streams:
+            code = _fn.context_wait_stream(ctx._h, st)
+            if code:
+                ctx.check(code)
+        args = None
+        ptr_list = [ptr_of[id(y.data)] for y in batches]
+        shape_list = [tuple(y.shape) for y in batches]
+        on_dev = 1
+    else:
+        args = [_tensor_arg(y) for y in batches]
+        ptr_list = [C.cast(a[0], _P).value for a in args]
+        shape_list = [a[2] for a in args]
+        on_dev = 0
+    order = len(shape_list[0])
+    if any(len(sh) != order for sh in shape_list):
         raise ValueError("ht_rise_update_many: batches of different tensor order")
-    ptrs = (_D * n)(*[a[0] for a in args])
-    shapes = (C.c_int64 * (n * order))(*[int(e) for a in args for e in a[2]])
+    ptrs = (_P * n)(*ptr_list)
+    shapes = (C.c_int64 * (n * order))(*[int(e) for sh in shape_list for e in sh])
     outs = (_P * n)()
     reps = (_UpdateReport * n)()
     eps = -1.0 if epsilon_rel is None else float(epsilon_rel)
-    code = _fn.ht_rise_update_many(ctx._h, h.handle, n, ptrs, on_dev.pop(), shapes, order, eps,
+    code = _fn.ht_rise_update_many(ctx._h, h.handle, n, ptrs, on_dev, shapes, order, eps,
                                    1 if adaptive_budget else 0, outs, reps)
     if code:
         ctx.check(code)
