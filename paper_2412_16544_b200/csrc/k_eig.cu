@@ -165,6 +165,127 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
 }
 
 // --------------------------------------------------------------------------
+// n <= kSymMaxN: the same rounds with A stored as its packed lower triangle,
+// so that A and V both fit in shared memory up to n = 135 (c5's 128-row leaf
+// Grams, whose V previously lived in global memory), and only the 2x2 blocks
+// P <= Q are updated (A' = J^T A J stays exactly symmetric; the (Q, P) block
+// is the transpose held in the same entries).
+// --------------------------------------------------------------------------
+constexpr int kSymMaxN = 135;  // n(n+1)/2 + n^2 doubles = 194 KB at n = 135
+
+__device__ __forceinline__ int sym_idx(int i, int j, int n) {  // packed lower, column-major
+    if (i < j) { const int t = i; i = j; j = t; }
+    return j * n - ((j * (j + 1)) >> 1) + i;
+}
+
+__global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const double* __restrict__ G, int n,
+                                                                    double* __restrict__ lambda,
+                                                                    double* __restrict__ Vout) {
+    extern __shared__ double smem[];
+    __shared__ double cs[kSymMaxN], sn[kSymMaxN];
+    __shared__ int prs[kSymMaxN], qrs[kSymMaxN];
+    __shared__ int rotated;
+    __shared__ double tr_abs;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int np = (n * (n + 1)) / 2;
+    double* A = smem;       // packed lower triangle
+    double* V = smem + np;  // n x n, column-major
+    for (int j = 0; j < n; ++j)
+        for (int i = j + tid; i < n; i += nt)
+            A[sym_idx(i, j, n)] = 0.5 * (G[i + static_cast<int64_t>(n) * j] + G[j + static_cast<int64_t>(n) * i]);
+    for (int e = tid; e < n * n; e += nt) V[e] = (e % n == e / n) ? 1.0 : 0.0;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int i = 0; i < n; ++i) t += fabs(A[sym_idx(i, i, n)]);
+        tr_abs = t;
+    }
+    __syncthreads();
+    const double floor_abs = 0x1p-53 * tr_abs;
+    const int m = n + (n & 1), half = m / 2;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        if (tid == 0) rotated = 0;
+        __syncthreads();
+        for (int round = 0; round < m - 1; ++round) {
+            for (int i = tid; i < half; i += nt) {
+                int p = tour_pos(i, round, m), q = tour_pos(m - 1 - i, round, m);
+                if (p > q) { const int t = p; p = q; q = t; }
+                double c = 1.0, s = 0.0;
+                if (q < n && jacobi_rotation(A[sym_idx(p, p, n)], A[sym_idx(q, q, n)], A[sym_idx(p, q, n)], floor_abs,
+                                             &c, &s))
+                    rotated = 1;
+                cs[i] = c; sn[i] = s; prs[i] = p; qrs[i] = q;
+            }
+            __syncthreads();
+            // blocks P <= Q (linear index over the upper triangle of pairs)
+            const int blocks = (half * (half + 1)) / 2;
+            for (int b = tid; b < blocks; b += nt) {
+                // Q-major: b = Q (Q + 1) / 2 + P, P <= Q
+                int Q = static_cast<int>((sqrtf(8.0f * static_cast<float>(b) + 1.0f) - 1.0f) * 0.5f);
+                while ((Q * (Q + 1)) / 2 > b) --Q;
+                while (((Q + 1) * (Q + 2)) / 2 <= b) ++Q;
+                const int P = b - (Q * (Q + 1)) / 2;
+                const double cP = cs[P], sP = sn[P], cQ = cs[Q], sQ = sn[Q];
+                if (sP == 0.0 && sQ == 0.0) continue;
+                const int pP = prs[P], qP = qrs[P], pQ = prs[Q], qQ = qrs[Q];
+                const bool okr = qP < n, okc = qQ < n;
+                if (P == Q) {
+                    if (!okr) continue;
+                    // diagonal block: [a_pp a_pq; a_pq a_qq] -> diag(.), pair annihilated
+                    const int ipp = sym_idx(pP, pP, n), iqq = sym_idx(qP, qP, n), ipq = sym_idx(pP, qP, n);
+                    const double x00 = A[ipp], x01 = A[ipq], x11 = A[iqq];
+                    const double y00 = cP * x00 - sP * x01, y01 = cP * x01 - sP * x11;
+                    const double y10 = sP * x00 + cP * x01, y11 = sP * x01 + cP * x11;
+                    A[ipp] = cP * y00 - sP * y01;
+                    A[iqq] = sP * y10 + cP * y11;
+                    A[ipq] = 0.0;
+                    continue;
+                }
+                const int i00 = sym_idx(pP, pQ, n);
+                const int i01 = okc ? sym_idx(pP, qQ, n) : 0;
+                const int i10 = okr ? sym_idx(qP, pQ, n) : 0;
+                const int i11 = (okr && okc) ? sym_idx(qP, qQ, n) : 0;
+                const double x00 = A[i00], x01 = okc ? A[i01] : 0.0, x10 = okr ? A[i10] : 0.0,
+                             x11 = (okr && okc) ? A[i11] : 0.0;
+                const double y00 = cP * x00 - sP * x10, y01 = cP * x01 - sP * x11;
+                const double y10 = sP * x00 + cP * x10, y11 = sP * x01 + cP * x11;
+                A[i00] = cQ * y00 - sQ * y01;
+                if (okc) A[i01] = sQ * y00 + cQ * y01;
+                if (okr) A[i10] = cQ * y10 - sQ * y11;
+                if (okr && okc) A[i11] = sQ * y10 + cQ * y11;
+            }
+            const int vitems = half * n;
+            for (int it = tid; it < vitems; it += nt) {
+                const int Q = it / n, r = it - Q * n;
+                const double s = sn[Q];
+                if (s == 0.0) continue;
+                const double c = cs[Q];
+                double* vp = V + n * prs[Q] + r;
+                double* vq = V + n * qrs[Q] + r;
+                const double x = *vp, y = *vq;
+                *vp = c * x - s * y;
+                *vq = s * x + c * y;
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+        if (!rotated) break;
+        __syncthreads();
+    }
+    // sort eigenpairs by descending eigenvalue (stable on index)
+    for (int i = tid; i < n; i += nt) {
+        const double li = A[sym_idx(i, i, n)];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+            const double lj = A[sym_idx(j, j, n)];
+            rank += (lj > li) || (lj == li && j < i);
+        }
+        lambda[rank] = li;
+        for (int r = 0; r < n; ++r) Vout[r + static_cast<int64_t>(n) * rank] = V[r + n * i];
+    }
+}
+
+// --------------------------------------------------------------------------
 // Large n: the same parallel cyclic Jacobi spread over a cluster of CTAs.
 // A and V live in global memory (L2); every CTA computes the round's
 // rotations itself (bit-identical: same inputs, same code), applies its
@@ -471,6 +592,20 @@ void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, do
     if (n > kSmemMaxNA) {
         jacobi_cluster_kernel<<<kClusterCTAs, kClusterThreads, 0, s>>>(G, static_cast<int>(n), lambda, V, work,
                                                                        work + n * n);
+        ++*launches;
+        return;
+    }
+    if (n <= kSymMaxN) {
+        const size_t ssmem = sizeof(double) * static_cast<size_t>(n * (n + 1) / 2 + n * n);
+        static bool configured_sym = false;
+        if (!configured_sym) {
+            cudaFuncSetAttribute(jacobi_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(double) * (kSymMaxN * (kSymMaxN + 1) / 2 +
+                                                                    kSymMaxN * kSymMaxN)));
+            configured_sym = true;
+        }
+        const int threads = n <= 32 ? 128 : (n <= 64 ? 256 : kJacobiThreads);
+        jacobi_sym_kernel<<<1, threads, ssmem, s>>>(G, static_cast<int>(n), lambda, V);
         ++*launches;
         return;
     }
