@@ -1528,8 +1528,8 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
     struct Slot {
         int64_t index = -1;
         DT y, latent;
-        BufPtr dsc;       // [0] ||y||^2, [1] batch count (sharded), [2] ||latent||^2
-        double* host = nullptr;  // pinned copy of dsc[0..2]
+        BufPtr dsc;       // [0] ||y||^2, [1] non-finite flag, [2] ||latent||^2, [8] batch count (sharded)
+        double* host = nullptr;  // pinned copy of dsc[0..8]
         double* mapped = nullptr;  // mapped host block the tail writes dsc[0], dsc[2] to
         bool fused = false;        // launched through the fused skip-path kernels
         bool used_fused = false;   // (report) any fused kernel in the encode
