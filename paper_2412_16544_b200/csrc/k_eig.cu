@@ -480,12 +480,13 @@ __global__ void __launch_bounds__(1024) posdef_kernel(const double* __restrict__
             colk[i] = v;
         }
         __syncthreads();
-        // trailing lower triangle: A[i, j] -= l_i l_j for k < j <= i
-        const int64_t mm = static_cast<int64_t>(m) * m;
-        for (int64_t e = tid; e < mm; e += nt) {
-            const int i = static_cast<int>(e % m), j = static_cast<int>(e / m);
-            if (i < j) continue;
-            A[(k + 1 + i) + static_cast<int64_t>(n) * (k + 1 + j)] -= colk[i] * colk[j];
+        // trailing lower triangle: A[i, j] -= l_i l_j for k < j <= i; warp w
+        // takes columns j = w, w + 32, ..., its lanes run down the column
+        const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+        for (int j = warp; j < m; j += nw) {
+            const double lj = colk[j];
+            double* col = A + static_cast<int64_t>(n) * (k + 1 + j) + (k + 1);
+            for (int i = j + lane; i < m; i += 32) col[i] -= colk[i] * lj;
         }
         __syncthreads();
     }

@@ -663,9 +663,10 @@ Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, do
         return truncate_cols_side(c, X, rows, cols_local, eps_abs, min_rank);
     }
     DT G = gram(c, t, mode, reduce);
-    if (!old && any_basis_when_full && rows > 112 && rows <= cols_global && rows <= kJacobiMaxN) {
-        // full-rank shortcut (large Grams only: the eigensolver's cost is in
-        // its many Jacobi rounds there): margin 1e-12 tr(G) >> n u ||G||
+    if (!old && any_basis_when_full && rows > 160 && rows <= cols_global && rows <= kJacobiMaxN) {
+        // full-rank shortcut for the Grams that need the cluster eigensolver
+        // (n > 160, tens of ms; a failed test costs ~2 ms): margin
+        // 1e-12 tr(G) >> n u ||G||
         std::vector<double> diag(static_cast<size_t>(rows));
         HTR_CUDA(cudaMemcpy2DAsync(diag.data(), sizeof(double), G.data(), sizeof(double) * static_cast<size_t>(rows + 1),
                                    sizeof(double), static_cast<size_t>(rows), cudaMemcpyDeviceToHost, c.s));
