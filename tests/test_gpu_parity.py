@@ -489,6 +489,22 @@ def test_quad_subtree_fused_matches_generic(ht):
         ht.ht_rise_update(rep, ht.DeviceTensor(bad, shape))
 
 
+def test_full_rank_transfer_shortcut_vs_oracle(ht):
+    """A transfer node whose unfolding is certified full rank (200 rows, 3200
+    columns, random data) takes the identity basis without an eigensolve;
+    ranks, discarded norms and reconstructions must equal the oracle's, whose
+    SVD keeps every direction too (truncated_svd.hpp:78-93)."""
+    rng = np.random.default_rng(606)
+    y = np.asfortranarray(rng.standard_normal((20, 10, 40, 40, 2)))
+    gpu, grep = ht.bht_l2r(y, ht.DimensionTree.balanced(4), 1e-3)
+    ref, rrep = ho.bht_l2r(y, ho.DimensionTree.balanced(4), 1e-3)
+    assert gpu.ranks() == ref.ranks()
+    assert gpu.ranks()[(1, 0)] == 200
+    b = gpu.basis_matrix((1, 0))
+    assert np.array_equal(b, np.eye(200))  # the shortcut ran
+    compare_reps(ht, gpu, ref, check_slices=True)
+
+
 def test_leading_modes_fused_matches_generic(ht):
     """Trees whose deepest layer starts with the leaves of modes 0 and 1
     (config 3's balanced(4) over 32 x 32 x 32 x 8) project both in one fused
