@@ -167,7 +167,11 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     const int npairs_all = (ntB + 1) / 2;
     // this CTA's contiguous range of column pairs [pb0, pb0 + npairs)
     const int pb0 = static_cast<int>(static_cast<int64_t>(npairs_all) * crank / C);
-    const int npairs = static_cast<int>(static_cast<int64_t>(npairs_all) * (crank + 1) / C) - pb0;
+    // an identity transfer basis (a full-rank node: rt = r1 r2, B = I) makes
+    // the latent Z_s itself, in the same layout: no pairs to project
+    const int npairs = a.identity_transfer
+                           ? 0
+                           : static_cast<int>(static_cast<int64_t>(npairs_all) * (crank + 1) / C) - pb0;
     const int full = npairs / kWarps * kWarps;
     const int rem = npairs - full;
     const int kparts = rem ? kWarps / rem : 1;
@@ -176,6 +180,17 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     double* out = a.latent + s * static_cast<int64_t>(r0) * rt;
     double* redbuf = U2s;
     double lsq = 0.0;
+    if (a.identity_transfer) {
+        // latent[a0 + r0 b] = Z_s[a0 + r0 (a1 + r1 a2)]: this CTA's share of the copy
+        const int total = r0 * rt;
+        const int c0 = static_cast<int>(static_cast<int64_t>(total) * crank / C);
+        const int c1 = static_cast<int>(static_cast<int64_t>(total) * (crank + 1) / C);
+        for (int e = c0 + tid; e < c1; e += kThreads) {
+            const double v = Zs[e];
+            out[e] = v;
+            lsq = fma(v, v, lsq);
+        }
+    }
     auto pair_tiles = [&](int pr, int ks0, int ks1, double (&acc)[MT][2][2]) {
         pr += pb0;
         const int kend = min(R12, 4 * ks1);
@@ -635,7 +650,7 @@ bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2) {
 }
 
 void launch_tail3(const Tail3Args& a, cudaStream_t s, int64_t* launches) {
-    if (a.variant == 2) {
+    if (a.variant == 2 && !a.identity_transfer) {
         const size_t psmem = tail3_pair_smem(a.n2, a.r0, a.r1, a.r2);
         if (psmem <= 220 * 1024) {
             switch ((a.r2 + 7) / 8) {

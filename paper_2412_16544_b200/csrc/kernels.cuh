@@ -175,8 +175,11 @@ struct Tail3Args {
     int variant = 0;  // 0 auto, 1 one sample per CTA, 2 sample pairs (falls back to 1 when it does not fit)
     int num_sms = kNumSMs;
     int csize = 1;    // CTAs per sample (a thread-block cluster), set by the launcher
+    bool identity_transfer = false;  // B == I (rt == r1 r2): latent = Z, no projection
 };
 bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2);
+// (identity_transfer is honoured by the per-sample/cluster kernel; the
+// sample-pair variant falls back to it)
 
 // Balanced 4-leaf subtree over 4 consecutive modes of extent 8, all ranks 4
 // (config 4): every contiguous 8^4 block o of X (O blocks, 16-byte aligned)

@@ -688,6 +688,7 @@ Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, do
                 tr_full.u = c.tensor({rows, rows});
                 // take_columns with a zero-input flag (flag[2] == 0) writes identity columns
                 launch_take_columns(nullptr, rows, rows, tr_full.u.data(), flag->p, c.s, &c.launches);
+                tr_full.u.buf->identity = true;
                 HTR_CUDA(cudaGetLastError());
                 return tr_full;
             }
@@ -976,7 +977,9 @@ bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent
     Tail3Args ta;
     ta.wslab = fa.wslab;
     ta.U2 = fa.U2;
-    ta.B = h.core(NodeId{1, 1}).data();
+    const DT& Bcore = h.core(NodeId{1, 1});
+    ta.B = Bcore.data();
+    ta.identity_transfer = Bcore.buf->identity && Bcore.offset == 0 && t.rt == t.r1 * t.r2;
     ta.r0 = t.r0;
     ta.r1 = t.r1;
     ta.r2 = t.r2;

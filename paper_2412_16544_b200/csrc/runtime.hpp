@@ -48,6 +48,7 @@ struct Buf {
     double* p = nullptr;
     int64_t n = 0;
     bool owned = true;
+    bool identity = false;  // holds exactly the identity matrix (a full-rank node's basis)
     Buf(StreamPtr st_, int64_t n_);
     /// Non-owning wrapper around caller memory (device pointers handed in
     /// through the C-ABI).

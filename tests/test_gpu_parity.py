@@ -505,6 +505,35 @@ def test_full_rank_transfer_shortcut_vs_oracle(ht):
     compare_reps(ht, gpu, ref, check_slices=True)
 
 
+def test_identity_transfer_tail_vs_generic_and_oracle(ht):
+    """(1,(2,3)) tree whose transfer node is full rank (r1 r2 = 196 > 160 rows,
+    224 columns): BHT-l2r gives it the identity basis, and the fused tail then
+    writes Z_s as the latent without a projection. Latents, skip decisions and
+    reconstructions must equal the generic chain's and the oracle's."""
+    rng = np.random.default_rng(196)
+    bases = [ro.random_orthonormal(64, 14, rng) for _ in range(3)]
+    y0 = ro.tucker_family_batch(bases, 16, rng)
+    # (eps 1e-4: far from the telescoped loss's guard band, so the fused path decides)
+    gpu, _ = ht.bht_l2r(y0, ht.tree_1_23(), 1e-4)
+    ref, _ = ho.bht_l2r(y0, ho.custom_tree_1_23(), 1e-4)
+    assert gpu.ranks() == ref.ranks()
+    assert gpu.ranks()[(1, 1)] == 196
+    assert np.array_equal(gpu.basis_matrix((1, 1)), np.eye(196))
+    y1 = ro.tucker_family_batch(bases, 5, rng)
+    ctx = gpu.ctx
+    la, pa = ht.encode(gpu, y1)
+    ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+    try:
+        lb, pb = ht.encode(gpu, y1)
+    finally:
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    assert np.linalg.norm(la - lb) <= 1e-12 * np.linalg.norm(lb)
+    g2, ug = ht.ht_rise_update(gpu, y1)
+    r2, ur = ho.ht_rise_update(ref, y1)
+    assert ug.used_fused_path and ug.skipped == ur.skipped
+    compare_reps(ht, g2, r2, check_slices=True)
+
+
 def test_leading_modes_fused_matches_generic(ht):
     """Trees whose deepest layer starts with the leaves of modes 0 and 1
     (config 3's balanced(4) over 32 x 32 x 32 x 8) project both in one fused
