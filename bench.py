@@ -323,12 +323,16 @@ def run_ours(args):
             # DMMA peak) against the measured step time
             rt = rk.get((1, 1), 0)
             r2 = rk.get((2, 1), 0)
-            tail_flops = 2.0 * n_local * (r0 * r1 * n2 * r2 + r0 * (r1 * r2) * rt)
+            # a full-rank transfer node (rt = r1 r2) holds the identity basis
+            # (BHT-l2r's Cholesky-certified shortcut): its projection is no work
+            ident = rt == r1 * r2 and np.array_equal(rep.basis_matrix((1, 1)), np.eye(rt))
+            tail_flops = 2.0 * n_local * (r0 * r1 * n2 * r2 + (0 if ident else r0 * (r1 * r2) * rt))
             t_hbm = local_bytes / (peak * 1e9) * 1e3
             t_fp64 = (flops + tail_flops) / (FP64_DMMA_TFLOPS * 1e12) * 1e3
             floor = max(t_hbm, t_fp64)
             roof["update"] = {"hbm_floor_ms": t_hbm, "fp64_floor_ms": t_fp64, "binding": "fp64" if t_fp64 > t_hbm else "hbm",
-                              "algorithmic_flops": flops + tail_flops, "ms_per_step": ms, "frac": floor / ms,
+                              "algorithmic_flops": flops + tail_flops, "identity_transfer": bool(ident),
+                              "ms_per_step": ms, "frac": floor / ms,
                               "hbm_frac": t_hbm / ms}
             roof["fp64_pipe"] = {"achieved": tf, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
                                  "frac": tf / FP64_DMMA_TFLOPS,
