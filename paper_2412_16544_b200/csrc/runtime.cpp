@@ -1736,9 +1736,12 @@ DT decode(Context& c, const Rep& h, const DT& latent, double* dst) {
             const TreeNode& n = h.tree.node(modes[pos]);
             if (n.kind != NodeKind::Transfer) continue;
             const Basis b = basis_of(h, n.id);
-            // multiply mode `pos` by the basis (alpha x r): M(q, j) = B[q + alpha j]
-            DT next = mode_mul(c, cur, static_cast<int>(pos), b.p, b.alpha, 1, b.alpha);
-            const Shape& cs = h.core(n.id).shape;
+            // multiply mode `pos` by the basis (alpha x r): M(q, j) = B[q + alpha j];
+            // an identity basis (a full-rank node) only splits the mode
+            const DT& core = h.core(n.id);
+            const bool ident = core.buf->identity && core.offset == 0 && b.alpha == b.r;
+            DT next = ident ? cur : mode_mul(c, cur, static_cast<int>(pos), b.p, b.alpha, 1, b.alpha);
+            const Shape& cs = core.shape;
             Shape sh = next.shape;
             sh[pos] = cs[0];
             sh.insert(sh.begin() + static_cast<std::ptrdiff_t>(pos) + 1, cs[1]);
