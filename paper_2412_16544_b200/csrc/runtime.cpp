@@ -1524,6 +1524,7 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
 std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep>& h0, int64_t n,
                                            const std::function<DT(int64_t)>& batch_of, double eps_override,
                                            bool adaptive) {
+    const auto t_entry = std::chrono::steady_clock::now();
     std::vector<UpdateOut> res;
     res.reserve(static_cast<size_t>(std::max<int64_t>(n, 0)));
     std::shared_ptr<Rep> cur = h0;
@@ -1674,8 +1675,10 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
 
     int cs = 0;          // slot of batch i when `pending`
     bool pending = false;
+    std::chrono::steady_clock::time_point t_first = t_entry;
     for (int64_t i = 0; i < n; ++i) {
         if (!pending) pending = launch(slots[cs], *cur, i, cur->acc);
+        if (i == 0) t_first = std::chrono::steady_clock::now();
         if (!pending) {
             UpdateOut u = ht_rise_update(c, *cur, batch(i), eps_override, adaptive);
             cur = u.rep;
@@ -1701,6 +1704,13 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         slots[cs ^ 1].dsc.reset();
     }
     HTR_CUDA(cudaStreamSynchronize(c.s));
+    if (timeline) {
+        const auto us = [&](std::chrono::steady_clock::time_point t) {
+            return std::chrono::duration<double, std::micro>(t - t_entry).count();
+        };
+        std::fprintf(stderr, "timeline host: first launch done %.1f us, exit %.1f us\n",
+                     res.empty() ? 0.0 : us(t_first), us(std::chrono::steady_clock::now()));
+    }
     if (timeline && tl.size() >= 2) {
         for (size_t k = 0; k + 1 < tl.size(); k += 2) {
             float busy = 0.f, gap = 0.f;
