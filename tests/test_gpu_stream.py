@@ -210,3 +210,29 @@ def test_stream_ragged_batches_and_options(ht):
             assert rs.accumulated == rm.accumulated
         assert np.array_equal(many[-1].root(), seq[-1][0].root())
         assert any(u.skipped for u in reports) and not all(u.skipped for u in reports)
+
+
+def test_stream_single_rank_nccl_generic_tree(ht):
+    """The deferred generic encode on the sharded path: a 4-way tree outside
+    the fused kernels, a 1-rank NCCL communicator (all-reduced scalars and
+    batch count read back by copy): identical to the plain context."""
+    rng = np.random.default_rng(4321)
+    bases = [ro.random_orthonormal(10, 3, rng) for _ in range(4)]
+    wide = [ro.random_orthonormal(10, 4, rng) for _ in range(4)]
+    batches = [np.asfortranarray(ro.tucker_family_batch(bases, 3, rng)) for _ in range(4)]
+    batches.append(np.asfortranarray(ro.tucker_family_batch(wide, 3, rng)))  # expands
+    batches.append(np.asfortranarray(ro.tucker_family_batch(wide, 2, rng)))
+    plain, comm = ht.Context(0), ht.Context(0)
+    comm.init_comm(ht.comm_unique_id(), 1, 0)
+    outs = []
+    for c in (plain, comm):
+        r0, _ = ht.bht_l2r(batches[0], ht.DimensionTree.balanced(4), 1e-6, ctx=c)
+        outs.append(ht.ht_rise_update_many(r0, [_dev(ht, b) for b in batches[1:]]))
+    (va, ua), (vb, ub) = outs
+    for a, b in zip(ua, ub):
+        _same_report(a, b)
+    assert any(not u.skipped for u in ua) and any(u.skipped for u in ua)
+    for m in range(1, va[-1].accumulated + 1):
+        assert np.array_equal(ht.reconstruct_slice(va[-1], m), ht.reconstruct_slice(vb[-1], m))
+    plain.close()
+    comm.close()
