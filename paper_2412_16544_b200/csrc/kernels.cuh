@@ -202,6 +202,19 @@ struct QuadArgs {
     double* host_out = nullptr;
     unsigned int* ticket = nullptr;
 };
+/// Fused two-leaf reconstruction X = (U0 (x) U1) W per slab (k_decode.cu).
+struct Decode2Args {
+    const double* W;  // [r0][r1][T]
+    int64_t T;
+    int r0, r1;
+    int64_t n0, n1;
+    const double* U0;  // n0 x r0, column-major
+    const double* U1;  // n1 x r1
+    double* X;         // [n0][n1][T]
+};
+bool decode2_supported(int64_t n0, int64_t n1, int64_t r0, int64_t r1);
+int launch_decode2(const Decode2Args& a, int num_sms, cudaStream_t s, int64_t* launches);
+
 bool quad_supported(int64_t extent, int64_t rank);
 /// Returns the grid size (number of partials written), -1 for an unaligned X.
 int launch_quad(const QuadArgs& a, bool finish, int num_sms, cudaStream_t s, int64_t* launches);

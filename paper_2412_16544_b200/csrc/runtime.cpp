@@ -1766,8 +1766,17 @@ DT decode(Context& c, const Rep& h, const DT& latent, double* dst) {
     // validate() forces in-order spans: mode k now carries leaf dimension k
     for (size_t k = 0; k < modes.size(); ++k)
         if (h.tree.node(modes[k]).leaf_dim != static_cast<Index>(k)) raise(HTR_ERR_RUNTIME, "decode: unexpected mode order");
-    std::vector<size_t> order(modes.size());
-    for (size_t k = 0; k < order.size(); ++k) order[k] = k;
+    // Leaves 0 and 1 last, in one fused kernel (k_decode.cu), when their
+    // extents and ranks fit it: the other leaves expand first, then every
+    // slab of the remaining modes and samples is reconstructed without an
+    // intermediate.
+    const Basis l0 = basis_of(h, modes[0]);
+    const Basis l1 = modes.size() >= 2 ? basis_of(h, modes[1]) : l0;
+    const bool fuse2 = c.fused && modes.size() >= 2 && cur.shape[0] == l0.r && cur.shape[1] == l1.r &&
+                       decode2_supported(l0.alpha, l1.alpha, l0.r, l1.r) &&
+                       (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
+    std::vector<size_t> order;
+    for (size_t k = fuse2 ? 2 : 0; k < modes.size(); ++k) order.push_back(k);
     auto growth = [&](size_t k) {
         const Basis b = basis_of(h, modes[k]);
         return static_cast<double>(b.alpha) / static_cast<double>(std::max<int64_t>(b.r, 1));
@@ -1776,7 +1785,35 @@ DT decode(Context& c, const Rep& h, const DT& latent, double* dst) {
     for (size_t i = 0; i < order.size(); ++i) {
         const size_t k = order[i];
         const Basis b = basis_of(h, modes[k]);
-        cur = mode_mul(c, cur, static_cast<int>(k), b.p, b.alpha, 1, b.alpha, i + 1 == order.size() ? dst : nullptr);
+        cur = mode_mul(c, cur, static_cast<int>(k), b.p, b.alpha, 1, b.alpha,
+                       !fuse2 && i + 1 == order.size() ? dst : nullptr);
+    }
+    if (fuse2) {
+        Shape os = cur.shape;
+        os[0] = l0.alpha;
+        os[1] = l1.alpha;
+        DT out;
+        if (dst) {
+            out.shape = os;
+            out.buf = std::make_shared<Buf>(c.st, dst, htrise::shape_product(os));
+        } else {
+            out = c.tensor(os);
+        }
+        Decode2Args a;
+        a.W = cur.data();
+        a.T = htrise::shape_product(cur.shape) / (l0.r * l1.r);
+        a.r0 = static_cast<int>(l0.r);
+        a.r1 = static_cast<int>(l1.r);
+        a.n0 = l0.alpha;
+        a.n1 = l1.alpha;
+        a.U0 = l0.p;
+        a.U1 = l1.p;
+        a.X = out.data();
+        if (a.T > 0) {
+            if (launch_decode2(a, c.num_sms, c.s, &c.launches) < 0) raise(HTR_ERR_RUNTIME, "decode: fused leaf kernel rejected its operands");
+            HTR_CUDA(cudaGetLastError());
+        }
+        return out;
     }
     return cur;
 }

@@ -706,3 +706,56 @@ def test_single_rank_nccl_path_matches_local(ht):
             assert np.array_equal(reps[0].core(n.id), reps[1].core(n.id)), n.id
     plain.close()
     comm.close()
+
+
+@pytest.mark.parametrize("dims,ranks,tree", [
+    ((32, 16, 5), (1, 1, 2), "1_23"),
+    ((64, 48, 6), (5, 9, 3), "1_23"),       # r0 mod 8 = 5: padded tile, no half step
+    ((128, 128, 4), (20, 20, 3), "1_23"),   # config 5's ranks: half-tile step on a0
+    ((128, 32, 4), (24, 13, 2), "1_23"),    # widest rank, ragged r1
+    ((64, 64, 3), (12, 4, 3), "1_23"),      # r0 mod 8 = 4
+    ((32, 112, 3), (17, 24, 2), "1_23"),    # r0 mod 8 = 1
+    ((64, 32, 6, 5), (8, 3, 2, 2), "balanced"),
+    ((64, 32, 4), (28, 5, 2), "1_23"),      # rank above the fused kernel's 24: generic chain
+])
+def test_fused_decode_matches_generic(ht, dims, ranks, tree):
+    """decode's last two leaf expansions in one kernel (k_decode.cu) equal the
+    per-mode chain (bht.hpp:437-455) and reconstruct the encoded batch."""
+    rng = np.random.default_rng(sum(dims) * 31 + sum(ranks))
+    bases = [ro.random_orthonormal(n, r, rng) for n, r in zip(dims, ranks)]
+    y = ro.tucker_family_batch(bases, 3, rng)
+    t = ht.tree_1_23() if tree == "1_23" else ht.DimensionTree.balanced(len(dims))
+    rep, _ = ht.bht_l2r(y, t, 1e-6)
+    assert set(ranks) <= set(rep.ranks().values())
+    lat, _ = ht.encode(rep, y)
+    ctx = rep.ctx
+    xa = ht.decode(rep, lat)
+    ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+    try:
+        xb = ht.decode(rep, lat)
+    finally:
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    assert np.linalg.norm(xa - xb) <= 1e-13 * np.linalg.norm(xb)
+    assert np.linalg.norm(xa - y) <= 1e-6 * np.linalg.norm(y)
+    # one-sample decode: the kernels before the fused one may differ with the
+    # sample count, so agreement is to rounding, not bit for bit
+    xs = ht.reconstruct_slice(rep, 2)
+    assert np.linalg.norm(xs - xa[..., 1]) <= 1e-13 * np.linalg.norm(xs)
+
+
+def test_fused_decode_kernel_runs(ht):
+    """The fused decode kernel is the one that runs for config 5's shapes."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    rng = np.random.default_rng(5)
+    bases = [ro.random_orthonormal(128, 20, rng) for _ in range(3)]
+    y = ro.tucker_family_batch(bases, 2, rng)
+    rep, _ = ht.bht_l2r(y, ht.tree_1_23(), 1e-6)
+    lat, _ = ht.encode(rep, y)
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        x = ht.decode(rep, lat)
+        rep.ctx.synchronize()
+    names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    assert any("decode2_kernel" in n for n in names), names
+    assert np.linalg.norm(x - y) <= 1e-6 * np.linalg.norm(y)
