@@ -172,6 +172,14 @@ HTR_API htr_status htr_decode(htr_context* ctx, const htr_rep* rep, const double
 HTR_API htr_status htr_reconstruct_slice(htr_context* ctx, const htr_rep* rep, int64_t m, double* out,
                                  int32_t out_on_device);
 
+/* Relative reconstruction error of one test tensor, the summand of
+ * relative_test_error (metrics.hpp:218-237): ||y - decode(encode(y))|| / ||y||
+ * (0 when ||y|| = 0). y is prod(dims) x N (order d + 1) or one sample
+ * (order d). The reconstruction is compared on the device and, where the
+ * fused decode kernel applies, never materialised. */
+HTR_API htr_status htr_relative_error(htr_context* ctx, const htr_rep* rep, const double* y, int32_t y_on_device,
+                              const int64_t* shape, int32_t order, double* rel_error);
+
 /* ---- representation values ------------------------------------------ */
 HTR_API htr_status htr_rep_free(htr_rep* rep);
 HTR_API htr_status htr_rep_clone(htr_context* ctx, const htr_rep* rep, htr_rep** out);

@@ -869,3 +869,21 @@ def reduction_ratio(h: HTRepresentation) -> float:
     """metrics.hpp:210-214."""
     r = h.root()
     return float(np.prod(h.dims)) / float(r.shape[0] * r.shape[1])
+
+
+def relative_test_error(h: HTRepresentation, test_set) -> float:
+    """metrics.hpp:218-237: mean over the set of ||y - decode(encode(y))|| / ||y||;
+    an order-d tensor gains a unit batch axis (224-226); zero tensors add 0
+    but still count in the mean (230-231)."""
+    test_set = list(test_set)
+    if not test_set:
+        raise ValueError("relative_test_error: empty test set")
+    total = 0.0
+    for t in test_set:
+        y = t.reshape(t.shape + (1,), order="F") if t.ndim == h.tree.dims() else t
+        back = decode(h, encode(h, y)[0])
+        ny = float(np.linalg.norm(y))
+        if ny == 0.0:
+            continue
+        total += float(np.linalg.norm(y - back)) / ny
+    return total / len(test_set)

@@ -322,6 +322,27 @@ htr_status htr_reconstruct_slice(htr_context* ctx, const htr_rep* rep, int64_t m
     });
 }
 
+htr_status htr_relative_error(htr_context* ctx, const htr_rep* rep, const double* y, int32_t y_on_device,
+                              const int64_t* shape, int32_t order, double* rel_error) {
+    return guarded(ctx, [&] {
+        htr::Context& c = C(ctx);
+        const htr::Rep& h = R(rep);
+        if (!rel_error) htr::raise(HTR_ERR_INVALID_ARGUMENT, "null output pointer");
+        Shape s = to_shape(shape, order);
+        if (static_cast<htrise::Index>(s.size()) == h.tree.dims()) s.push_back(1);  // metrics.hpp:224-226
+        htr::check_batch_input(s, h.tree, &h.dims, "encode");  // the reference fails inside encode
+        DT yt = input(c, y, y_on_device != 0, s);
+        htr::EncodeOut e = htr::encode(c, h, yt, false);
+        if (e.nonfinite) htr::raise(HTR_ERR_INVALID_ARGUMENT, "encode: non-finite input");
+        htr::BufPtr r = c.alloc(1);
+        htr::decode_residual_sq(c, h, e.latent, yt, r->p);
+        c.allreduce(r->p, 1);
+        double rsq = 0.0;
+        c.fetch(r->p, 1, &rsq);
+        *rel_error = e.ysq == 0.0 ? 0.0 : std::sqrt(rsq) / std::sqrt(e.ysq);
+    });
+}
+
 htr_status htr_rep_free(htr_rep* rep) {
     delete rep;
     return HTR_OK;

@@ -50,10 +50,14 @@ constexpr size_t decode2_smem_doubles() {
 }
 
 // N0T: n0 / 8 (i0 n-tiles); MT0: ceil(r0 / 8) (a0 tiles of step A's output)
-template <int N0T, int MT0>
+// RESID: instead of storing X, accumulate sum (X - Y)^2 (relative_test_error,
+// metrics.hpp:218-237) into one partial per warp; the reconstruction is never
+// written.
+template <int N0T, int MT0, bool RESID>
 __global__ void __launch_bounds__(kDecWarps * 32, 1)
     decode2_kernel(const double* __restrict__ W, int64_t T, int r0, int r1, int n1, const double* __restrict__ U0,
-                   const double* __restrict__ U1, double* __restrict__ X) {
+                   const double* __restrict__ U1, double* __restrict__ X, const double* __restrict__ Y,
+                   double* __restrict__ partials) {
     constexpr int HT = N0T > 8 ? 8 : N0T;  // n-tiles per pass (accumulator budget)
     constexpr int NH = N0T / HT;
     constexpr int n0 = 8 * N0T;
@@ -102,6 +106,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
     int buf = 0;
     const int np = n1 / 16;
     const int src_lane = (lane & ~3) | (t4 >> 1);
+    double rs = 0.0;
     for (int64_t t = gw; t < T; t += nw, buf ^= 1) {
         if (t + nw < T) {
             issue(t + nw, buf ^ 1);
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
                 wf[nt][ks] = (a0 < r0 && a1 < r1) ? wb[a0 + r0 * a1] : 0.0;
             }
         __syncwarp();  // this buffer is refilled two slabs later
-        double* xs = X + static_cast<int64_t>(n0) * n1 * t;
+        const int64_t xoff = static_cast<int64_t>(n0) * n1 * t;
         for (int p = 0; p < np; ++p) {
             double ca[2][MT0][2];
 #pragma unroll
@@ -164,6 +169,18 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
             }
 #pragma unroll
             for (int hh = 0; hh < NH; ++hh) {
+                const int64_t rowoff[2] = {xoff + static_cast<int64_t>(n0) * (16 * p + g4) + 8 * hh * HT + 2 * t4,
+                                           xoff + static_cast<int64_t>(n0) * (16 * p + 8 + g4) + 8 * hh * HT + 2 * t4};
+                double2 yv[RESID ? 2 : 1][RESID ? HT : 1];
+                if constexpr (RESID) {
+#pragma unroll
+                    for (int m = 0; m < 2; ++m)
+#pragma unroll
+                        for (int j = 0; j < HT; ++j)
+                            asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                                         : "=d"(yv[m][j].x), "=d"(yv[m][j].y)
+                                         : "l"(Y + rowoff[m] + 8 * j));
+                }
                 double acc[2][HT][2];
 #pragma unroll
                 for (int m = 0; m < 2; ++m)
@@ -186,38 +203,75 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
                     }
                 }
 #pragma unroll
-                for (int m = 0; m < 2; ++m) {
-                    double* row = xs + static_cast<int64_t>(n0) * (16 * p + 8 * m + g4) + 8 * hh * HT + 2 * t4;
+                for (int m = 0; m < 2; ++m)
 #pragma unroll
-                    for (int j = 0; j < HT; ++j)
-                        *reinterpret_cast<double2*>(row + 8 * j) = make_double2(acc[m][j][0], acc[m][j][1]);
-                }
+                    for (int j = 0; j < HT; ++j) {
+                        if constexpr (RESID) {
+                            const double d0 = acc[m][j][0] - yv[m][j].x, d1 = acc[m][j][1] - yv[m][j].y;
+                            rs = fma(d0, d0, fma(d1, d1, rs));
+                        } else {
+                            *reinterpret_cast<double2*>(X + rowoff[m] + 8 * j) = make_double2(acc[m][j][0], acc[m][j][1]);
+                        }
+                    }
             }
         }
     }
+    if constexpr (RESID) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+        if (lane == 0) partials[gw] = rs;
+    }
 }
 
-template <int N0T, int MT0>
+template <int N0T, int MT0, bool RESID>
 int launch_t(const Decode2Args& a, int num_sms, cudaStream_t s) {
     constexpr size_t smem = sizeof(double) * decode2_smem_doubles<N0T, MT0>();
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(decode2_kernel<N0T, MT0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(decode2_kernel<N0T, MT0, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         configured = true;
     }
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, (a.T + kDecWarps - 1) / kDecWarps)));
-    decode2_kernel<N0T, MT0><<<grid, kDecWarps * 32, smem, s>>>(a.W, a.T, a.r0, a.r1, static_cast<int>(a.n1), a.U0,
-                                                                 a.U1, a.X);
+    decode2_kernel<N0T, MT0, RESID><<<grid, kDecWarps * 32, smem, s>>>(a.W, a.T, a.r0, a.r1, static_cast<int>(a.n1),
+                                                                        a.U0, a.U1, a.X, a.Y, a.partials);
     return grid;
 }
 
-template <int N0T>
+template <int N0T, bool RESID>
 int launch_n0(const Decode2Args& a, int num_sms, cudaStream_t s) {
     const int mt0 = (a.r0 + 7) / 8;
-    if (mt0 == 1) return launch_t<N0T, 1>(a, num_sms, s);
-    if (mt0 == 2) return launch_t<N0T, 2>(a, num_sms, s);
-    return launch_t<N0T, 3>(a, num_sms, s);
+    if (mt0 == 1) return launch_t<N0T, 1, RESID>(a, num_sms, s);
+    if (mt0 == 2) return launch_t<N0T, 2, RESID>(a, num_sms, s);
+    return launch_t<N0T, 3, RESID>(a, num_sms, s);
+}
+
+template <bool RESID>
+int launch_r(const Decode2Args& a, int num_sms, cudaStream_t s) {
+    if (a.n0 == 32) return launch_n0<4, RESID>(a, num_sms, s);
+    if (a.n0 == 64) return launch_n0<8, RESID>(a, num_sms, s);
+    return launch_n0<16, RESID>(a, num_sms, s);
+}
+
+// sum (x - y)^2 per block (the generic path's residual)
+__global__ void __launch_bounds__(256) diff_sumsq_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                                         int64_t n, double* __restrict__ partials) {
+    __shared__ double sh[8];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double d = x[i] - y[i];
+        s = fma(d, d, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += sh[w];
+        partials[blockIdx.x] = t;
+    }
 }
 
 }  // namespace
@@ -229,11 +283,22 @@ bool decode2_supported(int64_t n0, int64_t n1, int64_t r0, int64_t r1) {
 
 int launch_decode2(const Decode2Args& a, int num_sms, cudaStream_t s, int64_t* launches) {
     if (!decode2_supported(a.n0, a.n1, a.r0, a.r1) || a.T < 1) return -1;
-    if ((reinterpret_cast<uintptr_t>(a.X) & 15u) != 0 || (reinterpret_cast<uintptr_t>(a.W) & 7u) != 0) return -1;
-    int grid;
-    if (a.n0 == 32) grid = launch_n0<4>(a, num_sms, s);
-    else if (a.n0 == 64) grid = launch_n0<8>(a, num_sms, s);
-    else grid = launch_n0<16>(a, num_sms, s);
+    if ((!a.Y && (reinterpret_cast<uintptr_t>(a.X) & 15u) != 0) || (reinterpret_cast<uintptr_t>(a.W) & 7u) != 0) return -1;
+    if (a.Y && (!a.partials || (reinterpret_cast<uintptr_t>(a.Y) & 15u) != 0)) return -1;
+    const int grid = a.Y ? launch_r<true>(a, num_sms, s) : launch_r<false>(a, num_sms, s);
+    ++*launches;
+    return grid;
+}
+
+int64_t decode2_partials(int64_t T, int num_sms) {
+    return static_cast<int64_t>(std::max<int64_t>(1, std::min<int64_t>(num_sms, (T + kDecWarps - 1) / kDecWarps))) *
+           kDecWarps;
+}
+
+int launch_diff_sumsq(const double* x, const double* y, int64_t n, double* partials, int num_sms, cudaStream_t s,
+                      int64_t* launches) {
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4 * num_sms, (n + 255) / 256)));
+    diff_sumsq_kernel<<<grid, 256, 0, s>>>(x, y, n, partials);
     ++*launches;
     return grid;
 }

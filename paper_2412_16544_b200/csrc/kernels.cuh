@@ -211,9 +211,16 @@ struct Decode2Args {
     const double* U0;  // n0 x r0, column-major
     const double* U1;  // n1 x r1
     double* X;         // [n0][n1][T]
+    const double* Y = nullptr;  // set: no X; one sum (X - Y)^2 per warp into partials
+    double* partials = nullptr;
 };
 bool decode2_supported(int64_t n0, int64_t n1, int64_t r0, int64_t r1);
 int launch_decode2(const Decode2Args& a, int num_sms, cudaStream_t s, int64_t* launches);
+/// Partials written by a residual-mode launch_decode2 over T slabs.
+int64_t decode2_partials(int64_t T, int num_sms);
+/// One sum (x - y)^2 per block into partials; returns the block count.
+int launch_diff_sumsq(const double* x, const double* y, int64_t n, double* partials, int num_sms, cudaStream_t s,
+                      int64_t* launches);
 
 bool quad_supported(int64_t extent, int64_t rank);
 /// Returns the grid size (number of partials written), -1 for an unaligned X.

@@ -1728,7 +1728,18 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
 // decode (bht.hpp:406-456)
 // ---------------------------------------------------------------------------
 
-DT decode(Context& c, const Rep& h, const DT& latent, double* dst) {
+namespace {
+DT decode_impl(Context& c, const Rep& h, const DT& latent, double* dst, const DT* ref, double* resid_out);
+}
+
+DT decode(Context& c, const Rep& h, const DT& latent, double* dst) { return decode_impl(c, h, latent, dst, nullptr, nullptr); }
+
+void decode_residual_sq(Context& c, const Rep& h, const DT& latent, const DT& y, double* out) {
+    decode_impl(c, h, latent, nullptr, &y, out);
+}
+
+namespace {
+DT decode_impl(Context& c, const Rep& h, const DT& latent, double* dst, const DT* ref, double* resid_out) {
     const int64_t r11 = h.root->r11, r12 = h.root->r12;
     if (latent.shape.size() != 3 || latent.shape[0] != r11 || latent.shape[1] != r12)
         raise(HTR_ERR_INVALID_ARGUMENT, "decode: latent ranks " + htrise::shape_to_string(latent.shape) +
@@ -1774,7 +1785,8 @@ DT decode(Context& c, const Rep& h, const DT& latent, double* dst) {
     const Basis l1 = modes.size() >= 2 ? basis_of(h, modes[1]) : l0;
     const bool fuse2 = c.fused && modes.size() >= 2 && cur.shape[0] == l0.r && cur.shape[1] == l1.r &&
                        decode2_supported(l0.alpha, l1.alpha, l0.r, l1.r) &&
-                       (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
+                       (reinterpret_cast<uintptr_t>(dst) & 15u) == 0 &&
+                       (!ref || (reinterpret_cast<uintptr_t>(ref->data()) & 15u) == 0);
     std::vector<size_t> order;
     for (size_t k = fuse2 ? 2 : 0; k < modes.size(); ++k) order.push_back(k);
     auto growth = [&](size_t k) {
@@ -1793,7 +1805,9 @@ DT decode(Context& c, const Rep& h, const DT& latent, double* dst) {
         os[0] = l0.alpha;
         os[1] = l1.alpha;
         DT out;
-        if (dst) {
+        if (ref) {
+            out.shape = os;
+        } else if (dst) {
             out.shape = os;
             out.buf = std::make_shared<Buf>(c.st, dst, htrise::shape_product(os));
         } else {
@@ -1808,14 +1822,38 @@ DT decode(Context& c, const Rep& h, const DT& latent, double* dst) {
         a.n1 = l1.alpha;
         a.U0 = l0.p;
         a.U1 = l1.p;
-        a.X = out.data();
+        BufPtr parts;
+        if (ref) {
+            a.X = nullptr;
+            a.Y = ref->data();
+            parts = c.alloc(decode2_partials(a.T, c.num_sms));
+            a.partials = parts->p;
+        } else {
+            a.X = out.data();
+        }
         if (a.T > 0) {
             if (launch_decode2(a, c.num_sms, c.s, &c.launches) < 0) raise(HTR_ERR_RUNTIME, "decode: fused leaf kernel rejected its operands");
             HTR_CUDA(cudaGetLastError());
+            if (ref) launch_sum_partials(parts->p, decode2_partials(a.T, c.num_sms), resid_out, c.s, &c.launches);
+        } else if (ref) {
+            HTR_CUDA(cudaMemsetAsync(resid_out, 0, sizeof(double), c.s));
         }
         return out;
     }
+    if (ref) {
+        const int64_t n = cur.size();
+        BufPtr parts = c.alloc(std::max<int64_t>(1, 4 * c.num_sms));
+        if (n > 0) {
+            const int nb = launch_diff_sumsq(cur.data(), ref->data(), n, parts->p, c.num_sms, c.s, &c.launches);
+            launch_sum_partials(parts->p, nb, resid_out, c.s, &c.launches);
+        } else {
+            HTR_CUDA(cudaMemsetAsync(resid_out, 0, sizeof(double), c.s));
+        }
+        HTR_CUDA(cudaGetLastError());
+    }
     return cur;
 }
+
+}  // namespace
 
 }  // namespace htr

@@ -255,6 +255,10 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
 
 /// bht.hpp:406-456; the result lands in `dst` (caller device memory) when given.
 DT decode(Context& c, const Rep& h, const DT& latent, double* dst = nullptr);
+/// sum (decode(latent) - y)^2 over this rank's samples into the device scalar
+/// `out`, without materialising the reconstruction where the fused decode
+/// kernel applies (relative_test_error, metrics.hpp:218-237).
+void decode_residual_sq(Context& c, const Rep& h, const DT& latent, const DT& y, double* out);
 
 /// Append latent slices [r11, r12, N] to a representation's root (value
 /// semantics: returns the new root view).

@@ -117,6 +117,7 @@ _SIGNATURES = {
     "htr_encode": (C.c_int32, [_P, _P, _D, C.c_int32, _I64, C.c_int32, _D, C.c_int32, _D]),
     "htr_decode": (C.c_int32, [_P, _P, _D, C.c_int32, _I64, _D, C.c_int32]),
     "htr_reconstruct_slice": (C.c_int32, [_P, _P, C.c_int64, _D, C.c_int32]),
+    "htr_relative_error": (C.c_int32, [_P, _P, _D, C.c_int32, _I64, C.c_int32, _D]),
     "htr_rep_free": (C.c_int32, [_P]),
     "htr_rep_clone": (C.c_int32, [_P, _P, C.POINTER(_P)]),
     "htr_rep_info": (C.c_int32, [_P, C.POINTER(C.c_int32), _I64, _I64, _D, _I64]),
@@ -887,6 +888,25 @@ def frobenius_norm(t, ctx: Optional[Context] = None) -> float:
     ctx.check(lib().htr_frobenius_norm(ctx.handle, p, on_dev, int(np.prod(shape)), C.byref(out)))
     del keep
     return float(out.value)
+
+
+def relative_error(h: HTRepresentation, y) -> float:
+    """||y - decode(encode(y))|| / ||y|| (0 for a zero tensor) of one test
+    tensor (order d or d + 1, host or DeviceTensor), computed on the GPU."""
+    ctx = h.ctx
+    p, on_dev, shape, keep = _tensor_arg(y, ctx)
+    out = C.c_double()
+    ctx.check(lib().htr_relative_error(ctx.handle, h.handle, p, on_dev, _shape_arr(shape), len(shape), C.byref(out)))
+    del keep
+    return float(out.value)
+
+
+def relative_test_error(h: HTRepresentation, test_set) -> float:
+    """metrics.hpp:218-237: mean per-tensor relative reconstruction error."""
+    test_set = list(test_set)
+    if not test_set:
+        raise ValueError("relative_test_error: empty test set")
+    return sum(relative_error(h, t) for t in test_set) / len(test_set)
 
 
 def compression_ratio(h: HTRepresentation) -> float:

@@ -44,3 +44,30 @@ busy = sum(tot.values()) / 3
 print(f"decode c5: {busy:.1f} us device time per call; 4.295 GB written -> {4.295e9 / (busy * 1e-6) / 1e9:.0f} GB/s")
 for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
     print(f"  {v / 3:9.1f} us  x{cnt[k] / 3:.0f}  {k[:90]}")
+
+# relative_test_error summand of the same batch (encode + residual decode,
+# the reconstruction compared in HBM and never written)
+ys = (C.c_int64 * 4)(*w.shape)
+err = C.c_double()
+
+
+def rte():
+    ctx.check(ht.lib().htr_relative_error(ctx.handle, rep._h, dp(y0), 1, ys, 4, C.byref(err)))
+
+
+rte()
+ctx.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(3):
+        rte()
+    ctx.synchronize()
+tot, cnt = defaultdict(float), defaultdict(int)
+for e in prof.events():
+    if e.device_type == torch.autograd.DeviceType.CUDA:
+        tot[e.name] += e.device_time_total
+        cnt[e.name] += 1
+busy = sum(tot.values()) / 3
+print(f"relative error c5 (rte {err.value:.3e}): {busy:.1f} us device time per call; "
+      f"4.295 GB read twice -> {2 * 4.295e9 / (busy * 1e-6) / 1e9:.0f} GB/s")
+for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+    print(f"  {v / 3:9.1f} us  x{cnt[k] / 3:.0f}  {k[:90]}")
