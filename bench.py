@@ -290,6 +290,43 @@ def run_ours(args):
                "d2h_bytes_per_step": 16, "ms_per_step": e2e_ms, "steps": args.e2e_steps,
                "host_buffer": "pinned", "d2h": "||y||^2 and ||latent||^2, written by the tail kernel to mapped host memory"}
 
+    # the step after the path: decode one batch's latents
+    # into device memory, and relative_test_error's summand of one batch
+    # (encode + residual decode, the reconstruction compared in HBM)
+    recon = None
+    if args.decode_steps > 0:
+        yd = ht.DeviceTensor(pool[0], shape)
+        lat, _ = ht.encode(rep, yd)
+        lat_d = ht.DeviceTensor(torch.from_numpy(np.ascontiguousarray(lat.transpose(2, 1, 0))).cuda(), lat.shape)
+        out_d = ht.DeviceTensor(pool[-1], shape)  # the last use of this pool slot
+        rel = ht.relative_error(rep, yd)  # warm-up (also the residual path's workspace)
+        ht.decode(rep, lat_d, out=out_d)
+        ctx.synchronize()
+
+        def timed(fn):
+            barrier()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(args.decode_steps):
+                fn()
+            e1.record(stream)
+            e1.synchronize()
+            t = e0.elapsed_time(e1) / args.decode_steps
+            if dist is not None:
+                tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            return t
+
+        dec_ms = timed(lambda: ht.decode(rep, lat_d, out=out_d))
+        rte_ms = timed(lambda: ht.relative_error(rep, yd))
+        recon = {"decode": {"ms_per_batch": dec_ms, "value": global_bytes / (dec_ms * 1e-3) / 1e9,
+                            "unit": "GB/s of reconstruction written", "kernel": "expand_kernel + decode2_kernel"},
+                 "relative_error": {"ms_per_batch": rte_ms, "value": global_bytes / (rte_ms * 1e-3) / 1e9,
+                                    "unit": "GB/s of test tensor", "rte": rel,
+                                    "kernels": "fused3 + tail3 (encode), expand + decode2<resid> (nothing written)"},
+                 "calls": args.decode_steps, "timing": "CUDA events around back-to-back C-ABI calls, device in/out"}
+
     peak, peak_kind = _peaks()
     traffic = None
     try:
@@ -356,7 +393,7 @@ def run_ours(args):
                              "value": call_value, "ms_per_step": call_ms, "skipped_updates": skipped,
                              "fused_path_updates": fused_used, "gpu_launches": int(call_launches)},
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clocks2.summary(), "clocks_per_call": clocks.summary()}
+                "clocks": clocks2.summary(), "clocks_per_call": clocks.summary(), "reconstruction": recon}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -372,6 +409,7 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--pool", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--decode-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -794,12 +794,20 @@ def encode(h: HTRepresentation, y):
     return lat.reshape(_latent_shape(h, shape[-1]), order="F"), float(err.value)
 
 
-def decode(h: HTRepresentation, latent) -> np.ndarray:
-    """bht.hpp:406-456."""
+def decode(h: HTRepresentation, latent, out: Optional[DeviceTensor] = None):
+    """bht.hpp:406-456. With `out` (a DeviceTensor of prod(dims) x N
+    elements) the reconstruction is written there in device memory and `out`
+    is returned; otherwise a host array."""
     ctx = h.ctx
     p, on_dev, shape, keep = _tensor_arg(latent, ctx)
     if len(shape) != 3:
         raise ValueError(f"decode: latent ranks {list(shape)} do not match root")
+    if out is not None:
+        if not isinstance(out, DeviceTensor) or tuple(out.shape) != tuple(h.dims) + (shape[2],):
+            raise ValueError("decode: out must be a DeviceTensor of shape dims + (N,)")
+        ctx.check(lib().htr_decode(ctx.handle, h.handle, p, on_dev, _shape_arr(shape), C.cast(out.ptr(), _D), 1))
+        del keep
+        return out
     out = np.zeros(int(np.prod(h.dims)) * shape[2], dtype=np.float64)
     ctx.check(lib().htr_decode(ctx.handle, h.handle, p, on_dev, _shape_arr(shape), _ptr(out), 0))
     del keep
