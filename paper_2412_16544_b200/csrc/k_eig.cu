@@ -172,15 +172,28 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
 // is the transpose held in the same entries).
 // --------------------------------------------------------------------------
 constexpr int kSymMaxN = 135;  // n(n+1)/2 + n^2 doubles = 194 KB at n = 135
+constexpr int kEigBatchMax = 8;
 
 __device__ __forceinline__ int sym_idx(int i, int j, int n) {  // packed lower, column-major
     if (i < j) { const int t = i; i = j; j = t; }
     return j * n - ((j * (j + 1)) >> 1) + i;
 }
 
-__global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const double* __restrict__ G, int n,
-                                                                    double* __restrict__ lambda,
-                                                                    double* __restrict__ Vout) {
+// one CTA per job of the batch: independent eigenproblems (the leaf Grams of
+// one layer) run side by side; each CTA's arithmetic does not depend on the
+// batch or the block size, so a batched solve equals the single ones bit for bit
+struct SymJobs {
+    const double* G[kEigBatchMax];
+    double* lambda[kEigBatchMax];
+    double* V[kEigBatchMax];
+    int n[kEigBatchMax];
+};
+
+__global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJobs jobs) {
+    const double* __restrict__ G = jobs.G[blockIdx.x];
+    const int n = jobs.n[blockIdx.x];
+    double* __restrict__ lambda = jobs.lambda[blockIdx.x];
+    double* __restrict__ Vout = jobs.V[blockIdx.x];
     extern __shared__ double smem[];
     __shared__ double cs[kSymMaxN], sn[kSymMaxN];
     __shared__ int prs[kSymMaxN], qrs[kSymMaxN];
@@ -217,14 +230,16 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const double
                 cs[i] = c; sn[i] = s; prs[i] = p; qrs[i] = q;
             }
             __syncthreads();
-            // blocks P <= Q (linear index over the upper triangle of pairs)
-            const int blocks = (half * (half + 1)) / 2;
-            for (int b = tid; b < blocks; b += nt) {
-                // Q-major: b = Q (Q + 1) / 2 + P, P <= Q
-                int Q = static_cast<int>((sqrtf(8.0f * static_cast<float>(b) + 1.0f) - 1.0f) * 0.5f);
-                while ((Q * (Q + 1)) / 2 > b) --Q;
-                while (((Q + 1) * (Q + 2)) / 2 <= b) ++Q;
-                const int P = b - (Q * (Q + 1)) / 2;
+            // blocks P <= Q: warp w takes the column pairs Q = qq and
+            // Q' = half - 1 - qq together (qq + 1 and Q' + 1 blocks: half + 1
+            // per qq) and its lanes stride over the concatenated P ranges
+            const int lane = tid & 31, nwarps = nt >> 5;
+            for (int qq = tid >> 5; qq <= half - 1 - qq; qq += nwarps) {
+              const int q2 = half - 1 - qq;
+              const int cnt = qq == q2 ? qq + 1 : half + 1;
+              for (int e = lane; e < cnt; e += 32) {
+                const int Q = e <= qq ? qq : q2;
+                const int P = e <= qq ? e : e - qq - 1;
                 const double cP = cs[P], sP = sn[P], cQ = cs[Q], sQ = sn[Q];
                 if (sP == 0.0 && sQ == 0.0) continue;
                 const int pP = prs[P], qP = qrs[P], pQ = prs[Q], qQ = qrs[Q];
@@ -253,6 +268,7 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const double
                 if (okc) A[i01] = sQ * y00 + cQ * y01;
                 if (okr) A[i10] = cQ * y10 - sQ * y11;
                 if (okr && okc) A[i11] = sQ * y10 + cQ * y11;
+              }
             }
             const int vitems = half * n;
             for (int it = tid; it < vitems; it += nt) {
@@ -606,7 +622,12 @@ void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, do
             configured_sym = true;
         }
         const int threads = n <= 32 ? 128 : (n <= 64 ? 256 : kJacobiThreads);
-        jacobi_sym_kernel<<<1, threads, ssmem, s>>>(G, static_cast<int>(n), lambda, V);
+        SymJobs jobs{};
+        jobs.G[0] = G;
+        jobs.lambda[0] = lambda;
+        jobs.V[0] = V;
+        jobs.n[0] = static_cast<int>(n);
+        jacobi_sym_kernel<<<1, threads, ssmem, s>>>(jobs);
         ++*launches;
         return;
     }
@@ -625,6 +646,35 @@ void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, do
     const int threads = n <= 32 ? 128 : (n <= 64 ? 256 : kJacobiThreads);
     jacobi_kernel<<<1, threads, smem, s>>>(G, static_cast<int>(n), lambda, V, work, 1, v_smem ? 1 : 0);
     ++*launches;
+}
+
+bool jacobi_batchable(int64_t n) { return n >= 1 && n <= kSymMaxN; }
+
+void launch_jacobi_eig_batch(const double* const* G, const int64_t* n, double* const* lambda, double* const* V,
+                             int count, cudaStream_t s, int64_t* launches) {
+    for (int b0 = 0; b0 < count; b0 += kEigBatchMax) {
+        const int cnt = std::min(count - b0, kEigBatchMax);
+        SymJobs jobs{};
+        int64_t nmax = 0;
+        for (int i = 0; i < cnt; ++i) {
+            jobs.G[i] = G[b0 + i];
+            jobs.lambda[i] = lambda[b0 + i];
+            jobs.V[i] = V[b0 + i];
+            jobs.n[i] = static_cast<int>(n[b0 + i]);
+            nmax = std::max(nmax, n[b0 + i]);
+        }
+        static bool configured_sym = false;
+        if (!configured_sym) {
+            cudaFuncSetAttribute(jacobi_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(double) * (kSymMaxN * (kSymMaxN + 1) / 2 +
+                                                                    kSymMaxN * kSymMaxN)));
+            configured_sym = true;
+        }
+        const size_t ssmem = sizeof(double) * static_cast<size_t>(nmax * (nmax + 1) / 2 + nmax * nmax);
+        const int threads = nmax <= 32 ? 128 : (nmax <= 64 ? 256 : kJacobiThreads);
+        jacobi_sym_kernel<<<cnt, threads, ssmem, s>>>(jobs);
+        ++*launches;
+    }
 }
 
 void launch_posdef_test(const double* G, int64_t n, double shift, double* work, double* flag, cudaStream_t s,

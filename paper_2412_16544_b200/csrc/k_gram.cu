@@ -1,0 +1,248 @@
+// Streaming Gram of a mode unfolding, G = Y_(k) Y_(k)^T (the input of every
+// truncation: truncated_svd of unfold(c, k), truncated_svd.hpp:53 via
+// bht.hpp:284 / ht_rise.hpp:158), for modes k >= 1 of a large tensor.
+//
+// View the tensor as Y[K, M, B] (K = prod of the extents before mode k,
+// contiguous; M = n_k; B = the rest): G[m, m'] = sum_b sum_k Y[k,m,b] Y[k,m',b].
+// Each CTA owns a contiguous range of (b, 16-row k chunk) units. One producer
+// warp streams the chunks by TMA (cp.async.bulk.tensor.3d, box 16 x M, 128-byte
+// swizzle) into an 8-deep shared-memory ring; the consumer warps each own one
+// 32 x 32 block of the lower triangle of G and accumulate it on DMMA 8x8x4
+// (A and B fragments are both rows of the same chunk; the swizzle makes the
+// fragment reads conflict-free). Diagonal blocks skip their upper tiles, so
+// the MMA work is that of the lower triangle (136 of 256 tiles at M = 128).
+// Every CTA writes its partial G; a fixed-order reduction sums the partials
+// and mirrors the triangle. Deterministic for a given grid.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "kernels.cuh"
+
+namespace htr {
+namespace {
+
+constexpr int kGStages = 8;
+constexpr int kGChunk = 16;  // k rows per chunk (128 B: the swizzle span)
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c[0]), "+d"(c[1])
+        : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(saddr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                      uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(saddr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(saddr(bar)), "l"(policy)
+        : "memory");
+}
+
+// element (row m, k) of a swizzled chunk [M][16 doubles]
+__device__ __forceinline__ int swz(int m, int k) { return m * kGChunk + ((((k >> 1) ^ (m & 7))) << 1) + (k & 1); }
+
+template <int MB>
+__host__ __device__ constexpr int consumer_warps() {
+    return MB * (MB + 1) / 2;
+}
+
+template <int MB>
+__global__ void __launch_bounds__((consumer_warps<MB>() + 1) * 32, 1)
+    gram_stream_kernel(int64_t units, int64_t kchunks, int M, double* __restrict__ partials,
+                       const __grid_constant__ CUtensorMap tmap) {
+    constexpr int CW = consumer_warps<MB>();
+    constexpr int MP = 32 * MB;  // padded rows per chunk
+    extern __shared__ __align__(1024) unsigned char gsm_raw[];
+    double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + kGStages * MP * kGChunk);
+    uint64_t* empty = full + kGStages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kGStages; ++s) {
+            bar_init(full + s, 1);
+            bar_init(empty + s, CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == CW) {
+        // producer: one lane issues the chunk copies kGStages ahead
+        if (lane == 0) {
+            uint64_t pol;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+            const uint32_t bytes = static_cast<uint32_t>(MP * kGChunk * sizeof(double));
+            for (int64_t u = u0, i = 0; u < u1; ++u, ++i) {
+                const int s = static_cast<int>(i % kGStages);
+                if (i >= kGStages) bar_wait(empty + s, static_cast<uint32_t>(((i / kGStages) - 1) & 1));
+                bar_expect_tx(full + s, bytes);
+                const int64_t b = u / kchunks, kc = u - b * kchunks;
+                tma3d(ring + s * MP * kGChunk, &tmap, static_cast<int>(kc * kGChunk), 0, static_cast<int>(b),
+                      full + s, pol);
+            }
+        }
+        return;
+    }
+    // consumer warp -> lower-triangle block (mb >= nb)
+    int mb = 0, nb = warp;
+    while (nb > mb) {
+        nb -= mb + 1;
+        ++mb;
+    }
+    const bool diag = mb == nb;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int64_t u = u0, i = 0; u < u1; ++u, ++i) {
+        const int s = static_cast<int>(i % kGStages);
+        bar_wait(full + s, static_cast<uint32_t>((i / kGStages) & 1));
+        const double* ch = ring + s * MP * kGChunk;
+#pragma unroll
+        for (int ks = 0; ks < kGChunk / 4; ++ks) {
+            const int k = 4 * ks + t4;
+            double af[4], bf[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) af[t] = ch[swz(32 * mb + 8 * t + g4, k)];
+            if (diag) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) bf[t] = af[t];
+            } else {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) bf[t] = ch[swz(32 * nb + 8 * t + g4, k)];
+            }
+#pragma unroll
+            for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+                for (int tj = 0; tj < 4; ++tj)
+                    if (!diag || tj <= ti) dmma(acc[ti][tj], af[ti], bf[tj]);
+        }
+        __syncwarp();
+        if (lane == 0) bar_arrive(empty + s);
+    }
+    double* out = partials + static_cast<int64_t>(blockIdx.x) * MP * MP;
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+        for (int tj = 0; tj < 4; ++tj) {
+            if (diag && tj > ti) continue;
+            const int m = 32 * mb + 8 * ti + g4, n = 32 * nb + 8 * tj + 2 * t4;
+            out[m + MP * n] = acc[ti][tj][0];
+            out[m + MP * (n + 1)] = acc[ti][tj][1];
+        }
+    (void)M;
+}
+
+// G[m, m'] = G[m', m] = sum over CTAs (in order) of the lower-triangle partial
+__global__ void gram_reduce_kernel(const double* __restrict__ partials, int nparts, int MP, int M,
+                                   double* __restrict__ G) {
+    const int64_t total = static_cast<int64_t>(M) * M;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int m = static_cast<int>(e % M), n = static_cast<int>(e / M);
+        const int r = m >= n ? m : n, c = m >= n ? n : m;  // lower-triangle source
+        double s = 0.0;
+        for (int p = 0; p < nparts; ++p) s += partials[static_cast<int64_t>(p) * MP * MP + r + static_cast<int64_t>(MP) * c];
+        G[m + static_cast<int64_t>(M) * n] = s;
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+template <int MB>
+size_t gram_smem_bytes() {
+    return sizeof(double) * kGStages * 32 * MB * kGChunk + 2 * kGStages * sizeof(uint64_t) + 1024;
+}
+
+template <int MB>
+int launch_mb(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, int grid, const CUtensorMap& map,
+              cudaStream_t s) {
+    const int64_t kchunks = (K + kGChunk - 1) / kGChunk;
+    const size_t smem = gram_smem_bytes<MB>();
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(gram_stream_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        configured = true;
+    }
+    gram_stream_kernel<MB><<<grid, (consumer_warps<MB>() + 1) * 32, smem, s>>>(B * kchunks, kchunks, static_cast<int>(M),
+                                                                               partials, map);
+    (void)Y;
+    return grid;
+}
+
+}  // namespace
+
+bool gram_stream_supported(const double* Y, int64_t K, int64_t M, int64_t B) {
+    return M >= 1 && M <= 128 && K >= 2 && (K & 1) == 0 && B >= 1 && B < (int64_t{1} << 31) &&
+           K < (int64_t{1} << 31) && (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && encoder() != nullptr;
+}
+
+int64_t gram_stream_partials(int64_t M, int num_sms) {
+    const int64_t MP = (M + 31) / 32 * 32;
+    return static_cast<int64_t>(num_sms) * MP * MP;
+}
+
+int launch_gram_stream(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,
+                       cudaStream_t s, int64_t* launches) {
+    if (!gram_stream_supported(Y, K, M, B)) return -1;
+    const int MB = static_cast<int>((M + 31) / 32);
+    const int MP = 32 * MB;
+    alignas(64) CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(B)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(K * 8), static_cast<cuuint64_t>(K * M * 8)};
+    cuuint32_t box[3] = {kGChunk, static_cast<cuuint32_t>(MP), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(Y), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return -1;
+    const int64_t units = B * ((K + kGChunk - 1) / kGChunk);
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, units)));
+    if (MB == 1) launch_mb<1>(Y, K, M, B, partials, grid, map, s);
+    else if (MB == 2) launch_mb<2>(Y, K, M, B, partials, grid, map, s);
+    else if (MB == 3) launch_mb<3>(Y, K, M, B, partials, grid, map, s);
+    else launch_mb<4>(Y, K, M, B, partials, grid, map, s);
+    gram_reduce_kernel<<<std::max(1, std::min(num_sms, static_cast<int>((M * M + 255) / 256))), 256, 0, s>>>(
+        partials, grid, MP, static_cast<int>(M), G);
+    *launches += 2;
+    return grid;
+}
+
+}  // namespace htr

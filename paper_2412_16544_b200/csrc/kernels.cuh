@@ -72,6 +72,12 @@ constexpr int64_t kJacobiMaxN = 2048;  // largest Gram the device eigensolver ta
 // parallel cyclic Jacobi in one CTA. Writes eigenvalues (descending) to
 // lambda and the matching eigenvectors as columns of V (n x n, col-major).
 // `work` must hold 2*n*n doubles when n exceeds the shared-memory limit.
+/// Eigenproblems the batched one-CTA solver takes (n <= 135).
+bool jacobi_batchable(int64_t n);
+/// Independent symmetric eigenproblems, one CTA each, side by side; each
+/// result equals launch_jacobi_eig's bit for bit. Every n must be batchable.
+void launch_jacobi_eig_batch(const double* const* G, const int64_t* n, double* const* lambda, double* const* V,
+                             int count, cudaStream_t s, int64_t* launches);
 void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, double* work, cudaStream_t s,
                        int64_t* launches);
 
@@ -202,6 +208,13 @@ struct QuadArgs {
     double* host_out = nullptr;
     unsigned int* ticket = nullptr;
 };
+/// Streaming Gram G = Y_(k) Y_(k)^T of Y viewed as [K, M, B] (K contiguous,
+/// M <= 128, K even; k_gram.cu). partials: gram_stream_partials doubles.
+bool gram_stream_supported(const double* Y, int64_t K, int64_t M, int64_t B);
+int64_t gram_stream_partials(int64_t M, int num_sms);
+int launch_gram_stream(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,
+                       cudaStream_t s, int64_t* launches);
+
 /// Fused two-leaf reconstruction X = (U0 (x) U1) W per slab (k_decode.cu).
 struct Decode2Args {
     const double* W;  // [r0][r1][T]

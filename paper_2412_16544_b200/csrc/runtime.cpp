@@ -294,6 +294,15 @@ void residual_energy(Context& c, const DT& t, int mode, const double* U, int64_t
 DT gram(Context& c, const DT& t, int mode, bool reduce) {
     const Split sp = split_at(t.shape, mode);
     DT G = c.tensor({sp.J, sp.J});
+    if (c.fused && sp.I * sp.J * sp.O >= (int64_t{1} << 22) && gram_stream_supported(t.data(), sp.I, sp.J, sp.O)) {
+        // large unfolding of a mode >= 1: the streaming lower-triangle kernel
+        BufPtr parts = c.alloc(gram_stream_partials(sp.J, c.num_sms));
+        if (launch_gram_stream(t.data(), sp.I, sp.J, sp.O, parts->p, G.data(), c.num_sms, c.s, &c.launches) > 0) {
+            HTR_CUDA(cudaGetLastError());
+            if (reduce) c.allreduce(G.data(), sp.J * sp.J);
+            return G;
+        }
+    }
     GemmDesc d;
     d.M = sp.J;
     d.N1 = sp.J;
@@ -327,6 +336,9 @@ void norm_sq(Context& c, const double* x, int64_t n, double* ysq, bool* nonfinit
 
 ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode);
 
+Truncation truncate_eig(Context& c, const BufPtr& lam, const BufPtr& V, int64_t rows, int64_t cols, double eps_abs,
+                        int64_t min_rank, const ProjectedGram& refine, double noise_scale);
+
 Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
                          const ProjectedGram& refine, double noise_scale) {
     const int64_t n = rows;
@@ -337,9 +349,16 @@ Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, do
     BufPtr lam = c.alloc(n);
     BufPtr V = c.alloc(n * n);
     BufPtr work = c.alloc(2 * n * n);
-    BufPtr info = c.alloc(4);
     launch_jacobi_eig(G.data(), n, lam->p, V->p, work->p, c.s, &c.launches);
     HTR_CUDA(cudaGetLastError());
+    return truncate_eig(c, lam, V, rows, cols, eps_abs, min_rank, refine, noise_scale);
+}
+
+Truncation truncate_eig(Context& c, const BufPtr& lam, const BufPtr& V, int64_t rows, int64_t cols, double eps_abs,
+                        int64_t min_rank, const ProjectedGram& refine, double noise_scale) {
+    const int64_t n = rows;
+    const int64_t k = std::min(rows, cols);
+    BufPtr info = c.alloc(4);
     if (refine) {
         std::vector<double> lh(static_cast<size_t>(n));
         c.fetch(lam->p, n, lh.data());
@@ -735,6 +754,59 @@ Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, do
     return truncate_gram(c, G, rows, cols_global, eps_abs, min_rank, refine, gtrace);
 }
 
+std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vector<int>& modes, double eps_abs,
+                                       int64_t min_rank, const std::vector<int64_t>& cols_global, bool sharded,
+                                       bool any_basis_when_full) {
+    // the unprojected truncations (no old basis) that take the plain Gram ->
+    // one-CTA eigensolver route are batched: their Grams first, then one
+    // launch solving all of them side by side (bit-identical to one by one)
+    const bool reduce = sharded && c.nccl_comm;
+    std::vector<char> batch(modes.size(), 0);
+    int nb = 0;
+    for (size_t i = 0; i < modes.size(); ++i) {
+        const int64_t rows = t.shape[static_cast<size_t>(modes[i])];
+        const int64_t cols_local = t.size() / rows;
+        const bool column_side = !reduce && rows > kColumnSideRows && cols_local < rows;
+        const bool posdef = any_basis_when_full && rows > 160 && rows <= cols_global[i] && rows <= kJacobiMaxN;
+        batch[i] = !column_side && !posdef && jacobi_batchable(rows);
+        nb += batch[i];
+    }
+    std::vector<Truncation> out(modes.size());
+    if (nb < 2) {
+        for (size_t i = 0; i < modes.size(); ++i)
+            out[i] = truncate_mode(c, t, modes[i], nullptr, eps_abs, min_rank, cols_global[i], sharded, any_basis_when_full);
+        return out;
+    }
+    std::vector<DT> grams;
+    std::vector<BufPtr> lams, vs;
+    std::vector<const double*> gp;
+    std::vector<int64_t> ns;
+    std::vector<double*> lp, vp;
+    for (size_t i = 0; i < modes.size(); ++i) {
+        if (!batch[i]) continue;
+        const int64_t rows = t.shape[static_cast<size_t>(modes[i])];
+        grams.push_back(gram(c, t, modes[i], reduce));
+        lams.push_back(c.alloc(rows));
+        vs.push_back(c.alloc(rows * rows));
+        gp.push_back(grams.back().data());
+        ns.push_back(rows);
+        lp.push_back(lams.back()->p);
+        vp.push_back(vs.back()->p);
+    }
+    launch_jacobi_eig_batch(gp.data(), ns.data(), lp.data(), vp.data(), nb, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+    for (size_t i = 0, j = 0; i < modes.size(); ++i) {
+        if (batch[i]) {
+            out[i] = truncate_eig(c, lams[j], vs[j], ns[j], cols_global[i], eps_abs, min_rank,
+                                  unfolding_refiner(c, t, modes[i], reduce), 0.0);
+            ++j;
+        } else {
+            out[i] = truncate_mode(c, t, modes[i], nullptr, eps_abs, min_rank, cols_global[i], sharded, any_basis_when_full);
+        }
+    }
+    return out;
+}
+
 namespace {
 
 /// t x_mode U^T. With energy_slot the explicit residual energy of the step
@@ -858,11 +930,13 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
     };
 
     // deepest layer: plain HOSVD of y over all leaves, then sequential projections
-    std::vector<Truncation> bases;
+    std::vector<int> leaf_modes;
+    std::vector<int64_t> leaf_cols;
     for (const TreeNode& n : tree.layer(p)) {
-        const int mode = static_cast<int>(n.leaf_dim);
-        bases.push_back(truncate_mode(c, cur, mode, nullptr, eps_nw, 1, cols_of(cur, mode), true, true));
+        leaf_modes.push_back(static_cast<int>(n.leaf_dim));
+        leaf_cols.push_back(cols_of(cur, leaf_modes.back()));
     }
+    std::vector<Truncation> bases = truncate_modes(c, cur, leaf_modes, eps_nw, 1, leaf_cols, true, true);
     RankMap ranks;
     for (size_t i = 0; i < bases.size(); ++i) {
         const TreeNode& n = tree.layer(p)[i];
@@ -884,11 +958,13 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
             eps_nw = adaptive_budget(eps_abs, std::max(0.0, ysq - cn * cn), svds_below(tree, l + 1));
         }
         cur.shape = layer_extents(*h, l, ranks, batch, false);
-        std::vector<Truncation> lb;
+        std::vector<int> lmodes;
+        std::vector<int64_t> lcols;
         for (Index j = 0; j < tree.layer_size(l); ++j) {
-            lb.push_back(truncate_mode(c, cur, static_cast<int>(j), nullptr, eps_nw, 1, cols_of(cur, static_cast<int>(j)),
-                                       true, true));
+            lmodes.push_back(static_cast<int>(j));
+            lcols.push_back(cols_of(cur, static_cast<int>(j)));
         }
+        std::vector<Truncation> lb = truncate_modes(c, cur, lmodes, eps_nw, 1, lcols, true, true);
         for (Index j = 0; j < tree.layer_size(l); ++j) {
             const TreeNode& n = tree.layer(l)[static_cast<size_t>(j)];
             Truncation& b = lb[static_cast<size_t>(j)];

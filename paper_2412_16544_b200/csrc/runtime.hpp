@@ -193,6 +193,11 @@ constexpr int64_t kColumnSideRows = 1024;
 /// full space spans the same subspace; `sigma` is left empty.
 Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, double eps_abs, int64_t min_rank,
                          int64_t cols_global, bool sharded = true, bool any_basis_when_full = false);
+/// truncate_mode (no old basis) of several modes of one tensor, in order;
+/// the eigensolves of those on the plain Gram route run as one batched launch.
+std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vector<int>& modes, double eps_abs,
+                                       int64_t min_rank, const std::vector<int64_t>& cols_global, bool sharded = true,
+                                       bool any_basis_when_full = false);
 
 // ---- algorithms --------------------------------------------------------------
 struct BuildOut {

@@ -759,3 +759,31 @@ def test_fused_decode_kernel_runs(ht):
     names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     assert any("decode2_kernel" in n for n in names), names
     assert np.linalg.norm(x - y) <= 1e-6 * np.linalg.norm(y)
+
+
+@pytest.mark.parametrize("dims,ranks", [
+    ((64, 37, 50), (6, 5, 7)),     # M = 37, 50: padded 32-row blocks, K chunks ragged (2368 = 148 x 16)
+    ((32, 128, 72), (4, 9, 12)),   # M = 128: ten consumer warps
+    ((50, 24, 96), (5, 3, 8)),     # K = 50 (not a chunk multiple: zero-filled tail chunk)
+])
+def test_streaming_gram_bht_matches_generic_and_oracle(ht, dims, ranks):
+    """BHT-l2r's leaf Grams of modes >= 1 on the streaming lower-triangle
+    kernel (k_gram.cu) give the generic engine's ranks and subspaces and the
+    oracle's decomposition."""
+    rng = np.random.default_rng(sum(dims) + sum(ranks))
+    bases = [ro.random_orthonormal(n, r, rng) for n, r in zip(dims, ranks)]
+    y = ro.tucker_family_batch(bases, 40, rng)
+    y += 1e-6 * rng.standard_normal(y.shape)
+    gpu, _ = ht.bht_l2r(y, ht.tree_1_23(), 1e-3)
+    ref, _ = ho.bht_l2r(y, ho.custom_tree_1_23(), 1e-3)
+    compare_reps(ht, gpu, ref)
+    ctx = gpu.ctx
+    ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+    try:
+        gen, _ = ht.bht_l2r(y, ht.tree_1_23(), 1e-3)
+    finally:
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    assert gpu.ranks() == gen.ranks()
+    for key in gpu.ranks():
+        if key != (0, 0):
+            assert sin_angle(gpu.basis_matrix(key), gen.basis_matrix(key)) <= 1e-10
