@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJob
     __syncthreads();
     const double floor_abs = 0x1p-53 * tr_abs;
     const int m = n + (n & 1), half = m / 2;
+    const int vq0 = tid / n, vr0 = tid - vq0 * n, vqs = nt / n, vrs = nt - vqs * n;
     for (int sweep = 0; sweep < 40; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
@@ -270,9 +271,13 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJob
                 if (okr && okc) A[i11] = sQ * y10 + cQ * y11;
               }
             }
-            const int vitems = half * n;
-            for (int it = tid; it < vitems; it += nt) {
-                const int Q = it / n, r = it - Q * n;
+            // V's column pairs: (Q, r) items walked incrementally (no division)
+            for (int Q = vq0, r = vr0; Q < half; Q += vqs, r += vrs) {
+                if (r >= n) {
+                    r -= n;
+                    ++Q;
+                    if (Q >= half) break;
+                }
                 const double s = sn[Q];
                 if (s == 0.0) continue;
                 const double c = cs[Q];
