@@ -294,8 +294,11 @@ void residual_energy(Context& c, const DT& t, int mode, const double* U, int64_t
 DT gram(Context& c, const DT& t, int mode, bool reduce) {
     const Split sp = split_at(t.shape, mode);
     DT G = c.tensor({sp.J, sp.J});
-    if (c.fused && sp.I * sp.J * sp.O >= (int64_t{1} << 22) && gram_stream_supported(t.data(), sp.I, sp.J, sp.O)) {
-        // large unfolding of a mode >= 1: the streaming lower-triangle kernel
+    if (c.fused && sp.J >= 24 && sp.I * sp.J * sp.O >= (int64_t{1} << 22) &&
+        gram_stream_supported(t.data(), sp.I, sp.J, sp.O)) {
+        // large unfolding of a mode >= 1 with >= 24 rows: the streaming
+        // lower-triangle kernel (its 32 x 32 warp blocks would be mostly
+        // padding for fewer rows)
         BufPtr parts = c.alloc(gram_stream_partials(sp.J, c.num_sms));
         if (launch_gram_stream(t.data(), sp.I, sp.J, sp.O, parts->p, G.data(), c.num_sms, c.s, &c.launches) > 0) {
             HTR_CUDA(cudaGetLastError());
