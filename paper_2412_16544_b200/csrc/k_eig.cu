@@ -171,8 +171,21 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
 // P <= Q are updated (A' = J^T A J stays exactly symmetric; the (Q, P) block
 // is the transpose held in the same entries).
 // --------------------------------------------------------------------------
-constexpr int kSymMaxN = 135;  // n(n+1)/2 + n^2 doubles = 194 KB at n = 135
-constexpr int kEigBatchMax = 8;
+constexpr int kSymMaxN = 184;        // with V split over CTAs (below)
+constexpr int kSymOneCta = 135;      // n(n+1)/2 + n^2 doubles = 194 KB at n = 135
+constexpr int kSymSmemDoubles = 27136;  // dynamic shared memory budget (212 KB)
+constexpr int kEigBatchMax = 16;     // CTAs per launch
+
+/// CTAs over which a solve's V rows are split: each CTA carries the whole
+/// packed A (it evolves identically in every CTA: same inputs, same code)
+/// and the rows [r0, r1) of V, so that A plus its V share fits in shared
+/// memory (n = 144, c3's transfer residual: 2 CTAs).
+__host__ __device__ __forceinline__ int sym_splits(int n) {
+    const int np = n * (n + 1) / 2;
+    for (int k = 1; k <= 4; ++k)
+        if (np + ((n + k - 1) / k) * n <= kSymSmemDoubles) return k;
+    return 0;
+}
 
 __device__ __forceinline__ int sym_idx(int i, int j, int n) {  // packed lower, column-major
     if (i < j) { const int t = i; i = j; j = t; }
@@ -184,9 +197,10 @@ __device__ __forceinline__ int sym_idx(int i, int j, int n) {  // packed lower, 
 // batch or the block size, so a batched solve equals the single ones bit for bit
 struct SymJobs {
     const double* G[kEigBatchMax];
-    double* lambda[kEigBatchMax];
+    double* lambda[kEigBatchMax];  // null on the CTAs that do not write eigenvalues
     double* V[kEigBatchMax];
     int n[kEigBatchMax];
+    int r0[kEigBatchMax], r1[kEigBatchMax];  // V rows held by this CTA
 };
 
 __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJobs jobs) {
@@ -194,6 +208,7 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJob
     const int n = jobs.n[blockIdx.x];
     double* __restrict__ lambda = jobs.lambda[blockIdx.x];
     double* __restrict__ Vout = jobs.V[blockIdx.x];
+    const int vr0 = jobs.r0[blockIdx.x], nr = jobs.r1[blockIdx.x] - vr0;
     extern __shared__ double smem[];
     __shared__ double cs[kSymMaxN], sn[kSymMaxN];
     __shared__ int prs[kSymMaxN], qrs[kSymMaxN];
@@ -202,11 +217,11 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJob
     const int tid = threadIdx.x, nt = blockDim.x;
     const int np = (n * (n + 1)) / 2;
     double* A = smem;       // packed lower triangle
-    double* V = smem + np;  // n x n, column-major
+    double* V = smem + np;  // rows [vr0, vr0 + nr) of V (nr x n, column-major)
     for (int j = 0; j < n; ++j)
         for (int i = j + tid; i < n; i += nt)
             A[sym_idx(i, j, n)] = 0.5 * (G[i + static_cast<int64_t>(n) * j] + G[j + static_cast<int64_t>(n) * i]);
-    for (int e = tid; e < n * n; e += nt) V[e] = (e % n == e / n) ? 1.0 : 0.0;
+    for (int e = tid; e < nr * n; e += nt) V[e] = (vr0 + e % nr == e / nr) ? 1.0 : 0.0;
     __syncthreads();
     if (tid == 0) {
         double t = 0.0;
@@ -216,7 +231,7 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJob
     __syncthreads();
     const double floor_abs = 0x1p-53 * tr_abs;
     const int m = n + (n & 1), half = m / 2;
-    const int vq0 = tid / n, vr0 = tid - vq0 * n, vqs = nt / n, vrs = nt - vqs * n;
+    const int vq0 = tid / nr, vrr0 = tid - vq0 * nr, vqs = nt / nr, vrs = nt - vqs * nr;
     for (int sweep = 0; sweep < 40; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
@@ -272,17 +287,17 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJob
               }
             }
             // V's column pairs: (Q, r) items walked incrementally (no division)
-            for (int Q = vq0, r = vr0; Q < half; Q += vqs, r += vrs) {
-                if (r >= n) {
-                    r -= n;
+            for (int Q = vq0, r = vrr0; Q < half; Q += vqs, r += vrs) {
+                if (r >= nr) {
+                    r -= nr;
                     ++Q;
                     if (Q >= half) break;
                 }
                 const double s = sn[Q];
                 if (s == 0.0) continue;
                 const double c = cs[Q];
-                double* vp = V + n * prs[Q] + r;
-                double* vq = V + n * qrs[Q] + r;
+                double* vp = V + nr * prs[Q] + r;
+                double* vq = V + nr * qrs[Q] + r;
                 const double x = *vp, y = *vq;
                 *vp = c * x - s * y;
                 *vq = s * x + c * y;
@@ -301,8 +316,8 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJob
             const double lj = A[sym_idx(j, j, n)];
             rank += (lj > li) || (lj == li && j < i);
         }
-        lambda[rank] = li;
-        for (int r = 0; r < n; ++r) Vout[r + static_cast<int64_t>(n) * rank] = V[r + n * i];
+        if (lambda) lambda[rank] = li;
+        for (int r = 0; r < nr; ++r) Vout[vr0 + r + static_cast<int64_t>(n) * rank] = V[r + nr * i];
     }
 }
 
@@ -611,28 +626,13 @@ __global__ void __launch_bounds__(512) orthonormalize_kernel(const double* U, in
 
 void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, double* work, cudaStream_t s,
                        int64_t* launches) {
+    if (jacobi_batchable(n)) {
+        launch_jacobi_eig_batch(&G, &n, &lambda, &V, 1, s, launches);
+        return;
+    }
     if (n > kSmemMaxNA) {
         jacobi_cluster_kernel<<<kClusterCTAs, kClusterThreads, 0, s>>>(G, static_cast<int>(n), lambda, V, work,
                                                                        work + n * n);
-        ++*launches;
-        return;
-    }
-    if (n <= kSymMaxN) {
-        const size_t ssmem = sizeof(double) * static_cast<size_t>(n * (n + 1) / 2 + n * n);
-        static bool configured_sym = false;
-        if (!configured_sym) {
-            cudaFuncSetAttribute(jacobi_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(sizeof(double) * (kSymMaxN * (kSymMaxN + 1) / 2 +
-                                                                    kSymMaxN * kSymMaxN)));
-            configured_sym = true;
-        }
-        const int threads = n <= 32 ? 128 : (n <= 64 ? 256 : kJacobiThreads);
-        SymJobs jobs{};
-        jobs.G[0] = G;
-        jobs.lambda[0] = lambda;
-        jobs.V[0] = V;
-        jobs.n[0] = static_cast<int>(n);
-        jacobi_sym_kernel<<<1, threads, ssmem, s>>>(jobs);
         ++*launches;
         return;
     }
@@ -653,33 +653,46 @@ void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, do
     ++*launches;
 }
 
-bool jacobi_batchable(int64_t n) { return n >= 1 && n <= kSymMaxN; }
+bool jacobi_batchable(int64_t n) { return n >= 1 && n <= kSymMaxN && sym_splits(static_cast<int>(n)) > 0; }
 
 void launch_jacobi_eig_batch(const double* const* G, const int64_t* n, double* const* lambda, double* const* V,
                              int count, cudaStream_t s, int64_t* launches) {
-    for (int b0 = 0; b0 < count; b0 += kEigBatchMax) {
-        const int cnt = std::min(count - b0, kEigBatchMax);
-        SymJobs jobs{};
-        int64_t nmax = 0;
-        for (int i = 0; i < cnt; ++i) {
-            jobs.G[i] = G[b0 + i];
-            jobs.lambda[i] = lambda[b0 + i];
-            jobs.V[i] = V[b0 + i];
-            jobs.n[i] = static_cast<int>(n[b0 + i]);
-            nmax = std::max(nmax, n[b0 + i]);
-        }
-        static bool configured_sym = false;
-        if (!configured_sym) {
-            cudaFuncSetAttribute(jacobi_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(sizeof(double) * (kSymMaxN * (kSymMaxN + 1) / 2 +
-                                                                    kSymMaxN * kSymMaxN)));
-            configured_sym = true;
-        }
-        const size_t ssmem = sizeof(double) * static_cast<size_t>(nmax * (nmax + 1) / 2 + nmax * nmax);
-        const int threads = nmax <= 32 ? 128 : (nmax <= 64 ? 256 : kJacobiThreads);
-        jacobi_sym_kernel<<<cnt, threads, ssmem, s>>>(jobs);
-        ++*launches;
+    static bool configured_sym = false;
+    if (!configured_sym) {
+        cudaFuncSetAttribute(jacobi_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sizeof(double) * kSymSmemDoubles));
+        configured_sym = true;
     }
+    SymJobs jobs{};
+    int blocks = 0;
+    int64_t smem_max = 0, nmax = 0;
+    auto flush = [&] {
+        if (blocks == 0) return;
+        const int threads = nmax <= 32 ? 128 : (nmax <= 64 ? 256 : kJacobiThreads);
+        jacobi_sym_kernel<<<blocks, threads, sizeof(double) * static_cast<size_t>(smem_max), s>>>(jobs);
+        ++*launches;
+        jobs = SymJobs{};
+        blocks = 0;
+        smem_max = nmax = 0;
+    };
+    for (int i = 0; i < count; ++i) {
+        const int ni = static_cast<int>(n[i]);
+        const int k = sym_splits(ni);
+        if (blocks + k > kEigBatchMax) flush();
+        const int rows = (ni + k - 1) / k;
+        for (int j = 0; j < k; ++j) {
+            jobs.G[blocks] = G[i];
+            jobs.lambda[blocks] = j == 0 ? lambda[i] : nullptr;
+            jobs.V[blocks] = V[i];
+            jobs.n[blocks] = ni;
+            jobs.r0[blocks] = std::min(ni, j * rows);
+            jobs.r1[blocks] = std::min(ni, (j + 1) * rows);
+            ++blocks;
+        }
+        smem_max = std::max<int64_t>(smem_max, ni * (ni + 1) / 2 + static_cast<int64_t>(rows) * ni);
+        nmax = std::max<int64_t>(nmax, ni);
+    }
+    flush();
 }
 
 void launch_posdef_test(const double* G, int64_t n, double shift, double* work, double* flag, cudaStream_t s,

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <tuple>
 
 #include "runtime.hpp"
 
@@ -652,6 +653,52 @@ Truncation truncate_cols_side(Context& c, const DT& X, int64_t rows, int64_t col
 
 }  // namespace
 
+namespace {
+/// The old-basis (residual) truncation's set-up on the unfolding Gram G:
+/// G <- (I - U U^T) G (I - U U^T), its noise scale (tr of the unprojected
+/// Gram) and the refiner that re-measures small eigenvalues on the residual.
+std::pair<double, ProjectedGram> residual_setup(Context& c, const DT& t, int mode, const Basis U, bool reduce, DT& G) {
+    const int64_t rows = t.shape[static_cast<size_t>(mode)];
+    // the residual Gram is formed by subtraction: its eigenvalues carry
+    // rounding noise on the scale of the unprojected Gram (its trace)
+    std::vector<double> diag(static_cast<size_t>(rows));
+    HTR_CUDA(cudaMemcpy2DAsync(diag.data(), sizeof(double), G.data(), sizeof(double) * static_cast<size_t>(rows + 1),
+                               sizeof(double), static_cast<size_t>(rows), cudaMemcpyDeviceToHost, c.s));
+    residual_gram(c, G, U);
+    HTR_CUDA(cudaStreamSynchronize(c.s));
+    double gtrace = 0.0;
+    for (double v : diag) gtrace += v;
+    // refinement measures the residual R = (I - U U^T) C directly:
+    // W^T R = ((I - U U^T) W)^T C
+    ProjectedGram refine = [&c, t, mode, U, reduce](const double* W, int64_t q) {
+        DT T = c.tensor({U.r, q});
+        {
+            GemmDesc d;  // T = U^T W
+            d.M = U.r; d.N1 = q; d.K1 = U.alpha;
+            d.A = U.p; d.sam = U.alpha; d.sak1 = 1;
+            d.B = W; d.sbk1 = 1; d.sbn1 = U.alpha;
+            d.C = T.data(); d.scm = 1; d.scn1 = U.r;
+            run_gemm(c, d);
+        }
+        DT Wp = c.tensor({U.alpha, q});
+        HTR_CUDA(cudaMemcpyAsync(Wp.data(), W, sizeof(double) * static_cast<size_t>(U.alpha * q),
+                                 cudaMemcpyDeviceToDevice, c.s));
+        {
+            GemmDesc d;  // Wp -= U T
+            d.M = U.alpha; d.N1 = q; d.K1 = U.r;
+            d.A = U.p; d.sam = 1; d.sak1 = U.alpha;
+            d.B = T.data(); d.sbk1 = 1; d.sbn1 = U.r;
+            d.C = Wp.data(); d.scm = 1; d.scn1 = U.alpha;
+            d.alpha = -1.0; d.beta = 1.0;
+            run_gemm(c, d);
+        }
+        DT B = mode_mul(c, t, mode, Wp.data(), q, U.alpha, 1);
+        return gram(c, B, mode, reduce);
+    };
+    return {gtrace, refine};
+}
+}  // namespace
+
 Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, double eps_abs, int64_t min_rank,
                          int64_t cols_global, bool sharded, bool any_basis_when_full) {
     const int64_t rows = t.shape[static_cast<size_t>(mode)];
@@ -717,49 +764,15 @@ Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, do
         }
     }
     if (!old) return truncate_gram(c, G, rows, cols_global, eps_abs, min_rank, unfolding_refiner(c, t, mode, reduce));
-    // the residual Gram is formed by subtraction: its eigenvalues carry
-    // rounding noise on the scale of the unprojected Gram (its trace)
-    std::vector<double> diag(static_cast<size_t>(rows));
-    HTR_CUDA(cudaMemcpy2DAsync(diag.data(), sizeof(double), G.data(), sizeof(double) * static_cast<size_t>(rows + 1),
-                               sizeof(double), static_cast<size_t>(rows), cudaMemcpyDeviceToHost, c.s));
-    const Basis U = *old;
-    residual_gram(c, G, U);
-    HTR_CUDA(cudaStreamSynchronize(c.s));
     double gtrace = 0.0;
-    for (double v : diag) gtrace += v;
-    // refinement measures the residual R = (I - U U^T) C directly:
-    // W^T R = ((I - U U^T) W)^T C
-    ProjectedGram refine = [&c, t, mode, U, reduce](const double* W, int64_t q) {
-        DT T = c.tensor({U.r, q});
-        {
-            GemmDesc d;  // T = U^T W
-            d.M = U.r; d.N1 = q; d.K1 = U.alpha;
-            d.A = U.p; d.sam = U.alpha; d.sak1 = 1;
-            d.B = W; d.sbk1 = 1; d.sbn1 = U.alpha;
-            d.C = T.data(); d.scm = 1; d.scn1 = U.r;
-            run_gemm(c, d);
-        }
-        DT Wp = c.tensor({U.alpha, q});
-        HTR_CUDA(cudaMemcpyAsync(Wp.data(), W, sizeof(double) * static_cast<size_t>(U.alpha * q),
-                                 cudaMemcpyDeviceToDevice, c.s));
-        {
-            GemmDesc d;  // Wp -= U T
-            d.M = U.alpha; d.N1 = q; d.K1 = U.r;
-            d.A = U.p; d.sam = 1; d.sak1 = U.alpha;
-            d.B = T.data(); d.sbk1 = 1; d.sbn1 = U.r;
-            d.C = Wp.data(); d.scm = 1; d.scn1 = U.alpha;
-            d.alpha = -1.0; d.beta = 1.0;
-            run_gemm(c, d);
-        }
-        DT B = mode_mul(c, t, mode, Wp.data(), q, U.alpha, 1);
-        return gram(c, B, mode, reduce);
-    };
+    ProjectedGram refine;
+    std::tie(gtrace, refine) = residual_setup(c, t, mode, *old, reduce, G);
     return truncate_gram(c, G, rows, cols_global, eps_abs, min_rank, refine, gtrace);
 }
 
 std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vector<int>& modes, double eps_abs,
                                        int64_t min_rank, const std::vector<int64_t>& cols_global, bool sharded,
-                                       bool any_basis_when_full) {
+                                       bool any_basis_when_full, const std::vector<Basis>* olds) {
     // the unprojected truncations (no old basis) that take the plain Gram ->
     // one-CTA eigensolver route are batched: their Grams first, then one
     // launch solving all of them side by side (bit-identical to one by one)
@@ -770,16 +783,21 @@ std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vecto
         const int64_t rows = t.shape[static_cast<size_t>(modes[i])];
         const int64_t cols_local = t.size() / rows;
         const bool column_side = !reduce && rows > kColumnSideRows && cols_local < rows;
-        const bool posdef = any_basis_when_full && rows > 160 && rows <= cols_global[i] && rows <= kJacobiMaxN;
+        const bool posdef =
+            !olds && any_basis_when_full && rows > 160 && rows <= cols_global[i] && rows <= kJacobiMaxN;
         batch[i] = !column_side && !posdef && jacobi_batchable(rows);
         nb += batch[i];
     }
     std::vector<Truncation> out(modes.size());
+    auto old_of = [&](size_t i) { return olds ? &(*olds)[i] : nullptr; };
     if (nb < 2) {
         for (size_t i = 0; i < modes.size(); ++i)
-            out[i] = truncate_mode(c, t, modes[i], nullptr, eps_abs, min_rank, cols_global[i], sharded, any_basis_when_full);
+            out[i] = truncate_mode(c, t, modes[i], old_of(i), eps_abs, min_rank, cols_global[i], sharded,
+                                   any_basis_when_full);
         return out;
     }
+    std::vector<ProjectedGram> refiners;
+    std::vector<double> noise;
     std::vector<DT> grams;
     std::vector<BufPtr> lams, vs;
     std::vector<const double*> gp;
@@ -789,6 +807,16 @@ std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vecto
         if (!batch[i]) continue;
         const int64_t rows = t.shape[static_cast<size_t>(modes[i])];
         grams.push_back(gram(c, t, modes[i], reduce));
+        if (olds) {
+            double gtrace = 0.0;
+            ProjectedGram refine;
+            std::tie(gtrace, refine) = residual_setup(c, t, modes[i], (*olds)[i], reduce, grams.back());
+            refiners.push_back(refine);
+            noise.push_back(gtrace);
+        } else {
+            refiners.push_back(unfolding_refiner(c, t, modes[i], reduce));
+            noise.push_back(0.0);
+        }
         lams.push_back(c.alloc(rows));
         vs.push_back(c.alloc(rows * rows));
         gp.push_back(grams.back().data());
@@ -800,11 +828,11 @@ std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vecto
     HTR_CUDA(cudaGetLastError());
     for (size_t i = 0, j = 0; i < modes.size(); ++i) {
         if (batch[i]) {
-            out[i] = truncate_eig(c, lams[j], vs[j], ns[j], cols_global[i], eps_abs, min_rank,
-                                  unfolding_refiner(c, t, modes[i], reduce), 0.0);
+            out[i] = truncate_eig(c, lams[j], vs[j], ns[j], cols_global[i], eps_abs, min_rank, refiners[j], noise[j]);
             ++j;
         } else {
-            out[i] = truncate_mode(c, t, modes[i], nullptr, eps_abs, min_rank, cols_global[i], sharded, any_basis_when_full);
+            out[i] = truncate_mode(c, t, modes[i], old_of(i), eps_abs, min_rank, cols_global[i], sharded,
+                                   any_basis_when_full);
         }
     }
     return out;
@@ -1508,11 +1536,7 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
     // the root is re-padded lazily: remember pending layer-1 growth
     int64_t pad0 = 0, pad1 = 0;
 
-    auto expand_node = [&](const TreeNode& n, const DT& cur, int mode) {
-        const Basis U = basis_of(*out, n.id);
-        const int64_t cols = static_cast<int64_t>(
-            std::llround(static_cast<double>(cur.size() / cur.shape[static_cast<size_t>(mode)]) * col_scale));
-        Truncation tb = truncate_mode(c, cur, mode, &U, eps_nw, 0, cols);
+    auto expand_node = [&](const TreeNode& n, const Basis& U, const Truncation& tb) {
         if (tb.rank == 0) return;
         // re-orthonormalise the new directions against the old basis and
         // append (expand_core, ht_rise.hpp:53-79)
@@ -1556,8 +1580,26 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
         }
     };
 
+    // every node of a layer truncates its residual against the same working
+    // tensor (ht_rise.hpp:157-162: all nodes expand, then all project), so the
+    // layer's truncations run first (eigensolves batched), then the expansions
+    auto expand_layer = [&](const std::vector<TreeNode>& nodes, const DT& cur, bool leaves) {
+        std::vector<int> modes;
+        std::vector<int64_t> cols;
+        std::vector<Basis> olds;
+        for (size_t j = 0; j < nodes.size(); ++j) {
+            const int mode = leaves ? static_cast<int>(nodes[j].leaf_dim) : static_cast<int>(j);
+            modes.push_back(mode);
+            cols.push_back(static_cast<int64_t>(
+                std::llround(static_cast<double>(cur.size() / cur.shape[static_cast<size_t>(mode)]) * col_scale)));
+            olds.push_back(basis_of(*out, nodes[j].id));
+        }
+        std::vector<Truncation> tbs = truncate_modes(c, cur, modes, eps_nw, 0, cols, true, false, &olds);
+        for (size_t j = 0; j < nodes.size(); ++j) expand_node(nodes[j], olds[j], tbs[j]);
+    };
+
     DT cur = y;
-    for (const TreeNode& n : tree.layer(p)) expand_node(n, cur, static_cast<int>(n.leaf_dim));
+    expand_layer(tree.layer(p), cur, true);
     for (const TreeNode& n : tree.layer(p)) cur = project(c, cur, static_cast<int>(n.leaf_dim), basis_of(*out, n.id), nullptr);
 
     for (Index l = p - 1; l >= 1; --l) {
@@ -1567,7 +1609,7 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
             eps_nw = adaptive_budget(rep.eps_des, std::max(0.0, ysq - cn2), svds_below(tree, l + 1));
         }
         cur.shape = layer_extents(*out, l, ranks, batch, false);
-        for (Index j = 0; j < tree.layer_size(l); ++j) expand_node(tree.layer(l)[static_cast<size_t>(j)], cur, static_cast<int>(j));
+        expand_layer(tree.layer(l), cur, false);
         for (Index j = 0; j < tree.layer_size(l); ++j)
             cur = project(c, cur, static_cast<int>(j), basis_of(*out, tree.layer(l)[static_cast<size_t>(j)].id), nullptr);
     }

@@ -197,7 +197,7 @@ Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, do
 /// the eigensolves of those on the plain Gram route run as one batched launch.
 std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vector<int>& modes, double eps_abs,
                                        int64_t min_rank, const std::vector<int64_t>& cols_global, bool sharded = true,
-                                       bool any_basis_when_full = false);
+                                       bool any_basis_when_full = false, const std::vector<Basis>* olds = nullptr);
 
 // ---- algorithms --------------------------------------------------------------
 struct BuildOut {

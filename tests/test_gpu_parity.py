@@ -787,3 +787,27 @@ def test_streaming_gram_bht_matches_generic_and_oracle(ht, dims, ranks):
     for key in gpu.ranks():
         if key != (0, 0):
             assert sin_angle(gpu.basis_matrix(key), gen.basis_matrix(key)) <= 1e-10
+
+
+@pytest.mark.parametrize("rows", [136, 144, 160, 170, 184])
+def test_truncated_svd_split_v_jacobi(ht, rows):
+    """136..184-row Grams: the packed-symmetric solver with V's rows split over
+    2-4 CTAs (each evolving the same A) agrees with the oracle."""
+    rng = np.random.default_rng(rows)
+    k = 15
+    u = ro.random_orthonormal(rows, k, rng)
+    m = u @ np.diag(np.logspace(0, -3, k)) @ rng.standard_normal((k, 3 * rows))
+    m += 1e-7 * rng.standard_normal(m.shape)
+    for frac in (1e-5, 1e-3, 0.2):
+        eps = frac * np.linalg.norm(m)
+        a = ht.truncated_svd(m, eps)
+        b = ho.truncated_svd(m, eps)
+        assert a.rank == b.rank, frac
+        assert abs(a.discarded_norm - b.discarded_norm) <= 1e-10 * np.linalg.norm(m)
+        assert sin_angle(b.u, a.u) <= 1e-8
+        assert np.max(np.abs(a.u.T @ a.u - np.eye(a.rank))) <= 1e-12
+    full = rng.standard_normal((rows, 2 * rows))  # full rank: every eigenvector
+    a = ht.truncated_svd(full, 1e-3 * np.linalg.norm(full))
+    b = ho.truncated_svd(full, 1e-3 * np.linalg.norm(full))
+    assert a.rank == b.rank == rows
+    assert np.max(np.abs(a.u.T @ a.u - np.eye(rows))) <= 1e-12
