@@ -210,8 +210,10 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJob
     double* __restrict__ Vout = jobs.V[blockIdx.x];
     const int vr0 = jobs.r0[blockIdx.x], nr = jobs.r1[blockIdx.x] - vr0;
     extern __shared__ double smem[];
-    __shared__ double cs[kSymMaxN], sn[kSymMaxN];
-    __shared__ int prs[kSymMaxN], qrs[kSymMaxN];
+    // rotation parameters, double-buffered by round parity: round r + 1's are
+    // computed while round r's V column pairs are being rotated
+    __shared__ double cs2[2][kSymMaxN / 2 + 1], sn2[2][kSymMaxN / 2 + 1];
+    __shared__ int prs2[2][kSymMaxN / 2 + 1], qrs2[2][kSymMaxN / 2 + 1];
     __shared__ int rotated;
     __shared__ double tr_abs;
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -232,20 +234,28 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJob
     const double floor_abs = 0x1p-53 * tr_abs;
     const int m = n + (n & 1), half = m / 2;
     const int vq0 = tid / nr, vrr0 = tid - vq0 * nr, vqs = nt / nr, vrs = nt - vqs * nr;
+    auto rotations = [&](int round, int buf) {
+        for (int i = tid; i < half; i += nt) {
+            int p = tour_pos(i, round, m), q = tour_pos(m - 1 - i, round, m);
+            if (p > q) { const int t = p; p = q; q = t; }
+            double c = 1.0, s = 0.0;
+            if (q < n && jacobi_rotation(A[sym_idx(p, p, n)], A[sym_idx(q, q, n)], A[sym_idx(p, q, n)], floor_abs,
+                                         &c, &s))
+                rotated = 1;
+            cs2[buf][i] = c; sn2[buf][i] = s; prs2[buf][i] = p; qrs2[buf][i] = q;
+        }
+    };
     for (int sweep = 0; sweep < 40; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
+        rotations(0, 0);
+        __syncthreads();
         for (int round = 0; round < m - 1; ++round) {
-            for (int i = tid; i < half; i += nt) {
-                int p = tour_pos(i, round, m), q = tour_pos(m - 1 - i, round, m);
-                if (p > q) { const int t = p; p = q; q = t; }
-                double c = 1.0, s = 0.0;
-                if (q < n && jacobi_rotation(A[sym_idx(p, p, n)], A[sym_idx(q, q, n)], A[sym_idx(p, q, n)], floor_abs,
-                                             &c, &s))
-                    rotated = 1;
-                cs[i] = c; sn[i] = s; prs[i] = p; qrs[i] = q;
-            }
-            __syncthreads();
+            const int buf = round & 1;
+            const double* cs = cs2[buf];
+            const double* sn = sn2[buf];
+            const int* prs = prs2[buf];
+            const int* qrs = qrs2[buf];
             // blocks P <= Q: warp w takes the column pairs Q = qq and
             // Q' = half - 1 - qq together (qq + 1 and Q' + 1 blocks: half + 1
             // per qq) and its lanes stride over the concatenated P ranges
@@ -286,6 +296,8 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_sym_kernel(const SymJob
                 if (okr && okc) A[i11] = sQ * y10 + cQ * y11;
               }
             }
+            __syncthreads();  // A after this round: the next round's rotations
+            if (round + 1 < m - 1) rotations(round + 1, buf ^ 1);
             // V's column pairs: (Q, r) items walked incrementally (no division)
             for (int Q = vq0, r = vrr0; Q < half; Q += vqs, r += vrs) {
                 if (r >= nr) {
