@@ -173,6 +173,69 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partials, int npar
     }
 }
 
+// Gram of a mode with at most 8 rows (c4's 8-extent modes): every (k, b)
+// column x = Y[k, :, b] is read once by one thread, which accumulates the
+// lower triangle of x x^T in registers; warp, CTA and grid sums in a fixed
+// order (partials per CTA, then gram_small_finish_kernel).
+constexpr int kSmallThreads = 256;
+
+template <int M>
+__global__ void __launch_bounds__(kSmallThreads) gram_small_kernel(const double* __restrict__ Y, uint32_t K,
+                                                                   uint32_t units, double* __restrict__ partials) {
+    constexpr int L = M * (M + 1) / 2;
+    double acc[L];
+#pragma unroll
+    for (int e = 0; e < L; ++e) acc[e] = 0.0;
+    for (uint32_t u = blockIdx.x * kSmallThreads + threadIdx.x; u < units; u += gridDim.x * kSmallThreads) {
+        const uint32_t b = u / K, k = u - b * K;
+        const double* col = Y + k + static_cast<uint64_t>(K) * M * b;
+        double x[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) x[m] = __ldg(col + static_cast<uint64_t>(K) * m);
+        int e = 0;
+#pragma unroll
+        for (int j = 0; j < M; ++j)
+#pragma unroll
+            for (int i = j; i < M; ++i, ++e) acc[e] = fma(x[i], x[j], acc[e]);
+    }
+    __shared__ double red[kSmallThreads / 32][L];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int e = 0; e < L; ++e) {
+        double v = acc[e];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[warp][e] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < L; e += kSmallThreads) {
+        double v = 0.0;
+        for (int w = 0; w < kSmallThreads / 32; ++w) v += red[w][e];
+        partials[static_cast<int64_t>(blockIdx.x) * L + e] = v;
+    }
+}
+
+__global__ void gram_small_finish_kernel(const double* __restrict__ partials, int nparts, int M,
+                                         double* __restrict__ G) {
+    // one warp per lower-triangle entry e (enumerated column by column):
+    // fixed lane striding and shuffle tree
+    const int L = M * (M + 1) / 2, e = blockIdx.x;
+    double v = 0.0;
+    for (int p = threadIdx.x; p < nparts; p += 32) v += partials[static_cast<int64_t>(p) * L + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) {
+        int j = 0, rem = e;
+        while (rem >= M - j) {
+            rem -= M - j;
+            ++j;
+        }
+        const int i = j + rem;
+        G[i + M * j] = v;
+        G[j + M * i] = v;
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -206,7 +269,40 @@ int launch_mb(const double* Y, int64_t K, int64_t M, int64_t B, double* partials
     return grid;
 }
 
+template <int M>
+int launch_small_m(const double* Y, int64_t K, int64_t B, double* partials, double* G, int num_sms, cudaStream_t s) {
+    const int64_t units = K * B;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4 * num_sms, (units + kSmallThreads - 1) / kSmallThreads)));
+    gram_small_kernel<M><<<grid, kSmallThreads, 0, s>>>(Y, static_cast<uint32_t>(K), static_cast<uint32_t>(units), partials);
+    gram_small_finish_kernel<<<M * (M + 1) / 2, 32, 0, s>>>(partials, grid, M, G);
+    return grid;
+}
+
 }  // namespace
+
+bool gram_small_supported(int64_t K, int64_t M, int64_t B) {
+    return M >= 1 && M <= 8 && K >= 1 && B >= 1 && K * B < (int64_t{1} << 31) && K * M * B < (int64_t{1} << 40);
+}
+
+int64_t gram_small_partials(int num_sms) { return static_cast<int64_t>(4 * num_sms) * 36; }
+
+int launch_gram_small(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,
+                      cudaStream_t s, int64_t* launches) {
+    if (!gram_small_supported(K, M, B)) return -1;
+    int grid;
+    switch (M) {
+        case 1: grid = launch_small_m<1>(Y, K, B, partials, G, num_sms, s); break;
+        case 2: grid = launch_small_m<2>(Y, K, B, partials, G, num_sms, s); break;
+        case 3: grid = launch_small_m<3>(Y, K, B, partials, G, num_sms, s); break;
+        case 4: grid = launch_small_m<4>(Y, K, B, partials, G, num_sms, s); break;
+        case 5: grid = launch_small_m<5>(Y, K, B, partials, G, num_sms, s); break;
+        case 6: grid = launch_small_m<6>(Y, K, B, partials, G, num_sms, s); break;
+        case 7: grid = launch_small_m<7>(Y, K, B, partials, G, num_sms, s); break;
+        default: grid = launch_small_m<8>(Y, K, B, partials, G, num_sms, s); break;
+    }
+    *launches += 2;
+    return grid;
+}
 
 bool gram_stream_supported(const double* Y, int64_t K, int64_t M, int64_t B) {
     return M >= 1 && M <= 128 && K >= 2 && (K & 1) == 0 && B >= 1 && B < (int64_t{1} << 31) &&

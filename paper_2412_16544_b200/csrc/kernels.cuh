@@ -214,6 +214,11 @@ bool gram_stream_supported(const double* Y, int64_t K, int64_t M, int64_t B);
 int64_t gram_stream_partials(int64_t M, int num_sms);
 int launch_gram_stream(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,
                        cudaStream_t s, int64_t* launches);
+/// The same Gram for M <= 8 rows (any K >= 1, incl. mode 0), one column per thread.
+bool gram_small_supported(int64_t K, int64_t M, int64_t B);
+int64_t gram_small_partials(int num_sms);
+int launch_gram_small(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,
+                      cudaStream_t s, int64_t* launches);
 
 /// Fused two-leaf reconstruction X = (U0 (x) U1) W per slab (k_decode.cu).
 struct Decode2Args {

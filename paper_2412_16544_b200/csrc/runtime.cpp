@@ -295,6 +295,14 @@ void residual_energy(Context& c, const DT& t, int mode, const double* U, int64_t
 DT gram(Context& c, const DT& t, int mode, bool reduce) {
     const Split sp = split_at(t.shape, mode);
     DT G = c.tensor({sp.J, sp.J});
+    if (c.fused && sp.J <= 8 && sp.I * sp.J * sp.O >= (int64_t{1} << 20) && gram_small_supported(sp.I, sp.J, sp.O)) {
+        // few rows (c4's 8-extent modes): one column per thread, registers
+        BufPtr parts = c.alloc(gram_small_partials(c.num_sms));
+        launch_gram_small(t.data(), sp.I, sp.J, sp.O, parts->p, G.data(), c.num_sms, c.s, &c.launches);
+        HTR_CUDA(cudaGetLastError());
+        if (reduce) c.allreduce(G.data(), sp.J * sp.J);
+        return G;
+    }
     if (c.fused && sp.J >= 24 && sp.I * sp.J * sp.O >= (int64_t{1} << 22) &&
         gram_stream_supported(t.data(), sp.I, sp.J, sp.O)) {
         // large unfolding of a mode >= 1 with >= 24 rows: the streaming

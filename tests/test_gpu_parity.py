@@ -811,3 +811,34 @@ def test_truncated_svd_split_v_jacobi(ht, rows):
     b = ho.truncated_svd(full, 1e-3 * np.linalg.norm(full))
     assert a.rank == b.rank == rows
     assert np.max(np.abs(a.u.T @ a.u - np.eye(rows))) <= 1e-12
+
+
+@pytest.mark.parametrize("dims,ranks", [
+    ((8, 8, 8, 8, 8, 8, 8, 8), (3, 4, 2, 4, 3, 4, 4, 2)),  # config 4's extents: every mode on the small-M kernel
+    ((5, 7, 6, 3, 64), (2, 3, 3, 2, 4)),                  # M = 5, 7, 6, 3 (and 64 on the generic engine)
+])
+def test_small_mode_gram_bht_matches_generic_and_oracle(ht, dims, ranks):
+    """Grams of modes with <= 8 rows on the one-column-per-thread kernel:
+    BHT-l2r equals the generic engine and the oracle."""
+    rng = np.random.default_rng(sum(dims) * 3 + sum(ranks))
+    bases = [ro.random_orthonormal(n, r, rng) for n, r in zip(dims, ranks)]
+    if len(dims) < 8:
+        y = ro.tucker_family_batch(bases, 300, rng)
+    else:  # 8-way: a sum of separable terms keeps the generator cheap (8^8 x 4 = 16.8M entries)
+        y = np.zeros(tuple(dims) + (4,))
+        for _ in range(3):
+            vecs = [b @ rng.standard_normal(b.shape[1]) for b in bases] + [rng.standard_normal(4)]
+            y += np.einsum("a,b,c,d,e,f,g,h,s->abcdefghs", *vecs)
+        y = np.asfortranarray(y)
+    y += 1e-6 * rng.standard_normal(y.shape)
+    tree = ht.DimensionTree.balanced(len(dims))
+    gpu, _ = ht.bht_l2r(y, tree, 1e-3)
+    ref, _ = ho.bht_l2r(y, ho.DimensionTree.balanced(len(dims)), 1e-3)
+    compare_reps(ht, gpu, ref)
+    ctx = gpu.ctx
+    ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+    try:
+        gen, _ = ht.bht_l2r(y, tree, 1e-3)
+    finally:
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    assert gpu.ranks() == gen.ranks()
