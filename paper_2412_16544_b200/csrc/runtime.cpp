@@ -129,6 +129,8 @@ Context::Context(int dev) : device(dev) {
     if (dev < 0 || dev >= count) raise(HTR_ERR_NO_DEVICE, "device index out of range");
     st = std::make_shared<Stream>(dev);
     s = st->s;
+    HTR_CUDA(cudaStreamCreateWithFlags(&s_aux, cudaStreamNonBlocking));
+    HTR_CUDA(cudaEventCreateWithFlags(&aux_ev, cudaEventDisableTiming));
     HTR_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     cudaMemPool_t pool;
     HTR_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -150,6 +152,11 @@ Context::Context(int dev) : device(dev) {
 
 Context::~Context() {
     if (s) cudaStreamSynchronize(s);
+    if (s_aux) {
+        cudaStreamSynchronize(s_aux);
+        cudaStreamDestroy(s_aux);
+    }
+    if (aux_ev) cudaEventDestroy(aux_ev);
     if (nccl_comm) nccl().commDestroy(static_cast<ncclComm_t>(nccl_comm));
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
@@ -707,6 +714,55 @@ std::pair<double, ProjectedGram> residual_setup(Context& c, const DT& t, int mod
 }
 }  // namespace
 
+namespace {
+/// Full-rank certificate of a Gram (the shortcut for the Grams that need the
+/// cluster eigensolver, n > 160, tens of ms; a failed test costs ~2 ms):
+/// Cholesky of G - (eps^2 + 1e-12 tr G) I on `st`; margin 1e-12 tr(G) >>
+/// n u ||G||. The trace is read on the context stream first.
+struct PosdefProbe {
+    bool launched = false;
+    BufPtr work, flag;
+};
+PosdefProbe posdef_launch(Context& c, const DT& G, int64_t rows, double eps_abs, cudaStream_t st) {
+    PosdefProbe pr;
+    std::vector<double> diag(static_cast<size_t>(rows));
+    HTR_CUDA(cudaMemcpy2DAsync(diag.data(), sizeof(double), G.data(), sizeof(double) * static_cast<size_t>(rows + 1),
+                               sizeof(double), static_cast<size_t>(rows), cudaMemcpyDeviceToHost, c.s));
+    HTR_CUDA(cudaStreamSynchronize(c.s));
+    double tr = 0.0;
+    for (double v : diag) tr += v;
+    if (!(tr > 0.0 && std::isfinite(tr))) return pr;
+    pr.work = c.alloc(rows * rows);
+    pr.flag = c.alloc(4);
+    HTR_CUDA(cudaMemsetAsync(pr.flag->p, 0, 4 * sizeof(double), c.s));
+    if (st != c.s) {  // the buffers and G are ordered on the context stream
+        HTR_CUDA(cudaEventRecord(c.aux_ev, c.s));
+        HTR_CUDA(cudaStreamWaitEvent(st, c.aux_ev, 0));
+    }
+    launch_posdef_test(G.data(), rows, eps_abs * eps_abs + 1e-12 * tr, pr.work->p, pr.flag->p, st, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+    pr.launched = true;
+    return pr;
+}
+/// Reads the certificate (synchronising `st`); on success *out is the
+/// identity basis of the full space.
+bool posdef_finish(Context& c, PosdefProbe& pr, int64_t rows, cudaStream_t st, Truncation* out) {
+    if (!pr.launched) return false;
+    double f = 0.0;
+    HTR_CUDA(cudaMemcpyAsync(&f, pr.flag->p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    HTR_CUDA(cudaStreamSynchronize(st));
+    if (f != 1.0) return false;
+    out->rank = rows;
+    out->discarded = 0.0;
+    out->u = c.tensor({rows, rows});
+    // take_columns with a zero-input flag (flag[2] == 0) writes identity columns
+    launch_take_columns(nullptr, rows, rows, out->u.data(), pr.flag->p, c.s, &c.launches);
+    out->u.buf->identity = true;
+    HTR_CUDA(cudaGetLastError());
+    return true;
+}
+}  // namespace
+
 Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, double eps_abs, int64_t min_rank,
                          int64_t cols_global, bool sharded, bool any_basis_when_full) {
     const int64_t rows = t.shape[static_cast<size_t>(mode)];
@@ -741,35 +797,9 @@ Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, do
     }
     DT G = gram(c, t, mode, reduce);
     if (!old && any_basis_when_full && rows > 160 && rows <= cols_global && rows <= kJacobiMaxN) {
-        // full-rank shortcut for the Grams that need the cluster eigensolver
-        // (n > 160, tens of ms; a failed test costs ~2 ms): margin
-        // 1e-12 tr(G) >> n u ||G||
-        std::vector<double> diag(static_cast<size_t>(rows));
-        HTR_CUDA(cudaMemcpy2DAsync(diag.data(), sizeof(double), G.data(), sizeof(double) * static_cast<size_t>(rows + 1),
-                                   sizeof(double), static_cast<size_t>(rows), cudaMemcpyDeviceToHost, c.s));
-        HTR_CUDA(cudaStreamSynchronize(c.s));
-        double tr = 0.0;
-        for (double v : diag) tr += v;
-        if (tr > 0.0 && std::isfinite(tr)) {
-            BufPtr work = c.alloc(rows * rows);
-            BufPtr flag = c.alloc(4);
-            HTR_CUDA(cudaMemsetAsync(flag->p, 0, 4 * sizeof(double), c.s));
-            launch_posdef_test(G.data(), rows, eps_abs * eps_abs + 1e-12 * tr, work->p, flag->p, c.s, &c.launches);
-            HTR_CUDA(cudaGetLastError());
-            double f = 0.0;
-            c.fetch(flag->p, 1, &f);
-            if (f == 1.0) {
-                Truncation tr_full;
-                tr_full.rank = rows;
-                tr_full.discarded = 0.0;
-                tr_full.u = c.tensor({rows, rows});
-                // take_columns with a zero-input flag (flag[2] == 0) writes identity columns
-                launch_take_columns(nullptr, rows, rows, tr_full.u.data(), flag->p, c.s, &c.launches);
-                tr_full.u.buf->identity = true;
-                HTR_CUDA(cudaGetLastError());
-                return tr_full;
-            }
-        }
+        PosdefProbe probe = posdef_launch(c, G, rows, eps_abs, c.s);
+        Truncation full;
+        if (posdef_finish(c, probe, rows, c.s, &full)) return full;
     }
     if (!old) return truncate_gram(c, G, rows, cols_global, eps_abs, min_rank, unfolding_refiner(c, t, mode, reduce));
     double gtrace = 0.0;
@@ -785,8 +815,8 @@ std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vecto
     // one-CTA eigensolver route are batched: their Grams first, then one
     // launch solving all of them side by side (bit-identical to one by one)
     const bool reduce = sharded && c.nccl_comm;
-    std::vector<char> batch(modes.size(), 0);
-    int nb = 0;
+    std::vector<char> batch(modes.size(), 0), pdef(modes.size(), 0);
+    int nb = 0, npd = 0;
     for (size_t i = 0; i < modes.size(); ++i) {
         const int64_t rows = t.shape[static_cast<size_t>(modes[i])];
         const int64_t cols_local = t.size() / rows;
@@ -794,15 +824,27 @@ std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vecto
         const bool posdef =
             !olds && any_basis_when_full && rows > 160 && rows <= cols_global[i] && rows <= kJacobiMaxN;
         batch[i] = !column_side && !posdef && jacobi_batchable(rows);
+        pdef[i] = !column_side && posdef;
         nb += batch[i];
+        npd += pdef[i];
     }
     std::vector<Truncation> out(modes.size());
     auto old_of = [&](size_t i) { return olds ? &(*olds)[i] : nullptr; };
-    if (nb < 2) {
+    if (nb < 2 && !(nb == 1 && npd > 0)) {
         for (size_t i = 0; i < modes.size(); ++i)
             out[i] = truncate_mode(c, t, modes[i], old_of(i), eps_abs, min_rank, cols_global[i], sharded,
                                    any_basis_when_full);
         return out;
+    }
+    // full-rank certificates run on the auxiliary stream, beside the batched
+    // eigensolve on the context stream (c5's layer 1: the 400-row transfer
+    // Gram's Cholesky next to the 128-row leaf solve)
+    std::vector<DT> pgrams(modes.size());
+    std::vector<PosdefProbe> probes(modes.size());
+    for (size_t i = 0; i < modes.size(); ++i) {
+        if (!pdef[i]) continue;
+        pgrams[i] = gram(c, t, modes[i], reduce);
+        probes[i] = posdef_launch(c, pgrams[i], t.shape[static_cast<size_t>(modes[i])], eps_abs, c.s_aux);
     }
     std::vector<ProjectedGram> refiners;
     std::vector<double> noise;
@@ -838,6 +880,11 @@ std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vecto
         if (batch[i]) {
             out[i] = truncate_eig(c, lams[j], vs[j], ns[j], cols_global[i], eps_abs, min_rank, refiners[j], noise[j]);
             ++j;
+        } else if (pdef[i]) {
+            const int64_t rows = t.shape[static_cast<size_t>(modes[i])];
+            if (!posdef_finish(c, probes[i], rows, c.s_aux, &out[i]))
+                out[i] = truncate_gram(c, pgrams[i], rows, cols_global[i], eps_abs, min_rank,
+                                       unfolding_refiner(c, t, modes[i], reduce));
         } else {
             out[i] = truncate_mode(c, t, modes[i], old_of(i), eps_abs, min_rank, cols_global[i], sharded,
                                    any_basis_when_full);

@@ -96,6 +96,8 @@ struct Context {
     int device = 0;
     StreamPtr st;
     cudaStream_t s = nullptr;
+    cudaStream_t s_aux = nullptr;  // side work beside s (full-rank certificates)
+    cudaEvent_t aux_ev = nullptr;
     int num_sms = kNumSMs;
     std::string err;
     int64_t launches = 0;
