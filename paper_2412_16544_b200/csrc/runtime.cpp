@@ -361,7 +361,6 @@ Truncation truncate_eig(Context& c, const BufPtr& lam, const BufPtr& V, int64_t 
 Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
                          const ProjectedGram& refine, double noise_scale) {
     const int64_t n = rows;
-    const int64_t k = std::min(rows, cols);
     if (n > kJacobiMaxN)
         raise(HTR_ERR_RUNTIME, "truncation of a " + std::to_string(n) + "-row unfolding exceeds the device eigensolver's " +
                                    std::to_string(kJacobiMaxN) + "-row limit");
