@@ -155,8 +155,11 @@ struct HTRepresentation {
         int32_t d = 0;
         int64_t acc = 0, nn = 0;
         double eps = 0.0;
-        int64_t dims[64];
-        device::check(htr_rep_info(h.get(), &d, dims, &acc, &eps, &nn));
+        device::check(htr_rep_info(h.get(), &d, nullptr, nullptr, nullptr, nullptr));
+        std::vector<int64_t> dims(static_cast<std::size_t>(std::max<int32_t>(d, 0)));
+        device::check(htr_rep_info(h.get(), &d, dims.data(), nullptr, &eps, &nn));
+        // the root held here is this rank's shard (the whole stream unsharded)
+        device::check(htr_rep_counts(h.get(), &acc, nullptr));
         std::vector<htr_node> nodes(static_cast<std::size_t>(nn));
         device::check(htr_rep_nodes(h.get(), nodes.data(), nn));
         std::vector<std::vector<TreeNode>> layers;
@@ -170,7 +173,7 @@ struct HTRepresentation {
             layers[static_cast<std::size_t>(x.layer)].push_back(t);
         }
         rep.tree = DimensionTree::from_layers(std::move(layers));
-        rep.dims = Shape(dims, dims + d);
+        rep.dims = Shape(dims.begin(), dims.end());
         rep.accumulated = acc;
         rep.epsilon_rel = eps;
         rep.cores.resize(static_cast<std::size_t>(rep.tree.depth()) + 1);

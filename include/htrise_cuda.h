@@ -127,6 +127,18 @@ HTR_API htr_status htr_comm_get_unique_id(uint8_t out[128]);
 HTR_API htr_status htr_context_init_comm(htr_context* ctx, const uint8_t unique_id[128], int32_t nranks,
                                  int32_t rank);
 
+/* Host-staged alternative to NCCL: `fn` sums n doubles in place over all
+ * ranks (element-wise, the same bits on every rank) and returns 0. The
+ * library drains its stream, hands the partial sums to `fn` in pinned host
+ * memory and copies the result back, so ranks never wait on one another's
+ * kernels. For transports without NCCL peers (several ranks' processes on one
+ * device in tests, a CPU transport such as gloo); the runtime path above the
+ * reduction is the same as with NCCL. Every rank installs a reducer with the
+ * same nranks. */
+typedef int32_t (*htr_host_reduce_fn)(double* buf, int64_t n, void* user);
+HTR_API htr_status htr_context_set_reducer(htr_context* ctx, htr_host_reduce_fn fn, void* user, int32_t nranks,
+                                           int32_t rank);
+
 /* ---- trees (dimension_tree.hpp) ------------------------------------- */
 /* DimensionTree::balanced(d) (dimension_tree.hpp:44-94); writes 2d-1 nodes. */
 HTR_API htr_status htr_tree_balanced(int64_t d, htr_node* out_nodes, int64_t capacity, int64_t* n_nodes,
@@ -185,6 +197,10 @@ HTR_API htr_status htr_rep_free(htr_rep* rep);
 HTR_API htr_status htr_rep_clone(htr_context* ctx, const htr_rep* rep, htr_rep** out);
 HTR_API htr_status htr_rep_info(const htr_rep* rep, int32_t* d, int64_t* dims, int64_t* accumulated,
                         double* epsilon_rel, int64_t* n_nodes);
+/* Samples held by this value: `local` slices in this rank's root shard and
+ * `global` streamed over all ranks (equal on an unsharded context;
+ * htr_rep_info's `accumulated` is the global count). */
+HTR_API htr_status htr_rep_counts(const htr_rep* rep, int64_t* local, int64_t* global);
 HTR_API htr_status htr_rep_nodes(const htr_rep* rep, htr_node* nodes, int64_t capacity);
 /* Core shape (2 entries for leaves, 3 otherwise; the root's last extent is
  * the LOCAL sample count on a sharded context). */

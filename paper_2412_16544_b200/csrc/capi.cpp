@@ -19,6 +19,7 @@ struct htr_rep {
 namespace htr {
 void comm_unique_id(uint8_t out[128]);
 void comm_init(Context& c, const uint8_t uid[128], int nranks, int rank);
+void set_reducer(Context& c, htr_host_reduce_fn fn, void* user, int nranks, int rank);
 }  // namespace htr
 
 namespace {
@@ -76,6 +77,10 @@ htr_status guarded_noctx(char* err, int64_t len, F&& f) {
 
 htr::Context& C(htr_context* c) {
     if (!c || !c->ctx) htr::raise(HTR_ERR_INVALID_ARGUMENT, "null context");
+    // every entry point runs on the context's device, whatever device the
+    // caller (torch, another library) made current
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != c->ctx->device) HTR_CUDA(cudaSetDevice(c->ctx->device));
     return *c->ctx;
 }
 
@@ -196,6 +201,10 @@ htr_status htr_comm_get_unique_id(uint8_t out[128]) {
 
 htr_status htr_context_init_comm(htr_context* ctx, const uint8_t unique_id[128], int32_t nranks, int32_t rank) {
     return guarded(ctx, [&] { htr::comm_init(C(ctx), unique_id, nranks, rank); });
+}
+
+htr_status htr_context_set_reducer(htr_context* ctx, htr_host_reduce_fn fn, void* user, int32_t nranks, int32_t rank) {
+    return guarded(ctx, [&] { htr::set_reducer(C(ctx), fn, user, nranks, rank); });
 }
 
 htr_status htr_tree_balanced(int64_t d, htr_node* out_nodes, int64_t capacity, int64_t* n_nodes, char* err,
@@ -362,6 +371,14 @@ htr_status htr_rep_info(const htr_rep* rep, int32_t* d, int64_t* dims, int64_t* 
         if (accumulated) *accumulated = h.acc_global;
         if (epsilon_rel) *epsilon_rel = h.eps_rel;
         if (n_nodes) *n_nodes = 2 * h.tree.dims() - 1;
+    });
+}
+
+htr_status htr_rep_counts(const htr_rep* rep, int64_t* local, int64_t* global) {
+    return guarded(nullptr, [&] {
+        const htr::Rep& h = R(rep);
+        if (local) *local = h.acc;
+        if (global) *global = h.acc_global;
     });
 }
 

@@ -226,12 +226,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
 template <int N0T, int MT0, bool RESID>
 int launch_t(const Decode2Args& a, int num_sms, cudaStream_t s) {
     constexpr size_t smem = sizeof(double) * decode2_smem_doubles<N0T, MT0>();
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(decode2_kernel<N0T, MT0, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        configured = true;
-    }
+    ensure_smem_limit(reinterpret_cast<const void*>(decode2_kernel<N0T, MT0, RESID>), smem);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, (a.T + kDecWarps - 1) / kDecWarps)));
     decode2_kernel<N0T, MT0, RESID><<<grid, kDecWarps * 32, smem, s>>>(a.W, a.T, a.r0, a.r1, static_cast<int>(a.n1),
                                                                         a.U0, a.U1, a.X, a.Y, a.partials);

@@ -653,13 +653,8 @@ void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, do
     // static + dynamic shared memory above 48 KB needs the opt-in (the
     // kernel's static arrays take ~17 KB): raise the limit once to the
     // largest in-smem problem
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sizeof(double) * std::max(2 * kSmemMaxN * kSmemMaxN,
-                                                                        kSmemMaxNA * kSmemMaxNA)));
-        configured = true;
-    }
+    ensure_smem_limit(reinterpret_cast<const void*>(jacobi_kernel),
+                      sizeof(double) * std::max(2 * kSmemMaxN * kSmemMaxN, kSmemMaxNA * kSmemMaxNA));
     const int threads = n <= 32 ? 128 : (n <= 64 ? 256 : kJacobiThreads);
     jacobi_kernel<<<1, threads, smem, s>>>(G, static_cast<int>(n), lambda, V, work, 1, v_smem ? 1 : 0);
     ++*launches;
@@ -669,12 +664,7 @@ bool jacobi_batchable(int64_t n) { return n >= 1 && n <= kSymMaxN && sym_splits(
 
 void launch_jacobi_eig_batch(const double* const* G, const int64_t* n, double* const* lambda, double* const* V,
                              int count, cudaStream_t s, int64_t* launches) {
-    static bool configured_sym = false;
-    if (!configured_sym) {
-        cudaFuncSetAttribute(jacobi_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sizeof(double) * kSymSmemDoubles));
-        configured_sym = true;
-    }
+    ensure_smem_limit(reinterpret_cast<const void*>(jacobi_sym_kernel), sizeof(double) * kSymSmemDoubles);
     SymJobs jobs{};
     int blocks = 0;
     int64_t smem_max = 0, nmax = 0;

@@ -387,11 +387,7 @@ int launch_impl(const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launc
     if (!make_batch_map(&map, a.Y, N0, N1, T)) return -1;
     const size_t smem = smem_bytes<N0, N1, MT0, MT1>();
     auto kfn = fused3_kernel<N0, N1, MT0, MT1>;
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = true;
-    }
+    ensure_smem_limit(reinterpret_cast<const void*>(kfn), smem);
     kfn<<<static_cast<unsigned>(B), kThreads, smem, s>>>(args, ri, map);
     ++*launches;
     if (!a.slab_gemm) return static_cast<int>(B);

@@ -647,12 +647,7 @@ template <int BM, int BN, bool AK, bool BKF>
 void launch_fast_t(const GemmDesc& d, const FastArgs& f, const Launch& L, dim3 grid, cudaStream_t s) {
     constexpr size_t smem = fast_smem_bytes<BM, BN, AK, BKF>();
     static_assert(sizeof(double) * BM * (BN + 2) <= smem, "C staging tile must fit the operand stages");
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(gemm_fast_kernel<BM, BN, AK, BKF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        configured = true;
-    }
+    ensure_smem_limit(reinterpret_cast<const void*>(gemm_fast_kernel<BM, BN, AK, BKF>), smem);
     gemm_fast_kernel<BM, BN, AK, BKF><<<grid, (BM / 32) * (BN / 32) * 32, smem, s>>>(d, f, L);
 }
 
@@ -689,12 +684,7 @@ int launch_expand(const double* t, int64_t I, int64_t J, int64_t O, const double
                   int64_t smj, double* out, int num_sms, cudaStream_t s, int64_t* launches) {
     // 16-byte rows: I even, aligned bases; J, Q within the resident tile
     if (J > XJ || Q > XQ || Q < 1 || J < 1 || (I & 1) || !aligned16(t) || !aligned16(out)) return -1;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(expand_smem_bytes()));
-        configured = true;
-    }
+    ensure_smem_limit(reinterpret_cast<const void*>(expand_kernel), expand_smem_bytes());
     const int64_t items = (I + XN - 1) / XN * O;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(items, 2 * num_sms)));
     expand_kernel<<<grid, XT, expand_smem_bytes(), s>>>(t, I, static_cast<int>(J), O, M, static_cast<int>(Q), smq, smj,
@@ -709,16 +699,9 @@ int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t 
     if (d.M <= 0 || N <= 0 || d.batch <= 0) return 0;
     if (K <= 0) return 0;  // extents are >= 1 by construction
     const Plan p = plan_for(d, num_sms);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(gemm_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(gemm_smem_bytes<64, 64>()));
-        cudaFuncSetAttribute(gemm_kernel<64, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(gemm_smem_bytes<64, 32>()));
-        cudaFuncSetAttribute(gemm_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(gemm_smem_bytes<32, 64>()));
-        configured = true;
-    }
+    ensure_smem_limit(reinterpret_cast<const void*>(gemm_kernel<64, 64>), gemm_smem_bytes<64, 64>());
+    ensure_smem_limit(reinterpret_cast<const void*>(gemm_kernel<64, 32>), gemm_smem_bytes<64, 32>());
+    ensure_smem_limit(reinterpret_cast<const void*>(gemm_kernel<32, 64>), gemm_smem_bytes<32, 64>());
     const bool a_kc = d.K1 > 1 ? d.sak1 == 1 : d.sak2 == 1;
     const bool b_kc = d.K1 > 1 ? d.sbk1 == 1 : d.sbk2 == 1;
     const bool b_nc = d.N1 > 1 ? d.sbn1 == 1 : d.sbn2 == 1;

@@ -258,11 +258,7 @@ int launch_mb(const double* Y, int64_t K, int64_t M, int64_t B, double* partials
               cudaStream_t s) {
     const int64_t kchunks = (K + kGChunk - 1) / kGChunk;
     const size_t smem = gram_smem_bytes<MB>();
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(gram_stream_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = true;
-    }
+    ensure_smem_limit(reinterpret_cast<const void*>(gram_stream_kernel<MB>), smem);
     gram_stream_kernel<MB><<<grid, (consumer_warps<MB>() + 1) * 32, smem, s>>>(B * kchunks, kchunks, static_cast<int>(M),
                                                                                partials, map);
     (void)Y;

@@ -322,12 +322,7 @@ int launch_quad(const QuadArgs& a, bool finish, int num_sms, cudaStream_t s, int
     const size_t smem = sizeof(double) * kQ2Warps * (kQ2Stages * kQ2Chunk + kQ2Scratch);
     auto kfn = split ? quad_stream_kernel<true, true>
                      : (finish ? quad_stream_kernel<true, false> : quad_stream_kernel<false, false>);
-    static bool configured[3] = {false, false, false};
-    const int slot = split ? 2 : (finish ? 1 : 0);
-    if (!configured[slot]) {
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured[slot] = true;
-    }
+    ensure_smem_limit(reinterpret_cast<const void*>(kfn), smem);
     kfn<<<grid, kQ2Threads, smem, s>>>(a);
     ++*launches;
     return grid;

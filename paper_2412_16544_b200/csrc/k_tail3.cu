@@ -576,12 +576,7 @@ size_t tail3_pair_smem(int64_t n2, int r0, int r1, int r2) {
 
 template <int NT, int NTB>
 void launch_pair_t(const Tail3Args& a, size_t smem, cudaStream_t s) {
-    static size_t configured = 0;
-    if (smem > 46 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(tail3_pair_kernel<NT, NTB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        configured = smem;
-    }
+    if (smem > 46 * 1024) ensure_smem_limit(reinterpret_cast<const void*>(tail3_pair_kernel<NT, NTB>), smem);
     tail3_pair_kernel<NT, NTB><<<static_cast<unsigned>((a.S + 1) / 2), kPairThreads, smem, s>>>(a);
 }
 
@@ -604,13 +599,11 @@ size_t tail3_smem(int64_t n2, int r0, int r1, int r2) {
 
 template <int NT, int MT>
 void launch_t(const Tail3Args& a, size_t smem, cudaStream_t s) {
-    static size_t configured[2] = {0, 0};
     const int cl = a.csize > 1 ? 1 : 0;
-    if (smem > 46 * 1024 && smem > configured[cl]) {  // margin for the static arrays
-        cudaFuncSetAttribute(cl ? tail3_kernel<NT, MT, true> : tail3_kernel<NT, MT, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured[cl] = smem;
-    }
+    if (smem > 46 * 1024)  // margin for the static arrays
+        ensure_smem_limit(cl ? reinterpret_cast<const void*>(tail3_kernel<NT, MT, true>)
+                             : reinterpret_cast<const void*>(tail3_kernel<NT, MT, false>),
+                          smem);
     // programmatic dependent launch after the fused leaf kernel (see
     // griddepcontrol.wait in the kernel)
     cudaLaunchConfig_t cfg = {};

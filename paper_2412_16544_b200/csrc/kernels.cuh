@@ -9,9 +9,31 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <set>
+#include <tuple>
+
 namespace htr {
 
 constexpr int kNumSMs = 148;  // B200; the launchers query the device anyway
+
+/// Raise a kernel's dynamic shared-memory limit to `bytes` on the current
+/// device. The attribute is per (function, device): remembered per pair
+/// (and per size, the largest applied so far) under a lock, so contexts on
+/// several devices and concurrent callers each configure what they launch.
+inline cudaError_t ensure_smem_limit(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, size_t>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    const auto key = std::make_tuple(fn, dev, bytes);
+    if (done.count(key)) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (e == cudaSuccess) done.insert(key);
+    return e;
+}
 
 // ---------------------------------------------------------------------------
 // Generic strided contraction ("mode product engine").

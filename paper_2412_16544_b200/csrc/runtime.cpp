@@ -107,11 +107,21 @@ void comm_unique_id(uint8_t out[128]) {
     std::memcpy(out, &id, 128);
 }
 
+void set_reducer(Context& c, htr_host_reduce_fn fn, void* user, int nranks, int rank) {
+    if (!fn) raise(HTR_ERR_INVALID_ARGUMENT, "set_reducer: null reduce function");
+    if (nranks < 1 || rank < 0 || rank >= nranks) raise(HTR_ERR_INVALID_ARGUMENT, "bad nranks/rank for set_reducer");
+    if (c.sharded()) raise(HTR_ERR_INVALID_ARGUMENT, "context already has a communicator");
+    c.reducer = fn;
+    c.reducer_user = user;
+    c.nranks = nranks;
+    c.rank = rank;
+}
+
 void comm_init(Context& c, const uint8_t uid[128], int nranks, int rank) {
     // An explicit call always builds a communicator, a single-rank one
     // included: every reduction then goes through NCCL exactly as at N > 1.
     if (nranks < 1 || rank < 0 || rank >= nranks) raise(HTR_ERR_INVALID_ARGUMENT, "bad nranks/rank for init_comm");
-    if (c.nccl_comm) raise(HTR_ERR_INVALID_ARGUMENT, "context already has a communicator");
+    if (c.sharded()) raise(HTR_ERR_INVALID_ARGUMENT, "context already has a communicator");
     ncclUniqueId id;
     std::memcpy(&id, uid, 128);
     ncclComm_t comm;
@@ -163,13 +173,32 @@ Context::~Context() {
     for (auto& se : slot_ev)
         for (auto& e : se)
             if (e) cudaEventDestroy(e);
+    if (h_red) cudaFreeHost(h_red);
     if (h_sc) cudaFreeHost(h_sc);
     if (h_map) cudaFreeHost(h_map);
     if (d_ticket) cudaFree(d_ticket);
 }
 
 void Context::allreduce(double* d, int64_t n) {
-    if (!nccl_comm || n == 0) return;
+    if (n == 0) return;
+    if (reducer) {
+        // host-staged: the partial sums reach the caller's transport through
+        // pinned memory; the stream is drained first, so no kernel of this
+        // rank waits on another rank's device work
+        if (n > h_red_cap) {
+            if (h_red) HTR_CUDA(cudaFreeHost(h_red));
+            h_red = nullptr;
+            HTR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_red), static_cast<size_t>(n) * sizeof(double)));
+            h_red_cap = n;
+        }
+        HTR_CUDA(cudaMemcpyAsync(h_red, d, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        HTR_CUDA(cudaStreamSynchronize(s));
+        if (reducer(h_red, n, reducer_user) != 0) raise(HTR_ERR_RUNTIME, "host reducer failed");
+        HTR_CUDA(cudaMemcpyAsync(d, h_red, static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice, s));
+        // (the next allreduce drains the stream before reusing h_red)
+        return;
+    }
+    if (!nccl_comm) return;
     nccl_check(nccl().allReduce(d, d, static_cast<size_t>(n), ncclDouble, ncclSum,
                                 static_cast<ncclComm_t>(nccl_comm), s),
                "ncclAllReduce");
@@ -766,7 +795,7 @@ Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, do
                          int64_t cols_global, bool sharded, bool any_basis_when_full) {
     const int64_t rows = t.shape[static_cast<size_t>(mode)];
     const int64_t cols_local = t.size() / rows;
-    const bool reduce = sharded && c.nccl_comm;
+    const bool reduce = sharded && c.sharded();
     if (!reduce && rows > kColumnSideRows && cols_local < rows) {
         // tall unfolding on one rank: decompose the smaller, column-side Gram
         int64_t inner = 1, outer = 1;
@@ -813,7 +842,7 @@ std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vecto
     // the unprojected truncations (no old basis) that take the plain Gram ->
     // one-CTA eigensolver route are batched: their Grams first, then one
     // launch solving all of them side by side (bit-identical to one by one)
-    const bool reduce = sharded && c.nccl_comm;
+    const bool reduce = sharded && c.sharded();
     std::vector<char> batch(modes.size(), 0), pdef(modes.size(), 0);
     int nb = 0, npd = 0;
     for (size_t i = 0; i < modes.size(); ++i) {
@@ -939,7 +968,7 @@ DT project(Context& c, const DT& t, int mode, const Basis& b, double* energy_slo
 }
 
 int64_t global_batch(Context& c, int64_t local) {
-    if (!c.nccl_comm) return local;
+    if (!c.sharded()) return local;
     c.h_sc[0] = static_cast<double>(local);
     HTR_CUDA(cudaMemcpyAsync(c.d_sc->p + 8, c.h_sc, sizeof(double), cudaMemcpyHostToDevice, c.s));
     c.allreduce(c.d_sc->p + 8, 1);
@@ -1241,6 +1270,15 @@ bool launch_skip_encode_fused(Context& c, const Rep& h, const DT& y, const DT* l
            launch_skip_encode8(c, h, y, latent_target, sc, latent, ev0, ev1, host_out);
 }
 
+double residual_sq_global(Context& c, const Rep& h, const DT& latent, const DT& y) {
+    BufPtr r = c.alloc(1);
+    decode_residual_sq(c, h, latent, y, r->p);
+    c.allreduce(r->p, 1);
+    double v = 0.0;
+    c.fetch(r->p, 1, &v);
+    return v;
+}
+
 EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* latent_target, double* sc_deferred) {
     const DimensionTree& tree = h.tree;
     const Index d = tree.dims(), p = tree.depth();
@@ -1254,7 +1292,7 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
     // (the context's events and mapped block are not per call: a deferred
     // encode uses neither)
     const bool prof = c.profile && !sc_deferred;
-    double* host_out = (c.nccl_comm || sc_deferred) ? nullptr : c.d_map;
+    double* host_out = (c.sharded() || sc_deferred) ? nullptr : c.d_map;
     // the generic kernels accumulate into the scalar slots; the fused
     // leaf+tail path assigns sc[0] and sc[2] and needs no clearing
     bool zeroed = false;
@@ -1263,6 +1301,10 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
         zeroed = true;
     };
 
+    // sharded: every rank all-reduces the same 16 + nslots slots, whichever
+    // kernels its shard took, so none may hold stale values (the fused
+    // kernels assign only sc[0] and sc[2])
+    if (c.sharded()) zero_scalars();
     DT cur = y;
     bool leaves_done = false;
     bool tail_done = false;  // latent and ||latent||^2 already produced
@@ -1431,21 +1473,22 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
         out.scan_valid = ysq_scanned;
         return out;
     }
-    if (c.nccl_comm) {
+    if (c.sharded()) {
         // the global batch count rides on the same all-reduce (slot 8)
         c.h_sc[8] = static_cast<double>(batch);
         HTR_CUDA(cudaMemcpyAsync(sc + 8, c.h_sc + 8, sizeof(double), cudaMemcpyHostToDevice, c.s));
     }
-    if (tail_done && !c.nccl_comm) {
+    if (tail_done && !c.sharded()) {
         // the fused tail wrote both norms to mapped host memory
         HTR_CUDA(cudaStreamSynchronize(c.s));
         c.h_sc[0] = c.h_map[0];
+        c.h_sc[1] = 0.0;  // no full scan ran
         c.h_sc[2] = c.h_map[2];
     } else {
         c.allreduce(sc, 16 + nslots);
         c.fetch(sc, 16 + nslots, c.h_sc);
     }
-    out.gbatch = c.nccl_comm ? static_cast<int64_t>(std::llround(c.h_sc[8])) : batch;
+    out.gbatch = c.sharded() ? static_cast<int64_t>(std::llround(c.h_sc[8])) : batch;
     if (prof && leaves_done) {
         float ms = 0.f;
         HTR_CUDA(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
@@ -1453,7 +1496,10 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
         ++c.fused_calls;
     }
     out.ysq = c.h_sc[0];
-    out.nonfinite = ysq_scanned ? c.h_sc[1] != 0.0 : !std::isfinite(out.ysq);
+    // sc[1]: (all-reduced) count of full scans that met a non-finite element;
+    // zero where no scan ran. Both it and ||y||^2 are global, so the rescan
+    // below (a collective) runs on every rank or on none.
+    out.nonfinite = c.h_sc[1] != 0.0;
     const double latsq = c.h_sc[2];
     if (exact) {
         double loss = 0.0;
@@ -1462,8 +1508,18 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
     } else {
         out.proj_sq = std::max(0.0, out.ysq - latsq);
     }
-    if (out.nonfinite && !ysq_scanned) {
-        // a fused pass saw inf/nan in ||y||^2: distinguish overflow from
+    if (!exact && !out.nonfinite && std::isfinite(out.ysq) && out.proj_sq < kTelescopeFloor * out.ysq) {
+        // the telescoped loss is accurate to ~1e-15 ||y||^2 absolute: below
+        // the floor its square root would drift from the reference's
+        // explicit-residual value (bht.hpp:357-365) by more than 1e-10 ||y||,
+        // so the loss is re-measured as ||y - decode(latent)||^2 (the same
+        // quantity: the step residuals of nested orthogonal projections add
+        // up to it), one more read of y
+        out.proj_sq = residual_sq_global(c, h, out.latent, y);
+        out.exact = true;
+    }
+    if (!out.nonfinite && !std::isfinite(out.ysq)) {
+        // inf/nan in ||y||^2 without a scan's flag: distinguish overflow from
         // non-finite input with the explicit scan
         double s = 0.0;
         bool bad = false;
@@ -1768,11 +1824,14 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         const int64_t l0 = c.launches;
         sl.started = std::chrono::steady_clock::now();
         sl.dsc = c.alloc(16);  // [0] ||y||^2, [1] non-finite flag, [2] ||latent||^2, [8] batch count
+        // sharded: all ranks reduce the block whichever path their shard
+        // took, so it starts zeroed (the fused kernels assign [0] and [2] only)
+        if (c.sharded()) HTR_CUDA(cudaMemsetAsync(sl.dsc->p, 0, 16 * sizeof(double), c.s));
         mark();
         double* mapped_dev = c.d_map + (sl.mapped - c.h_map);
         sl.fused = c.fused && launch_skip_encode_fused(c, h, sl.y, target, sl.dsc->p, &sl.latent,
                                                        c.profile ? sl.t0 : nullptr, c.profile ? sl.t1 : nullptr,
-                                                       c.nccl_comm ? nullptr : mapped_dev);
+                                                       c.sharded() ? nullptr : mapped_dev);
         sl.used_fused = sl.fused;
         sl.scan_valid = false;
         if (!sl.fused) {
@@ -1783,13 +1842,13 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
             sl.used_fused = e.fused;
             sl.scan_valid = e.scan_valid;
         }
-        if (c.nccl_comm) {
+        if (c.sharded()) {
             // the global batch count rides on the skip test's all-reduce
             sl.host[8] = static_cast<double>(nb);
             HTR_CUDA(cudaMemcpyAsync(sl.dsc->p + 8, sl.host + 8, sizeof(double), cudaMemcpyHostToDevice, c.s));
             c.allreduce(sl.dsc->p, 9);
         }
-        if (c.nccl_comm || !sl.fused)
+        if (c.sharded() || !sl.fused)
             HTR_CUDA(cudaMemcpyAsync(sl.host, sl.dsc->p, 9 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
         HTR_CUDA(cudaEventRecord(sl.done, c.s));
         mark();
@@ -1804,10 +1863,12 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
     auto decide = [&](Slot& sl, const Rep& h) -> std::shared_ptr<Rep> {
         HTR_CUDA(cudaEventSynchronize(sl.done));
         const int64_t nb = sl.y.shape[static_cast<size_t>(d)];
-        const double* v = (c.nccl_comm || !sl.fused) ? sl.host : sl.mapped;
+        const double* v = (c.sharded() || !sl.fused) ? sl.host : sl.mapped;
         const double ysq = v[0], latsq = v[2];
-        const int64_t gbatch = c.nccl_comm ? static_cast<int64_t>(std::llround(v[8])) : nb;
-        if (sl.scan_valid && v[1] != 0.0) return nullptr;  // non-finite input: the per-call path raises
+        const int64_t gbatch = c.sharded() ? static_cast<int64_t>(std::llround(v[8])) : nb;
+        // non-finite input (the per-call path raises); sharded, the flag is
+        // the all-reduced count, identical on every rank
+        if ((c.sharded() || sl.scan_valid) && v[1] != 0.0) return nullptr;
         if (c.profile && sl.fused) {
             float ms = 0.f;
             HTR_CUDA(cudaEventElapsedTime(&ms, sl.t0, sl.t1));
@@ -1817,7 +1878,12 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         if (!std::isfinite(ysq)) return nullptr;
         const double eps_rel = effective_eps_rel(eps_override >= 0 ? eps_override : h.eps_rel);
         const double eps_des = eps_rel * std::sqrt(ysq);
-        const double proj_sq = std::max(0.0, ysq - latsq);
+        double proj_sq = std::max(0.0, ysq - latsq);
+        bool refined = false;
+        if (proj_sq < kTelescopeFloor * ysq) {  // as in encode(): re-measure explicitly
+            proj_sq = residual_sq_global(c, h, sl.latent, sl.y);
+            refined = true;
+        }
         if (std::abs(proj_sq - eps_des * eps_des) <= 1e-12 * ysq) return nullptr;
         const double proj_error = std::sqrt(proj_sq);
         if (!(proj_error <= eps_des)) return nullptr;
@@ -1831,6 +1897,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         r.proj_error = proj_error;
         r.eps_des = eps_des;
         r.used_fused_path = sl.used_fused ? 1 : 0;
+        r.used_exact_loss = refined ? 1 : 0;
         int k = 0;
         for (const auto& [id, rk] : out->ranks()) {
             if (k >= HTR_MAX_NODES) break;

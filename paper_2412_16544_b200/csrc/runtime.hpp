@@ -116,9 +116,17 @@ struct Context {
     cudaEvent_t slot_ev[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
     double fused_ms = 0.0, gemm_ms = 0.0;
     int64_t fused_calls = 0, gemm_calls = 0;
-    // batch-axis sharding over NCCL (dlopen'd)
+    // batch-axis sharding over NCCL (dlopen'd), or through a host-staged
+    // reducer installed by the caller (htr_context_set_reducer)
     int nranks = 1, rank = 0;
     void* nccl_comm = nullptr;
+    htr_host_reduce_fn reducer = nullptr;
+    void* reducer_user = nullptr;
+    double* h_red = nullptr;  // pinned staging buffer of the host reducer
+    int64_t h_red_cap = 0;
+    /// Every global quantity goes through allreduce (the context is one rank
+    /// of a batch-sharded run).
+    bool sharded() const { return nccl_comm != nullptr || reducer != nullptr; }
 
     explicit Context(int dev);
     ~Context();
@@ -207,6 +215,12 @@ struct BuildOut {
     htr_build_report report;
 };
 BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_rel, bool adaptive);
+
+/// Below proj^2 = kTelescopeFloor * ||y||^2 the telescoped loss ||y||^2 -
+/// ||latent||^2 is replaced by the explicit ||y - decode(latent)||^2.
+constexpr double kTelescopeFloor = 1e-10;
+/// ||decode(latent) - y||^2 summed over all ranks.
+double residual_sq_global(Context& c, const Rep& h, const DT& latent, const DT& y);
 
 struct EncodeOut {
     DT latent;

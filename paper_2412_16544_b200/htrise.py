@@ -93,6 +93,9 @@ _P = C.c_void_p
 _D = C.POINTER(C.c_double)
 _I64 = C.POINTER(C.c_int64)
 
+# htr_host_reduce_fn: int32 (*)(double* buf, int64 n, void* user)
+_REDUCE_FN = C.CFUNCTYPE(C.c_int32, _D, C.c_int64, _P)
+
 _SIGNATURES = {
     "htr_context_create": (C.c_int32, [C.c_int32, C.POINTER(_P)]),
     "htr_context_destroy": (C.c_int32, [_P]),
@@ -106,6 +109,7 @@ _SIGNATURES = {
     "htr_context_reset_timing": (C.c_int32, [_P]),
     "htr_comm_get_unique_id": (C.c_int32, [C.POINTER(C.c_uint8)]),
     "htr_context_init_comm": (C.c_int32, [_P, C.POINTER(C.c_uint8), C.c_int32, C.c_int32]),
+    "htr_context_set_reducer": (C.c_int32, [_P, _REDUCE_FN, _P, C.c_int32, C.c_int32]),
     "htr_tree_balanced": (C.c_int32, [C.c_int64, C.POINTER(_Node), C.c_int64, _I64, C.c_char_p, C.c_int64]),
     "htr_tree_validate": (C.c_int32, [C.POINTER(_Node), C.c_int64, C.c_char_p, C.c_int64]),
     "htr_bht_l2r": (C.c_int32, [_P, _D, C.c_int32, _I64, C.c_int32, C.POINTER(_Node), C.c_int64, C.c_double,
@@ -122,6 +126,7 @@ _SIGNATURES = {
     "htr_rep_clone": (C.c_int32, [_P, _P, C.POINTER(_P)]),
     "htr_rep_info": (C.c_int32, [_P, C.POINTER(C.c_int32), _I64, _I64, _D, _I64]),
     "htr_rep_nodes": (C.c_int32, [_P, C.POINTER(_Node), C.c_int64]),
+    "htr_rep_counts": (C.c_int32, [_P, _I64, _I64]),
     "htr_rep_core_shape": (C.c_int32, [_P, C.c_int32, C.c_int32, _I64, C.POINTER(C.c_int32)]),
     "htr_rep_core_get": (C.c_int32, [_P, _P, C.c_int32, C.c_int32, _D, C.c_int32]),
     "htr_rep_import": (C.c_int32, [_P, C.POINTER(_Node), C.c_int64, _I64, C.c_int32, C.POINTER(_D), _I64,
@@ -236,6 +241,17 @@ class Context:
         self.check(lib().htr_context_init_comm(self._h, buf, nranks, rank))
         self.world = nranks
 
+    def set_reducer(self, reduce, nranks: int, rank: int):
+        """Host-staged collective instead of NCCL (htr_context_set_reducer):
+        ``reduce(array)`` must sum the float64 numpy array in place over all
+        ranks (e.g. ``torch.distributed.all_reduce`` on a gloo group). The
+        library hands it drained, pinned partial sums, so ranks never wait on
+        one another's kernels."""
+
+        self._reduce_cb = host_reduce_callback(reduce)  # kept alive with the context
+        self.check(lib().htr_context_set_reducer(self._h, self._reduce_cb, None, int(nranks), int(rank)))
+        self.world = nranks
+
     def close(self):
         if self._h:
             lib().htr_context_destroy(self._h)
@@ -246,6 +262,38 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def host_reduce_callback(reduce):
+    """C callback (htr_host_reduce_fn) around ``reduce(array)``, which sums a
+    float64 numpy view of the library's pinned buffer in place over all
+    ranks. Exceptions become a non-zero status (the library then raises)."""
+
+    def cb(buf, n, _user):
+        try:
+            if n > 0:
+                reduce(np.ctypeslib.as_array(buf, shape=(int(n),)))
+            return 0
+        except Exception:  # noqa: BLE001 - reported as a runtime error by the library
+            import traceback
+
+            traceback.print_exc()
+            return 1
+
+    return _REDUCE_FN(cb)
+
+
+def gloo_reducer(group=None):
+    """``reduce`` for Context.set_reducer over a torch.distributed group
+    (gloo on the host): an element-wise sum, the same bits on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    def reduce(a: np.ndarray):
+        t = torch.from_numpy(a)  # shares the pinned buffer
+        dist.all_reduce(t, group=group)
+
+    return reduce
 
 
 def comm_unique_id() -> bytes:
@@ -497,7 +545,8 @@ class HTRepresentation:
 
     def _info(self):
         d = C.c_int32()
-        dims = (C.c_int64 * 64)()
+        self.ctx.check(lib().htr_rep_info(self._h, C.byref(d), None, None, None, None))
+        dims = (C.c_int64 * max(1, d.value))()
         acc = C.c_int64()
         eps = C.c_double()
         nn = C.c_int64()
@@ -524,9 +573,17 @@ class HTRepresentation:
 
     @property
     def accumulated(self) -> int:
+        """Tensors streamed so far, over all ranks."""
         if self._acc is None:
             self._info()
         return self._acc
+
+    @property
+    def local_count(self) -> int:
+        """Slices held in this rank's root shard (== accumulated unsharded)."""
+        loc = C.c_int64()
+        self.ctx.check(lib().htr_rep_counts(self._h, C.byref(loc), None))
+        return int(loc.value)
 
     @property
     def epsilon_rel(self) -> float:
@@ -607,7 +664,7 @@ class HTRepresentation:
         if not defect <= tol:
             raise RuntimeError(f"HTRepresentation: orthonormality defect {defect} exceeds {tol}")
         r = self.root()
-        if r.ndim != 3 or r.shape[2] != self.accumulated:
+        if r.ndim != 3 or r.shape[2] != self.local_count:
             raise ValueError("HTRepresentation: root batch extent mismatch")
 
     def reserve(self, samples: int):
@@ -671,7 +728,7 @@ def ht_rise_update(h: HTRepresentation, y, epsilon_rel: Optional[float] = None, 
     del keep
     n = rep.n_nodes
     ids = list(zip(rep.node_layer[:n], rep.node_pos[:n]))
-    acc = None if h._acc is None else h._acc + shape[-1] * ctx.world
+    acc = None if (h._acc is None or ctx.world > 1) else h._acc + shape[-1]
     return HTRepresentation(out, ctx, h._tree, h._dims, acc, h._eps), UpdateReport(
         bool(rep.skipped), rep.proj_error, rep.eps_des, dict(zip(ids, rep.added_ranks[:n])),
         dict(zip(ids, rep.new_ranks[:n])), rep.seconds, bool(rep.used_fused_path), bool(rep.used_exact_loss),
@@ -743,7 +800,7 @@ def ht_rise_update_many(h: HTRepresentation, batches, epsilon_rel: Optional[floa
     acc = h._acc
     for i in range(n):
         if acc is not None:
-            acc += int(shapes[i * order + order - 1]) * ctx.world
+            acc = None if ctx.world > 1 else acc + int(shapes[i * order + order - 1])
         values.append(HTRepresentation(_P(outs[i]), ctx, h._tree, h._dims, acc, h._eps))
     return values, _Reports(reps)
 

@@ -137,3 +137,44 @@ def test_two_rank_sharded_decomposition_matches_unsharded():
         assert worst <= 1e-9, (rank, worst)
         assert same_skip, rank
         assert proj_rel <= 1e-4, (rank, proj_rel)
+
+
+def _reducer_worker(rank, world, port, out_q):
+    """The library's host-reducer plumbing (htr_host_reduce_fn built by
+    htrise.host_reduce_callback over a gloo group), called the way
+    Context::allreduce calls it: a C double buffer summed in place."""
+    import ctypes as C
+
+    from paper_2412_16544_b200 import htrise as ht
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cb = ht.host_reduce_callback(ht.gloo_reducer())
+        buf = (C.c_double * 5)(*[rank + 0.5 * i for i in range(5)])
+        rc = cb(buf, 5, None)
+        empty = cb(buf, 0, None)
+        failing = ht.host_reduce_callback(lambda a: (_ for _ in ()).throw(RuntimeError("transport down")))
+        rc_fail = failing(buf, 5, None)
+        out_q.put((rank, rc, empty, rc_fail, list(buf)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_reducer_callback_sums_over_ranks(world):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_reducer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [sum(r + 0.5 * i for r in range(world)) for i in range(5)]
+    for rank, rc, empty, rc_fail, vals in results:
+        assert rc == 0 and empty == 0 and rc_fail == 1, rank
+        assert vals == want, (rank, vals, want)
