@@ -461,6 +461,7 @@ htr_status htr_rep_import(htr_context* ctx, const htr_node* nodes, int64_t n_nod
             }
         }
         h->acc_global = accumulated;
+        htr::measure_defect(c, *h);
         HTR_CUDA(cudaStreamSynchronize(c.s));
         *out = new htr_rep{h};
     });

@@ -92,6 +92,36 @@ __global__ void sum_partials_kernel(const double* partials, int64_t n, double* o
     if (threadIdx.x == 0) out[0] = s;
 }
 
+constexpr int kDefectMax = 64;
+struct DefectJobs {
+    const double* U[kDefectMax];
+    int64_t alpha[kDefectMax], r[kDefectMax];
+};
+
+__global__ void __launch_bounds__(256) basis_defect_kernel(DefectJobs jobs, double* out) {
+    const double* U = jobs.U[blockIdx.x];
+    const int64_t alpha = jobs.alpha[blockIdx.x], r = jobs.r[blockIdx.x];
+    double acc = 0.0;
+    // entries (a, b), a <= b, of U^T U - I; off-diagonal ones count twice
+    for (int64_t ab = threadIdx.x; ab < r * r; ab += blockDim.x) {
+        const int64_t a = ab % r, b = ab / r;
+        if (a > b) continue;
+        double d = 0.0;
+        for (int64_t i = 0; i < alpha; ++i) d = fma(U[i + alpha * a], U[i + alpha * b], d);
+        if (a == b) d -= 1.0;
+        acc = fma(a == b ? 1.0 : 2.0, d * d, acc);
+    }
+    __shared__ double red[8];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+        out[blockIdx.x] = sqrt(t);
+    }
+}
+
 // truncated_svd.hpp:74-99 on sigma_i^2 = max(lambda_i, 0), i < k.
 __global__ void rank_rule_kernel(const double* lambda, int64_t k, int64_t n, double eps_abs, int64_t min_rank,
                                  const double* trace_src, double* info) {
@@ -581,6 +611,21 @@ int launch_pair_project(const double* t, int64_t I, int64_t J0, int64_t J1, int6
                                                            static_cast<int>(Q0), U1, static_cast<int>(Q1), out, ysq);
     ++*launches;
     return blocks;
+}
+
+void launch_basis_defect(const double* const* U, const int64_t* alpha, const int64_t* r, int count, double* out,
+                         cudaStream_t s, int64_t* launches) {
+    for (int i0 = 0; i0 < count; i0 += kDefectMax) {
+        DefectJobs jobs{};
+        const int n = std::min(kDefectMax, count - i0);
+        for (int i = 0; i < n; ++i) {
+            jobs.U[i] = U[i0 + i];
+            jobs.alpha[i] = alpha[i0 + i];
+            jobs.r[i] = U[i0 + i] ? r[i0 + i] : 0;
+        }
+        basis_defect_kernel<<<n, 256, 0, s>>>(jobs, out + i0);
+        ++*launches;
+    }
 }
 
 void launch_fill(double* dst, int64_t n, double value, cudaStream_t s, int64_t* launches) {

@@ -10,28 +10,30 @@
 #include <cuda_runtime.h>
 
 #include <mutex>
-#include <set>
-#include <tuple>
+#include <map>
+#include <utility>
 
 namespace htr {
 
 constexpr int kNumSMs = 148;  // B200; the launchers query the device anyway
 
-/// Raise a kernel's dynamic shared-memory limit to `bytes` on the current
-/// device. The attribute is per (function, device): remembered per pair
-/// (and per size, the largest applied so far) under a lock, so contexts on
-/// several devices and concurrent callers each configure what they launch.
+/// Raise a kernel's dynamic shared-memory limit to at least `bytes` on the
+/// current device. The attribute is per (function, device); the largest
+/// value applied so far is remembered per pair under a lock and the limit
+/// only ever grows (it is never rewritten while launches of the kernel may
+/// be in flight), so contexts on several devices and concurrent callers each
+/// configure what they launch.
 inline cudaError_t ensure_smem_limit(const void* fn, size_t bytes) {
     static std::mutex mu;
-    static std::set<std::tuple<const void*, int, size_t>> done;
+    static std::map<std::pair<const void*, int>, size_t> applied;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> g(mu);
-    const auto key = std::make_tuple(fn, dev, bytes);
-    if (done.count(key)) return cudaSuccess;
+    size_t& cur = applied[std::make_pair(fn, dev)];
+    if (bytes <= cur) return cudaSuccess;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
-    if (e == cudaSuccess) done.insert(key);
+    if (e == cudaSuccess) cur = bytes;
     return e;
 }
 
@@ -135,6 +137,11 @@ void launch_unfold(const double* src, int64_t inner, int64_t ext, int64_t outer,
 // info[0..1].
 void launch_orthonormalize_new(const double* U, int64_t alpha, int64_t r, double* W, int64_t q, double* info,
                                double* work, cudaStream_t s, int64_t* launches);
+
+// Orthonormality defects of `count` bases U_i (alpha_i x r_i, col-major):
+// out[i] = ||U_i^T U_i - I||_F, one CTA per basis (r_i = 0 writes 0).
+void launch_basis_defect(const double* const* U, const int64_t* alpha, const int64_t* r, int count, double* out,
+                         cudaStream_t s, int64_t* launches);
 
 // out[i, q, o] = sum_j M(q, j) t[i, j, o] with M(q, j) = M[q*smq + j*smj],
 // J, Q <= 32 (streaming, one thread per fibre). When energy != nullptr the

@@ -453,6 +453,14 @@ Truncation truncate_eig(Context& c, const BufPtr& lam, const BufPtr& V, int64_t 
     }
     t.u = c.tensor({rows, t.rank});
     launch_take_columns(V->p, n, t.rank, t.u.data(), info->p, c.s, &c.launches);
+    if (t.rank > 0 && !zero) {
+        // CholeskyQR2 of the retained eigenvectors: the span is unchanged and
+        // U^T U - I drops to the u level (it bounds the telescoped skip
+        // test's error, telescope_floor_sq)
+        BufPtr oinfo = c.alloc(4);
+        BufPtr work = c.alloc(t.rank * t.rank + 16);
+        launch_orthonormalize_new(nullptr, rows, 0, t.u.data(), t.rank, oinfo->p, work->p, c.s, &c.launches);
+    }
     HTR_CUDA(cudaGetLastError());
     return t;
 }
@@ -1103,6 +1111,7 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
     h->root->committed = batch;
     h->acc = batch;
     h->acc_global = gbatch;
+    measure_defect(c, *h);
     out.rep = h;
     return out;
 }
@@ -1268,6 +1277,38 @@ bool launch_skip_encode_fused(Context& c, const Rep& h, const DT& y, const DT* l
                               DT* latent, cudaEvent_t ev0, cudaEvent_t ev1, double* host_out) {
     return launch_skip_encode3(c, h, y, latent_target, sc, latent, ev0, ev1, host_out) ||
            launch_skip_encode8(c, h, y, latent_target, sc, latent, ev0, ev1, host_out);
+}
+
+double telescope_floor_sq(const Rep& h) {
+    const double beta = 2.0 * h.defect + 16.0 * 0x1p-53;
+    const double f = beta / (2.0 * kProjErrorTol);
+    return f * f;
+}
+
+void measure_defect(Context& c, Rep& h) {
+    std::vector<const double*> U;
+    std::vector<int64_t> al, rr;
+    for (Index l = 1; l <= h.tree.depth(); ++l)
+        for (const TreeNode& n : h.tree.layer(l)) {
+            const DT& core = h.core(n.id);
+            const Basis b = basis_of(h, n.id);
+            const bool ident = core.buf && core.buf->identity && core.offset == 0 && b.alpha == b.r;
+            U.push_back(ident || b.r == 0 ? nullptr : b.p);
+            al.push_back(b.alpha);
+            rr.push_back(b.r);
+        }
+    if (U.empty()) {
+        h.defect = 0.0;
+        return;
+    }
+    BufPtr out = c.alloc(static_cast<int64_t>(U.size()));
+    launch_basis_defect(U.data(), al.data(), rr.data(), static_cast<int>(U.size()), out->p, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+    std::vector<double> d(U.size());
+    c.fetch(out->p, static_cast<int64_t>(d.size()), d.data());
+    double sum = 0.0;
+    for (double v : d) sum += v;
+    h.defect = sum;
 }
 
 double residual_sq_global(Context& c, const Rep& h, const DT& latent, const DT& y) {
@@ -1508,13 +1549,12 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
     } else {
         out.proj_sq = std::max(0.0, out.ysq - latsq);
     }
-    if (!exact && !out.nonfinite && std::isfinite(out.ysq) && out.proj_sq < kTelescopeFloor * out.ysq) {
-        // the telescoped loss is accurate to ~1e-15 ||y||^2 absolute: below
-        // the floor its square root would drift from the reference's
-        // explicit-residual value (bht.hpp:357-365) by more than 1e-10 ||y||,
-        // so the loss is re-measured as ||y - decode(latent)||^2 (the same
-        // quantity: the step residuals of nested orthogonal projections add
-        // up to it), one more read of y
+    if (!exact && !out.nonfinite && std::isfinite(out.ysq) && out.proj_sq < telescope_floor_sq(h) * out.ysq) {
+        // below the floor the telescoped loss's square root could drift from
+        // the reference's explicit-residual value (bht.hpp:357-365) by more
+        // than kProjErrorTol ||y||, so the loss is re-measured as
+        // ||y - decode(latent)||^2 (the same quantity: the step residuals of
+        // nested orthogonal projections add up to it), one more read of y
         out.proj_sq = residual_sq_global(c, h, out.latent, y);
         out.exact = true;
     }
@@ -1744,6 +1784,7 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
     } else {
         append_root(c, *out, h, cur);
     }
+    measure_defect(c, *out);
     return finish(out);
 }
 
@@ -1880,7 +1921,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         const double eps_des = eps_rel * std::sqrt(ysq);
         double proj_sq = std::max(0.0, ysq - latsq);
         bool refined = false;
-        if (proj_sq < kTelescopeFloor * ysq) {  // as in encode(): re-measure explicitly
+        if (proj_sq < telescope_floor_sq(h) * ysq) {  // as in encode(): re-measure explicitly
             proj_sq = residual_sq_global(c, h, sl.latent, sl.y);
             refined = true;
         }

@@ -84,6 +84,9 @@ struct Rep {
     int64_t acc = 0;         // slices held locally (this rank's shard)
     int64_t acc_global = 0;  // total tensors streamed (all ranks)
     double eps_rel = 0.0;
+    /// sum over the non-root bases of ||U^T U - I||_F (identity bases count 0):
+    /// bounds the telescoped loss's error (see telescope_floor_sq)
+    double defect = 0.0;
 
     const DT& core(NodeId id) const {
         return cores.at(static_cast<size_t>(id.layer)).at(static_cast<size_t>(id.pos));
@@ -216,9 +219,17 @@ struct BuildOut {
 };
 BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_rel, bool adaptive);
 
-/// Below proj^2 = kTelescopeFloor * ||y||^2 the telescoped loss ||y||^2 -
-/// ||latent||^2 is replaced by the explicit ||y - decode(latent)||^2.
-constexpr double kTelescopeFloor = 1e-10;
+/// The skip test's telescoped loss ||y||^2 - ||latent||^2 carries an
+/// absolute error of at most beta ||y||^2, beta = 2 D + 16 u, D the bases'
+/// orthonormality defect sum (Rep::defect): the nested projections are exact
+/// projectors only up to U^T U - I. Its square root is then within
+/// kProjErrorTol ||y|| of the explicit-residual value whenever proj^2 >=
+/// telescope_floor_sq(h) ||y||^2 = (beta / (2 kProjErrorTol))^2 ||y||^2;
+/// below that the loss is re-measured as ||y - decode(latent)||^2.
+constexpr double kProjErrorTol = 1e-9;
+double telescope_floor_sq(const Rep& h);
+/// Rep::defect of every non-root basis (one launch + one read-back).
+void measure_defect(Context& c, Rep& h);
 /// ||decode(latent) - y||^2 summed over all ranks.
 double residual_sq_global(Context& c, const Rep& h, const DT& latent, const DT& y);
 
