@@ -111,6 +111,7 @@ HTR_API htr_status htr_synchronize(htr_context* ctx);
 #define HTR_OPT_FUSED_ENCODE 2    /* 1 (default): fused DMMA leaf-projection kernel where it applies */
 #define HTR_OPT_PROFILE_EVENTS 3  /* 1: record per-kernel CUDA events for the bench */
 #define HTR_OPT_TAIL_KERNEL 4     /* skip-path tail of (1,(2,3)) trees: 0 auto (default: one sample per CTA), 1 one sample per CTA, 2 sample pairs */
+#define HTR_OPT_EIG_SOLVER 5      /* truncation eigensolver: 1 (default) Householder tridiagonal + bisection + inverse iteration, 0 Jacobi */
 HTR_API htr_status htr_context_set_option(htr_context* ctx, int32_t option, double value);
 /* Kernel launches issued on this context so far (monotonic counter). */
 HTR_API int64_t htr_context_launch_count(const htr_context* ctx);

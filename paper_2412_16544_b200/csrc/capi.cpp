@@ -169,6 +169,7 @@ htr_status htr_context_set_option(htr_context* ctx, int32_t option, double value
                 if (value < 0 || value > 2) htr::raise(HTR_ERR_INVALID_ARGUMENT, "tail kernel option: 0, 1 or 2");
                 c.tail_kernel = static_cast<int>(value);
                 break;
+            case HTR_OPT_EIG_SOLVER: c.tridiag = value != 0.0; break;
             default: htr::raise(HTR_ERR_INVALID_ARGUMENT, "unknown option " + std::to_string(option));
         }
     });

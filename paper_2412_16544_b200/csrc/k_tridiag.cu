@@ -1,0 +1,488 @@
+// Symmetric eigen-truncation through a tridiagonal reduction: the device
+// replacement of the reference's thin SVD (Eigen::BDCSVD,
+// truncated_svd.hpp:29-45) on the Gram G = M M^T of an unfolding.
+//
+//   tridiag_eigvals_kernel   one CTA per Gram: Householder reduction
+//                            Q^T G Q = T (the matrix in shared memory up to
+//                            n = 160, else in the L2-resident workspace),
+//                            then every eigenvalue of T by parallel
+//                            multisection on Sturm counts (8 lanes per
+//                            eigenvalue). Writes lambda (descending) and the
+//                            reflectors / T into the workspace.
+//   tridiag_vectors_kernel   one CTA per Gram, after the rank rule: the r
+//                            leading eigenvectors of T by inverse iteration
+//                            (a warp per cluster of close eigenvalues,
+//                            re-orthogonalised within the cluster as LAPACK
+//                            dstein does), then U = Q Z by applying the
+//                            reflectors column-parallel (no block barrier).
+//
+// The reference's rank rule needs the eigenvalues to absolute accuracy
+// ~u ||G|| (the Gram itself carries ~n u ||G|| of rounding), which the
+// backward-stable reduction plus bisection to ~2 ulp of ||T|| provides; only
+// the retained subspace's basis is formed (any orthonormal basis of it is a
+// valid truncated_svd factor up to rotation; parity is checked by principal
+// angles). Everything is deterministic (fixed reduction trees, no atomics),
+// so ranks of a sharded run, which solve bit-identical Grams, agree.
+#include <algorithm>
+#include <cfloat>
+
+#include "kernels.cuh"
+
+namespace htr {
+namespace {
+
+constexpr int kTriThreads = 1024;
+constexpr int kTriSmemMaxN = 160;  // A (n x n) in shared memory: 200 KB at n = 160
+constexpr int kTriBatch = 16;
+constexpr int kVecThreads = 512;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+/// Sum over the CTA, the same value (same bits) in every thread.
+__device__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();  // red is free
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    return warp_sum(lane < nw ? red[lane] : 0.0);
+}
+__device__ double block_max(double v, double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    return warp_max(lane < nw ? red[lane] : -DBL_MAX);
+}
+__device__ double block_min(double v, double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_min(v);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    return warp_min(lane < nw ? red[lane] : DBL_MAX);
+}
+
+// workspace layout per job (doubles): [A n*n | d n | e n | tau n | lam_asc n | scale 1]
+__host__ __device__ __forceinline__ int64_t tri_off_d(int n) { return static_cast<int64_t>(n) * n; }
+
+struct TriJobs {
+    const double* G[kTriBatch];
+    double* lam[kTriBatch];  // n eigenvalues, descending (unscaled)
+    double* W[kTriBatch];    // workspace, tridiag_workspace_doubles(n)
+    int n[kTriBatch];
+};
+
+/// Number of eigenvalues of T (d, e2 = e^2) below x (Sturm count on the LDL^T
+/// pivots, LAPACK dlaebz's pivmin safeguard).
+__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
+    double q = d[0] - x;
+    if (fabs(q) <= pivmin) q = -pivmin;
+    int c = q < 0.0;
+    for (int i = 1; i < n; ++i) {
+        q = (d[i] - x) - e2[i - 1] / q;
+        if (fabs(q) <= pivmin) q = -pivmin;
+        c += q < 0.0;
+    }
+    return c;
+}
+
+__global__ void __launch_bounds__(kTriThreads) tridiag_eigvals_kernel(const TriJobs jobs, int use_smem) {
+    const int n = jobs.n[blockIdx.x];
+    const double* __restrict__ G = jobs.G[blockIdx.x];
+    double* __restrict__ W = jobs.W[blockIdx.x];
+    double* __restrict__ lam_out = jobs.lam[blockIdx.x];
+    extern __shared__ double smem[];
+    __shared__ double red[32];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    double* A = use_smem ? smem : W;
+    double* vv = use_smem ? smem + nn : W + tri_off_d(n) + 5 * n + 1;  // 3 vectors of n
+    double* pw = vv + n;
+    double* ww = pw + n;
+    double* dg = W + tri_off_d(n);
+    double* eg = dg + n;
+    double* taug = eg + n;
+    double* lam_asc = taug + n;
+
+    // exact power-of-two scaling to max |G| ~ 1 (no overflow in the norms)
+    double gm = 0.0;
+    for (int64_t i = tid; i < nn; i += nt) gm = fmax(gm, fabs(G[i]));
+    gm = block_max(gm, red);
+    int ex = 0;
+    if (gm > 0.0 && gm <= DBL_MAX) frexp(gm, &ex);
+    const double sc = ldexp(1.0, -ex), unsc = ldexp(1.0, ex);
+    for (int64_t i = tid; i < nn; i += nt) {
+        const int64_t r = i % n, c = i / n;
+        A[i] = 0.5 * (G[r + n * c] + G[c + n * r]) * sc;
+    }
+    __syncthreads();
+
+    // Householder reduction to tridiagonal form (dsytd2, lower): step k
+    // annihilates A[k+2:, k] with H_k = I - tau v v^T acting on rows k+1..
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m = n - k - 1;
+        double* x = A + (k + 1) + static_cast<int64_t>(n) * k;
+        double ps = 0.0;
+        for (int i = 1 + tid; i < m; i += nt) ps = fma(x[i], x[i], ps);
+        const double xn2 = block_sum(ps, red);
+        const double alpha = x[0];
+        double tau = 0.0, beta = alpha, scale = 0.0;
+        if (xn2 > 0.0) {
+            beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+            tau = (beta - alpha) / beta;
+            scale = 1.0 / (alpha - beta);
+        }
+        for (int i = tid; i < m; i += nt) {
+            const double vi = i == 0 ? 1.0 : x[i] * scale;
+            vv[i] = vi;
+            if (i > 0) x[i] = vi;  // reflector stored below the subdiagonal
+        }
+        if (tid == 0) {
+            x[0] = beta;
+            taug[k] = tau;
+        }
+        __syncthreads();
+        if (tau == 0.0) continue;
+        double* A22 = A + (k + 1) + static_cast<int64_t>(n) * (k + 1);
+        // p = tau A22 v (A22 symmetric: column j dotted with v)
+        for (int j = warp; j < m; j += nw) {
+            const double* col = A22 + static_cast<int64_t>(n) * j;
+            double s = 0.0;
+            for (int i = lane; i < m; i += 32) s = fma(col[i], vv[i], s);
+            s = warp_sum(s);
+            if (lane == 0) pw[j] = tau * s;
+        }
+        __syncthreads();
+        double pd = 0.0;
+        for (int i = tid; i < m; i += nt) pd = fma(pw[i], vv[i], pd);
+        const double K = 0.5 * tau * block_sum(pd, red);
+        for (int i = tid; i < m; i += nt) ww[i] = pw[i] - K * vv[i];
+        __syncthreads();
+        // A22 -= v w^T + w v^T (both triangles)
+        for (int j = warp; j < m; j += nw) {
+            double* col = A22 + static_cast<int64_t>(n) * j;
+            const double vj = vv[j], wj = ww[j];
+            for (int i = lane; i < m; i += 32) col[i] -= fma(vv[i], wj, ww[i] * vj);
+        }
+        __syncthreads();
+    }
+    // T: diagonal and subdiagonal; reflectors to the workspace
+    for (int i = tid; i < n; i += nt) {
+        dg[i] = A[i + static_cast<int64_t>(n) * i];
+        eg[i] = i + 1 < n ? A[i + 1 + static_cast<int64_t>(n) * i] : 0.0;
+        if (i + 2 >= n) taug[i] = 0.0;
+    }
+    if (use_smem)
+        for (int64_t i = tid; i < nn; i += nt) {
+            const int64_t r = i % n, c = i / n;
+            if (r >= c + 2) W[i] = A[i];
+        }
+    __syncthreads();
+
+    // eigenvalues of T: multisection, 8 lanes (8 points) per eigenvalue
+    __shared__ double d[1024], e2[1024];  // n <= 1024 (tridiag_supported)
+    for (int i = tid; i < n; i += nt) {
+        d[i] = dg[i];
+        e2[i] = eg[i] * eg[i];
+    }
+    __syncthreads();
+    double lo_g = DBL_MAX, hi_g = -DBL_MAX, emax = 0.0;
+    for (int i = tid; i < n; i += nt) {
+        const double r = (i > 0 ? fabs(eg[i - 1]) : 0.0) + (i + 1 < n ? fabs(eg[i]) : 0.0);
+        lo_g = fmin(lo_g, d[i] - r);
+        hi_g = fmax(hi_g, d[i] + r);
+        emax = fmax(emax, e2[i]);
+    }
+    lo_g = block_min(lo_g, red);
+    hi_g = block_max(hi_g, red);
+    emax = block_max(emax, red);
+    const double bnorm = fmax(fabs(lo_g), fabs(hi_g));
+    const double pivmin = DBL_MIN * fmax(1.0, emax);
+    const double atol = 4.0 * DBL_EPSILON * bnorm + pivmin;
+    lo_g -= atol + 2.0 * DBL_EPSILON * bnorm * n;
+    hi_g += atol + 2.0 * DBL_EPSILON * bnorm * n;
+    const int g = tid >> 3, gl = tid & 7, ngroups = nt >> 3;
+    const unsigned gshift = static_cast<unsigned>(lane & ~7);
+    for (int j0 = 0; j0 < n; j0 += ngroups) {
+        const int j = j0 + g;
+        double lo = lo_g, hi = hi_g;
+        bool done = j >= n;
+        for (int it = 0; it < 64; ++it) {
+            if (!done && hi - lo <= fmax(atol, 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)))) done = true;
+            if (__all_sync(0xffffffffu, done)) break;
+            const double xs = lo + (hi - lo) * (gl + 1) * (1.0 / 9.0);
+            const int cnt = done ? 0 : sturm_count(d, e2, n, xs, pivmin);
+            // first point of the group whose count exceeds j
+            const unsigned ball = (__ballot_sync(0xffffffffu, !done && cnt > j) >> gshift) & 0xffu;
+            const int p = ball ? __ffs(ball) - 1 : 8;
+            const double xp = __shfl_sync(0xffffffffu, xs, static_cast<int>(gshift) + (p < 8 ? p : 7));
+            const double xq = __shfl_sync(0xffffffffu, xs, static_cast<int>(gshift) + (p > 0 ? p - 1 : 0));
+            if (!done) {
+                const double nlo = p > 0 ? xq : lo;
+                const double nhi = p < 8 ? xp : hi;
+                lo = nlo;
+                hi = nhi;
+            }
+        }
+        if (j < n && gl == 0) lam_asc[j] = 0.5 * (lo + hi);
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += nt) lam_out[n - 1 - i] = lam_asc[i] * unsc;
+    if (tid == 0) W[tri_off_d(n) + 4 * n] = unsc;
+}
+
+struct VecJobs {
+    const double* W[kTriBatch];
+    const double* info[kTriBatch];  // rank rule output: [2] = trace (0 -> zero input)
+    double* U[kTriBatch];           // n x r
+    int n[kTriBatch], r[kTriBatch];
+};
+
+/// (T - x I) y = b by Gaussian elimination with partial pivoting of the
+/// tridiagonal matrix (one thread; LAPACK dlagtf/dlagts). Pivots below `tol`
+/// in magnitude are perturbed to +-tol (inverse iteration's standard guard).
+struct TriLU {
+    double *u0, *u1, *u2, *l;
+    unsigned char* piv;
+};
+__device__ void tri_factor(const double* d, const double* e, int n, double x, double tol, const TriLU& f) {
+    double p0 = d[0] - x, p1 = n > 1 ? e[0] : 0.0, p2 = 0.0;
+    for (int k = 0; k + 1 < n; ++k) {
+        const double q0 = e[k], q1 = d[k + 1] - x, q2 = k + 2 < n ? e[k + 1] : 0.0;
+        if (fabs(p0) >= fabs(q0)) {
+            if (fabs(p0) < tol) p0 = p0 < 0.0 ? -tol : tol;
+            const double mult = q0 / p0;
+            f.u0[k] = p0; f.u1[k] = p1; f.u2[k] = p2; f.l[k] = mult; f.piv[k] = 0;
+            p0 = q1 - mult * p1;
+            p1 = q2 - mult * p2;
+        } else {
+            const double mult = p0 / q0;
+            f.u0[k] = q0; f.u1[k] = q1; f.u2[k] = q2; f.l[k] = mult; f.piv[k] = 1;
+            const double np0 = p1 - mult * q1, np1 = p2 - mult * q2;
+            p0 = np0;
+            p1 = np1;
+        }
+        p2 = 0.0;
+    }
+    if (fabs(p0) < tol) p0 = p0 < 0.0 ? -tol : tol;
+    f.u0[n - 1] = p0;
+    f.u1[n - 1] = 0.0;
+    f.u2[n - 1] = 0.0;
+}
+__device__ void tri_solve(int n, const TriLU& f, double* y) {
+    for (int k = 0; k + 1 < n; ++k) {
+        if (f.piv[k]) {
+            const double t = y[k];
+            y[k] = y[k + 1];
+            y[k + 1] = t;
+        }
+        y[k + 1] -= f.l[k] * y[k];
+    }
+    for (int k = n - 1; k >= 0; --k) {
+        double s = y[k];
+        if (k + 1 < n) s -= f.u1[k] * y[k + 1];
+        if (k + 2 < n) s -= f.u2[k] * y[k + 2];
+        y[k] = s / f.u0[k];
+    }
+}
+
+__device__ __forceinline__ double hash_uniform(uint32_t a, uint32_t b) {
+    uint32_t h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    h *= 0x297A2D39u;
+    h ^= h >> 15;
+    return (static_cast<double>(h) + 0.5) * (2.0 / 4294967296.0) - 1.0;  // (-1, 1)
+}
+
+__global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const VecJobs jobs, int vec_warps) {
+    const int n = jobs.n[blockIdx.x], r = jobs.r[blockIdx.x];
+    const double* __restrict__ W = jobs.W[blockIdx.x];
+    double* __restrict__ U = jobs.U[blockIdx.x];
+    const bool zero = jobs.info[blockIdx.x][2] == 0.0;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    if (r <= 0) return;
+    if (zero) {  // zero input: the reference's canonical identity columns (truncated_svd.hpp:66-72)
+        for (int64_t i = tid; i < static_cast<int64_t>(n) * r; i += nt) U[i] = (i % n == i / n) ? 1.0 : 0.0;
+        return;
+    }
+    extern __shared__ double smem[];
+    const double* dg = W + tri_off_d(n);
+    const double* eg = dg + n;
+    const double* taug = eg + n;
+    const double* lam_asc = taug + n;
+    // clusters of the r leading eigenvalues (ascending j = n - r .. n - 1):
+    // a new cluster starts where the gap exceeds 1e-3 ||T||_1 (dstein's ORTOL)
+    __shared__ int cstart[1024 + 1];
+    __shared__ int ncl;
+    double* d = smem;
+    double* e = smem + n;
+    for (int i = tid; i < n; i += nt) {
+        d[i] = dg[i];
+        e[i] = eg[i];
+    }
+    __syncthreads();
+    __shared__ double onenrm;
+    if (tid == 0) {
+        double t = 0.0;
+        for (int i = 0; i < n; ++i)
+            t = fmax(t, fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0));
+        onenrm = t;
+        const double ortol = 1e-3 * t;
+        int c = 0;
+        for (int j = n - r; j < n; ++j)
+            if (j == n - r || lam_asc[j] - lam_asc[j - 1] > ortol) cstart[c++] = j;
+        cstart[c] = n;
+        ncl = c;
+    }
+    __syncthreads();
+    const double tol = fmax(DBL_EPSILON * onenrm, DBL_MIN);
+    // per-warp scratch: u0 u1 u2 l y (5 n doubles) + piv (n bytes)
+    double* scratch = smem + 2 * n;
+    const int per = 5 * n + (n + 7) / 8;
+    for (int cl = warp; cl < ncl; cl += vec_warps) {
+        if (warp >= vec_warps) break;
+        double* ws = scratch + static_cast<int64_t>(warp) * per;
+        TriLU f{ws, ws + n, ws + 2 * n, ws + 3 * n, reinterpret_cast<unsigned char*>(ws + 5 * n)};
+        double* y = ws + 4 * n;
+        double xprev = 0.0;
+        for (int j = cstart[cl]; j < cstart[cl + 1]; ++j) {
+            double xj = lam_asc[j];
+            if (j > cstart[cl]) {  // separate coincident eigenvalues slightly (dstein)
+                const double pertol = 10.0 * fabs(DBL_EPSILON * xj);
+                if (xj - xprev < pertol) xj = xprev + pertol;
+            }
+            xprev = xj;
+            if (lane == 0) tri_factor(d, e, n, xj, tol, f);
+            for (int i = lane; i < n; i += 32) y[i] = hash_uniform(static_cast<uint32_t>(j), static_cast<uint32_t>(i));
+            __syncwarp();
+            for (int it = 0; it < 3; ++it) {
+                if (lane == 0) tri_solve(n, f, y);
+                __syncwarp();
+                // orthogonalise against the cluster's earlier vectors (twice)
+                for (int pass = 0; pass < 2; ++pass)
+                    for (int p = cstart[cl]; p < j; ++p) {
+                        const double* up = U + static_cast<int64_t>(n) * (n - 1 - p);
+                        double s = 0.0;
+                        for (int i = lane; i < n; i += 32) s = fma(up[i], y[i], s);
+                        s = warp_sum(s);
+                        for (int i = lane; i < n; i += 32) y[i] -= s * up[i];
+                        __syncwarp();
+                    }
+                // normalise (largest entry positive on the last pass)
+                double s = 0.0, mx = 0.0;
+                int imx = 0;
+                for (int i = lane; i < n; i += 32) {
+                    s = fma(y[i], y[i], s);
+                    if (fabs(y[i]) > mx) { mx = fabs(y[i]); imx = i; }
+                }
+                s = warp_sum(s);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double om = __shfl_xor_sync(0xffffffffu, mx, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, imx, o);
+                    if (om > mx || (om == mx && oi < imx)) { mx = om; imx = oi; }
+                }
+                double inv = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+                if (it == 2 && y[imx] < 0.0) inv = -inv;
+                __syncwarp();
+                for (int i = lane; i < n; i += 32) y[i] *= inv;
+                __syncwarp();
+            }
+            double* uj = U + static_cast<int64_t>(n) * (n - 1 - j);
+            for (int i = lane; i < n; i += 32) uj[i] = y[i];
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // U = H_0 H_1 ... H_{n-3} Z: each warp applies every reflector to its own
+    // columns (no block barrier), reflector k last-to-first
+    for (int c = warp; c < r; c += nw) {
+        double* z = U + static_cast<int64_t>(n) * c;
+        for (int k = n - 3; k >= 0; --k) {
+            const double tau = taug[k];
+            if (tau == 0.0) continue;
+            const double* v = W + (k + 1) + static_cast<int64_t>(n) * k;  // v[0] = 1 implicit
+            const int m = n - k - 1;
+            double s = 0.0;
+            for (int i = lane; i < m; i += 32) s = fma(i == 0 ? 1.0 : v[i], z[k + 1 + i], s);
+            s = tau * warp_sum(s);
+            for (int i = lane; i < m; i += 32) z[k + 1 + i] -= s * (i == 0 ? 1.0 : v[i]);
+            __syncwarp();
+        }
+    }
+}
+
+}  // namespace
+
+int64_t tridiag_workspace_doubles(int64_t n) { return n * n + 8 * n + 8; }
+
+bool tridiag_supported(int64_t n) { return n >= 1 && n <= 1024; }
+
+void launch_tridiag_eigvals(const double* const* G, const int64_t* n, double* const* lambda, double* const* W,
+                            int count, cudaStream_t s, int64_t* launches) {
+    for (int i0 = 0; i0 < count;) {
+        // one launch per run of jobs with the same storage mode
+        const bool sm = n[i0] <= kTriSmemMaxN;
+        TriJobs jobs{};
+        int k = 0;
+        int64_t nmax = 0;
+        while (i0 + k < count && k < kTriBatch && (n[i0 + k] <= kTriSmemMaxN) == sm) {
+            jobs.G[k] = G[i0 + k];
+            jobs.lam[k] = lambda[i0 + k];
+            jobs.W[k] = W[i0 + k];
+            jobs.n[k] = static_cast<int>(n[i0 + k]);
+            nmax = std::max(nmax, n[i0 + k]);
+            ++k;
+        }
+        const size_t smem = sm ? sizeof(double) * static_cast<size_t>(nmax * nmax + 3 * nmax) : 0;
+        if (smem > 46 * 1024) ensure_smem_limit(reinterpret_cast<const void*>(tridiag_eigvals_kernel), smem);
+        tridiag_eigvals_kernel<<<k, kTriThreads, smem, s>>>(jobs, sm ? 1 : 0);
+        ++*launches;
+        i0 += k;
+    }
+}
+
+void launch_tridiag_vectors(const double* const* W, const double* const* info, const int64_t* n, const int64_t* r,
+                            double* const* U, int count, cudaStream_t s, int64_t* launches) {
+    for (int i0 = 0; i0 < count; i0 += kTriBatch) {
+        VecJobs jobs{};
+        const int k = std::min(kTriBatch, count - i0);
+        int64_t nmax = 1;
+        for (int i = 0; i < k; ++i) {
+            jobs.W[i] = W[i0 + i];
+            jobs.info[i] = info[i0 + i];
+            jobs.U[i] = U[i0 + i];
+            jobs.n[i] = static_cast<int>(n[i0 + i]);
+            jobs.r[i] = static_cast<int>(r[i0 + i]);
+            nmax = std::max(nmax, n[i0 + i]);
+        }
+        // shared memory: d, e and per-warp inverse-iteration scratch
+        const int64_t per = 5 * nmax + (nmax + 7) / 8;
+        const int64_t budget = 200 * 1024 / 8 - 2 * nmax;
+        const int vw = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kVecThreads / 32, budget / per)));
+        const size_t smem = sizeof(double) * static_cast<size_t>(2 * nmax + vw * per);
+        if (smem > 46 * 1024) ensure_smem_limit(reinterpret_cast<const void*>(tridiag_vectors_kernel), smem);
+        tridiag_vectors_kernel<<<k, kVecThreads, smem, s>>>(jobs, vw);
+        ++*launches;
+    }
+}
+
+}  // namespace htr

@@ -105,6 +105,20 @@ void launch_jacobi_eig_batch(const double* const* G, const int64_t* n, double* c
 void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, double* work, cudaStream_t s,
                        int64_t* launches);
 
+// Tridiagonal route of the symmetric eigen-truncation (k_tridiag.cu), for
+// 1 <= n <= 1024: launch_tridiag_eigvals reduces each G_i (n_i x n_i,
+// symmetric) to tridiagonal form in workspace W_i
+// (tridiag_workspace_doubles(n_i)) and writes all its eigenvalues, descending,
+// to lambda_i; launch_tridiag_vectors then writes the r_i leading
+// eigenvectors to U_i (n_i x r_i, orthonormal), or identity columns when
+// info_i[2] == 0 (the rank rule's zero-input flag). One CTA per problem.
+bool tridiag_supported(int64_t n);
+int64_t tridiag_workspace_doubles(int64_t n);
+void launch_tridiag_eigvals(const double* const* G, const int64_t* n, double* const* lambda, double* const* W,
+                            int count, cudaStream_t s, int64_t* launches);
+void launch_tridiag_vectors(const double* const* W, const double* const* info, const int64_t* n, const int64_t* r,
+                            double* const* U, int count, cudaStream_t s, int64_t* launches);
+
 // flag[0] = 1 if G - shift I (n x n, symmetric) is positive definite (one-CTA
 // Cholesky on `work`, n * n doubles), else 0.
 void launch_posdef_test(const double* G, int64_t n, double shift, double* work, double* flag, cudaStream_t s,

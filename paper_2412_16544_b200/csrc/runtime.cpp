@@ -387,8 +387,91 @@ ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode);
 Truncation truncate_eig(Context& c, const BufPtr& lam, const BufPtr& V, int64_t rows, int64_t cols, double eps_abs,
                         int64_t min_rank, const ProjectedGram& refine, double noise_scale);
 
+/// A Gram reduced to tridiagonal form with all its eigenvalues (descending)
+/// on the device (k_tridiag.cu); W keeps the reflectors for the vectors.
+struct TriSolve {
+    BufPtr lam, W;
+    int64_t n = 0;
+};
+
+TriSolve tri_alloc(Context& c, int64_t n) {
+    TriSolve t;
+    t.n = n;
+    t.lam = c.alloc(n);
+    t.W = c.alloc(tridiag_workspace_doubles(n));
+    return t;
+}
+
+Truncation truncate_jacobi(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
+                           const ProjectedGram& refine, double noise_scale);
+
+/// The rank rule (truncated_svd.hpp:74-99) on a tridiagonal solve's
+/// eigenvalues and the retained eigenvectors. A truncation whose tolerance
+/// sits at the Gram's rounding floor re-measures its small eigenvalues
+/// through `refine`, which needs every eigenvector: that (rare) case takes
+/// the Jacobi solver on the untouched Gram instead.
+Truncation finish_tri(Context& c, const TriSolve& ts, const DT& G, int64_t rows, int64_t cols, double eps_abs,
+                      int64_t min_rank, const ProjectedGram& refine, double noise_scale) {
+    const int64_t n = rows;
+    const int64_t k = std::min(rows, cols);
+    if (refine) {
+        std::vector<double> lh(static_cast<size_t>(n));
+        c.fetch(ts.lam->p, n, lh.data());
+        const double lmax = std::max({lh[0], noise_scale, 0.0});
+        if (lmax > 0.0 && eps_abs * eps_abs < 1e-7 * lmax) {
+            int64_t s0 = 0;
+            while (s0 < n && lh[static_cast<size_t>(s0)] >= 1e-6 * lmax) ++s0;
+            if (s0 < n) return truncate_jacobi(c, G, rows, cols, eps_abs, min_rank, refine, noise_scale);
+        }
+    }
+    BufPtr info = c.alloc(4);
+    launch_rank_rule(ts.lam->p, k, n, eps_abs, min_rank, nullptr, info->p, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+    double h[4];
+    c.fetch(info->p, 3, h);
+    Truncation t;
+    t.rank = static_cast<int64_t>(h[0]);
+    t.discarded = h[1];
+    const bool zero = h[2] == 0.0;
+    if (t.rank > 0) {
+        std::vector<double> l(static_cast<size_t>(t.rank));
+        c.fetch(ts.lam->p, t.rank, l.data());
+        t.sigma.resize(static_cast<size_t>(t.rank));
+        for (int64_t i = 0; i < t.rank; ++i)
+            t.sigma[static_cast<size_t>(i)] = zero ? 0.0 : std::sqrt(std::max(0.0, l[static_cast<size_t>(i)]));
+    }
+    t.u = c.tensor({rows, t.rank});
+    if (t.rank > 0) {
+        const double* Wp = ts.W->p;
+        const double* ip = info->p;
+        double* up = t.u.data();
+        launch_tridiag_vectors(&Wp, &ip, &n, &t.rank, &up, 1, c.s, &c.launches);
+        if (!zero) {  // CholeskyQR2 polish (as truncate_eig)
+            BufPtr oinfo = c.alloc(4);
+            BufPtr work = c.alloc(t.rank * t.rank + 16);
+            launch_orthonormalize_new(nullptr, rows, 0, t.u.data(), t.rank, oinfo->p, work->p, c.s, &c.launches);
+        }
+    }
+    HTR_CUDA(cudaGetLastError());
+    return t;
+}
+
 Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
                          const ProjectedGram& refine, double noise_scale) {
+    if (c.tridiag && tridiag_supported(rows)) {
+        TriSolve ts = tri_alloc(c, rows);
+        const double* gp = G.data();
+        double* lp = ts.lam->p;
+        double* wp = ts.W->p;
+        launch_tridiag_eigvals(&gp, &rows, &lp, &wp, 1, c.s, &c.launches);
+        HTR_CUDA(cudaGetLastError());
+        return finish_tri(c, ts, G, rows, cols, eps_abs, min_rank, refine, noise_scale);
+    }
+    return truncate_jacobi(c, G, rows, cols, eps_abs, min_rank, refine, noise_scale);
+}
+
+Truncation truncate_jacobi(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
+                           const ProjectedGram& refine, double noise_scale) {
     const int64_t n = rows;
     if (n > kJacobiMaxN)
         raise(HTR_ERR_RUNTIME, "truncation of a " + std::to_string(n) + "-row unfolding exceeds the device eigensolver's " +
@@ -859,7 +942,7 @@ std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vecto
         const bool column_side = !reduce && rows > kColumnSideRows && cols_local < rows;
         const bool posdef =
             !olds && any_basis_when_full && rows > 160 && rows <= cols_global[i] && rows <= kJacobiMaxN;
-        batch[i] = !column_side && !posdef && jacobi_batchable(rows);
+        batch[i] = !column_side && !posdef && (c.tridiag ? tridiag_supported(rows) : jacobi_batchable(rows));
         pdef[i] = !column_side && posdef;
         nb += batch[i];
         npd += pdef[i];
@@ -904,17 +987,30 @@ std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vecto
             noise.push_back(0.0);
         }
         lams.push_back(c.alloc(rows));
-        vs.push_back(c.alloc(rows * rows));
+        vs.push_back(c.tridiag ? nullptr : c.alloc(rows * rows));
         gp.push_back(grams.back().data());
         ns.push_back(rows);
         lp.push_back(lams.back()->p);
-        vp.push_back(vs.back()->p);
+        vp.push_back(vs.back() ? vs.back()->p : nullptr);
     }
-    launch_jacobi_eig_batch(gp.data(), ns.data(), lp.data(), vp.data(), nb, c.s, &c.launches);
+    std::vector<TriSolve> tris;
+    if (c.tridiag) {
+        std::vector<double*> wp;
+        for (size_t j = 0; j < ns.size(); ++j) {
+            tris.push_back(TriSolve{lams[j], c.alloc(tridiag_workspace_doubles(ns[j])), ns[j]});
+            wp.push_back(tris.back().W->p);
+        }
+        launch_tridiag_eigvals(gp.data(), ns.data(), lp.data(), wp.data(), nb, c.s, &c.launches);
+    } else {
+        launch_jacobi_eig_batch(gp.data(), ns.data(), lp.data(), vp.data(), nb, c.s, &c.launches);
+    }
     HTR_CUDA(cudaGetLastError());
     for (size_t i = 0, j = 0; i < modes.size(); ++i) {
         if (batch[i]) {
-            out[i] = truncate_eig(c, lams[j], vs[j], ns[j], cols_global[i], eps_abs, min_rank, refiners[j], noise[j]);
+            out[i] = c.tridiag ? finish_tri(c, tris[j], grams[j], ns[j], cols_global[i], eps_abs, min_rank,
+                                            refiners[j], noise[j])
+                               : truncate_eig(c, lams[j], vs[j], ns[j], cols_global[i], eps_abs, min_rank,
+                                              refiners[j], noise[j]);
             ++j;
         } else if (pdef[i]) {
             const int64_t rows = t.shape[static_cast<size_t>(modes[i])];

@@ -108,6 +108,7 @@ struct Context {
     bool fused = true;
     bool profile = false;
     int tail_kernel = 0;  // HTR_OPT_TAIL_KERNEL
+    bool tridiag = true;  // HTR_OPT_EIG_SOLVER: 1 tridiagonal + bisection (default), 0 Jacobi
     double* h_sc = nullptr;  // pinned scalars
     double* h_map = nullptr; // mapped pinned scalars written by kernels (64 doubles)
     double* d_map = nullptr; // its device address

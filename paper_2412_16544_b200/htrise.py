@@ -54,6 +54,7 @@ OPT_EXACT_LOSS = 1
 OPT_FUSED_ENCODE = 2
 OPT_PROFILE_EVENTS = 3
 OPT_TAIL_KERNEL = 4
+OPT_EIG_SOLVER = 5
 
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhtrise_cuda.so")
 

@@ -1,0 +1,117 @@
+"""The truncation eigensolvers (truncated_svd.hpp:53-100 on a Gram) against
+the oracle's LAPACK SVD: the default tridiagonal route (Householder
+reduction + multisection + inverse iteration, k_tridiag.cu) and the Jacobi
+route (HTR_OPT_EIG_SOLVER = 0) on the same inputs: identical ranks,
+discarded norms within 1e-10 ||M||, retained subspaces within 1e-8
+principal angle, orthonormal factors."""
+import numpy as np
+import pytest
+
+from oracle import htrise_oracle as ho
+from oracle import ref_oracles as ro
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ht():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2412_16544_b200 import htrise
+
+    htrise.set_default_context(htrise.Context(0))
+    return htrise
+
+
+def sin_angle(u, v):
+    if u.shape[1] == 0 and v.shape[1] == 0:
+        return 0.0
+    return float(np.linalg.norm(v - u @ (u.T @ v), 2))
+
+
+def _check(ht, m, eps, min_rank=1):
+    b = ho.truncated_svd(m, eps, min_rank)
+    out = []
+    for solver in (1, 0):
+        ctx = ht.default_context()
+        ctx.set_option(ht.OPT_EIG_SOLVER, solver)
+        try:
+            a = ht.truncated_svd(m, eps, min_rank)
+        finally:
+            ctx.set_option(ht.OPT_EIG_SOLVER, 1)
+        assert a.rank == b.rank, (solver, m.shape, a.rank, b.rank)
+        assert abs(a.discarded_norm - b.discarded_norm) <= 1e-10 * max(np.linalg.norm(m), 1e-300)
+        assert np.max(np.abs(a.u.T @ a.u - np.eye(a.rank)), initial=0.0) <= 1e-12
+        out.append(a)
+    return out, b
+
+
+@pytest.mark.parametrize("rows", [1, 2, 3, 7, 16, 33, 64, 100, 128, 144, 160, 161, 250, 400])
+def test_random_spectra(ht, rows):
+    rng = np.random.default_rng(4000 + rows)
+    cols = 3 * rows + 5
+    k = min(rows, 24)
+    u = ro.random_orthonormal(rows, k, rng)
+    m = u @ np.diag(np.logspace(0, -4, k)) @ rng.standard_normal((k, cols))
+    m += 1e-7 * rng.standard_normal(m.shape)
+    for frac in (1e-5, 1e-3, 0.05, 0.5):
+        eps = frac * np.linalg.norm(m)
+        (a, _), b = _check(ht, m, eps)
+        assert sin_angle(b.u, a.u) <= 1e-8, (rows, frac, sin_angle(b.u, a.u))
+
+
+def test_clustered_and_repeated_singular_values(ht):
+    """Tight clusters (inverse iteration re-orthogonalises within them) and
+    exactly repeated singular values: the retained subspace is determined
+    whenever the cut falls between clusters."""
+    rng = np.random.default_rng(77)
+    n, cols = 96, 500
+    sig = np.concatenate([np.full(10, 5.0), 3.0 + 1e-9 * np.arange(12), np.full(20, 1.0), 1e-6 * np.ones(54)])
+    u = ro.random_orthonormal(n, n, rng)
+    v = ro.random_orthonormal(cols, n, rng)
+    m = u @ np.diag(sig) @ v.T
+    for eps_sq_tail in (sig[10:] ** 2, sig[22:] ** 2, sig[42:] ** 2):
+        eps = float(np.sqrt(np.sum(eps_sq_tail))) * 1.0001
+        (a, _), b = _check(ht, m, eps)
+        assert sin_angle(b.u, a.u) <= 1e-8
+
+
+def test_full_rank_and_zero_and_kats(ht):
+    rng = np.random.default_rng(5)
+    m = rng.standard_normal((40, 200))
+    (a, _), b = _check(ht, m, 0.0)  # keeps every direction
+    assert a.rank == 40
+    (a, _), b = _check(ht, np.diag([4.0, 3.0]), 3.0)
+    assert a.rank == 1 and abs(abs(a.u[0, 0]) - 1) <= 1e-12
+    (a, _), b = _check(ht, np.zeros((5, 9)), 0.1)
+    assert a.rank == 1 and np.array_equal(a.u[:, 0], [1.0, 0, 0, 0, 0])
+    (a, _), b = _check(ht, np.zeros((5, 9)), 0.1, min_rank=0)
+    assert a.rank == 0
+    # rank one, huge and tiny scales (power-of-two scaling inside the solver)
+    x = rng.standard_normal((30, 1)) @ rng.standard_normal((1, 70))
+    for s in (1e-150, 1.0, 1e140):
+        (a, _), b = _check(ht, s * x, 1e-3 * s * np.linalg.norm(x))
+        assert a.rank == 1 and sin_angle(b.u, a.u) <= 1e-10
+
+
+def test_tridiagonal_is_the_default_and_faster(ht):
+    """The default solver is the tridiagonal route; on a 128-row Gram (a c5
+    leaf) it beats the Jacobi route (wall clock of the whole truncation)."""
+    import time
+
+    rng = np.random.default_rng(9)
+    m = ro.random_orthonormal(128, 20, rng) @ rng.standard_normal((20, 4000))
+    m += 1e-6 * rng.standard_normal(m.shape)
+    eps = 1e-3 * np.linalg.norm(m)
+    ctx = ht.default_context()
+    times = {}
+    for solver in (1, 0):
+        ctx.set_option(ht.OPT_EIG_SOLVER, solver)
+        ht.truncated_svd(m, eps)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            ht.truncated_svd(m, eps)
+        times[solver] = (time.perf_counter() - t0) / 3
+    ctx.set_option(ht.OPT_EIG_SOLVER, 1)
+    assert times[1] < times[0], times
