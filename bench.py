@@ -104,40 +104,81 @@ def _dist_env():
     return world, rank, local
 
 
-def cpu_baseline(seconds_budget: float = 12.0):
-    """The oracle port (numpy restatement of ht_rise.hpp) timed on host cores
-    on a bounded sample of the same workload: skip-path updates of 128^3
-    slices drawn from config 5's generator."""
+def _host_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                info["lscpu_model"] = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return info
+
+
+def _c5_host_batch(w, b, n):
+    """Batch b of config 5 (n samples) in host memory, canonical order: the
+    device generator's bytes when a GPU is present (the same bytes the GPU
+    arm streams), else the same generator on the CPU."""
     import numpy as np
     import torch
+
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    y = w.make_batch(b, dev, batch=n).cpu().numpy()
+    return np.asfortranarray(y.reshape((n,) + tuple(reversed(w.dims))).transpose(3, 2, 1, 0))
+
+
+def cpu_reference(steps: int, warmup: int, budget_s: float, all_cores: bool = True):
+    """The reference's algorithm on the host: the oracle port (numpy
+    restatement of ht_rise.hpp:99-186, op for op; the reference itself needs
+    Eigen, absent here) timing FULL config-5 updates (256 samples, 4.295 GB,
+    the same workload as the GPU step) with ONE thread, as the reference runs
+    (no OpenMP/threads, CMakeLists.txt:1-20; OPENBLAS limited to 1 through
+    threadpoolctl), the way the reference times them (UpdateReport.seconds,
+    ht_rise.hpp:102-121). The stream is seeded untimed by the oracle's
+    BHT-l2r on a 32-sample batch (ranks 20/20/20/400, as at 256). At most
+    `steps` timed updates, fewer when the `budget_s` wall-clock budget runs
+    out (at least one). Optionally one more update with every host thread,
+    reported separately."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
 
     from oracle import htrise_oracle as ho
     from paper_2412_16544_b200.workloads import CONFIGS
 
     w = CONFIGS["c5"]
-    n = 4  # samples per oracle batch (bounded sample; 4 x 16.8 MB)
-    y0 = w.make_batch(0, "cpu", batch=n).numpy().reshape((n, 128, 128, 128)).transpose(3, 2, 1, 0)
-    y1 = w.make_batch(1, "cpu", batch=n).numpy().reshape((n, 128, 128, 128)).transpose(3, 2, 1, 0)
-    tree = ho.custom_tree_1_23()
-    rep, _ = ho.bht_l2r(np.asfortranarray(y0), tree, w.eps)
-    y1 = np.asfortranarray(y1)
-    t0 = time.perf_counter()
-    reps = 0
-    while True:
-        _, upd = ho.ht_rise_update(rep, y1)
-        reps += 1
-        if time.perf_counter() - t0 > seconds_budget:
-            break
-    dt = time.perf_counter() - t0
-    threads = torch.get_num_threads()
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=threads)
-    except Exception:
-        pass
-    return {"value": 8.0 * y1.size * reps / dt / 1e9, "unit": UNIT, "cores": int(threads), "kind": "port",
-            "sample": f"{reps} oracle ht_rise_update calls on 128^3 x {n} slices of config 5 "
-                      f"(skip path, numpy/OpenBLAS), {dt:.1f} s"}
+    t_seed = time.perf_counter()
+    rep, _ = ho.bht_l2r(_c5_host_batch(w, 0, 32), ho.custom_tree_1_23(), w.eps)
+    t_seed = time.perf_counter() - t_seed
+    y = _c5_host_batch(w, 1, w.batch)
+    nbytes = 8.0 * y.size
+    t_start = time.perf_counter()
+    times = []
+    skipped = 0
+    with threadpool_limits(1):
+        for _ in range(min(warmup, 1)):
+            ho.ht_rise_update(rep, y)
+        while len(times) < max(1, steps):
+            _, upd = ho.ht_rise_update(rep, y)
+            times.append(upd.seconds)
+            skipped += int(upd.skipped)
+            if time.perf_counter() - t_start + times[-1] > budget_s:
+                break
+    mean = sum(times) / len(times)
+    out = {"value": nbytes / mean / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
+           "seconds_per_update": mean, "updates_timed": len(times), "skipped": skipped,
+           "sample": f"{len(times)} full config-5 ht_rise_update calls (256 x 128^3 f64, 4.295 GB each, skip path) "
+                     f"of the oracle port, 1 thread, UpdateReport.seconds; stream seeded untimed by BHT-l2r on "
+                     f"32 samples ({t_seed:.0f} s)",
+           "host": _host_info()}
+    if all_cores:
+        with threadpool_limits(os.cpu_count()):
+            _, upd = ho.ht_rise_update(rep, y)
+        out["all_cores"] = {"value": nbytes / upd.seconds / 1e9, "unit": UNIT, "cores": os.cpu_count(),
+                            "seconds_per_update": upd.seconds,
+                            "sample": "1 full config-5 update, OpenBLAS on every host thread (numpy's "
+                                      "elementwise passes stay single-threaded)"}
+    return out
 
 
 def run_reference(args):
@@ -145,14 +186,14 @@ def run_reference(args):
     if rank != 0:
         return 0
     from paper_2412_16544_b200.workloads import CONFIGS
-    cb = cpu_baseline(seconds_budget=max(5.0, 4.0 * max(1, args.steps)))
-    steps_ms = 8.0 * 128 ** 3 * 256 / (cb["value"] * 1e9) * 1e3
+    cb = cpu_reference(args.steps, args.warmup, budget_s=args.ref_budget)
+    steps_ms = cb["seconds_per_update"] * 1e3
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": steps_ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "steps": cb["updates_timed"], "warmup": min(args.warmup, 1), "ms_per_step": steps_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"c5: {CONFIGS['c5'].description}", "batch_bytes": 8 * 128 ** 3 * 256,
-                       "samples_per_gpu": 256, "parallelism": "host threads (numpy/OpenBLAS)",
-                       "sample": "bounded CPU sample of the same workload (see cpu_baseline.sample)"},
+                       "samples_per_gpu": 256, "parallelism": "1 host thread (the reference is single-threaded)",
+                       "sample": "full 256-sample updates, count bounded by the time budget (cpu_baseline.sample)"},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -167,6 +208,8 @@ def run_ours(args):
     from paper_2412_16544_b200.workloads import CONFIGS
 
     world, rank, local = _dist_env()
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPUs")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -380,7 +423,7 @@ def run_ours(args):
     if rank == 0:
         cb = None
         if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_baseline(seconds_budget=args.cpu_seconds)
+            cb = cpu_reference(1, 0, budget_s=args.cpu_seconds)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -410,9 +453,23 @@ def main():
     ap.add_argument("--pool", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--decode-steps", type=int, default=3)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=30.0)
+    ap.add_argument("--ref-budget", type=float, default=150.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.impl == "ours" and args.gpus > 1 and env_world is None:
+        # one process per GPU: launch ourselves under torchrun
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
+    if env_world is not None and int(env_world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -543,6 +543,93 @@ __global__ void __launch_bounds__(1024) posdef_kernel(const double* __restrict__
 }
 
 // --------------------------------------------------------------------------
+// Blocked form of the same test (panels of 32 columns; the runtime runs the
+// trailing updates A22 -= P P^T on the DMMA GEMM engine between panels).
+// --------------------------------------------------------------------------
+constexpr int kCholB = 32;
+
+__global__ void chol_prepare_kernel(const double* __restrict__ G, int n, double shift, double* __restrict__ A,
+                                    double* __restrict__ flag) {
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nn;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = e % n, c = e / n;
+        A[e] = G[e] - (r == c ? shift : 0.0);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) flag[0] = 1.0;
+}
+
+/// Columns [kb, kb + b) of rows [kb, n): the b x b diagonal block by one
+/// warp (lane i owns row i; no block barrier per column), the rows below by
+/// forward substitution against it, one row per thread (b = 32 there: only
+/// the last panel is narrower, and it has no rows below). A non-positive
+/// pivot clears flag[0]; later panels then return at once.
+__global__ void __launch_bounds__(256, 1) chol_panel_kernel(double* __restrict__ A, int n, int kb, int b,
+                                                         double* __restrict__ flag) {
+    __shared__ double D[kCholB][kCholB + 1];
+    __shared__ int ok;
+    if (flag[0] != 1.0) return;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < b * b; e += nt) {
+        const int i = e % b, j = e / b;
+        D[i][j] = i >= j ? A[(kb + i) + static_cast<int64_t>(n) * (kb + j)] : 0.0;
+    }
+    if (tid == 0) ok = 1;
+    __syncthreads();
+    if (tid < 32) {
+        const int lane = tid;
+        for (int k = 0; k < b; ++k) {
+            const double piv = D[k][k];
+            if (!(piv > 0.0)) {  // the same value in every lane
+                if (lane == 0) ok = 0;
+                break;
+            }
+            const double lkk = sqrt(piv);
+            __syncwarp();
+            if (lane == k) D[k][k] = lkk;
+            if (lane > k && lane < b) D[lane][k] /= lkk;
+            __syncwarp();
+            if (lane > k && lane < b) {
+                const double lik = D[lane][k];
+                for (int j = k + 1; j <= lane; ++j) D[lane][j] -= lik * D[j][k];
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    if (!ok) {
+        if (tid == 0) flag[0] = 0.0;
+        return;
+    }
+    for (int e = tid; e < b * b; e += nt) {
+        const int i = e % b, j = e / b;
+        if (i >= j) A[(kb + i) + static_cast<int64_t>(n) * (kb + j)] = D[i][j];
+    }
+    if (b != kCholB) return;
+    // (volatile: the factor is re-read from shared memory per row instead of
+    // being hoisted into 528 registers)
+    volatile double(*Dv)[kCholB + 1] = D;
+    __shared__ double Dinv[kCholB];
+    if (tid < kCholB) Dinv[tid] = 1.0 / D[tid][tid];
+    __syncthreads();
+    volatile double* Di = Dinv;
+    for (int r = kb + kCholB + tid; r < n; r += nt) {
+        double x[kCholB];
+#pragma unroll
+        for (int j = 0; j < kCholB; ++j) x[j] = A[r + static_cast<int64_t>(n) * (kb + j)];
+#pragma unroll
+        for (int j = 0; j < kCholB; ++j) {
+            double v = x[j];
+#pragma unroll
+            for (int l = 0; l < j; ++l) v = fma(-Dv[j][l], x[l], v);
+            x[j] = v * Di[j];
+        }
+#pragma unroll
+        for (int j = 0; j < kCholB; ++j) A[r + static_cast<int64_t>(n) * (kb + j)] = x[j];
+    }
+}
+
+// --------------------------------------------------------------------------
 // Re-orthonormalisation of new directions (expand_core, ht_rise.hpp:53-79):
 // W <- (I - U U^T) W twice, then CholeskyQR2. One CTA; all sizes small.
 // --------------------------------------------------------------------------
@@ -596,6 +683,63 @@ __device__ void block_cholqr(int64_t alpha, double* W, int64_t q, double* Gm) {
         }
     }
     __syncthreads();
+}
+
+/// CholeskyQR2 of W (alpha x q, q <= 32) staged in shared memory: the Gram
+/// by warps (lanes over rows, shuffle sums), its Cholesky by one warp (lane
+/// = row, no block barrier per column), W L^{-T} by forward substitution
+/// one row per thread. The polish of every truncation's retained basis.
+constexpr int kQrMaxQ = 32;
+__global__ void __launch_bounds__(512) cholqr2_smem_kernel(double* __restrict__ Wg, int alpha, int q,
+                                                           double* __restrict__ info) {
+    extern __shared__ double Ws[];  // alpha x q, column-major
+    __shared__ double L[kQrMaxQ][kQrMaxQ + 1];
+    __shared__ double Linv[kQrMaxQ];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    const int n = alpha * q;
+    for (int e = tid; e < n; e += nt) Ws[e] = Wg[e];
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int ab = warp; ab < q * q; ab += nw) {
+            const int a = ab % q, b = ab / q;
+            if (a < b) continue;
+            const double* wa = Ws + alpha * a;
+            const double* wb = Ws + alpha * b;
+            double s = 0.0;
+            for (int i = lane; i < alpha; i += 32) s = fma(wa[i], wb[i], s);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) L[a][b] = s;
+        }
+        __syncthreads();
+        if (warp == 0) {  // in-place lower Cholesky, lane = row
+            for (int k = 0; k < q; ++k) {
+                const double dkk = sqrt(fmax(L[k][k], 1e-300));
+                __syncwarp();
+                if (lane == k) { L[k][k] = dkk; Linv[k] = 1.0 / dkk; }
+                if (lane > k && lane < q) L[lane][k] /= dkk;
+                __syncwarp();
+                if (lane > k && lane < q) {
+                    const double lik = L[lane][k];
+                    for (int j = k + 1; j <= lane; ++j) L[lane][j] -= lik * L[j][k];
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < alpha; i += nt)
+            for (int j = 0; j < q; ++j) {
+                double v = Ws[i + alpha * j];
+                for (int k = 0; k < j; ++k) v = fma(-L[j][k], Ws[i + alpha * k], v);
+                Ws[i + alpha * j] = v * Linv[j];
+            }
+        __syncthreads();
+    }
+    for (int e = tid; e < n; e += nt) Wg[e] = Ws[e];
+    if (tid == 0 && info) {  // no old basis: defect 0, ||W||_F of an orthonormal W
+        info[0] = 0.0;
+        info[1] = sqrt(static_cast<double>(q));
+    }
 }
 
 __global__ void __launch_bounds__(512) orthonormalize_kernel(const double* U, int64_t alpha, int64_t r, double* W,
@@ -703,8 +847,29 @@ void launch_posdef_test(const double* G, int64_t n, double shift, double* work, 
     ++*launches;
 }
 
+void launch_chol_prepare(const double* G, int64_t n, double shift, double* A, double* flag, cudaStream_t s,
+                         int64_t* launches) {
+    const int64_t nn = n * n;
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(296, (nn + 255) / 256)));
+    chol_prepare_kernel<<<blocks, 256, 0, s>>>(G, static_cast<int>(n), shift, A, flag);
+    ++*launches;
+}
+
+void launch_chol_panel(double* A, int64_t n, int64_t kb, int64_t b, double* flag, cudaStream_t s, int64_t* launches) {
+    chol_panel_kernel<<<1, 256, 0, s>>>(A, static_cast<int>(n), static_cast<int>(kb), static_cast<int>(b), flag);
+    ++*launches;
+}
+
 void launch_orthonormalize_new(const double* U, int64_t alpha, int64_t r, double* W, int64_t q, double* info,
                                double* work, cudaStream_t s, int64_t* launches) {
+    if (r == 0 && q >= 1 && q <= kQrMaxQ && alpha * q <= 16384) {
+        // the polish of a fresh basis (no old columns): shared-memory CholeskyQR2
+        const size_t smem = sizeof(double) * static_cast<size_t>(alpha * q);
+        ensure_smem_limit(reinterpret_cast<const void*>(cholqr2_smem_kernel), smem);
+        cholqr2_smem_kernel<<<1, 512, smem, s>>>(W, static_cast<int>(alpha), static_cast<int>(q), info);
+        ++*launches;
+        return;
+    }
     orthonormalize_kernel<<<1, 512, 0, s>>>(U, alpha, r, W, q, info, work);
     ++*launches;
 }

@@ -236,6 +236,87 @@ __global__ void gram_small_finish_kernel(const double* __restrict__ partials, in
     }
 }
 
+// Gram of a mode with 9..32 rows (c1's 16-row leaves, c3's 32-row mode 0,
+// any mode incl. 0): Y viewed as [K, M, B], columns (k, b) taken 4 at a
+// time as the k dimension of m8n8k4 DMMAs. Lane (g, t) loads rows 8 mt + g
+// of column 4 q + t once; that value is both the A fragment of row tile mt
+// and the B fragment of column tile mt, so the lower-triangle blocks
+// (mt >= nt) accumulate in registers. Per-CTA partials in a fixed order,
+// then gram_small_finish_kernel.
+constexpr int kMidWarps = 8;
+
+template <int MT>
+__global__ void __launch_bounds__(kMidWarps * 32) gram_mid_kernel(const double* __restrict__ Y, uint32_t K,
+                                                                  uint32_t M, uint32_t units4, uint32_t units,
+                                                                  double* __restrict__ partials) {
+    constexpr int NB = MT * (MT + 1) / 2;
+    double acc[NB][2];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+    const uint32_t gw = blockIdx.x * kMidWarps + warp, nw = gridDim.x * kMidWarps;
+    for (uint32_t q = gw; q < units4; q += nw) {
+        const uint32_t u = 4 * q + t;  // column (k, b) = (u % K, u / K)
+        double a[MT];
+        if (u < units) {
+            const uint32_t bb = u / K, k = u - bb * K;
+            const double* col = Y + k + static_cast<uint64_t>(K) * M * bb;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const uint32_t m = 8 * mt + g;
+                a[mt] = m < M ? __ldg(col + static_cast<uint64_t>(K) * m) : 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) a[mt] = 0.0;
+        }
+        int b = 0;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt <= mt; ++nt, ++b) dmma(acc[b], a[mt], a[nt]);
+    }
+    // lower triangle (i >= j) of the M x M Gram, enumerated column by column
+    // as in gram_small (entry e of column j, row i)
+    __shared__ double red[kMidWarps][32 * 33 / 2];
+    const int L = static_cast<int>(M * (M + 1) / 2);
+    for (int e = lane; e < L; e += 32) red[warp][e] = 0.0;
+    __syncwarp();
+    int b = 0;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt <= mt; ++nt, ++b)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = 8 * mt + g, j = 8 * nt + 2 * t + h;
+                if (i < static_cast<int>(M) && j <= i) {
+                    const int e = j * static_cast<int>(M) - (j * (j - 1)) / 2 + (i - j);
+                    red[warp][e] = acc[b][h];
+                }
+            }
+    __syncthreads();
+    for (int e = threadIdx.x; e < L; e += kMidWarps * 32) {
+        double v = 0.0;
+        for (int w = 0; w < kMidWarps; ++w) v += red[w][e];
+        partials[static_cast<int64_t>(blockIdx.x) * L + e] = v;
+    }
+}
+
+template <int MT>
+int launch_mid_mt(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,
+                  cudaStream_t s) {
+    const int64_t units = K * B, units4 = (units + 3) / 4;
+    const int grid = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(2 * num_sms, (units4 + kMidWarps - 1) / kMidWarps)));
+    gram_mid_kernel<MT><<<grid, kMidWarps * 32, 0, s>>>(Y, static_cast<uint32_t>(K), static_cast<uint32_t>(M),
+                                                       static_cast<uint32_t>(units4), static_cast<uint32_t>(units),
+                                                       partials);
+    gram_small_finish_kernel<<<static_cast<unsigned>(M * (M + 1) / 2), 32, 0, s>>>(partials, grid,
+                                                                                   static_cast<int>(M), G);
+    return grid;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -281,6 +362,25 @@ bool gram_small_supported(int64_t K, int64_t M, int64_t B) {
 }
 
 int64_t gram_small_partials(int num_sms) { return static_cast<int64_t>(4 * num_sms) * 36; }
+
+bool gram_mid_supported(int64_t K, int64_t M, int64_t B) {
+    return M >= 9 && M <= 32 && K >= 1 && B >= 1 && K * B < (int64_t{1} << 31) - 8 && K * M * B < (int64_t{1} << 40);
+}
+
+int64_t gram_mid_partials(int num_sms) { return static_cast<int64_t>(2 * num_sms) * (32 * 33 / 2); }
+
+int launch_gram_mid(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,
+                    cudaStream_t s, int64_t* launches) {
+    if (!gram_mid_supported(K, M, B)) return -1;
+    int grid;
+    switch ((M + 7) / 8) {
+        case 2: grid = launch_mid_mt<2>(Y, K, M, B, partials, G, num_sms, s); break;
+        case 3: grid = launch_mid_mt<3>(Y, K, M, B, partials, G, num_sms, s); break;
+        default: grid = launch_mid_mt<4>(Y, K, M, B, partials, G, num_sms, s); break;
+    }
+    *launches += 2;
+    return grid;
+}
 
 int launch_gram_small(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,
                       cudaStream_t s, int64_t* launches) {

@@ -292,11 +292,29 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
         if (!last) return;
         __threadfence();
         // last CTA: ||y||^2 from the first launch's partials and ||latent||^2
-        // from this launch's, both in index order
+        // from this launch's: loads in parallel, a fixed reduction tree
+        // (lane-strided sums, shuffle tree, warps in order)
+        double y2 = 0.0, l2 = 0.0;
+        for (int64_t k = tid; k < a.n_ysq; k += kQ2Threads) y2 += __ldcg(a.ysq_partials + k);
+        for (unsigned k = tid; k < gridDim.x; k += kQ2Threads) l2 += __ldcg(a.partials + k);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            y2 += __shfl_xor_sync(0xffffffffu, y2, off);
+            l2 += __shfl_xor_sync(0xffffffffu, l2, off);
+        }
+        __shared__ double red2[2][kQ2Warps];
+        if (lane == 0) {
+            red2[0][warp] = y2;
+            red2[1][warp] = l2;
+        }
+        __syncthreads();
         if (tid == 0) {
-            double y2 = 0.0, l2 = 0.0;
-            for (int64_t k = 0; k < a.n_ysq; ++k) y2 += __ldcg(a.ysq_partials + k);
-            for (unsigned k = 0; k < gridDim.x; ++k) l2 += __ldcg(a.partials + k);
+            y2 = 0.0;
+            l2 = 0.0;
+            for (int w = 0; w < kQ2Warps; ++w) {
+                y2 += red2[0][w];
+                l2 += red2[1][w];
+            }
             a.sc[0] = y2;
             a.sc[2] = l2;
             if (a.host_out) {

@@ -102,23 +102,34 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
     return c;
 }
 
-__global__ void __launch_bounds__(kTriThreads) tridiag_eigvals_kernel(const TriJobs jobs, int use_smem) {
+/// Householder reduction Q^T G Q = T (dsytd2, lower) of one Gram per CTA.
+/// Three block barriers per column: the reflector is formed from the
+/// column's norm (accumulated by the previous column's update), the
+/// matrix-vector product p = tau A22 v also accumulates p . v per warp, and
+/// the rank-2 update A22 -= v w^T + w v^T (w = p - K v formed on the fly)
+/// also accumulates the next column's norm. Writes d, e, tau, the
+/// reflectors (below the subdiagonal of the workspace matrix) and the scale.
+/// T > 0: every row of the trailing matrix is held by one lane as
+/// i = lane + 32 t, t < T (n <= 32 T + 1), with v and w in registers; T = 0:
+/// strided loops (the global-memory path, larger n).
+template <int T>
+__global__ void __launch_bounds__(kTriThreads) tridiag_reduce_kernel(const __grid_constant__ TriJobs jobs,
+                                                                     int use_smem) {
     const int n = jobs.n[blockIdx.x];
     const double* __restrict__ G = jobs.G[blockIdx.x];
     double* __restrict__ W = jobs.W[blockIdx.x];
-    double* __restrict__ lam_out = jobs.lam[blockIdx.x];
     extern __shared__ double smem[];
     __shared__ double red[32];
+    __shared__ double pdp[32];
+    __shared__ double xn2_next;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     const int64_t nn = static_cast<int64_t>(n) * n;
     double* A = use_smem ? smem : W;
-    double* vv = use_smem ? smem + nn : W + tri_off_d(n) + 5 * n + 1;  // 3 vectors of n
+    double* vv = use_smem ? smem + nn : W + tri_off_d(n) + 5 * n + 1;  // 2 vectors of n
     double* pw = vv + n;
-    double* ww = pw + n;
     double* dg = W + tri_off_d(n);
     double* eg = dg + n;
     double* taug = eg + n;
-    double* lam_asc = taug + n;
 
     // exact power-of-two scaling to max |G| ~ 1 (no overflow in the norms)
     double gm = 0.0;
@@ -127,20 +138,18 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_eigvals_kernel(const TriJ
     int ex = 0;
     if (gm > 0.0 && gm <= DBL_MAX) frexp(gm, &ex);
     const double sc = ldexp(1.0, -ex), unsc = ldexp(1.0, ex);
-    for (int64_t i = tid; i < nn; i += nt) {
-        const int64_t r = i % n, c = i / n;
-        A[i] = 0.5 * (G[r + n * c] + G[c + n * r]) * sc;
-    }
+    for (int c = 0; c < n; ++c)
+        for (int r = tid; r < n; r += nt) A[r + static_cast<int64_t>(n) * c] = 0.5 * (G[r + static_cast<int64_t>(n) * c] + G[c + static_cast<int64_t>(n) * r]) * sc;
     __syncthreads();
-
-    // Householder reduction to tridiagonal form (dsytd2, lower): step k
-    // annihilates A[k+2:, k] with H_k = I - tau v v^T acting on rows k+1..
+    double xn2 = 0.0;
+    if (n > 2) {
+        double ps = 0.0;
+        for (int i = 2 + tid; i < n; i += nt) ps = fma(A[i], A[i], ps);
+        xn2 = block_sum(ps, red);
+    }
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1;
         double* x = A + (k + 1) + static_cast<int64_t>(n) * k;
-        double ps = 0.0;
-        for (int i = 1 + tid; i < m; i += nt) ps = fma(x[i], x[i], ps);
-        const double xn2 = block_sum(ps, red);
         const double alpha = x[0];
         double tau = 0.0, beta = alpha, scale = 0.0;
         if (xn2 > 0.0) {
@@ -158,29 +167,86 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_eigvals_kernel(const TriJ
             taug[k] = tau;
         }
         __syncthreads();
-        if (tau == 0.0) continue;
         double* A22 = A + (k + 1) + static_cast<int64_t>(n) * (k + 1);
-        // p = tau A22 v (A22 symmetric: column j dotted with v)
-        for (int j = warp; j < m; j += nw) {
-            const double* col = A22 + static_cast<int64_t>(n) * j;
-            double s = 0.0;
-            for (int i = lane; i < m; i += 32) s = fma(col[i], vv[i], s);
-            s = warp_sum(s);
-            if (lane == 0) pw[j] = tau * s;
+        if (tau == 0.0) {
+            // nothing to update; the next column's norm directly
+            double ps = 0.0;
+            for (int i = 2 + tid; i < m; i += nt) ps = fma(A22[i], A22[i], ps);
+            xn2 = block_sum(ps, red);
+            continue;
+        }
+        // p = tau A22 v (column j dotted with v), and p . v per warp
+        double pdw = 0.0;
+        if constexpr (T > 0) {
+            double vr[T];
+#pragma unroll
+            for (int t = 0; t < T; ++t) vr[t] = lane + 32 * t < m ? vv[lane + 32 * t] : 0.0;
+            for (int j = warp; j < m; j += nw) {
+                const double* col = A22 + static_cast<int64_t>(n) * j;
+                double s = 0.0;
+#pragma unroll
+                for (int t = 0; t < T; ++t)
+                    if (lane + 32 * t < m) s = fma(col[lane + 32 * t], vr[t], s);
+                s = tau * warp_sum(s);
+                if (lane == 0) pw[j] = s;
+                pdw = fma(s, vv[j], pdw);
+            }
+            if (lane == 0) pdp[warp] = pdw;
+            __syncthreads();
+            const double K = 0.5 * tau * warp_sum(lane < nw ? pdp[lane] : 0.0);
+            double wr[T];
+#pragma unroll
+            for (int t = 0; t < T; ++t) wr[t] = lane + 32 * t < m ? fma(-K, vr[t], pw[lane + 32 * t]) : 0.0;
+            // A22 -= v w^T + w v^T with w = p - K v; the warp holding column 0
+            // (the next column to reduce) also sums its rows >= 2 squared
+            for (int j = warp; j < m; j += nw) {
+                double* col = A22 + static_cast<int64_t>(n) * j;
+                const double vj = vv[j], wj = fma(-K, vj, pw[j]);
+                double s = 0.0;
+#pragma unroll
+                for (int t = 0; t < T; ++t) {
+                    const int i = lane + 32 * t;
+                    if (i < m) {
+                        const double a = col[i] - fma(vr[t], wj, wr[t] * vj);
+                        col[i] = a;
+                        if (i >= 2) s = fma(a, a, s);
+                    }
+                }
+                if (j == 0) {
+                    s = warp_sum(s);
+                    if (lane == 0) xn2_next = s;
+                }
+            }
+        } else {
+            for (int j = warp; j < m; j += nw) {
+                const double* col = A22 + static_cast<int64_t>(n) * j;
+                double s = 0.0;
+                for (int i = lane; i < m; i += 32) s = fma(col[i], vv[i], s);
+                s = tau * warp_sum(s);
+                if (lane == 0) pw[j] = s;
+                pdw = fma(s, vv[j], pdw);
+            }
+            if (lane == 0) pdp[warp] = pdw;
+            __syncthreads();
+            const double K = 0.5 * tau * warp_sum(lane < nw ? pdp[lane] : 0.0);
+            for (int j = warp; j < m; j += nw) {
+                double* col = A22 + static_cast<int64_t>(n) * j;
+                const double vj = vv[j], wj = fma(-K, vj, pw[j]);
+                double s = 0.0;
+                for (int i = lane; i < m; i += 32) {
+                    const double wi = fma(-K, vv[i], pw[i]);
+                    const double a = col[i] - fma(vv[i], wj, wi * vj);
+                    col[i] = a;
+                    if (j == 0 && i >= 2) s = fma(a, a, s);
+                }
+                if (j == 0) {
+                    s = warp_sum(s);
+                    if (lane == 0) xn2_next = s;
+                }
+            }
         }
         __syncthreads();
-        double pd = 0.0;
-        for (int i = tid; i < m; i += nt) pd = fma(pw[i], vv[i], pd);
-        const double K = 0.5 * tau * block_sum(pd, red);
-        for (int i = tid; i < m; i += nt) ww[i] = pw[i] - K * vv[i];
-        __syncthreads();
-        // A22 -= v w^T + w v^T (both triangles)
-        for (int j = warp; j < m; j += nw) {
-            double* col = A22 + static_cast<int64_t>(n) * j;
-            const double vj = vv[j], wj = ww[j];
-            for (int i = lane; i < m; i += 32) col[i] -= fma(vv[i], wj, ww[i] * vj);
-        }
-        __syncthreads();
+        xn2 = xn2_next;
     }
     // T: diagonal and subdiagonal; reflectors to the workspace
     for (int i = tid; i < n; i += nt) {
@@ -189,62 +255,66 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_eigvals_kernel(const TriJ
         if (i + 2 >= n) taug[i] = 0.0;
     }
     if (use_smem)
-        for (int64_t i = tid; i < nn; i += nt) {
-            const int64_t r = i % n, c = i / n;
-            if (r >= c + 2) W[i] = A[i];
-        }
-    __syncthreads();
+        for (int c = 0; c + 2 < n; ++c)
+            for (int r = c + 2 + tid; r < n; r += nt) W[r + static_cast<int64_t>(n) * c] = A[r + static_cast<int64_t>(n) * c];
+    if (tid == 0) W[tri_off_d(n) + 4 * n] = unsc;
+}
 
-    // eigenvalues of T: multisection, 8 lanes (8 points) per eigenvalue
+/// Every eigenvalue of T by multisection on Sturm counts: one warp per
+/// eigenvalue (32 points per step, 5 bits), 4 warps per CTA, CTAs of all
+/// jobs side by side (grid.y = job). Absolute accuracy ~4 u ||T||.
+constexpr int kBisWarps = 4;
+__global__ void __launch_bounds__(kBisWarps * 32) tridiag_bisect_kernel(const __grid_constant__ TriJobs jobs) {
+    const int job = blockIdx.y;
+    const int n = jobs.n[job];
+    const int j = blockIdx.x * kBisWarps + (threadIdx.x >> 5);
+    if (blockIdx.x * kBisWarps >= n) return;
+    const double* __restrict__ W = jobs.W[job];
+    double* __restrict__ lam_out = jobs.lam[job];
     __shared__ double d[1024], e2[1024];  // n <= 1024 (tridiag_supported)
-    for (int i = tid; i < n; i += nt) {
-        d[i] = dg[i];
-        e2[i] = eg[i] * eg[i];
-    }
-    __syncthreads();
+    __shared__ double red[32];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    const double* dg = W + tri_off_d(n);
+    const double* eg = dg + n;
+    const double unsc = W[tri_off_d(n) + 4 * n];
     double lo_g = DBL_MAX, hi_g = -DBL_MAX, emax = 0.0;
     for (int i = tid; i < n; i += nt) {
-        const double r = (i > 0 ? fabs(eg[i - 1]) : 0.0) + (i + 1 < n ? fabs(eg[i]) : 0.0);
-        lo_g = fmin(lo_g, d[i] - r);
-        hi_g = fmax(hi_g, d[i] + r);
-        emax = fmax(emax, e2[i]);
+        const double di = dg[i], ei = i + 1 < n ? eg[i] : 0.0, em = i > 0 ? eg[i - 1] : 0.0;
+        d[i] = di;
+        e2[i] = ei * ei;
+        const double r = fabs(em) + fabs(ei);
+        lo_g = fmin(lo_g, di - r);
+        hi_g = fmax(hi_g, di + r);
+        emax = fmax(emax, ei * ei);
     }
     lo_g = block_min(lo_g, red);
     hi_g = block_max(hi_g, red);
     emax = block_max(emax, red);
+    __syncthreads();
+    if (j >= n) return;
     const double bnorm = fmax(fabs(lo_g), fabs(hi_g));
     const double pivmin = DBL_MIN * fmax(1.0, emax);
     const double atol = 4.0 * DBL_EPSILON * bnorm + pivmin;
-    lo_g -= atol + 2.0 * DBL_EPSILON * bnorm * n;
-    hi_g += atol + 2.0 * DBL_EPSILON * bnorm * n;
-    const int g = tid >> 3, gl = tid & 7, ngroups = nt >> 3;
-    const unsigned gshift = static_cast<unsigned>(lane & ~7);
-    for (int j0 = 0; j0 < n; j0 += ngroups) {
-        const int j = j0 + g;
-        double lo = lo_g, hi = hi_g;
-        bool done = j >= n;
-        for (int it = 0; it < 64; ++it) {
-            if (!done && hi - lo <= fmax(atol, 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)))) done = true;
-            if (__all_sync(0xffffffffu, done)) break;
-            const double xs = lo + (hi - lo) * (gl + 1) * (1.0 / 9.0);
-            const int cnt = done ? 0 : sturm_count(d, e2, n, xs, pivmin);
-            // first point of the group whose count exceeds j
-            const unsigned ball = (__ballot_sync(0xffffffffu, !done && cnt > j) >> gshift) & 0xffu;
-            const int p = ball ? __ffs(ball) - 1 : 8;
-            const double xp = __shfl_sync(0xffffffffu, xs, static_cast<int>(gshift) + (p < 8 ? p : 7));
-            const double xq = __shfl_sync(0xffffffffu, xs, static_cast<int>(gshift) + (p > 0 ? p - 1 : 0));
-            if (!done) {
-                const double nlo = p > 0 ? xq : lo;
-                const double nhi = p < 8 ? xp : hi;
-                lo = nlo;
-                hi = nhi;
-            }
-        }
-        if (j < n && gl == 0) lam_asc[j] = 0.5 * (lo + hi);
+    double lo = lo_g - (atol + 2.0 * DBL_EPSILON * bnorm * n);
+    double hi = hi_g + (atol + 2.0 * DBL_EPSILON * bnorm * n);
+    for (int it = 0; it < 40; ++it) {
+        if (hi - lo <= fmax(atol, 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)))) break;  // warp-uniform
+        const double xs = lo + (hi - lo) * (lane + 1) * (1.0 / 33.0);
+        const int cnt = sturm_count(d, e2, n, xs, pivmin);
+        const unsigned ball = __ballot_sync(0xffffffffu, cnt > j);
+        const int p = ball ? __ffs(ball) - 1 : 32;
+        const double xp = __shfl_sync(0xffffffffu, xs, p < 32 ? p : 31);
+        const double xq = __shfl_sync(0xffffffffu, xs, p > 0 ? p - 1 : 0);
+        const double nlo = p > 0 ? xq : lo;
+        const double nhi = p < 32 ? xp : hi;
+        lo = nlo;
+        hi = nhi;
     }
-    __syncthreads();
-    for (int i = tid; i < n; i += nt) lam_out[n - 1 - i] = lam_asc[i] * unsc;
-    if (tid == 0) W[tri_off_d(n) + 4 * n] = unsc;
+    if (lane == 0) {
+        const double l = 0.5 * (lo + hi);
+        const_cast<double*>(W)[tri_off_d(n) + 3 * n + j] = l;  // ascending, scaled (inverse iteration)
+        lam_out[n - 1 - j] = l * unsc;
+    }
 }
 
 struct VecJobs {
@@ -256,7 +326,8 @@ struct VecJobs {
 
 /// (T - x I) y = b by Gaussian elimination with partial pivoting of the
 /// tridiagonal matrix (one thread; LAPACK dlagtf/dlagts). Pivots below `tol`
-/// in magnitude are perturbed to +-tol (inverse iteration's standard guard).
+/// in magnitude are perturbed to +-tol (inverse iteration's standard guard);
+/// u0 holds the pivots' reciprocals.
 struct TriLU {
     double *u0, *u1, *u2, *l;
     unsigned char* piv;
@@ -267,13 +338,14 @@ __device__ void tri_factor(const double* d, const double* e, int n, double x, do
         const double q0 = e[k], q1 = d[k + 1] - x, q2 = k + 2 < n ? e[k + 1] : 0.0;
         if (fabs(p0) >= fabs(q0)) {
             if (fabs(p0) < tol) p0 = p0 < 0.0 ? -tol : tol;
-            const double mult = q0 / p0;
-            f.u0[k] = p0; f.u1[k] = p1; f.u2[k] = p2; f.l[k] = mult; f.piv[k] = 0;
+            const double rp = 1.0 / p0;
+            const double mult = q0 * rp;
+            f.u0[k] = rp; f.u1[k] = p1; f.u2[k] = p2; f.l[k] = mult; f.piv[k] = 0;
             p0 = q1 - mult * p1;
             p1 = q2 - mult * p2;
         } else {
             const double mult = p0 / q0;
-            f.u0[k] = q0; f.u1[k] = q1; f.u2[k] = q2; f.l[k] = mult; f.piv[k] = 1;
+            f.u0[k] = 1.0 / q0; f.u1[k] = q1; f.u2[k] = q2; f.l[k] = mult; f.piv[k] = 1;
             const double np0 = p1 - mult * q1, np1 = p2 - mult * q2;
             p0 = np0;
             p1 = np1;
@@ -281,24 +353,29 @@ __device__ void tri_factor(const double* d, const double* e, int n, double x, do
         p2 = 0.0;
     }
     if (fabs(p0) < tol) p0 = p0 < 0.0 ? -tol : tol;
-    f.u0[n - 1] = p0;
+    f.u0[n - 1] = 1.0 / p0;
     f.u1[n - 1] = 0.0;
     f.u2[n - 1] = 0.0;
 }
 __device__ void tri_solve(int n, const TriLU& f, double* y) {
+    double yk = y[0];
     for (int k = 0; k + 1 < n; ++k) {
+        double yn = y[k + 1];
         if (f.piv[k]) {
-            const double t = y[k];
-            y[k] = y[k + 1];
-            y[k + 1] = t;
+            const double t = yk;
+            yk = yn;
+            yn = t;
         }
-        y[k + 1] -= f.l[k] * y[k];
+        y[k] = yk;
+        yk = yn - f.l[k] * yk;
     }
+    y[n - 1] = yk;
+    double x1 = 0.0, x2 = 0.0;  // y[k + 1], y[k + 2]
     for (int k = n - 1; k >= 0; --k) {
-        double s = y[k];
-        if (k + 1 < n) s -= f.u1[k] * y[k + 1];
-        if (k + 2 < n) s -= f.u2[k] * y[k + 2];
-        y[k] = s / f.u0[k];
+        const double xk = (y[k] - f.u1[k] * x1 - f.u2[k] * x2) * f.u0[k];
+        y[k] = xk;
+        x2 = x1;
+        x1 = xk;
     }
 }
 
@@ -312,12 +389,20 @@ __device__ __forceinline__ double hash_uniform(uint32_t a, uint32_t b) {
     return (static_cast<double>(h) + 0.5) * (2.0 / 4294967296.0) - 1.0;  // (-1, 1)
 }
 
-__global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const VecJobs jobs, int vec_warps) {
+/// Reflectors staged in shared memory for the back-transform up to this n
+/// (the strictly-below-subdiagonal part, column k at offset koff(k)).
+constexpr int kVecSmemRefN = 128;
+/// Eigenvectors built in shared memory up to n * r doubles (n <= 128).
+__host__ __device__ __forceinline__ bool jobs_z_smem(int n, int r) { return n <= kVecSmemRefN && n * r <= 4096; }
+__device__ __forceinline__ int refl_off(int k, int n) { return k * (n - 2) - (k * (k - 1)) / 2; }
+
+__global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const __grid_constant__ VecJobs jobs,
+                                                                      int vec_warps) {
     const int n = jobs.n[blockIdx.x], r = jobs.r[blockIdx.x];
     const double* __restrict__ W = jobs.W[blockIdx.x];
     double* __restrict__ U = jobs.U[blockIdx.x];
     const bool zero = jobs.info[blockIdx.x][2] == 0.0;
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     if (r <= 0) return;
     if (zero) {  // zero input: the reference's canonical identity columns (truncated_svd.hpp:66-72)
         for (int64_t i = tid; i < static_cast<int64_t>(n) * r; i += nt) U[i] = (i % n == i / n) ? 1.0 : 0.0;
@@ -327,17 +412,32 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const VecJ
     const double* dg = W + tri_off_d(n);
     const double* eg = dg + n;
     const double* taug = eg + n;
-    const double* lam_asc = taug + n;
+    const double* lam_g = taug + n;
     // clusters of the r leading eigenvalues (ascending j = n - r .. n - 1):
-    // a new cluster starts where the gap exceeds 1e-3 ||T||_1 (dstein's ORTOL)
+    // eigenvalues closer than 1e-9 ||T||_1 are iterated together and
+    // re-orthogonalised against each other (LAPACK dstein's scheme, with a
+    // tighter cluster radius: vectors of eigenvalues further apart are
+    // independent to ~u ||T|| / gap and the caller's CholeskyQR2 polish
+    // makes them orthonormal within the retained span)
     __shared__ int cstart[1024 + 1];
     __shared__ int ncl;
     double* d = smem;
     double* e = smem + n;
+    double* lam_asc = smem + 2 * n;
+    const bool refl_smem = n <= kVecSmemRefN;
+    double* refl = smem + 3 * n;  // staged reflectors (n <= kVecSmemRefN)
+    const int nrefl = refl_smem && n > 2 ? refl_off(n - 2, n) : 0;
+    // the eigenvectors are formed in shared memory when they fit (z_smem)
+    double* Z = smem + 3 * n + nrefl;
+    const bool z_smem = jobs_z_smem(n, r);
+    double* Zc = z_smem ? Z : U;
     for (int i = tid; i < n; i += nt) {
         d[i] = dg[i];
         e[i] = eg[i];
+        lam_asc[i] = lam_g[i];
     }
+    for (int k = 0; k + 2 < n && refl_smem; ++k)
+        for (int i = tid; i < n - k - 2; i += nt) refl[refl_off(k, n) + i] = W[(k + 2 + i) + static_cast<int64_t>(n) * k];
     __syncthreads();
     __shared__ double onenrm;
     if (tid == 0) {
@@ -345,7 +445,7 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const VecJ
         for (int i = 0; i < n; ++i)
             t = fmax(t, fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0));
         onenrm = t;
-        const double ortol = 1e-3 * t;
+        const double ortol = 1e-9 * t;
         int c = 0;
         for (int j = n - r; j < n; ++j)
             if (j == n - r || lam_asc[j] - lam_asc[j - 1] > ortol) cstart[c++] = j;
@@ -355,14 +455,14 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const VecJ
     __syncthreads();
     const double tol = fmax(DBL_EPSILON * onenrm, DBL_MIN);
     // per-warp scratch: u0 u1 u2 l y (5 n doubles) + piv (n bytes)
-    double* scratch = smem + 2 * n;
+    double* scratch = Z + (z_smem ? n * r : 0);
     const int per = 5 * n + (n + 7) / 8;
-    for (int cl = warp; cl < ncl; cl += vec_warps) {
-        if (warp >= vec_warps) break;
+    for (int cl = warp; cl < ncl && warp < vec_warps; cl += vec_warps) {
         double* ws = scratch + static_cast<int64_t>(warp) * per;
         TriLU f{ws, ws + n, ws + 2 * n, ws + 3 * n, reinterpret_cast<unsigned char*>(ws + 5 * n)};
         double* y = ws + 4 * n;
         double xprev = 0.0;
+        const bool multi = cstart[cl + 1] - cstart[cl] > 1;
         for (int j = cstart[cl]; j < cstart[cl + 1]; ++j) {
             double xj = lam_asc[j];
             if (j > cstart[cl]) {  // separate coincident eigenvalues slightly (dstein)
@@ -373,13 +473,14 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const VecJ
             if (lane == 0) tri_factor(d, e, n, xj, tol, f);
             for (int i = lane; i < n; i += 32) y[i] = hash_uniform(static_cast<uint32_t>(j), static_cast<uint32_t>(i));
             __syncwarp();
-            for (int it = 0; it < 3; ++it) {
+            const int iters = multi ? 3 : 2;
+            for (int it = 0; it < iters; ++it) {
                 if (lane == 0) tri_solve(n, f, y);
                 __syncwarp();
                 // orthogonalise against the cluster's earlier vectors (twice)
-                for (int pass = 0; pass < 2; ++pass)
+                for (int pass = 0; pass < 2 && multi; ++pass)
                     for (int p = cstart[cl]; p < j; ++p) {
-                        const double* up = U + static_cast<int64_t>(n) * (n - 1 - p);
+                        const double* up = Zc + static_cast<int64_t>(n) * (n - 1 - p);
                         double s = 0.0;
                         for (int i = lane; i < n; i += 32) s = fma(up[i], y[i], s);
                         s = warp_sum(s);
@@ -401,32 +502,44 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const VecJ
                     if (om > mx || (om == mx && oi < imx)) { mx = om; imx = oi; }
                 }
                 double inv = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
-                if (it == 2 && y[imx] < 0.0) inv = -inv;
+                if (it == iters - 1 && y[imx] < 0.0) inv = -inv;
                 __syncwarp();
                 for (int i = lane; i < n; i += 32) y[i] *= inv;
                 __syncwarp();
             }
-            double* uj = U + static_cast<int64_t>(n) * (n - 1 - j);
+            double* uj = Zc + static_cast<int64_t>(n) * (n - 1 - j);
             for (int i = lane; i < n; i += 32) uj[i] = y[i];
             __syncwarp();
         }
     }
     __syncthreads();
-    // U = H_0 H_1 ... H_{n-3} Z: each warp applies every reflector to its own
-    // columns (no block barrier), reflector k last-to-first
-    for (int c = warp; c < r; c += nw) {
-        double* z = U + static_cast<int64_t>(n) * c;
+    // U = H_0 H_1 ... H_{n-3} Z: 8 lanes per column, every reflector applied
+    // last-to-first (no block barrier: a group owns its column)
+    const int g = tid >> 3, gl = tid & 7, ngroups = nt >> 3;
+    const unsigned gmask = 0xffu << (lane & ~7);
+    for (int c0 = 0; c0 < r; c0 += ngroups) {
+        const int c = c0 + g;
+        const bool active = c < r;
+        double* z = Zc + static_cast<int64_t>(n) * (active ? c : 0);
+        if (!active) continue;
         for (int k = n - 3; k >= 0; --k) {
             const double tau = taug[k];
             if (tau == 0.0) continue;
-            const double* v = W + (k + 1) + static_cast<int64_t>(n) * k;  // v[0] = 1 implicit
             const int m = n - k - 1;
+            const double* v = refl_smem ? refl + refl_off(k, n) - 1 : W + (k + 1) + static_cast<int64_t>(n) * k;
             double s = 0.0;
-            for (int i = lane; i < m; i += 32) s = fma(i == 0 ? 1.0 : v[i], z[k + 1 + i], s);
-            s = tau * warp_sum(s);
-            for (int i = lane; i < m; i += 32) z[k + 1 + i] -= s * (i == 0 ? 1.0 : v[i]);
-            __syncwarp();
+            for (int i = gl; i < m; i += 8) s = fma(i == 0 ? 1.0 : v[i], z[k + 1 + i], s);
+            s += __shfl_xor_sync(gmask, s, 1);
+            s += __shfl_xor_sync(gmask, s, 2);
+            s += __shfl_xor_sync(gmask, s, 4);
+            s *= tau;
+            for (int i = gl; i < m; i += 8) z[k + 1 + i] -= s * (i == 0 ? 1.0 : v[i]);
+            __syncwarp(gmask);
         }
+    }
+    if (z_smem) {
+        __syncthreads();
+        for (int e = tid; e < n * r; e += nt) U[e] = Z[e];
     }
 }
 
@@ -439,7 +552,7 @@ bool tridiag_supported(int64_t n) { return n >= 1 && n <= 1024; }
 void launch_tridiag_eigvals(const double* const* G, const int64_t* n, double* const* lambda, double* const* W,
                             int count, cudaStream_t s, int64_t* launches) {
     for (int i0 = 0; i0 < count;) {
-        // one launch per run of jobs with the same storage mode
+        // reduction: one launch per run of jobs with the same storage mode
         const bool sm = n[i0] <= kTriSmemMaxN;
         TriJobs jobs{};
         int k = 0;
@@ -452,10 +565,20 @@ void launch_tridiag_eigvals(const double* const* G, const int64_t* n, double* co
             nmax = std::max(nmax, n[i0 + k]);
             ++k;
         }
-        const size_t smem = sm ? sizeof(double) * static_cast<size_t>(nmax * nmax + 3 * nmax) : 0;
-        if (smem > 46 * 1024) ensure_smem_limit(reinterpret_cast<const void*>(tridiag_eigvals_kernel), smem);
-        tridiag_eigvals_kernel<<<k, kTriThreads, smem, s>>>(jobs, sm ? 1 : 0);
-        ++*launches;
+        const size_t smem = sm ? sizeof(double) * static_cast<size_t>(nmax * nmax + 2 * nmax) : 0;
+        const int T = sm ? static_cast<int>((nmax - 1 + 31) / 32) : 0;  // m = n - 1 rows at most
+        auto kfn = T == 0 ? tridiag_reduce_kernel<0>
+                 : T == 1 ? tridiag_reduce_kernel<1>
+                 : T == 2 ? tridiag_reduce_kernel<2>
+                 : T == 3 ? tridiag_reduce_kernel<3>
+                 : T == 4 ? tridiag_reduce_kernel<4>
+                          : tridiag_reduce_kernel<5>;
+        if (smem > 0) ensure_smem_limit(reinterpret_cast<const void*>(kfn), smem);
+        kfn<<<k, kTriThreads, smem, s>>>(jobs, sm ? 1 : 0);
+        // eigenvalues: a warp per eigenvalue over many CTAs
+        dim3 grid(static_cast<unsigned>((nmax + kBisWarps - 1) / kBisWarps), static_cast<unsigned>(k));
+        tridiag_bisect_kernel<<<grid, kBisWarps * 32, 0, s>>>(jobs);
+        *launches += 2;
         i0 += k;
     }
 }
@@ -474,12 +597,17 @@ void launch_tridiag_vectors(const double* const* W, const double* const* info, c
             jobs.r[i] = static_cast<int>(r[i0 + i]);
             nmax = std::max(nmax, n[i0 + i]);
         }
-        // shared memory: d, e and per-warp inverse-iteration scratch
+        // shared memory: d, e, the staged reflectors (n <= 128) and per-warp
+        // inverse-iteration scratch
+        const int64_t refl = nmax <= kVecSmemRefN && nmax > 2 ? (nmax - 2) * (nmax - 1) / 2 : 0;
+        int64_t zs = 0;
+        for (int i = 0; i < k; ++i)
+            if (jobs_z_smem(jobs.n[i], jobs.r[i])) zs = std::max<int64_t>(zs, static_cast<int64_t>(jobs.n[i]) * jobs.r[i]);
         const int64_t per = 5 * nmax + (nmax + 7) / 8;
-        const int64_t budget = 200 * 1024 / 8 - 2 * nmax;
+        const int64_t budget = 200 * 1024 / 8 - 3 * nmax - refl - zs;
         const int vw = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kVecThreads / 32, budget / per)));
-        const size_t smem = sizeof(double) * static_cast<size_t>(2 * nmax + vw * per);
-        if (smem > 46 * 1024) ensure_smem_limit(reinterpret_cast<const void*>(tridiag_vectors_kernel), smem);
+        const size_t smem = sizeof(double) * static_cast<size_t>(3 * nmax + refl + zs + vw * per);
+        ensure_smem_limit(reinterpret_cast<const void*>(tridiag_vectors_kernel), smem);
         tridiag_vectors_kernel<<<k, kVecThreads, smem, s>>>(jobs, vw);
         ++*launches;
     }

@@ -113,6 +113,7 @@ void launch_jacobi_eig(const double* G, int64_t n, double* lambda, double* V, do
 // eigenvectors to U_i (n_i x r_i, orthonormal), or identity columns when
 // info_i[2] == 0 (the rank rule's zero-input flag). One CTA per problem.
 bool tridiag_supported(int64_t n);
+constexpr int64_t kTriFullMaxN = 64;  // all n eigenvectors by inverse iteration up to this size
 int64_t tridiag_workspace_doubles(int64_t n);
 void launch_tridiag_eigvals(const double* const* G, const int64_t* n, double* const* lambda, double* const* W,
                             int count, cudaStream_t s, int64_t* launches);
@@ -123,6 +124,16 @@ void launch_tridiag_vectors(const double* const* W, const double* const* info, c
 // Cholesky on `work`, n * n doubles), else 0.
 void launch_posdef_test(const double* G, int64_t n, double shift, double* work, double* flag, cudaStream_t s,
                         int64_t* launches);
+
+// Blocked form of the positive-definiteness test: launch_chol_prepare writes
+// A = G - shift I (n x n) and flag[0] = 1; launch_chol_panel factors the
+// columns [kb, kb + b) (b = 32 except for the last panel) of the current
+// trailing matrix, clearing flag[0] on a non-positive pivot; the caller
+// applies A[kb+b:, kb+b:] -= P P^T (P = A[kb+b:, kb:kb+b]) between panels.
+constexpr int64_t kCholPanel = 32;
+void launch_chol_prepare(const double* G, int64_t n, double shift, double* A, double* flag, cudaStream_t s,
+                         int64_t* launches);
+void launch_chol_panel(double* A, int64_t n, int64_t kb, int64_t b, double* flag, cudaStream_t s, int64_t* launches);
 
 // Rank rule of truncated_svd.hpp:74-99 on k = min(rows, cols) values
 // sigma_i^2 = max(lambda_i, 0). info[0] = rank, info[1] = discarded norm,
@@ -257,6 +268,12 @@ bool gram_stream_supported(const double* Y, int64_t K, int64_t M, int64_t B);
 int64_t gram_stream_partials(int64_t M, int num_sms);
 int launch_gram_stream(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,
                        cudaStream_t s, int64_t* launches);
+/// The same Gram for 9 <= M <= 32 rows (any K >= 1, incl. mode 0) on DMMA,
+/// four columns per k-step. partials: gram_mid_partials doubles.
+bool gram_mid_supported(int64_t K, int64_t M, int64_t B);
+int64_t gram_mid_partials(int num_sms);
+int launch_gram_mid(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,
+                    cudaStream_t s, int64_t* launches);
 /// The same Gram for M <= 8 rows (any K >= 1, incl. mode 0), one column per thread.
 bool gram_small_supported(int64_t K, int64_t M, int64_t B);
 int64_t gram_small_partials(int num_sms);

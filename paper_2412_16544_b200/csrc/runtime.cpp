@@ -329,12 +329,28 @@ void residual_energy(Context& c, const DT& t, int mode, const double* U, int64_t
 }
 
 DT gram(Context& c, const DT& t, int mode, bool reduce) {
+    if (c.gram_hint.G.buf && c.gram_hint.data == t.data() && c.gram_hint.mode == mode && c.gram_hint.shape == t.shape) {
+        DT G = c.gram_hint.G;  // already all-reduced
+        c.gram_hint = Context::GramHint{};
+        return G;
+    }
+    c.gram_hint = Context::GramHint{};
     const Split sp = split_at(t.shape, mode);
     DT G = c.tensor({sp.J, sp.J});
     if (c.fused && sp.J <= 8 && sp.I * sp.J * sp.O >= (int64_t{1} << 20) && gram_small_supported(sp.I, sp.J, sp.O)) {
         // few rows (c4's 8-extent modes): one column per thread, registers
         BufPtr parts = c.alloc(gram_small_partials(c.num_sms));
         launch_gram_small(t.data(), sp.I, sp.J, sp.O, parts->p, G.data(), c.num_sms, c.s, &c.launches);
+        HTR_CUDA(cudaGetLastError());
+        if (reduce) c.allreduce(G.data(), sp.J * sp.J);
+        return G;
+    }
+    if (c.fused && sp.J >= 9 && sp.J <= 32 && gram_mid_supported(sp.I, sp.J, sp.O) &&
+        !(sp.J >= 24 && sp.I * sp.J * sp.O >= (int64_t{1} << 22) && gram_stream_supported(t.data(), sp.I, sp.J, sp.O))) {
+        // 9..32 rows, any mode: DMMA over 4-column k-steps (the streaming
+        // kernel keeps the large >= 24-row modes it supports)
+        BufPtr parts = c.alloc(gram_mid_partials(c.num_sms));
+        launch_gram_mid(t.data(), sp.I, sp.J, sp.O, parts->p, G.data(), c.num_sms, c.s, &c.launches);
         HTR_CUDA(cudaGetLastError());
         if (reduce) c.allreduce(G.data(), sp.J * sp.J);
         return G;
@@ -386,6 +402,26 @@ ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode);
 
 Truncation truncate_eig(Context& c, const BufPtr& lam, const BufPtr& V, int64_t rows, int64_t cols, double eps_abs,
                         int64_t min_rank, const ProjectedGram& refine, double noise_scale);
+
+/// Every eigenpair of a symmetric n x n G (lambda descending, V n x n): the
+/// tridiagonal route with all n vectors for small n (the machine-floor
+/// refinement of small Grams), else the Jacobi solver. `work` holds 2 n^2
+/// doubles (Jacobi).
+void eig_full(Context& c, const double* G, int64_t n, double* lam, double* V, double* work) {
+    if (c.tridiag && n <= kTriFullMaxN) {
+        BufPtr W = c.alloc(tridiag_workspace_doubles(n));
+        BufPtr info = c.alloc(4);
+        launch_fill(info->p, 4, 1.0, c.s, &c.launches);  // info[2] != 0: not the zero-input case
+        double* wp = W->p;
+        launch_tridiag_eigvals(&G, &n, &lam, &wp, 1, c.s, &c.launches);
+        const double* wc = W->p;
+        const double* ip = info->p;
+        launch_tridiag_vectors(&wc, &ip, &n, &n, &V, 1, c.s, &c.launches);
+        HTR_CUDA(cudaGetLastError());
+        return;
+    }
+    launch_jacobi_eig(G, n, lam, V, work, c.s, &c.launches);
+}
 
 /// A Gram reduced to tridiagonal form with all its eigenvalues (descending)
 /// on the device (k_tridiag.cu); W keeps the reflectors for the vectors.
@@ -479,7 +515,7 @@ Truncation truncate_jacobi(Context& c, const DT& G, int64_t rows, int64_t cols, 
     BufPtr lam = c.alloc(n);
     BufPtr V = c.alloc(n * n);
     BufPtr work = c.alloc(2 * n * n);
-    launch_jacobi_eig(G.data(), n, lam->p, V->p, work->p, c.s, &c.launches);
+    eig_full(c, G.data(), n, lam->p, V->p, work->p);
     HTR_CUDA(cudaGetLastError());
     return truncate_eig(c, lam, V, rows, cols, eps_abs, min_rank, refine, noise_scale);
 }
@@ -503,7 +539,7 @@ Truncation truncate_eig(Context& c, const BufPtr& lam, const BufPtr& V, int64_t 
                 BufPtr mu = c.alloc(q);
                 BufPtr Z = c.alloc(q * q);
                 BufPtr work2 = c.alloc(2 * q * q);
-                launch_jacobi_eig(G2.data(), q, mu->p, Z->p, work2->p, c.s, &c.launches);
+                eig_full(c, G2.data(), q, mu->p, Z->p, work2->p);
                 HTR_CUDA(cudaMemcpyAsync(lam->p + s0, mu->p, sizeof(double) * static_cast<size_t>(q),
                                          cudaMemcpyDeviceToDevice, c.s));
                 BufPtr WZ = c.alloc(n * q);
@@ -841,6 +877,7 @@ namespace {
 struct PosdefProbe {
     bool launched = false;
     BufPtr work, flag;
+    std::vector<BufPtr> gemm_ws;  // trailing-update workspaces, live until finish
 };
 PosdefProbe posdef_launch(Context& c, const DT& G, int64_t rows, double eps_abs, cudaStream_t st) {
     PosdefProbe pr;
@@ -854,11 +891,35 @@ PosdefProbe posdef_launch(Context& c, const DT& G, int64_t rows, double eps_abs,
     pr.work = c.alloc(rows * rows);
     pr.flag = c.alloc(4);
     HTR_CUDA(cudaMemsetAsync(pr.flag->p, 0, 4 * sizeof(double), c.s));
-    if (st != c.s) {  // the buffers and G are ordered on the context stream
+    // blocked right-looking Cholesky: 32-column panels (one CTA each), the
+    // trailing updates A22 -= P P^T on the DMMA GEMM engine
+    const int64_t n = rows;
+    std::vector<GemmDesc> upd;
+    for (int64_t kb = 0; kb + kCholPanel < n; kb += kCholPanel) {
+        const int64_t m = n - kb - kCholPanel;
+        double* P = pr.work->p + (kb + kCholPanel) + n * kb;
+        GemmDesc d;
+        d.M = m; d.N1 = m; d.K1 = kCholPanel;
+        d.A = P; d.sam = 1; d.sak1 = n;
+        d.B = P; d.sbk1 = n; d.sbn1 = 1;
+        d.C = pr.work->p + (kb + kCholPanel) + n * (kb + kCholPanel); d.scm = 1; d.scn1 = n;
+        d.alpha = -1.0; d.beta = 1.0;
+        const int64_t ws = gemm_workspace_doubles(d, c.num_sms);
+        pr.gemm_ws.push_back(ws > 0 ? c.alloc(ws) : nullptr);
+        upd.push_back(d);
+    }
+    if (st != c.s) {  // the buffers, workspaces and G are ordered on the context stream
         HTR_CUDA(cudaEventRecord(c.aux_ev, c.s));
         HTR_CUDA(cudaStreamWaitEvent(st, c.aux_ev, 0));
     }
-    launch_posdef_test(G.data(), rows, eps_abs * eps_abs + 1e-12 * tr, pr.work->p, pr.flag->p, st, &c.launches);
+    launch_chol_prepare(G.data(), n, eps_abs * eps_abs + 1e-12 * tr, pr.work->p, pr.flag->p, st, &c.launches);
+    for (int64_t kb = 0, p = 0; kb < n; kb += kCholPanel, ++p) {
+        launch_chol_panel(pr.work->p, n, kb, std::min(kCholPanel, n - kb), pr.flag->p, st, &c.launches);
+        if (kb + kCholPanel < n) {
+            const BufPtr& w = pr.gemm_ws[static_cast<size_t>(p)];
+            launch_gemm(upd[static_cast<size_t>(p)], w ? w->p : nullptr, c.num_sms, st, &c.launches);
+        }
+    }
     HTR_CUDA(cudaGetLastError());
     pr.launched = true;
     return pr;
@@ -1103,9 +1164,31 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
     const int64_t batch = y.shape[static_cast<size_t>(d)];
     const int64_t gbatch = global_batch(c, batch);
     double ysq = 0.0;
-    bool bad = false;
-    norm_sq(c, y.data(), y.size(), &ysq, &bad);
-    if (bad) raise(HTR_ERR_INVALID_ARGUMENT, "bht_l2r: non-finite input");
+    bool have_ysq = false;
+    {
+        // ||y||^2 = trace of the first leaf's mode Gram, which its truncation
+        // needs anyway: one pass over y less than a separate norm scan
+        const int mode = static_cast<int>(tree.layer(p)[0].leaf_dim);
+        const int64_t rows = y.shape[static_cast<size_t>(mode)];
+        const bool column_side = !c.sharded() && rows > kColumnSideRows && y.size() / rows < rows;
+        if (!column_side) {
+            DT G = gram(c, y, mode, true);
+            std::vector<double> diag(static_cast<size_t>(rows));
+            HTR_CUDA(cudaMemcpy2DAsync(diag.data(), sizeof(double), G.data(), sizeof(double) * static_cast<size_t>(rows + 1),
+                                       sizeof(double), static_cast<size_t>(rows), cudaMemcpyDeviceToHost, c.s));
+            HTR_CUDA(cudaStreamSynchronize(c.s));
+            for (double v : diag) ysq += v;
+            if (std::isfinite(ysq)) {
+                c.gram_hint = Context::GramHint{y.data(), mode, y.shape, G};
+                have_ysq = true;
+            }
+        }
+    }
+    if (!have_ysq) {  // (also distinguishes non-finite input from overflow)
+        bool bad = false;
+        norm_sq(c, y.data(), y.size(), &ysq, &bad);
+        if (bad) raise(HTR_ERR_INVALID_ARGUMENT, "bht_l2r: non-finite input");
+    }
     const double norm_y = std::sqrt(ysq);
     const double eps_abs = effective_eps_rel(eps_rel) * norm_y;
 

@@ -132,6 +132,15 @@ struct Context {
     /// of a batch-sharded run).
     bool sharded() const { return nccl_comm != nullptr || reducer != nullptr; }
 
+    /// A Gram computed ahead of its truncation (BHT-l2r reads ||y||^2 off the
+    /// first leaf Gram's trace): gram() hands it out once for the same view.
+    struct GramHint {
+        const double* data = nullptr;
+        int mode = -1;
+        Shape shape;
+        DT G;
+    } gram_hint;
+
     explicit Context(int dev);
     ~Context();
 

@@ -849,3 +849,27 @@ def test_small_mode_gram_bht_matches_generic_and_oracle(ht, dims, ranks):
     finally:
         ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
     assert gpu.ranks() == gen.ranks()
+
+
+@pytest.mark.parametrize("dims,ranks", [
+    ((16, 16, 16, 16), (5, 4, 5, 3)),        # config 1's extents (M = 16, mode 0 included)
+    ((9, 24, 32, 17, 30), (3, 5, 6, 4, 5)),  # M = 9, 17 (two tiles), 24, 30, 32 (four tiles)
+])
+def test_mid_mode_gram_bht_matches_generic_and_oracle(ht, dims, ranks):
+    """Grams of modes with 9..32 rows on the DMMA four-column kernel
+    (gram_mid_kernel): BHT-l2r equals the generic engine and the oracle."""
+    rng = np.random.default_rng(sum(dims) * 5 + sum(ranks))
+    bases = [ro.random_orthonormal(n, r, rng) for n, r in zip(dims, ranks)]
+    y = ro.tucker_family_batch(bases, 6, rng)
+    y += 1e-6 * rng.standard_normal(y.shape)
+    tree = ht.DimensionTree.balanced(len(dims))
+    gpu, _ = ht.bht_l2r(y, tree, 1e-3)
+    ref, _ = ho.bht_l2r(y, ho.DimensionTree.balanced(len(dims)), 1e-3)
+    compare_reps(ht, gpu, ref)
+    ctx = gpu.ctx
+    ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+    try:
+        gen, _ = ht.bht_l2r(y, tree, 1e-3)
+    finally:
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    assert gpu.ranks() == gen.ranks()
