@@ -15,63 +15,13 @@
 #include <string>
 #include <vector>
 
+#include "htrise/context.hpp"
 #include "htrise/dimension_tree.hpp"
 #include "htrise/tensor.hpp"
 #include "htrise_cuda.h"
 
 namespace htrise {
 namespace device {
-
-[[noreturn]] inline void throw_status(htr_status code, const std::string& msg) {
-    switch (code) {
-        case HTR_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
-        case HTR_ERR_OUT_OF_RANGE: throw std::out_of_range(msg);
-        default: throw std::runtime_error(msg);
-    }
-}
-
-/// Process-wide default context on device 0 (or $HTRISE_DEVICE).
-class Context {
-public:
-    static Context& instance() {
-        static Context c;
-        return c;
-    }
-    htr_context* get() {
-        std::call_once(once_, [this] {
-            int dev = 0;
-            if (const char* e = std::getenv("HTRISE_DEVICE")) dev = std::atoi(e);
-            htr_context* c = nullptr;
-            const htr_status st = htr_context_create(dev, &c);
-            if (st != HTR_OK) {
-                const std::string msg = c ? htr_last_error(c) : "htr_context_create failed";
-                htr_context_destroy(c);
-                error_ = msg;
-                code_ = st;
-                return;
-            }
-            ctx_ = c;
-        });
-        if (!ctx_) throw_status(code_, error_);
-        return ctx_;
-    }
-    void check(htr_status st) {
-        if (st != HTR_OK) throw_status(st, htr_last_error(ctx_));
-    }
-    ~Context() {
-        if (ctx_) htr_context_destroy(ctx_);
-    }
-
-private:
-    Context() = default;
-    std::once_flag once_;
-    htr_context* ctx_ = nullptr;
-    std::string error_;
-    htr_status code_ = HTR_OK;
-};
-
-inline htr_context* ctx() { return Context::instance().get(); }
-inline void check(htr_status st) { Context::instance().check(st); }
 
 /// Owning handle of a device-resident representation value.
 using RepHandle = std::shared_ptr<htr_rep>;

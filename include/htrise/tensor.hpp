@@ -9,10 +9,11 @@
 // column-major Matrix/Vector of its own with the subset of the Eigen API the
 // htrise interfaces expose (data/rows/cols/operator()/transpose/norm/...).
 //
-// These host utilities are the value-type plumbing around the GPU path; the
-// hot path (bht_l2r / encode / ht_rise_update / decode) runs as sm_100a
-// kernels behind include/htrise_cuda.h and never calls into this file's
-// arithmetic.
+// The arithmetic -- Matrix products, mode_multiply, contract, permute_axes
+// and the products multi_contract composes -- runs on the device through
+// include/htrise_cuda.h (htr_matmul, htr_mode_multiply, htr_contract,
+// htr_permute_axes); what stays on the host is value plumbing (storage,
+// unfold/fold/reshape/concat/pad/slice copies, element access).
 #pragma once
 
 #include <algorithm>
@@ -26,6 +27,8 @@
 #include <string>
 #include <utility>
 #include <vector>
+
+#include "htrise/context.hpp"
 
 namespace htrise {
 
@@ -190,17 +193,12 @@ public:
         return m;
     }
 
+    /// Product on the device (htr_matmul; Eigen's GEMM in the reference).
     Matrix operator*(const Matrix& b) const {
         if (cols_ != b.rows_) throw std::invalid_argument("Matrix: product shape mismatch");
         Matrix c(rows_, b.cols_);
-        for (Index j = 0; j < b.cols_; ++j)
-            for (Index k = 0; k < cols_; ++k) {
-                const double bkj = b(k, j);
-                if (bkj == 0.0) continue;
-                const double* ak = a_.data() + rows_ * k;
-                double* cj = c.a_.data() + rows_ * j;
-                for (Index i = 0; i < rows_; ++i) cj[i] += ak[i] * bkj;
-            }
+        if (rows_ == 0 || b.cols_ == 0) return c;
+        device::check(htr_matmul(device::ctx(), a_.data(), rows_, cols_, b.a_.data(), b.cols_, c.a_.data()));
         return c;
     }
     Matrix operator-(const Matrix& b) const { return zip(b, std::minus<double>()); }
@@ -369,25 +367,11 @@ inline DenseTensor permute_axes(const DenseTensor& t, const std::vector<Index>& 
             throw std::invalid_argument("permute_axes: invalid permutation");
         used[static_cast<std::size_t>(p)] = 1;
     }
-    Shape in_stride(static_cast<std::size_t>(d)), out_shape(static_cast<std::size_t>(d));
-    Index acc = 1;
-    for (Index k = 0; k < d; ++k) {
-        in_stride[static_cast<std::size_t>(k)] = acc;
-        acc *= t.extent(k);
-    }
+    Shape out_shape(static_cast<std::size_t>(d));
     for (Index k = 0; k < d; ++k) out_shape[static_cast<std::size_t>(k)] = t.extent(perm[static_cast<std::size_t>(k)]);
     DenseTensor out(out_shape);
-    Shape idx(static_cast<std::size_t>(d), 0);
-    for (Index flat = 0; flat < t.size(); ++flat) {
-        Index src = 0;
-        for (Index k = 0; k < d; ++k)
-            src += idx[static_cast<std::size_t>(k)] * in_stride[static_cast<std::size_t>(perm[static_cast<std::size_t>(k)])];
-        out.data()[flat] = t.data()[src];
-        for (Index k = 0; k < d; ++k) {
-            if (++idx[static_cast<std::size_t>(k)] < out_shape[static_cast<std::size_t>(k)]) break;
-            idx[static_cast<std::size_t>(k)] = 0;
-        }
-    }
+    device::check(htr_permute_axes(device::ctx(), t.data(), t.shape().data(), static_cast<int32_t>(d), perm.data(),
+                                   out.data()));
     return out;
 }
 
@@ -401,14 +385,17 @@ inline DenseTensor contract(const DenseTensor& a, Index da, const DenseTensor& b
         throw std::invalid_argument("contract: extent mismatch " + std::to_string(a.extent(da)) +
                                     " vs " + std::to_string(b.extent(db)));
     }
-    Matrix prod = unfold(a, da).transpose() * unfold(b, db);
     Shape out;
     for (Index k = 0; k < a.order(); ++k)
         if (k != da) out.push_back(a.extent(k));
     for (Index k = 0; k < b.order(); ++k)
         if (k != db) out.push_back(b.extent(k));
     if (out.empty()) out = {1};
-    return DenseTensor(out, Vector(std::vector<double>(prod.data(), prod.data() + prod.size())));
+    DenseTensor r(out);
+    device::check(htr_contract(device::ctx(), a.data(), a.shape().data(), static_cast<int32_t>(a.order()),
+                               static_cast<int32_t>(da), b.data(), b.shape().data(), static_cast<int32_t>(b.order()),
+                               static_cast<int32_t>(db), r.data()));
+    return r;
 }
 
 /// Replace mode `mode` of t by the rows of m (q x extent(mode)).
@@ -420,7 +407,11 @@ inline DenseTensor mode_multiply(const DenseTensor& t, Index mode, const Matrix&
     }
     Shape out = t.shape();
     out[static_cast<std::size_t>(mode)] = m.rows();
-    return fold(m * unfold(t, mode), out, mode);
+    DenseTensor r(out);
+    if (m.rows() == 0) return r;
+    device::check(htr_mode_multiply(device::ctx(), t.data(), 0, t.shape().data(), static_cast<int32_t>(t.order()),
+                                    static_cast<int32_t>(mode), m.data(), m.rows(), r.data(), 0));
+    return r;
 }
 
 /// One factor of a multi-index contraction (reference tensor.hpp:318-323).

@@ -228,6 +228,20 @@ HTR_API htr_status htr_truncated_svd(htr_context* ctx, const double* m, int32_t 
 HTR_API htr_status htr_mode_multiply(htr_context* ctx, const double* t, int32_t t_on_device, const int64_t* shape,
                              int32_t order, int32_t mode, const double* m, int64_t q, double* out,
                              int32_t out_on_device);
+/* Dense products of the tensor algebra (reference tensor.hpp, Eigen's GEMM
+ * in the reference), host buffers in and out, computed on the device:
+ *  htr_matmul:       C (m x n) = A (m x k) B (k x n), column-major
+ *                    (Matrix::operator*, the GEMM behind unfold-based products);
+ *  htr_contract:     contract(a, da, b, db) (tensor.hpp:273-296): out is
+ *                    a's remaining modes then b's, canonical;
+ *  htr_permute_axes: permute_axes (tensor.hpp:219-267): output mode k is
+ *                    input mode perm[k] (order <= 16). */
+HTR_API htr_status htr_matmul(htr_context* ctx, const double* a, int64_t m, int64_t k, const double* b, int64_t n,
+                              double* c);
+HTR_API htr_status htr_contract(htr_context* ctx, const double* a, const int64_t* a_shape, int32_t a_order, int32_t da,
+                                const double* b, const int64_t* b_shape, int32_t b_order, int32_t db, double* out);
+HTR_API htr_status htr_permute_axes(htr_context* ctx, const double* t, const int64_t* shape, int32_t order,
+                                    const int64_t* perm, double* out);
 /* compute_residual (ht_rise.hpp:31-38): R = C - U (U^T C). */
 HTR_API htr_status htr_compute_residual(htr_context* ctx, const double* u, int64_t rows, int64_t r, const double* c,
                                 int64_t cols, double* out);

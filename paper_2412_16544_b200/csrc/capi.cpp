@@ -526,6 +526,82 @@ htr_status htr_mode_multiply(htr_context* ctx, const double* t, int32_t t_on_dev
     });
 }
 
+htr_status htr_matmul(htr_context* ctx, const double* a, int64_t m, int64_t k, const double* b, int64_t n, double* c_out) {
+    return guarded(ctx, [&] {
+        htr::Context& c = C(ctx);
+        if (m < 0 || k < 0 || n < 0) htr::raise(HTR_ERR_INVALID_ARGUMENT, "Matrix: product shape mismatch");
+        if (m == 0 || n == 0) return;
+        if (k == 0) {
+            std::memset(c_out, 0, sizeof(double) * static_cast<size_t>(m * n));
+            return;
+        }
+        DT at = input(c, a, false, {m, k});
+        DT bt = input(c, b, false, {k, n});
+        DT ct = c.tensor({m, n});
+        htr::GemmDesc d;
+        d.M = m; d.N1 = n; d.K1 = k;
+        d.A = at.data(); d.sam = 1; d.sak1 = m;
+        d.B = bt.data(); d.sbk1 = 1; d.sbn1 = k;
+        d.C = ct.data(); d.scm = 1; d.scn1 = m;
+        htr::run_gemm(c, d);
+        output(c, ct.data(), m * n, c_out, false);
+    });
+}
+
+htr_status htr_contract(htr_context* ctx, const double* a, const int64_t* a_shape, int32_t a_order, int32_t da,
+                        const double* b, const int64_t* b_shape, int32_t b_order, int32_t db, double* out) {
+    return guarded(ctx, [&] {
+        htr::Context& c = C(ctx);
+        Shape sa = to_shape(a_shape, a_order), sb = to_shape(b_shape, b_order);
+        if (da < 0 || da >= a_order || db < 0 || db >= b_order)
+            htr::raise(HTR_ERR_INVALID_ARGUMENT, "contract: mode out of range");
+        const int64_t K = sa[static_cast<size_t>(da)];
+        if (K != sb[static_cast<size_t>(db)])
+            htr::raise(HTR_ERR_INVALID_ARGUMENT, "contract: extent mismatch " + std::to_string(K) + " vs " +
+                                                     std::to_string(sb[static_cast<size_t>(db)]));
+        DT at = input(c, a, false, sa), bt = input(c, b, false, sb);
+        auto unfold = [&](const DT& t, int mode) {
+            int64_t inner = 1, outer = 1;
+            for (int k = 0; k < mode; ++k) inner *= t.shape[static_cast<size_t>(k)];
+            for (size_t k = static_cast<size_t>(mode) + 1; k < t.shape.size(); ++k) outer *= t.shape[k];
+            DT u = c.tensor({t.shape[static_cast<size_t>(mode)], inner * outer});
+            htr::launch_unfold(t.data(), inner, t.shape[static_cast<size_t>(mode)], outer, u.data(), c.s, &c.launches);
+            HTR_CUDA(cudaGetLastError());
+            return u;
+        };
+        DT ua = unfold(at, da), ub = unfold(bt, db);
+        const int64_t ra = ua.shape[1], rb = ub.shape[1];
+        DT ct = c.tensor({ra, rb});
+        htr::GemmDesc d;  // C = A_(da)^T B_(db)
+        d.M = ra; d.N1 = rb; d.K1 = K;
+        d.A = ua.data(); d.sam = K; d.sak1 = 1;
+        d.B = ub.data(); d.sbk1 = 1; d.sbn1 = K;
+        d.C = ct.data(); d.scm = 1; d.scn1 = ra;
+        htr::run_gemm(c, d);
+        output(c, ct.data(), ra * rb, out, false);
+    });
+}
+
+htr_status htr_permute_axes(htr_context* ctx, const double* t, const int64_t* shape, int32_t order, const int64_t* perm,
+                            double* out) {
+    return guarded(ctx, [&] {
+        htr::Context& c = C(ctx);
+        Shape s = to_shape(shape, order);
+        if (order > 16) htr::raise(HTR_ERR_INVALID_ARGUMENT, "permute_axes: at most 16 modes");
+        std::vector<char> used(static_cast<size_t>(order), 0);
+        for (int32_t k = 0; k < order; ++k) {
+            if (perm[k] < 0 || perm[k] >= order || used[static_cast<size_t>(perm[k])])
+                htr::raise(HTR_ERR_INVALID_ARGUMENT, "permute_axes: invalid permutation");
+            used[static_cast<size_t>(perm[k])] = 1;
+        }
+        DT tt = input(c, t, false, s);
+        DT o = c.tensor(s);
+        htr::launch_permute(tt.data(), s.data(), order, perm, o.data(), c.s, &c.launches);
+        HTR_CUDA(cudaGetLastError());
+        output(c, o.data(), o.size(), out, false);
+    });
+}
+
 htr_status htr_compute_residual(htr_context* ctx, const double* u, int64_t rows, int64_t r, const double* cm,
                                 int64_t cols, double* out) {
     return guarded(ctx, [&] {

@@ -628,6 +628,48 @@ void launch_basis_defect(const double* const* U, const int64_t* alpha, const int
     }
 }
 
+constexpr int kPermMax = 16;
+struct PermArgs {
+    int d;
+    int64_t out_ext[kPermMax];
+    int64_t src_stride[kPermMax];  // stride in the source of output mode k
+};
+
+__global__ void permute_kernel(const double* __restrict__ src, int64_t n, const __grid_constant__ PermArgs a,
+                               double* __restrict__ dst) {
+    for (int64_t flat = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; flat < n;
+         flat += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int64_t rem = flat, off = 0;
+        for (int k = 0; k < a.d; ++k) {
+            const int64_t e = a.out_ext[k];
+            const int64_t i = rem % e;
+            rem /= e;
+            off += i * a.src_stride[k];
+        }
+        dst[flat] = src[off];
+    }
+}
+
+void launch_permute(const double* src, const int64_t* shape, int d, const int64_t* perm, double* dst, cudaStream_t s,
+                    int64_t* launches) {
+    PermArgs a{};
+    a.d = d;
+    int64_t in_stride[kPermMax];
+    int64_t acc = 1, n = 1;
+    for (int k = 0; k < d; ++k) {
+        in_stride[k] = acc;
+        acc *= shape[k];
+    }
+    for (int k = 0; k < d; ++k) {
+        a.out_ext[k] = shape[perm[k]];
+        a.src_stride[k] = in_stride[perm[k]];
+        n *= a.out_ext[k];
+    }
+    if (n == 0) return;
+    permute_kernel<<<blocks_for(n), 256, 0, s>>>(src, n, a, dst);
+    ++*launches;
+}
+
 void launch_fill(double* dst, int64_t n, double value, cudaStream_t s, int64_t* launches) {
     if (n == 0) return;
     fill_kernel<<<blocks_for(n), 256, 0, s>>>(dst, n, value);

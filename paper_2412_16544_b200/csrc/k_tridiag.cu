@@ -574,7 +574,9 @@ void launch_tridiag_eigvals(const double* const* G, const int64_t* n, double* co
                  : T == 4 ? tridiag_reduce_kernel<4>
                           : tridiag_reduce_kernel<5>;
         if (smem > 0) ensure_smem_limit(reinterpret_cast<const void*>(kfn), smem);
-        kfn<<<k, kTriThreads, smem, s>>>(jobs, sm ? 1 : 0);
+        // (small matrices: fewer threads, cheaper barriers and loop overhead)
+        const int threads = nmax <= 32 ? 128 : (nmax <= 64 ? 256 : kTriThreads);
+        kfn<<<k, threads, smem, s>>>(jobs, sm ? 1 : 0);
         // eigenvalues: a warp per eigenvalue over many CTAs
         dim3 grid(static_cast<unsigned>((nmax + kBisWarps - 1) / kBisWarps), static_cast<unsigned>(k));
         tridiag_bisect_kernel<<<grid, kBisWarps * 32, 0, s>>>(jobs);

@@ -163,6 +163,11 @@ void launch_unfold(const double* src, int64_t inner, int64_t ext, int64_t outer,
 void launch_orthonormalize_new(const double* U, int64_t alpha, int64_t r, double* W, int64_t q, double* info,
                                double* work, cudaStream_t s, int64_t* launches);
 
+// dst = src with its axes permuted: output mode k is input mode perm[k]
+// (d <= 16, canonical layouts).
+void launch_permute(const double* src, const int64_t* shape, int d, const int64_t* perm, double* dst, cudaStream_t s,
+                    int64_t* launches);
+
 // Orthonormality defects of `count` bases U_i (alpha_i x r_i, col-major):
 // out[i] = ||U_i^T U_i - I||_F, one CTA per basis (r_i = 0 writes 0).
 void launch_basis_defect(const double* const* U, const int64_t* alpha, const int64_t* r, int count, double* out,
@@ -262,6 +267,19 @@ struct QuadArgs {
     double* host_out = nullptr;
     unsigned int* ticket = nullptr;
 };
+/// Two adjacent modes projected in one read (k_proj2.cu): Y viewed as
+/// [n0, n1, n2, S] -> C[n0, r1, r2, S] = Y x_1 U1^T x_2 U2^T (U1 n1 x r1,
+/// U2 n2 x r2, column-major). n0 % 8 == 0, n1 % 4 == 0, n1 <= 256, r <= 24.
+struct Proj2Args {
+    const double* Y = nullptr;
+    int64_t n0 = 0, n1 = 0, n2 = 0, S = 0;
+    const double* U1 = nullptr;
+    const double* U2 = nullptr;
+    int r1 = 0, r2 = 0;
+    double* C = nullptr;
+};
+bool proj2_supported(const Proj2Args& a);
+int launch_proj2(const Proj2Args& a, cudaStream_t s, int64_t* launches);
 /// Streaming Gram G = Y_(k) Y_(k)^T of Y viewed as [K, M, B] (K contiguous,
 /// M <= 128, K even; k_gram.cu). partials: gram_stream_partials doubles.
 bool gram_stream_supported(const double* Y, int64_t K, int64_t M, int64_t B);

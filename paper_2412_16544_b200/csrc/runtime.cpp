@@ -403,6 +403,18 @@ ProjectedGram unfolding_refiner(Context& c, const DT& t, int mode);
 Truncation truncate_eig(Context& c, const BufPtr& lam, const BufPtr& V, int64_t rows, int64_t cols, double eps_abs,
                         int64_t min_rank, const ProjectedGram& refine, double noise_scale);
 
+/// Relative tolerance below which a truncation's small eigenvalues are
+/// re-measured (eps^2 < refine_threshold(n) * lambda_max): the Gram's
+/// eigenvalues carry an absolute error ~n u lambda_max each, so a tail sum of
+/// up to n of them is uncertain by ~n^2 u lambda_max; above 1e5 times that
+/// the rank rule's decision cannot move, below it the tail is re-measured
+/// through a projected Gram (then resolved to ~u sigma_max like the
+/// reference's direct SVD). Capped at 1e-7 (the former fixed threshold).
+double refine_threshold(int64_t n) {
+    const double nn = static_cast<double>(std::max<int64_t>(n, 1));
+    return std::min(1e-7, 1e5 * nn * nn * 0x1p-53);
+}
+
 /// Every eigenpair of a symmetric n x n G (lambda descending, V n x n): the
 /// tridiagonal route with all n vectors for small n (the machine-floor
 /// refinement of small Grams), else the Jacobi solver. `work` holds 2 n^2
@@ -454,7 +466,7 @@ Truncation finish_tri(Context& c, const TriSolve& ts, const DT& G, int64_t rows,
         std::vector<double> lh(static_cast<size_t>(n));
         c.fetch(ts.lam->p, n, lh.data());
         const double lmax = std::max({lh[0], noise_scale, 0.0});
-        if (lmax > 0.0 && eps_abs * eps_abs < 1e-7 * lmax) {
+        if (lmax > 0.0 && eps_abs * eps_abs < refine_threshold(n) * lmax) {
             int64_t s0 = 0;
             while (s0 < n && lh[static_cast<size_t>(s0)] >= 1e-6 * lmax) ++s0;
             if (s0 < n) return truncate_jacobi(c, G, rows, cols, eps_abs, min_rank, refine, noise_scale);
@@ -529,7 +541,7 @@ Truncation truncate_eig(Context& c, const BufPtr& lam, const BufPtr& V, int64_t 
         std::vector<double> lh(static_cast<size_t>(n));
         c.fetch(lam->p, n, lh.data());
         const double lmax = std::max({lh[0], noise_scale, 0.0});
-        if (lmax > 0.0 && eps_abs * eps_abs < 1e-7 * lmax) {
+        if (lmax > 0.0 && eps_abs * eps_abs < refine_threshold(n) * lmax) {
             int64_t s0 = 0;
             while (s0 < n && lh[static_cast<size_t>(s0)] >= 1e-6 * lmax) ++s0;
             const int64_t q = n - s0;
@@ -1132,6 +1144,52 @@ DT project(Context& c, const DT& t, int mode, const Basis& b, double* energy_slo
     return coeff;
 }
 
+/// t x_mode U1^T x_(mode+1) U2^T in one read of t (k_proj2.cu) when the
+/// shapes fit the fused kernel; false (nothing launched) otherwise.
+bool project_pair(Context& c, const DT& t, int mode, const Basis& b1, const Basis& b2, DT* out) {
+    if (!c.fused || mode + 2 > static_cast<int>(t.shape.size())) return false;
+    const Split sp = split_at(t.shape, mode);  // [I, J, O]
+    Proj2Args a;
+    a.Y = t.data();
+    a.n0 = sp.I;
+    a.n1 = sp.J;
+    a.n2 = t.shape[static_cast<size_t>(mode) + 1];
+    a.S = sp.O / a.n2;
+    a.U1 = b1.p;
+    a.U2 = b2.p;
+    a.r1 = static_cast<int>(b1.r);
+    a.r2 = static_cast<int>(b2.r);
+    if (b1.alpha != a.n1 || b2.alpha != a.n2 || !proj2_supported(a)) return false;
+    Shape os = t.shape;
+    os[static_cast<size_t>(mode)] = b1.r;
+    os[static_cast<size_t>(mode) + 1] = b2.r;
+    DT o = c.tensor(os);
+    a.C = o.data();
+    if (launch_proj2(a, c.s, &c.launches) < 0) return false;
+    HTR_CUDA(cudaGetLastError());
+    *out = o;
+    return true;
+}
+
+/// The projections of a layer's leaves in layer order (bht.hpp:290-293,
+/// ht_rise.hpp:160-162); two leaves over adjacent modes go through the fused
+/// pair kernel when it applies.
+DT project_leaves(Context& c, DT cur, const std::vector<TreeNode>& leaves, const std::vector<Basis>& bases) {
+    for (size_t i = 0; i < leaves.size();) {
+        const int mode = static_cast<int>(leaves[i].leaf_dim);
+        DT pr;
+        if (i + 1 < leaves.size() && leaves[i + 1].leaf_dim == leaves[i].leaf_dim + 1 &&
+            project_pair(c, cur, mode, bases[i], bases[i + 1], &pr)) {
+            cur = pr;
+            i += 2;
+            continue;
+        }
+        cur = project(c, cur, mode, bases[i], nullptr);
+        ++i;
+    }
+    return cur;
+}
+
 int64_t global_batch(Context& c, int64_t local) {
     if (!c.sharded()) return local;
     c.h_sc[0] = static_cast<double>(local);
@@ -1246,10 +1304,10 @@ BuildOut bht_l2r(Context& c, const DT& y, const DimensionTree& tree, double eps_
         ranks[n.id] = bases[i].rank;
         record(n.id, bases[i].rank, bases[i].discarded);
     }
-    for (size_t i = 0; i < bases.size(); ++i) {
-        const TreeNode& n = tree.layer(p)[i];
-        cur = project(c, cur, static_cast<int>(n.leaf_dim), {bases[i].u.data(), bases[i].u.shape[0], bases[i].rank},
-                      nullptr);
+    {
+        std::vector<Basis> lb;
+        for (const Truncation& b : bases) lb.push_back({b.u.data(), b.u.shape[0], b.rank});
+        cur = project_leaves(c, cur, tree.layer(p), lb);
     }
     push_norm(cur);
 
@@ -1929,7 +1987,11 @@ UpdateOut ht_rise_update(Context& c, const Rep& h, const DT& y, double eps_overr
 
     DT cur = y;
     expand_layer(tree.layer(p), cur, true);
-    for (const TreeNode& n : tree.layer(p)) cur = project(c, cur, static_cast<int>(n.leaf_dim), basis_of(*out, n.id), nullptr);
+    {
+        std::vector<Basis> lb;
+        for (const TreeNode& n : tree.layer(p)) lb.push_back(basis_of(*out, n.id));
+        cur = project_leaves(c, cur, tree.layer(p), lb);
+    }
 
     for (Index l = p - 1; l >= 1; --l) {
         if (adaptive) {
@@ -1990,11 +2052,13 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         bool fused = false;        // launched through the fused skip-path kernels
         bool used_fused = false;   // (report) any fused kernel in the encode
         bool scan_valid = false;   // dsc[1] is the non-finite flag of a full scan
+        bool resid = false;        // dsc[4] holds ||y - decode(latent)||^2 (explicit loss, enqueued ahead)
         cudaEvent_t done = nullptr, t0 = nullptr, t1 = nullptr;
         int64_t launches = 0;
         std::chrono::steady_clock::time_point started;
     };
     Slot slots[2];
+    bool refine_hint = false;  // the last decided batch needed the explicit loss
     // HTR_TIMELINE=1: device timeline of the stream (events around each
     // launch), printed to stderr at the end (diagnostics only)
     static const bool timeline = std::getenv("HTR_TIMELINE") != nullptr;
@@ -2062,13 +2126,19 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
             sl.used_fused = e.fused;
             sl.scan_valid = e.scan_valid;
         }
+        // the explicit loss, enqueued behind the encode when the previous
+        // batch needed it (its telescoped loss sat below the accuracy floor,
+        // as every batch of a stream near the floor does): the decision then
+        // reads it without another host round trip
+        sl.resid = refine_hint;
+        if (sl.resid) decode_residual_sq(c, h, sl.latent, sl.y, sl.dsc->p + 4);
         if (c.sharded()) {
             // the global batch count rides on the skip test's all-reduce
             sl.host[8] = static_cast<double>(nb);
             HTR_CUDA(cudaMemcpyAsync(sl.dsc->p + 8, sl.host + 8, sizeof(double), cudaMemcpyHostToDevice, c.s));
             c.allreduce(sl.dsc->p, 9);
         }
-        if (c.sharded() || !sl.fused)
+        if (c.sharded() || !sl.fused || sl.resid)
             HTR_CUDA(cudaMemcpyAsync(sl.host, sl.dsc->p, 9 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
         HTR_CUDA(cudaEventRecord(sl.done, c.s));
         mark();
@@ -2083,7 +2153,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
     auto decide = [&](Slot& sl, const Rep& h) -> std::shared_ptr<Rep> {
         HTR_CUDA(cudaEventSynchronize(sl.done));
         const int64_t nb = sl.y.shape[static_cast<size_t>(d)];
-        const double* v = (c.sharded() || !sl.fused) ? sl.host : sl.mapped;
+        const double* v = (c.sharded() || !sl.fused || sl.resid) ? sl.host : sl.mapped;
         const double ysq = v[0], latsq = v[2];
         const int64_t gbatch = c.sharded() ? static_cast<int64_t>(std::llround(v[8])) : nb;
         // non-finite input (the per-call path raises); sharded, the flag is
@@ -2101,9 +2171,10 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         double proj_sq = std::max(0.0, ysq - latsq);
         bool refined = false;
         if (proj_sq < telescope_floor_sq(h) * ysq) {  // as in encode(): re-measure explicitly
-            proj_sq = residual_sq_global(c, h, sl.latent, sl.y);
+            proj_sq = sl.resid ? v[4] : residual_sq_global(c, h, sl.latent, sl.y);
             refined = true;
         }
+        refine_hint = refined;
         if (std::abs(proj_sq - eps_des * eps_des) <= 1e-12 * ysq) return nullptr;
         const double proj_error = std::sqrt(proj_sq);
         if (!(proj_error <= eps_des)) return nullptr;

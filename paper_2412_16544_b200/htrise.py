@@ -139,6 +139,9 @@ _SIGNATURES = {
                                       C.c_int32]),
     "htr_compute_residual": (C.c_int32, [_P, _D, C.c_int64, C.c_int64, _D, C.c_int64, _D]),
     "htr_frobenius_norm": (C.c_int32, [_P, _D, C.c_int32, C.c_int64, _D]),
+    "htr_matmul": (C.c_int32, [_P, _D, C.c_int64, C.c_int64, _D, C.c_int64, _D]),
+    "htr_contract": (C.c_int32, [_P, _D, _I64, C.c_int32, C.c_int32, _D, _I64, C.c_int32, C.c_int32, _D]),
+    "htr_permute_axes": (C.c_int32, [_P, _D, _I64, C.c_int32, _I64, _D]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

@@ -86,6 +86,44 @@ static double rel_err(const DenseTensor& a, const DenseTensor& b) {
 int main() {
     std::mt19937_64 rng(77002);
 
+    {  // tensor algebra on the device (tensor.hpp:219-380) against plain loops
+        DenseTensor a = random_tensor({3, 4, 5}, rng), b = random_tensor({6, 4, 2}, rng);
+        DenseTensor c = contract(a, 1, b, 1);  // [3, 5, 6, 2]
+        CHECK((c.shape() == Shape{3, 5, 6, 2}));
+        double worst = 0.0;
+        for (Index i = 0; i < 3; ++i)
+            for (Index k = 0; k < 5; ++k)
+                for (Index p = 0; p < 6; ++p)
+                    for (Index q = 0; q < 2; ++q) {
+                        double s = 0.0;
+                        for (Index j = 0; j < 4; ++j) s += a({i, j, k}) * b({p, j, q});
+                        worst = std::max(worst, std::abs(c({i, k, p, q}) - s));
+                    }
+        CHECK(worst <= 1e-12);
+        CHECK(throws<std::invalid_argument>([&] { contract(a, 0, b, 0); }));
+        DenseTensor pt = permute_axes(a, {2, 0, 1});  // out(k, i, j) = a(i, j, k)
+        CHECK((pt.shape() == Shape{5, 3, 4}));
+        bool same = true;
+        for (Index i = 0; i < 3; ++i)
+            for (Index j = 0; j < 4; ++j)
+                for (Index k = 0; k < 5; ++k) same = same && pt({k, i, j}) == a({i, j, k});
+        CHECK(same);
+        CHECK(throws<std::invalid_argument>([&] { permute_axes(a, {0, 0, 1}); }));
+        Matrix m = random_orthonormal(7, 4, rng), n = random_orthonormal(4, 3, rng);
+        Matrix mn = m * n;
+        double err = 0.0;
+        for (Index i = 0; i < 7; ++i)
+            for (Index j = 0; j < 3; ++j) {
+                double s = 0.0;
+                for (Index k = 0; k < 4; ++k) s += m(i, k) * n(k, j);
+                err = std::max(err, std::abs(mn(i, j) - s));
+            }
+        CHECK(err <= 1e-14);
+        CHECK(throws<std::invalid_argument>([&] { (void)(m * m); }));
+        DenseTensor mm = mode_multiply(a, 2, random_orthonormal(5, 2, rng).transpose());
+        CHECK((mm.shape() == Shape{3, 4, 2}));
+    }
+
     {  // test_truncated_svd.cpp:22-36
         Matrix m = Matrix::Zero(2, 2);
         m(0, 0) = 4.0;

@@ -873,3 +873,36 @@ def test_mid_mode_gram_bht_matches_generic_and_oracle(ht, dims, ranks):
     finally:
         ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
     assert gpu.ranks() == gen.ranks()
+
+
+@pytest.mark.parametrize("dims,ranks", [
+    ((16, 12, 20), (5, 7, 9)),       # small extents, one a1 tile
+    ((64, 64, 64), (7, 12, 10)),     # config 2's extents
+    ((128, 128, 37), (20, 20, 17)),  # config 5's leaf extents, a ragged last round of slabs
+    ((24, 8, 32), (3, 8, 24)),       # r2 = 24: three a2 tiles
+])
+def test_pair_projection_bht_matches_generic_and_oracle(ht, dims, ranks):
+    """The deepest-layer leaf projections of (1,(2,3)) trees (modes 1 and 2)
+    in one read on the DMMA pair kernel (k_proj2.cu): BHT-l2r and an
+    expanding update equal the generic engine (two strided GEMMs) and the
+    oracle."""
+    rng = np.random.default_rng(sum(dims) * 7 + sum(ranks))
+    bases = [ro.random_orthonormal(n, r, rng) for n, r in zip(dims, ranks)]
+    y = ro.tucker_family_batch(bases, 5, rng) + 1e-7 * rng.standard_normal(tuple(dims) + (5,))
+    gpu, _ = ht.bht_l2r(y, ht.tree_1_23(), 1e-4)
+    ref, _ = ho.bht_l2r(y, ho.custom_tree_1_23(), 1e-4)
+    compare_reps(ht, gpu, ref)
+    ctx = gpu.ctx
+    ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+    try:
+        gen, _ = ht.bht_l2r(y, ht.tree_1_23(), 1e-4)
+    finally:
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    assert gpu.ranks() == gen.ranks()
+    # an update with new directions: the re-projection after the expansion
+    bases2 = [np.linalg.qr(np.hstack([b, rng.standard_normal((b.shape[0], 2))]))[0] for b in bases]
+    y2 = ro.tucker_family_batch(bases2, 4, rng)
+    g2, u = ht.ht_rise_update(gpu, y2)
+    r2, ur = ho.ht_rise_update(ref, y2)
+    assert u.skipped == ur.skipped and not u.skipped
+    compare_reps(ht, g2, r2)

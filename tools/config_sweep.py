@@ -31,6 +31,31 @@ for name in a.configs.split(","):
         (skip_t if upd.skipped else full_t).append(upd.seconds)
         fused += upd.used_fused_path
         del yb
+    # the same kind of batches as one stream (ht_rise_update_many, batches
+    # resident on the device): per-batch time with the host round trips
+    # pipelined behind the device work (CUDA events on the library stream)
+    P = min(nb - 1, 8 if w.bytes_per_batch < 1e9 else 3)
+    K = 24
+    stream_ms = None
+    if P >= 1:
+        pool = [ht.DeviceTensor(w.make_batch(b, "cuda"), w.shape) for b in range(1, P + 1)]
+        rep.reserve(rep.accumulated + (2 * K + 4) * w.batch)
+        vals, _ = ht.ht_rise_update_many(rep, [pool[i % P] for i in range(4)])
+        rep = vals[-1]
+        ctx.synchronize()
+        st = torch.cuda.ExternalStream(ctx.stream())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(st)
+        vals, reps = ht.ht_rise_update_many(rep, [pool[i % P] for i in range(K)])
+        e1.record(st)
+        e1.synchronize()
+        wall = time.perf_counter() - t0
+        stream_ms = e0.elapsed_time(e1) / K
+        stream_wall_ms = 1e3 * wall / K
+        stream_skips = sum(int(r.skipped) for r in reps)
+        rep = vals[-1]
+        del pool, vals
     gb = w.bytes_per_batch / 1e9
     med = sorted(skip_t)[len(skip_t) // 2] if skip_t else None
     row = {"config": name, "batch_GB": round(gb, 4), "bht_l2r_ms": round(1e3 * t_bht, 2),
@@ -41,6 +66,10 @@ for name in a.configs.split(","):
            "skip_ms_first": round(1e3 * skip_t[0], 3) if skip_t else None,
            "nonskip_ms_mean": round(1e3 * sum(full_t) / len(full_t), 3) if full_t else None,
            "skip_GBps_median": round(gb / med, 1) if skip_t else None,
+           "stream_ms_per_batch": round(stream_ms, 4) if stream_ms else None,
+           "stream_wall_ms_per_batch": round(stream_wall_ms, 4) if stream_ms else None,
+           "stream_skips": f"{stream_skips}/{K}" if stream_ms else None,
+           "stream_GBps": round(gb / stream_ms * 1e3, 1) if stream_ms else None,
            "ranks": {str(k): v for k, v in rep.ranks().items()}}
     rows.append(row)
     print(json.dumps(row), flush=True)
