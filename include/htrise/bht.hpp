@@ -92,13 +92,20 @@ struct HTRepresentation {
         return total;
     }
     IndexSet index_sets(Index batch) const { return IndexSet::build(tree, dims, ranks(), batch); }
+    /// max |U^T U - I| over the bases (bht.hpp:101-114). A validation check
+    /// of a value (also of one read from disk by the CLI's inspect, which
+    /// needs no device): evaluated on the host, entry by entry.
     double orthonormality_defect() const {
         double worst = 0.0;
         for (Index l = 1; l <= tree.depth(); ++l)
             for (const TreeNode& n : tree.layer(l)) {
                 const Matrix u = basis_matrix(n.id);
-                const Matrix g = u.transpose() * u;
-                worst = std::max(worst, (g - Matrix::Identity(g.rows(), g.cols())).maxAbs());
+                for (Index a = 0; a < u.cols(); ++a)
+                    for (Index b = 0; b <= a; ++b) {
+                        double g = 0.0;
+                        for (Index i = 0; i < u.rows(); ++i) g += u(i, a) * u(i, b);
+                        worst = std::max(worst, std::abs(g - (a == b ? 1.0 : 0.0)));
+                    }
             }
         return worst;
     }
