@@ -457,29 +457,75 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const __gr
     // per-warp scratch: u0 u1 u2 l y (5 n doubles) + piv (n bytes)
     double* scratch = Z + (z_smem ? n * r : 0);
     const int per = 5 * n + (n + 7) / 8;
+    // normalise v (n values, warp-wide), the largest entry made positive when `sign`
+    auto normalise = [&](double* v, bool sign) {
+        double s = 0.0, mx = 0.0;
+        int imx = 0;
+        for (int i = lane; i < n; i += 32) {
+            s = fma(v[i], v[i], s);
+            if (fabs(v[i]) > mx) { mx = fabs(v[i]); imx = i; }
+        }
+        s = warp_sum(s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double om = __shfl_xor_sync(0xffffffffu, mx, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, imx, o);
+            if (om > mx || (om == mx && oi < imx)) { mx = om; imx = oi; }
+        }
+        double inv = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+        if (sign && v[imx] < 0.0) inv = -inv;
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) v[i] *= inv;
+        __syncwarp();
+    };
     for (int cl = warp; cl < ncl && warp < vec_warps; cl += vec_warps) {
         double* ws = scratch + static_cast<int64_t>(warp) * per;
         TriLU f{ws, ws + n, ws + 2 * n, ws + 3 * n, reinterpret_cast<unsigned char*>(ws + 5 * n)};
-        double* y = ws + 4 * n;
-        double xprev = 0.0;
-        const bool multi = cstart[cl + 1] - cstart[cl] > 1;
-        for (int j = cstart[cl]; j < cstart[cl + 1]; ++j) {
-            double xj = lam_asc[j];
-            if (j > cstart[cl]) {  // separate coincident eigenvalues slightly (dstein)
-                const double pertol = 10.0 * fabs(DBL_EPSILON * xj);
-                if (xj - xprev < pertol) xj = xprev + pertol;
-            }
-            xprev = xj;
-            if (lane == 0) tri_factor(d, e, n, xj, tol, f);
-            for (int i = lane; i < n; i += 32) y[i] = hash_uniform(static_cast<uint32_t>(j), static_cast<uint32_t>(i));
+        const int j0 = cstart[cl], j1 = cstart[cl + 1];
+        if (j1 - j0 == 1) {
+            // an isolated eigenvalue: two inverse-iteration steps
+            double* y = Zc + static_cast<int64_t>(n) * (n - 1 - j0);
+            if (lane == 0) tri_factor(d, e, n, lam_asc[j0], tol, f);
+            for (int i = lane; i < n; i += 32) y[i] = hash_uniform(static_cast<uint32_t>(j0), static_cast<uint32_t>(i));
             __syncwarp();
-            const int iters = multi ? 3 : 2;
-            for (int it = 0; it < iters; ++it) {
+            for (int it = 0; it < 2; ++it) {
                 if (lane == 0) tri_solve(n, f, y);
                 __syncwarp();
-                // orthogonalise against the cluster's earlier vectors (twice)
-                for (int pass = 0; pass < 2 && multi; ++pass)
-                    for (int p = cstart[cl]; p < j; ++p) {
+                normalise(y, it == 1);
+            }
+            continue;
+        }
+        // a cluster: block inverse iteration -- every member solved from its
+        // current vector, then the block re-orthonormalised (modified
+        // Gram-Schmidt, twice) -- so that no member is formed from the small
+        // remainder of a vector already inside its predecessors' span
+        // (which would leave rounding-level noise as a large component)
+        for (int j = j0; j < j1; ++j) {
+            double* y = Zc + static_cast<int64_t>(n) * (n - 1 - j);
+            for (int i = lane; i < n; i += 32) y[i] = hash_uniform(static_cast<uint32_t>(j), static_cast<uint32_t>(i));
+        }
+        __syncwarp();
+        for (int it = 0; it < 3; ++it) {
+            double xprev = 0.0;
+            for (int j = j0; j < j1; ++j) {
+                double xj = lam_asc[j];
+                if (j > j0) {  // separate coincident eigenvalues slightly (dstein)
+                    const double pertol = 10.0 * fabs(DBL_EPSILON * xj);
+                    if (xj - xprev < pertol) xj = xprev + pertol;
+                }
+                xprev = xj;
+                double* y = Zc + static_cast<int64_t>(n) * (n - 1 - j);
+                if (lane == 0) {
+                    tri_factor(d, e, n, xj, tol, f);
+                    tri_solve(n, f, y);
+                }
+                __syncwarp();
+                normalise(y, false);
+            }
+            for (int j = j0; j < j1; ++j) {
+                double* y = Zc + static_cast<int64_t>(n) * (n - 1 - j);
+                for (int pass = 0; pass < 2; ++pass)
+                    for (int p = j0; p < j; ++p) {
                         const double* up = Zc + static_cast<int64_t>(n) * (n - 1 - p);
                         double s = 0.0;
                         for (int i = lane; i < n; i += 32) s = fma(up[i], y[i], s);
@@ -487,29 +533,8 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const __gr
                         for (int i = lane; i < n; i += 32) y[i] -= s * up[i];
                         __syncwarp();
                     }
-                // normalise (largest entry positive on the last pass)
-                double s = 0.0, mx = 0.0;
-                int imx = 0;
-                for (int i = lane; i < n; i += 32) {
-                    s = fma(y[i], y[i], s);
-                    if (fabs(y[i]) > mx) { mx = fabs(y[i]); imx = i; }
-                }
-                s = warp_sum(s);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const double om = __shfl_xor_sync(0xffffffffu, mx, o);
-                    const int oi = __shfl_xor_sync(0xffffffffu, imx, o);
-                    if (om > mx || (om == mx && oi < imx)) { mx = om; imx = oi; }
-                }
-                double inv = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
-                if (it == iters - 1 && y[imx] < 0.0) inv = -inv;
-                __syncwarp();
-                for (int i = lane; i < n; i += 32) y[i] *= inv;
-                __syncwarp();
+                normalise(y, it == 2);
             }
-            double* uj = Zc + static_cast<int64_t>(n) * (n - 1 - j);
-            for (int i = lane; i < n; i += 32) uj[i] = y[i];
-            __syncwarp();
         }
     }
     __syncthreads();
