@@ -53,3 +53,17 @@ print("bht ranks", rb.ranks())
 y2 = np.asfortranarray(rng.standard_normal((140, 4, 4, 8, 3)))
 rc, _ = ht.bht_l2r(y2, ht.DimensionTree.balanced(4), 1e-3)
 print("bht ranks", rc.ranks())
+# round 2: the BASELINE configs c1-c3 at their stated sizes (c2/c3: first
+# batches) -- tridiagonal eigensolver, DMMA mid-size Grams, the fused pair
+# projection, the stream API with the explicit loss enqueued ahead -- and a
+# machine-floor truncation (full eigenvector set, block inverse iteration)
+for name, nb in (("c1", 1), ("c2", 4), ("c3", 3)):
+    w = CONFIGS[name]
+    r, _ = ht.bht_l2r(ht.DeviceTensor(w.make_batch(0, "cuda"), w.shape), w.tree(), w.eps)
+    if nb > 1:
+        vals, reps = ht.ht_rise_update_many(r, [ht.DeviceTensor(w.make_batch(b, "cuda"), w.shape) for b in range(1, nb)])
+        print(name, "stream", [x.skipped for x in reps], vals[-1].ranks())
+    else:
+        print(name, "bht", r.ranks())
+m = np.linalg.qr(rng.standard_normal((40, 10)))[0] @ rng.standard_normal((10, 90))
+print("floor truncation rank", ht.truncated_svd(m, 1e-13 * np.linalg.norm(m), 0).rank)
