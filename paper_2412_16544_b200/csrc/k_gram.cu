@@ -159,6 +159,111 @@ __global__ void __launch_bounds__((consumer_warps<MB>() + 1) * 32, 1)
     (void)M;
 }
 
+// Gram of mode 0 (rows contiguous: X = Y viewed as [M, C], M <= 128): column
+// chunks of 32 staged in shared memory with a row pitch of M + 8 (the
+// fragment reads of lanes (g, t) -- row 8 i + g, column 4 s + t -- land on 32
+// distinct banks), double buffered with cp.async; one warp per 32 x 32
+// lower-triangle block as in gram_stream_kernel. Per-CTA partials, then
+// gram_reduce_kernel.
+constexpr int kG0Cols = 32;
+
+template <int MB>
+__global__ void __launch_bounds__(consumer_warps<MB>() * 32, 1)
+    gram_mode0_kernel(const double* __restrict__ X, int M, int64_t C, double* __restrict__ partials) {
+    constexpr int MP = 32 * MB;
+    constexpr int PITCH = MP + 8;
+    constexpr int NT = consumer_warps<MB>() * 32;
+    extern __shared__ __align__(16) double g0s[];  // [2][kG0Cols][PITCH]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int64_t nch = (C + kG0Cols - 1) / kG0Cols;
+    const int64_t c0 = nch * blockIdx.x / gridDim.x, c1 = nch * (blockIdx.x + 1) / gridDim.x;
+    // stage chunk q into buffer b: 16-byte copies (M even), zero rows >= M and columns >= C
+    auto stage = [&](int64_t q, int b) {
+        double* dst = g0s + b * kG0Cols * PITCH;
+        const int halves = MP / 2;
+        for (int e = tid; e < kG0Cols * halves; e += NT) {
+            const int col = e / halves, h = e - col * halves, m = 2 * h;
+            const int64_t cg = q * kG0Cols + col;
+            double* d = dst + col * PITCH + m;
+            if (cg < C && m < M) {
+                const double* src = X + cg * M + m;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(d))),
+                             "l"(src)
+                             : "memory");
+            } else {
+                d[0] = 0.0;
+                d[1] = 0.0;
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int mb = 0, nb = warp;
+    while (nb > mb) {
+        nb -= mb + 1;
+        ++mb;
+    }
+    const bool diag = mb == nb;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (c0 < c1) stage(c0, 0);
+    for (int64_t q = c0; q < c1; ++q) {
+        const int b = static_cast<int>((q - c0) & 1);
+        if (q + 1 < c1) {
+            stage(q + 1, b ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const double* ch = g0s + b * kG0Cols * PITCH;
+#pragma unroll
+        for (int ks = 0; ks < kG0Cols / 4; ++ks) {
+            const double* col = ch + (4 * ks + t4) * PITCH;
+            double af[4], bf[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) af[t] = col[32 * mb + 8 * t + g4];
+            if (diag) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) bf[t] = af[t];
+            } else {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) bf[t] = col[32 * nb + 8 * t + g4];
+            }
+#pragma unroll
+            for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+                for (int tj = 0; tj < 4; ++tj)
+                    if (!diag || tj <= ti) dmma(acc[ti][tj], af[ti], bf[tj]);
+        }
+        __syncthreads();  // the buffer is refilled two chunks later
+    }
+    double* out = partials + static_cast<int64_t>(blockIdx.x) * MP * MP;
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+        for (int tj = 0; tj < 4; ++tj) {
+            if (diag && tj > ti) continue;
+            const int m = 32 * mb + 8 * ti + g4, n = 32 * nb + 8 * tj + 2 * t4;
+            out[m + MP * n] = acc[ti][tj][0];
+            out[m + MP * (n + 1)] = acc[ti][tj][1];
+        }
+}
+
+template <int MB>
+int launch_mode0_mb(const double* X, int64_t M, int64_t C, double* partials, double* G, int num_sms, cudaStream_t s) {
+    constexpr int MP = 32 * MB;
+    const int64_t nch = (C + kG0Cols - 1) / kG0Cols;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, nch)));
+    const size_t smem = sizeof(double) * 2 * kG0Cols * (MP + 8);
+    ensure_smem_limit(reinterpret_cast<const void*>(gram_mode0_kernel<MB>), smem);
+    gram_mode0_kernel<MB><<<grid, consumer_warps<MB>() * 32, smem, s>>>(X, static_cast<int>(M), C, partials);
+    return grid;
+}
+
 // G[m, m'] = G[m', m] = sum over CTAs (in order) of the lower-triangle partial
 __global__ void gram_reduce_kernel(const double* __restrict__ partials, int nparts, int MP, int M,
                                    double* __restrict__ G) {
@@ -408,6 +513,25 @@ bool gram_stream_supported(const double* Y, int64_t K, int64_t M, int64_t B) {
 int64_t gram_stream_partials(int64_t M, int num_sms) {
     const int64_t MP = (M + 31) / 32 * 32;
     return static_cast<int64_t>(num_sms) * MP * MP;
+}
+
+bool gram_mode0_supported(const double* X, int64_t M, int64_t C) {
+    return M >= 2 && M <= 128 && (M % 2) == 0 && C >= 1 && (reinterpret_cast<uintptr_t>(X) & 15u) == 0;
+}
+
+int launch_gram_mode0(const double* X, int64_t M, int64_t C, double* partials, double* G, int num_sms, cudaStream_t s,
+                      int64_t* launches) {
+    if (!gram_mode0_supported(X, M, C)) return -1;
+    const int MB = static_cast<int>((M + 31) / 32);
+    int grid;
+    if (MB == 1) grid = launch_mode0_mb<1>(X, M, C, partials, G, num_sms, s);
+    else if (MB == 2) grid = launch_mode0_mb<2>(X, M, C, partials, G, num_sms, s);
+    else if (MB == 3) grid = launch_mode0_mb<3>(X, M, C, partials, G, num_sms, s);
+    else grid = launch_mode0_mb<4>(X, M, C, partials, G, num_sms, s);
+    gram_reduce_kernel<<<std::max(1, std::min(num_sms, static_cast<int>((M * M + 255) / 256))), 256, 0, s>>>(
+        partials, grid, 32 * MB, static_cast<int>(M), G);
+    *launches += 2;
+    return grid;
 }
 
 int launch_gram_stream(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,

@@ -286,6 +286,11 @@ bool gram_stream_supported(const double* Y, int64_t K, int64_t M, int64_t B);
 int64_t gram_stream_partials(int64_t M, int num_sms);
 int launch_gram_stream(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, double* G, int num_sms,
                        cudaStream_t s, int64_t* launches);
+/// The Gram of mode 0 (X = [M, C], rows contiguous, M even, M <= 128) on
+/// DMMA from shared-memory column chunks; partials: gram_stream_partials(M).
+bool gram_mode0_supported(const double* X, int64_t M, int64_t C);
+int launch_gram_mode0(const double* X, int64_t M, int64_t C, double* partials, double* G, int num_sms, cudaStream_t s,
+                      int64_t* launches);
 /// The same Gram for 9 <= M <= 32 rows (any K >= 1, incl. mode 0) on DMMA,
 /// four columns per k-step. partials: gram_mid_partials doubles.
 bool gram_mid_supported(int64_t K, int64_t M, int64_t B);

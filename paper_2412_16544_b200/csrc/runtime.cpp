@@ -345,6 +345,15 @@ DT gram(Context& c, const DT& t, int mode, bool reduce) {
         if (reduce) c.allreduce(G.data(), sp.J * sp.J);
         return G;
     }
+    if (c.fused && sp.I == 1 && sp.J > 32 && sp.J * sp.O >= (int64_t{1} << 16) &&
+        gram_mode0_supported(t.data(), sp.J, sp.O)) {
+        // mode 0 (rows contiguous), 33..128 rows: shared-memory column chunks on DMMA
+        BufPtr parts = c.alloc(gram_stream_partials(sp.J, c.num_sms));
+        launch_gram_mode0(t.data(), sp.J, sp.O, parts->p, G.data(), c.num_sms, c.s, &c.launches);
+        HTR_CUDA(cudaGetLastError());
+        if (reduce) c.allreduce(G.data(), sp.J * sp.J);
+        return G;
+    }
     if (c.fused && sp.J >= 9 && sp.J <= 32 && gram_mid_supported(sp.I, sp.J, sp.O) &&
         !(sp.J >= 24 && sp.I * sp.J * sp.O >= (int64_t{1} << 22) && gram_stream_supported(t.data(), sp.I, sp.J, sp.O))) {
         // 9..32 rows, any mode: DMMA over 4-column k-steps (the streaming

@@ -927,3 +927,27 @@ def test_pair_projection_bht_matches_generic_and_oracle(ht, dims, ranks):
     r2, ur = ho.ht_rise_update(ref, y2)
     assert u.skipped == ur.skipped and not u.skipped
     compare_reps(ht, g2, r2)
+
+
+@pytest.mark.parametrize("dims,ranks,n", [
+    ((64, 10, 9), (7, 4, 5), 150),     # mode 0 with 64 rows (two 32-row blocks)
+    ((34, 12, 10), (9, 5, 4), 200),    # 34 rows: a padded second block
+    ((128, 6, 5), (15, 3, 3), 120),    # config 5's 128-row mode 0
+])
+def test_mode0_gram_bht_matches_generic_and_oracle(ht, dims, ranks, n):
+    """Grams of mode 0 with 33..128 rows on the shared-memory DMMA kernel
+    (gram_mode0_kernel): BHT-l2r equals the generic engine and the oracle."""
+    rng = np.random.default_rng(sum(dims) * 11 + n)
+    bases = [ro.random_orthonormal(d, r, rng) for d, r in zip(dims, ranks)]
+    y = ro.tucker_family_batch(bases, n, rng) + 1e-6 * rng.standard_normal(tuple(dims) + (n,))
+    tree = ht.DimensionTree.balanced(3)
+    gpu, _ = ht.bht_l2r(y, tree, 1e-3)
+    ref, _ = ho.bht_l2r(y, ho.DimensionTree.balanced(3), 1e-3)
+    compare_reps(ht, gpu, ref)
+    ctx = gpu.ctx
+    ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+    try:
+        gen, _ = ht.bht_l2r(y, tree, 1e-3)
+    finally:
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    assert gpu.ranks() == gen.ranks()
