@@ -271,7 +271,9 @@ __global__ void __launch_bounds__(kBisWarps * 32) tridiag_bisect_kernel(const __
     if (blockIdx.x * kBisWarps >= n) return;
     const double* __restrict__ W = jobs.W[job];
     double* __restrict__ lam_out = jobs.lam[job];
-    __shared__ double d[1024], e2[1024];  // n <= 1024 (tridiag_supported)
+    extern __shared__ double bsm[];  // d, e^2 (2 n doubles)
+    double* d = bsm;
+    double* e2 = bsm + n;
     __shared__ double red[32];
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     const double* dg = W + tri_off_d(n);
@@ -392,6 +394,9 @@ __device__ __forceinline__ double hash_uniform(uint32_t a, uint32_t b) {
 /// Reflectors staged in shared memory for the back-transform up to this n
 /// (the strictly-below-subdiagonal part, column k at offset koff(k)).
 constexpr int kVecSmemRefN = 128;
+/// Above this n the vector kernel keeps T and its scratch in the workspace.
+constexpr int kVecSmemN = 1024;
+constexpr int kTriMaxN = 8192;
 /// Eigenvectors built in shared memory up to n * r doubles (n <= 128).
 __host__ __device__ __forceinline__ bool jobs_z_smem(int n, int r) { return n <= kVecSmemRefN && n * r <= 4096; }
 __device__ __forceinline__ int refl_off(int k, int n) { return k * (n - 2) - (k * (k - 1)) / 2; }
@@ -419,11 +424,16 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const __gr
     // tighter cluster radius: vectors of eigenvalues further apart are
     // independent to ~u ||T|| / gap and the caller's CholeskyQR2 polish
     // makes them orthonormal within the retained span)
-    __shared__ int cstart[1024 + 1];
+    // n > kVecSmemN: T, the cluster table and the per-warp scratch stay in
+    // the (L2-resident) workspace instead of shared memory
+    const bool big = n > kVecSmemN;
+    double* wbig = const_cast<double*>(W) + tri_off_d(n) + 8 * n + 8;
+    __shared__ int cstart_s[kVecSmemN + 1];
     __shared__ int ncl;
-    double* d = smem;
-    double* e = smem + n;
-    double* lam_asc = smem + 2 * n;
+    int* cstart = big ? reinterpret_cast<int*>(wbig) : cstart_s;
+    double* d = big ? const_cast<double*>(dg) : smem;
+    double* e = big ? const_cast<double*>(eg) : smem + n;
+    double* lam_asc = big ? const_cast<double*>(lam_g) : smem + 2 * n;
     const bool refl_smem = n <= kVecSmemRefN;
     double* refl = smem + 3 * n;  // staged reflectors (n <= kVecSmemRefN)
     const int nrefl = refl_smem && n > 2 ? refl_off(n - 2, n) : 0;
@@ -431,7 +441,7 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const __gr
     double* Z = smem + 3 * n + nrefl;
     const bool z_smem = jobs_z_smem(n, r);
     double* Zc = z_smem ? Z : U;
-    for (int i = tid; i < n; i += nt) {
+    for (int i = tid; i < n && !big; i += nt) {
         d[i] = dg[i];
         e[i] = eg[i];
         lam_asc[i] = lam_g[i];
@@ -455,7 +465,7 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const __gr
     __syncthreads();
     const double tol = fmax(DBL_EPSILON * onenrm, DBL_MIN);
     // per-warp scratch: u0 u1 u2 l y (5 n doubles) + piv (n bytes)
-    double* scratch = Z + (z_smem ? n * r : 0);
+    double* scratch = big ? wbig + (n + 2) : Z + (z_smem ? n * r : 0);
     const int per = 5 * n + (n + 7) / 8;
     // normalise v (n values, warp-wide), the largest entry made positive when `sign`
     auto normalise = [&](double* v, bool sign) {
@@ -570,9 +580,13 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const __gr
 
 }  // namespace
 
-int64_t tridiag_workspace_doubles(int64_t n) { return n * n + 8 * n + 8; }
+int64_t tridiag_workspace_doubles(int64_t n) {
+    // + for n > kVecSmemN: the cluster table and 16 warps' inverse-iteration scratch
+    const int64_t big = n > kVecSmemN ? (n + 2) + (kVecThreads / 32) * (5 * n + (n + 7) / 8) : 0;
+    return n * n + 8 * n + 8 + big;
+}
 
-bool tridiag_supported(int64_t n) { return n >= 1 && n <= 1024; }
+bool tridiag_supported(int64_t n) { return n >= 1 && n <= kTriMaxN; }
 
 void launch_tridiag_eigvals(const double* const* G, const int64_t* n, double* const* lambda, double* const* W,
                             int count, cudaStream_t s, int64_t* launches) {
@@ -604,7 +618,9 @@ void launch_tridiag_eigvals(const double* const* G, const int64_t* n, double* co
         kfn<<<k, threads, smem, s>>>(jobs, sm ? 1 : 0);
         // eigenvalues: a warp per eigenvalue over many CTAs
         dim3 grid(static_cast<unsigned>((nmax + kBisWarps - 1) / kBisWarps), static_cast<unsigned>(k));
-        tridiag_bisect_kernel<<<grid, kBisWarps * 32, 0, s>>>(jobs);
+        const size_t bsmem = sizeof(double) * static_cast<size_t>(2 * nmax);
+        ensure_smem_limit(reinterpret_cast<const void*>(tridiag_bisect_kernel), bsmem);
+        tridiag_bisect_kernel<<<grid, kBisWarps * 32, bsmem, s>>>(jobs);
         *launches += 2;
         i0 += k;
     }
@@ -612,9 +628,11 @@ void launch_tridiag_eigvals(const double* const* G, const int64_t* n, double* co
 
 void launch_tridiag_vectors(const double* const* W, const double* const* info, const int64_t* n, const int64_t* r,
                             double* const* U, int count, cudaStream_t s, int64_t* launches) {
-    for (int i0 = 0; i0 < count; i0 += kTriBatch) {
+    for (int i0 = 0; i0 < count;) {
         VecJobs jobs{};
-        const int k = std::min(kTriBatch, count - i0);
+        // a job above kVecSmemN runs alone (its memory lives in the workspace)
+        int k = 0;
+        while (i0 + k < count && k < kTriBatch && (k == 0 || (n[i0 + k] <= kVecSmemN && n[i0] <= kVecSmemN))) ++k;
         int64_t nmax = 1;
         for (int i = 0; i < k; ++i) {
             jobs.W[i] = W[i0 + i];
@@ -631,12 +649,15 @@ void launch_tridiag_vectors(const double* const* W, const double* const* info, c
         for (int i = 0; i < k; ++i)
             if (jobs_z_smem(jobs.n[i], jobs.r[i])) zs = std::max<int64_t>(zs, static_cast<int64_t>(jobs.n[i]) * jobs.r[i]);
         const int64_t per = 5 * nmax + (nmax + 7) / 8;
+        const bool big = nmax > kVecSmemN;
         const int64_t budget = 200 * 1024 / 8 - 3 * nmax - refl - zs;
-        const int vw = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kVecThreads / 32, budget / per)));
-        const size_t smem = sizeof(double) * static_cast<size_t>(3 * nmax + refl + zs + vw * per);
-        ensure_smem_limit(reinterpret_cast<const void*>(tridiag_vectors_kernel), smem);
+        const int vw = big ? kVecThreads / 32
+                           : static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kVecThreads / 32, budget / per)));
+        const size_t smem = big ? 0 : sizeof(double) * static_cast<size_t>(3 * nmax + refl + zs + vw * per);
+        if (smem > 0) ensure_smem_limit(reinterpret_cast<const void*>(tridiag_vectors_kernel), smem);
         tridiag_vectors_kernel<<<k, kVecThreads, smem, s>>>(jobs, vw);
         ++*launches;
+        i0 += k;
     }
 }
 

@@ -531,8 +531,13 @@ Truncation truncate_jacobi(Context& c, const DT& G, int64_t rows, int64_t cols, 
                            const ProjectedGram& refine, double noise_scale) {
     const int64_t n = rows;
     if (n > kJacobiMaxN)
-        raise(HTR_ERR_RUNTIME, "truncation of a " + std::to_string(n) + "-row unfolding exceeds the device eigensolver's " +
-                                   std::to_string(kJacobiMaxN) + "-row limit");
+        raise(HTR_ERR_RUNTIME, "truncation of a " + std::to_string(n) + "-row unfolding " +
+                                   (c.tridiag && tridiag_supported(n)
+                                        ? "at a tolerance near the Gram's rounding floor (re-measuring its small "
+                                          "eigenvalues needs every eigenvector) exceeds the " +
+                                              std::to_string(kJacobiMaxN) + "-row limit of that path"
+                                        : "exceeds the device eigensolver's " + std::to_string(kJacobiMaxN) +
+                                              "-row limit"));
     BufPtr lam = c.alloc(n);
     BufPtr V = c.alloc(n * n);
     BufPtr work = c.alloc(2 * n * n);
@@ -996,8 +1001,55 @@ Truncation truncate_mode(Context& c, const DT& t, int mode, const Basis* old, do
         }
         return truncate_cols_side(c, X, rows, cols_local, eps_abs, min_rank);
     }
+    if (reduce && rows > kColumnSideRows && cols_global < rows) {
+        // tall unfolding, batch-sharded: the column-side Gram needs every
+        // column, so each rank gathers the whole unfolding -- its own columns
+        // are one contiguous block (the batch axis is the slowest) -- through
+        // an all-reduce of a zero-initialised buffer and truncates it like a
+        // single rank; every rank computes the same bits
+        int64_t inner = 1, outer = 1;
+        for (int k = 0; k < mode; ++k) inner *= t.shape[static_cast<size_t>(k)];
+        for (size_t k = static_cast<size_t>(mode) + 1; k < t.shape.size(); ++k) outer *= t.shape[k];
+        const int64_t batch = t.shape.back();
+        const int64_t per_sample = inner * (outer / batch);  // unfolding columns per sample
+        BufPtr counts = c.alloc(c.nranks);
+        HTR_CUDA(cudaMemsetAsync(counts->p, 0, sizeof(double) * static_cast<size_t>(c.nranks), c.s));
+        c.h_sc[0] = static_cast<double>(batch);
+        HTR_CUDA(cudaMemcpyAsync(counts->p + c.rank, c.h_sc, sizeof(double), cudaMemcpyHostToDevice, c.s));
+        c.allreduce(counts->p, c.nranks);
+        std::vector<double> cnt(static_cast<size_t>(c.nranks));
+        c.fetch(counts->p, c.nranks, cnt.data());
+        int64_t s_off = 0, s_all = 0;
+        for (int r = 0; r < c.nranks; ++r) {
+            if (r < c.rank) s_off += static_cast<int64_t>(std::llround(cnt[static_cast<size_t>(r)]));
+            s_all += static_cast<int64_t>(std::llround(cnt[static_cast<size_t>(r)]));
+        }
+        const int64_t cols_all = per_sample * s_all;
+        DT X = c.tensor({rows, cols_all});
+        HTR_CUDA(cudaMemsetAsync(X.data(), 0, sizeof(double) * static_cast<size_t>(rows * cols_all), c.s));
+        launch_unfold(t.data(), inner, rows, outer, X.data() + rows * per_sample * s_off, c.s, &c.launches);
+        HTR_CUDA(cudaGetLastError());
+        c.allreduce(X.data(), rows * cols_all);
+        if (old && old->r > 0) {
+            DT T = c.tensor({old->r, cols_all});
+            GemmDesc d;  // T = U^T X
+            d.M = old->r; d.N1 = cols_all; d.K1 = rows;
+            d.A = old->p; d.sam = rows; d.sak1 = 1;
+            d.B = X.data(); d.sbk1 = 1; d.sbn1 = rows;
+            d.C = T.data(); d.scm = 1; d.scn1 = old->r;
+            run_gemm(c, d);
+            GemmDesc e;  // X -= U T
+            e.M = rows; e.N1 = cols_all; e.K1 = old->r;
+            e.A = old->p; e.sam = 1; e.sak1 = rows;
+            e.B = T.data(); e.sbk1 = 1; e.sbn1 = old->r;
+            e.C = X.data(); e.scm = 1; e.scn1 = rows;
+            e.alpha = -1.0; e.beta = 1.0;
+            run_gemm(c, e);
+        }
+        return truncate_cols_side(c, X, rows, cols_all, eps_abs, min_rank);
+    }
     DT G = gram(c, t, mode, reduce);
-    if (!old && any_basis_when_full && rows > 160 && rows <= cols_global && rows <= kJacobiMaxN) {
+    if (!old && any_basis_when_full && rows > 160 && rows <= cols_global && tridiag_supported(rows)) {
         PosdefProbe probe = posdef_launch(c, G, rows, eps_abs, c.s);
         Truncation full;
         if (posdef_finish(c, probe, rows, c.s, &full)) return full;
@@ -1021,9 +1073,9 @@ std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vecto
     for (size_t i = 0; i < modes.size(); ++i) {
         const int64_t rows = t.shape[static_cast<size_t>(modes[i])];
         const int64_t cols_local = t.size() / rows;
-        const bool column_side = !reduce && rows > kColumnSideRows && cols_local < rows;
+        const bool column_side = rows > kColumnSideRows && (reduce ? cols_global[i] < rows : cols_local < rows);
         const bool posdef =
-            !olds && any_basis_when_full && rows > 160 && rows <= cols_global[i] && rows <= kJacobiMaxN;
+            !olds && any_basis_when_full && rows > 160 && rows <= cols_global[i] && tridiag_supported(rows);
         batch[i] = !column_side && !posdef && (c.tridiag ? tridiag_supported(rows) : jacobi_batchable(rows));
         pdef[i] = !column_side && posdef;
         nb += batch[i];

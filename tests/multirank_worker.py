@@ -49,12 +49,47 @@ def core_digest(rep) -> str:
     return h.hexdigest()
 
 
-def run_case(case, rank, world, ctx):
+class TuckerWorkload:
+    """A seeded Tucker-family stream on the (1,(2,3)) tree (test cases the
+    BASELINE configs do not reach, e.g. a transfer node with more rows than
+    its unfolding has columns)."""
+
+    def __init__(self, spec):
+        self.dims = tuple(spec["dims"])
+        self.ranks = tuple(spec["ranks"])
+        self.batch = spec["batch"]
+        self.eps = spec["eps"]
+        self.seed = spec["seed"]
+
+    def tree(self):
+        return ht.tree_1_23()
+
+    def make_host(self, b):
+        rng = np.random.default_rng(self.seed)
+        bases = [np.linalg.qr(rng.standard_normal((n, r)))[0] for n, r in zip(self.dims, self.ranks)]
+        rng_b = np.random.default_rng(self.seed * 1000 + b)
+        cores = rng_b.standard_normal(tuple(self.ranks) + (self.batch,))
+        y = np.einsum("abcs,ia,jb,kc->ijks", cores, *bases)
+        return np.asfortranarray(y + 1e-9 * rng_b.standard_normal(y.shape))
+
+    def make_batch(self, b, device="cuda"):
+        y = self.make_host(b)
+        return torch.from_numpy(np.ascontiguousarray(y.transpose(3, 2, 1, 0))).to(device).reshape(-1)
+
+
+def workload_of(case):
     import dataclasses
 
+    if case.get("custom"):
+        return TuckerWorkload(case["custom"])
     w = CONFIGS[case["config"]]
     if case.get("batch"):
         w = dataclasses.replace(w, batch=case["batch"])
+    return w
+
+
+def run_case(case, rank, world, ctx):
+    w = workload_of(case)
     ref = case["oracle"]  # per batch: ranks, skipped, proj_error, eps_des; final rep
     nb = case["n_batches"]
     numel = int(np.prod(w.dims))

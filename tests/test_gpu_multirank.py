@@ -45,22 +45,31 @@ def _host(t, shape):
     return np.asfortranarray(t.cpu().numpy().reshape(tuple(reversed(shape))).transpose())
 
 
-def _oracle_case(config, n_batches, batch=None):
+def _oracle_case(config, n_batches, batch=None, custom=None):
     from paper_2412_16544_b200.workloads import CONFIGS
 
-    w = CONFIGS[config]
-    if batch:
-        w = dataclasses.replace(w, batch=batch)
-    tree = ho.custom_tree_1_23() if w.tree_kind == "1_23" else ho.DimensionTree.balanced(len(w.dims))
-    shape = tuple(w.dims) + (w.batch,)
-    ref, _ = ho.bht_l2r(_host(w.make_batch(0, "cuda"), shape), tree, w.eps)
+    if custom:
+        sys.path.insert(0, os.path.dirname(WORKER))
+        from multirank_worker import TuckerWorkload
+
+        w = TuckerWorkload(custom)
+        tree = ho.custom_tree_1_23()
+        host_batch = w.make_host
+    else:
+        w = CONFIGS[config]
+        if batch:
+            w = dataclasses.replace(w, batch=batch)
+        tree = ho.custom_tree_1_23() if w.tree_kind == "1_23" else ho.DimensionTree.balanced(len(w.dims))
+        shape = tuple(w.dims) + (w.batch,)
+        host_batch = lambda b: _host(w.make_batch(b, "cuda"), shape)  # noqa: E731
+    ref, _ = ho.bht_l2r(host_batch(0), tree, w.eps)
     ranks = [ref.ranks()]
     updates = []
     for b in range(1, n_batches):
-        ref, r = ho.ht_rise_update(ref, _host(w.make_batch(b, "cuda"), shape))
+        ref, r = ho.ht_rise_update(ref, host_batch(b))
         ranks.append(ref.ranks())
         updates.append({"skipped": bool(r.skipped), "proj_error": float(r.proj_error), "eps_des": float(r.eps_des)})
-    return {"config": config, "batch": batch, "n_batches": n_batches,
+    return {"config": config, "batch": batch, "n_batches": n_batches, "custom": custom,
             "oracle": {"ranks": ranks, "updates": updates, "final": ref}}
 
 
@@ -117,6 +126,17 @@ def test_three_ranks_uneven_shards(cuda, tmp_path):
     count come from the all-reduce, not from world * local."""
     cases = [_oracle_case("c2", 3), _oracle_case("c3", 26)]
     _check(_run_world(3, cases, tmp_path), len(cases), 3)
+
+
+def test_two_ranks_tall_transfer_gathered(cuda, tmp_path):
+    """A transfer node whose unfolding has more rows (35 x 35 = 1225) than
+    columns over all ranks (r0 x 6 samples): the column-side truncation
+    needs every column, so the sharded runtime gathers the unfolding
+    (all-reduce of a zero-initialised buffer) and every rank truncates the
+    same bits -- BHT-l2r and an expanding update."""
+    tall = {"dims": [24, 40, 40], "ranks": [5, 35, 35], "batch": 6, "eps": 1e-6, "seed": 7}
+    cases = [_oracle_case("tall", 2, custom=tall)]
+    _check(_run_world(2, cases, tmp_path), len(cases), 2)
 
 
 def test_four_ranks(cuda, tmp_path):

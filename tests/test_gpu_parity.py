@@ -94,9 +94,8 @@ def test_truncated_svd_random_vs_oracle(ht):
 @pytest.mark.parametrize("shape", [(1300, 40), (2100, 3), (1100, 1200)])
 def test_truncated_svd_large_unfolding(ht, shape):
     """Tall unfoldings go through the column-side Gram (1300 x 40, 2100 x 3);
-    a wide 1100-row one through the cluster eigensolver. All agree with the
-    oracle; past the solver's 2048-row limit on both sides the call fails
-    cleanly."""
+    wide 1100- and 2100-row ones through the tridiagonal eigensolver. All
+    agree with the oracle."""
     rows, cols = shape
     rng = np.random.default_rng(rows + cols)
     k = min(12, cols)
@@ -112,8 +111,18 @@ def test_truncated_svd_large_unfolding(ht, shape):
         assert sin_angle(b.u, a.u) <= 1e-8
         assert np.max(np.abs(a.u.T @ a.u - np.eye(a.rank))) <= 1e-12
     if shape == (2100, 3):
-        with pytest.raises(RuntimeError):
-            ht.truncated_svd(rng.standard_normal((2100, 2100)), 0.1)
+        # a wide unfolding beyond the Jacobi solvers' 2048 rows: the
+        # tridiagonal route (workspace-resident above 1024 rows)
+        k2 = 40
+        u2 = ro.random_orthonormal(2100, k2, rng)
+        m2 = u2 @ np.diag(np.logspace(0, -2, k2)) @ rng.standard_normal((k2, 2200))
+        m2 += 1e-7 * rng.standard_normal(m2.shape)
+        eps2 = 1e-3 * np.linalg.norm(m2)
+        a2, b2 = ht.truncated_svd(m2, eps2), ho.truncated_svd(m2, eps2)
+        assert a2.rank == b2.rank
+        assert abs(a2.discarded_norm - b2.discarded_norm) <= 1e-10 * np.linalg.norm(m2)
+        assert sin_angle(b2.u, a2.u) <= 1e-8
+        assert np.max(np.abs(a2.u.T @ a2.u - np.eye(a2.rank))) <= 1e-12
         z = ht.truncated_svd(np.zeros(shape), 0.1)  # zero matrix: identity column
         assert z.rank == 1 and z.u[0, 0] == 1.0 and np.count_nonzero(z.u) == 1
 
