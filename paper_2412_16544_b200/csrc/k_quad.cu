@@ -42,7 +42,9 @@ constexpr int kQBlock = QN * QN * QN * QN;  // elements per subtree block
 // rows are read with the same rotation). P1 partials are reduced over the 4
 // j-lanes by shuffles, then mode e2 runs per chunk and modes e3 + the
 // transfers per block, as above.
-constexpr int kQ2Warps = 8;
+constexpr int kQ2Warps = 8;   // finishing launch (one chunk per warp in the split mode)
+constexpr int kQ1Warps = 12;  // streaming pass over y
+constexpr int kQ1Stages = 2;
 constexpr int kQ2Threads = kQ2Warps * 32;
 constexpr int kQ2Stages = 3;
 constexpr int kQ2Chunk = 512;                        // doubles (4 KB): one e3 slice of a block
@@ -50,42 +52,42 @@ constexpr int kQ2Scratch = 128 + 512 + 256 + 64 + 16;  // S1 (one chunk), S2, S3
 
 __device__ __forceinline__ uint32_t q_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
-template <bool FINISH, bool SPLIT>
-__global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadArgs a) {
+template <bool FINISH, bool SPLIT, int NW, int NST>
+__global__ void __launch_bounds__(NW * 32, 1) quad_stream_kernel(const QuadArgs a) {
     // SPLIT (few blocks: the finishing launch): one CTA per block, warp w
     // takes chunk w (e3 = w); warp 0 finishes the block after a CTA barrier
-    static_assert(!SPLIT || kQ2Warps == QN, "one chunk per warp");
+    static_assert(!SPLIT || NW == QN, "one chunk per warp");
     __shared__ double Us[4][QN * QR];
     __shared__ double Ts[3][QR * QR * QR];
-    __shared__ double red[kQ2Warps];
-    __shared__ __align__(8) uint64_t full[kQ2Warps][kQ2Stages];
+    __shared__ double red[NW];
+    __shared__ __align__(8) uint64_t full[NW][NST];
     extern __shared__ __align__(128) double dyn[];  // [warp][stage][512] then [warp][scratch]
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int e = tid; e < 4 * QN * QR; e += kQ2Threads) {
+    for (int e = tid; e < 4 * QN * QR; e += (NW * 32)) {
         const int m = e / (QN * QR), r = e % (QN * QR), j = r / QR, q = r % QR;
         Us[m][r] = a.U[m][j + QN * q];
     }
-    for (int e = tid; e < 3 * QR * QR * QR; e += kQ2Threads) {
+    for (int e = tid; e < 3 * QR * QR * QR; e += (NW * 32)) {
         const int m = e / (QR * QR * QR), r = e % (QR * QR * QR), k = r / QR, b = r % QR;
         const double* T = m == 0 ? a.T01 : (m == 1 ? a.T23 : a.T);
         Ts[m][r] = T[k + QR * QR * b];
     }
-    double* ring = dyn + warp * kQ2Stages * kQ2Chunk;
-    double* S1 = dyn + kQ2Warps * kQ2Stages * kQ2Chunk + warp * kQ2Scratch;  // [k16][e2]
-    double* S2 = (SPLIT ? dyn + kQ2Warps * kQ2Stages * kQ2Chunk : S1) + 128;  // [k16][a2][e3] (CTA-shared in SPLIT)
+    double* ring = dyn + warp * NST * kQ2Chunk;
+    double* S1 = dyn + NW * NST * kQ2Chunk + warp * kQ2Scratch;  // [k16][e2]
+    double* S2 = (SPLIT ? dyn + NW * NST * kQ2Chunk : S1) + 128;  // [k16][a2][e3] (CTA-shared in SPLIT)
     double* S3 = S2 + 512;   // [(a0,a1,a2)][a3]
     double* V01 = S3 + 256;
     double* V = V01 + 64;
     uint64_t* bar = full[warp];
 
     const int64_t units = a.O;
-    const int64_t gw = static_cast<int64_t>(blockIdx.x) * kQ2Warps + warp;
-    const int64_t nw = static_cast<int64_t>(gridDim.x) * kQ2Warps;
+    const int64_t gw = static_cast<int64_t>(blockIdx.x) * NW + warp;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * NW;
     const int64_t my_units = gw < units ? (units - gw + nw - 1) / nw : 0;
     const int64_t chunks = SPLIT ? (blockIdx.x < units ? 1 : 0) : my_units * QN;
     auto issue = [&](int64_t g) {  // lane 0: chunk g of this warp's sequence
-        const int st = static_cast<int>(g % kQ2Stages);
+        const int st = static_cast<int>(g % NST);
         const int64_t o = SPLIT ? static_cast<int64_t>(blockIdx.x) : gw + (g / QN) * nw;
         const double* src = a.X + kQBlock * o + kQ2Chunk * (SPLIT ? warp : static_cast<int>(g % QN));
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(q_smem(&bar[st])),
@@ -98,10 +100,10 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
             : "memory");
     };
     if (lane == 0) {
-        for (int k = 0; k < kQ2Stages; ++k)
+        for (int k = 0; k < NST; ++k)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(q_smem(&bar[k])) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int k = 0; k < kQ2Stages && k < chunks; ++k) issue(k);
+        for (int k = 0; k < NST && k < chunks; ++k) issue(k);
     }
     __syncthreads();
 
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
         __syncwarp();
         if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (g + kQ2Stages < chunks) issue(g + kQ2Stages);
+            if (g + NST < chunks) issue(g + NST);
         }
         // reduce-scatter P1 over the 4 j-lanes of this e2 (fixed order): lane
         // j ends with the sums of row x0 = j, which is what it stores.
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
         __syncwarp();
         if constexpr (SPLIT) continue;  // the block is finished after the loop
         const bool block_done = k3 == QN - 1;
-        if (++st == kQ2Stages) {
+        if (++st == NST) {
             st = 0;
             parity ^= 1u;
         }
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
     __shared__ bool last;
     if (tid == 0) {
         double sum = 0.0;
-        for (int w = 0; w < kQ2Warps; ++w) sum += red[w];
+        for (int w = 0; w < NW; ++w) sum += red[w];
         a.partials[blockIdx.x] = sum;
         if constexpr (FINISH) {
             __threadfence();
@@ -295,14 +297,14 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
         // from this launch's: loads in parallel, a fixed reduction tree
         // (lane-strided sums, shuffle tree, warps in order)
         double y2 = 0.0, l2 = 0.0;
-        for (int64_t k = tid; k < a.n_ysq; k += kQ2Threads) y2 += __ldcg(a.ysq_partials + k);
-        for (unsigned k = tid; k < gridDim.x; k += kQ2Threads) l2 += __ldcg(a.partials + k);
+        for (int64_t k = tid; k < a.n_ysq; k += (NW * 32)) y2 += __ldcg(a.ysq_partials + k);
+        for (unsigned k = tid; k < gridDim.x; k += (NW * 32)) l2 += __ldcg(a.partials + k);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             y2 += __shfl_xor_sync(0xffffffffu, y2, off);
             l2 += __shfl_xor_sync(0xffffffffu, l2, off);
         }
-        __shared__ double red2[2][kQ2Warps];
+        __shared__ double red2[2][NW];
         if (lane == 0) {
             red2[0][warp] = y2;
             red2[1][warp] = l2;
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quad_stream_kernel(const QuadAr
         if (tid == 0) {
             y2 = 0.0;
             l2 = 0.0;
-            for (int w = 0; w < kQ2Warps; ++w) {
+            for (int w = 0; w < NW; ++w) {
                 y2 += red2[0][w];
                 l2 += red2[1][w];
             }
@@ -337,9 +339,21 @@ int launch_quad(const QuadArgs& a, bool finish, int num_sms, cudaStream_t s, int
     const int grid = split ? static_cast<int>(a.O)
                            : static_cast<int>(std::max<int64_t>(
                                  1, std::min<int64_t>(num_sms, (a.O + kQ2Warps - 1) / kQ2Warps)));
+    if (!finish) {
+        // the streaming pass over y: 12 warps with two-stage rings (more
+        // warps in flight per SM to cover the per-chunk dependency chains)
+        constexpr int NW = kQ1Warps, NST = kQ1Stages;
+        const int grid1 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, (a.O + NW - 1) / NW)));
+        const size_t smem = sizeof(double) * NW * (NST * kQ2Chunk + kQ2Scratch);
+        auto kfn = quad_stream_kernel<false, false, NW, NST>;
+        ensure_smem_limit(reinterpret_cast<const void*>(kfn), smem);
+        kfn<<<grid1, NW * 32, smem, s>>>(a);
+        ++*launches;
+        return grid1;
+    }
     const size_t smem = sizeof(double) * kQ2Warps * (kQ2Stages * kQ2Chunk + kQ2Scratch);
-    auto kfn = split ? quad_stream_kernel<true, true>
-                     : (finish ? quad_stream_kernel<true, false> : quad_stream_kernel<false, false>);
+    auto kfn = split ? quad_stream_kernel<true, true, kQ2Warps, kQ2Stages>
+                     : quad_stream_kernel<true, false, kQ2Warps, kQ2Stages>;
     ensure_smem_limit(reinterpret_cast<const void*>(kfn), smem);
     kfn<<<grid, kQ2Threads, smem, s>>>(a);
     ++*launches;
