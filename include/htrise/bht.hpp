@@ -248,12 +248,13 @@ inline double adaptive_budget(double eps_abs, double achieved_err_sq, Index svd_
     return std::sqrt(rem_sq) / std::sqrt(static_cast<double>(svd_remaining));
 }
 
-inline BhtResult bht_l2r(const DenseTensor& y, const DimensionTree& tree, double eps_rel,
-                         const DecompositionOptions& opts = {}) {
+namespace detail {
+inline BhtResult bht_l2r_at(const double* y, int32_t on_device, const Shape& shape, const DimensionTree& tree,
+                            double eps_rel, const DecompositionOptions& opts) {
     std::vector<htr_node> nodes = device::nodes_of(tree);
     htr_rep* out = nullptr;
     htr_build_report rep{};
-    device::check(htr_bht_l2r(device::ctx(), y.data(), 0, y.shape().data(), static_cast<int32_t>(y.order()),
+    device::check(htr_bht_l2r(device::ctx(), y, on_device, shape.data(), static_cast<int32_t>(shape.size()),
                               nodes.data(), static_cast<int64_t>(nodes.size()), eps_rel, opts.adaptive_budget ? 1 : 0,
                               &out, &rep));
     BhtResult r{HTRepresentation::from_device(device::wrap(out)), {}};
@@ -263,18 +264,41 @@ inline BhtResult bht_l2r(const DenseTensor& y, const DimensionTree& tree, double
     r.report.eps_nw_initial = rep.eps_nw_initial;
     return r;
 }
+}  // namespace detail
 
-inline std::pair<LatentBatch, double> encode(const HTRepresentation& h, const DenseTensor& y) {
+inline BhtResult bht_l2r(const DenseTensor& y, const DimensionTree& tree, double eps_rel,
+                         const DecompositionOptions& opts = {}) {
+    return detail::bht_l2r_at(y.data(), 0, y.shape(), tree, eps_rel, opts);
+}
+
+/// The same on a batch already in device memory (extension: no host copy).
+inline BhtResult bht_l2r(const device::DeviceBatch& y, const DimensionTree& tree, double eps_rel,
+                         const DecompositionOptions& opts = {}) {
+    return detail::bht_l2r_at(y.data(), 1, y.shape(), tree, eps_rel, opts);
+}
+
+namespace detail {
+inline std::pair<LatentBatch, double> encode_at(const HTRepresentation& h, const double* y, int32_t on_device,
+                                                const Shape& shape) {
     const Shape& rs = h.root().shape();  // r11 x r12 x n_acc
-    const Index batch = y.extent(y.order() - 1);
-    if (y.order() != h.tree.dims() + 1)
-        throw std::invalid_argument("encode: tensor order " + std::to_string(y.order()) + " does not match tree over " +
+    const Index order = static_cast<Index>(shape.size());
+    const Index batch = shape.back();
+    if (order != h.tree.dims() + 1)
+        throw std::invalid_argument("encode: tensor order " + std::to_string(order) + " does not match tree over " +
                                     std::to_string(h.tree.dims()) + " dims plus batch");
     DenseTensor latent({rs[0], rs[1], batch});
     double proj = 0.0;
-    device::check(htr_encode(device::ctx(), h.device_handle(), y.data(), 0, y.shape().data(),
-                             static_cast<int32_t>(y.order()), latent.data(), 0, &proj));
+    device::check(htr_encode(device::ctx(), h.device_handle(), y, on_device, shape.data(), static_cast<int32_t>(order),
+                             latent.data(), 0, &proj));
     return {LatentBatch{std::move(latent)}, proj};
+}
+}  // namespace detail
+
+inline std::pair<LatentBatch, double> encode(const HTRepresentation& h, const DenseTensor& y) {
+    return detail::encode_at(h, y.data(), 0, y.shape());
+}
+inline std::pair<LatentBatch, double> encode(const HTRepresentation& h, const device::DeviceBatch& y) {
+    return detail::encode_at(h, y.data(), 1, y.shape());
 }
 
 inline DenseTensor decode(const HTRepresentation& h, const LatentBatch& latent) {

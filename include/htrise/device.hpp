@@ -23,6 +23,39 @@
 namespace htrise {
 namespace device {
 
+/// A batch resident in device memory (htr_device_alloc), canonical layout:
+/// what the device-side ingest (normalize_on_device, metrics.hpp) produces and
+/// what bht_l2r / encode / ht_rise_update accept without a host copy.
+class DeviceBatch {
+public:
+    DeviceBatch() = default;
+    explicit DeviceBatch(Shape shape) : shape_(std::move(shape)) {
+        double* p = nullptr;
+        check(htr_device_alloc(ctx(), shape_product(shape_), &p));
+        p_ = std::shared_ptr<double>(p, [](double* q) { htr_device_free(Context::instance().get(), q); });
+    }
+    static DeviceBatch upload(const DenseTensor& t) {
+        DeviceBatch b(t.shape());
+        check(htr_copy(ctx(), b.data(), 1, t.data(), 0, t.size()));
+        return b;
+    }
+    DenseTensor download() const {
+        DenseTensor t(shape_);
+        check(htr_copy(ctx(), t.data(), 0, data(), 1, size()));
+        return t;
+    }
+    const Shape& shape() const { return shape_; }
+    Index order() const { return static_cast<Index>(shape_.size()); }
+    Index extent(Index k) const { return shape_.at(static_cast<std::size_t>(k)); }
+    Index size() const { return shape_product(shape_); }
+    const double* data() const { return p_.get(); }
+    double* data() { return p_.get(); }
+
+private:
+    Shape shape_;
+    std::shared_ptr<double> p_;
+};
+
 /// Owning handle of a device-resident representation value.
 using RepHandle = std::shared_ptr<htr_rep>;
 inline RepHandle wrap(htr_rep* r) {

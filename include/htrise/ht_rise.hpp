@@ -77,12 +77,14 @@ inline DenseTensor pad_with_zeros(const DenseTensor& core, Index slot, Index r_e
     return pad_zeros(core, slot, r_extra);
 }
 
-inline std::pair<HTRepresentation, UpdateReport> ht_rise_update(const HTRepresentation& h, const DenseTensor& y,
-                                                                const UpdateOptions& opts = {}) {
+namespace detail {
+inline std::pair<HTRepresentation, UpdateReport> ht_rise_update_at(const HTRepresentation& h, const double* y,
+                                                                   int32_t on_device, const Shape& shape,
+                                                                   const UpdateOptions& opts) {
     htr_rep* out = nullptr;
     htr_update_report rep{};
-    device::check(htr_ht_rise_update(device::ctx(), h.device_handle(), y.data(), 0, y.shape().data(),
-                                     static_cast<int32_t>(y.order()), opts.epsilon_rel.value_or(-1.0),
+    device::check(htr_ht_rise_update(device::ctx(), h.device_handle(), y, on_device, shape.data(),
+                                     static_cast<int32_t>(shape.size()), opts.epsilon_rel.value_or(-1.0),
                                      opts.adaptive_budget ? 1 : 0, &out, &rep));
     UpdateReport r;
     r.skipped = rep.skipped != 0;
@@ -95,6 +97,19 @@ inline std::pair<HTRepresentation, UpdateReport> ht_rise_update(const HTRepresen
         r.new_ranks[id] = rep.new_ranks[i];
     }
     return {HTRepresentation::from_device(device::wrap(out)), std::move(r)};
+}
+}  // namespace detail
+
+inline std::pair<HTRepresentation, UpdateReport> ht_rise_update(const HTRepresentation& h, const DenseTensor& y,
+                                                                const UpdateOptions& opts = {}) {
+    return detail::ht_rise_update_at(h, y.data(), 0, y.shape(), opts);
+}
+
+/// The same on a batch already in device memory (extension: no host copy).
+inline std::pair<HTRepresentation, UpdateReport> ht_rise_update(const HTRepresentation& h,
+                                                                const device::DeviceBatch& y,
+                                                                const UpdateOptions& opts = {}) {
+    return detail::ht_rise_update_at(h, y.data(), 1, y.shape(), opts);
 }
 
 /// Extension (not in the reference): ht_rise_update over a sequence of

@@ -2,9 +2,11 @@
 // ledger (reference /root/reference/proj/include/htrise/metrics.hpp:
 // NormalizationMethod 15-33, NormalizationParams 38-46, normalize 93-171,
 // denormalize 174-197, compression_ratio 200-207, reduction_ratio 210-214,
-// relative_test_error 218-237). normalize/denormalize run on the host: they
-// belong to the CLI ingest step above the accelerated path and are here so
-// the HTRS ledger (io.hpp) round-trips the reference's records.
+// relative_test_error 218-237). normalize / denormalize keep the
+// reference's host semantics (sequential sums in storage order, so recorded
+// ledgers match the reference's bit for bit); normalize_on_device is the
+// device prepass the CLI's ingest uses (the batch stays in HBM for the
+// compression calls).
 #pragma once
 
 #include <algorithm>
@@ -127,6 +129,41 @@ inline std::pair<DenseTensor, NormalizationParams> normalize(const DenseTensor& 
         for (Index i = 0; i < n; ++i) v[i] = (v[i] - mu) / sc;
     });
     return {std::move(out), std::move(p)};
+}
+
+/// normalize on the device (htr_normalize): the batch is uploaded once and
+/// stays there, scaled in place, for the compression calls that follow (the
+/// CLI's ingest path). Maxima are exact; the unitvec / z-score sums are
+/// deterministic tree reductions, so a recorded scale can differ from the
+/// host version's sequential sum in the last bit.
+inline std::pair<device::DeviceBatch, NormalizationParams> normalize_on_device(
+    const DenseTensor& y, NormalizationMethod method, std::optional<Index> field_axis = std::nullopt) {
+    NormalizationParams p;
+    p.method = method;
+    p.field_axis = field_axis;
+    if (field_axis) detail::require_mode(y.order(), *field_axis, "normalize");
+    const std::size_t fields = field_axis ? static_cast<std::size_t>(y.extent(*field_axis)) : 1;
+    p.scale.assign(fields, 1.0);
+    p.offset.assign(fields, 0.0);
+    std::vector<int32_t> fl(fields, 0);
+    device::DeviceBatch b = device::DeviceBatch::upload(y);
+    const int32_t m = method == NormalizationMethod::MaxAbs    ? 1
+                      : method == NormalizationMethod::UnitVec ? 2
+                      : method == NormalizationMethod::ZScore  ? 3
+                                                               : 0;
+    device::check(htr_normalize(device::ctx(), b.data(), 1, b.shape().data(), static_cast<int32_t>(b.order()), m,
+                                field_axis ? static_cast<int32_t>(*field_axis) : -1, b.data(), 1, p.scale.data(),
+                                p.offset.data(), fl.data()));
+    p.floored.assign(fields, false);
+    for (std::size_t f = 0; f < fields; ++f) p.floored[f] = fl[f] != 0;
+    return {std::move(b), std::move(p)};
+}
+
+/// ||y|| of a device batch (htr_frobenius_norm).
+inline double frobenius_norm(const device::DeviceBatch& y) {
+    double out = 0.0;
+    device::check(htr_frobenius_norm(device::ctx(), y.data(), 1, y.size(), &out));
+    return out;
 }
 
 /// Inverse of normalize for recorded parameters.

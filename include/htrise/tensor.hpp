@@ -375,7 +375,12 @@ inline DenseTensor permute_axes(const DenseTensor& t, const std::vector<Index>& 
     return out;
 }
 
-inline double frobenius_norm(const DenseTensor& t) { return t.values().norm(); }
+/// ||t|| on the device (htr_frobenius_norm).
+inline double frobenius_norm(const DenseTensor& t) {
+    double out = 0.0;
+    device::check(htr_frobenius_norm(device::ctx(), t.data(), 0, t.size(), &out));
+    return out;
+}
 
 /// Contract a(mode da) with b(mode db); result modes: a's rest then b's rest.
 inline DenseTensor contract(const DenseTensor& a, Index da, const DenseTensor& b, Index db) {

@@ -242,6 +242,29 @@ HTR_API htr_status htr_contract(htr_context* ctx, const double* a, const int64_t
                                 const double* b, const int64_t* b_shape, int32_t b_order, int32_t db, double* out);
 HTR_API htr_status htr_permute_axes(htr_context* ctx, const double* t, const int64_t* shape, int32_t order,
                                     const int64_t* perm, double* out);
+/* Device memory for batches the caller keeps on the device (e.g. ingested
+ * and normalised there before compression): cudaMalloc'd on the context's
+ * device; htr_copy moves n doubles between host and device buffers. */
+HTR_API htr_status htr_device_alloc(htr_context* ctx, int64_t n, double** ptr);
+HTR_API htr_status htr_device_free(htr_context* ctx, double* ptr);
+HTR_API htr_status htr_copy(htr_context* ctx, double* dst, int32_t dst_on_device, const double* src,
+                            int32_t src_on_device, int64_t n);
+
+/* normalize (metrics.hpp:93-171) on the device: method 0 none, 1 maxabs,
+ * 2 unitvec, 3 zscore (population sigma); field_axis -1 for one field, else
+ * one field per slice along that mode. scale / offset / floored receive one
+ * entry per field (zero scales floored to 1); out receives the scaled tensor
+ * (out may equal y on the device: in place). The per-field maxima are exact;
+ * sums are deterministic tree reductions (the reference sums sequentially:
+ * the recorded scales may differ in the last bit). */
+HTR_API htr_status htr_normalize(htr_context* ctx, const double* y, int32_t y_on_device, const int64_t* shape,
+                                 int32_t order, int32_t method, int32_t field_axis, double* out,
+                                 int32_t out_on_device, double* scale, double* offset, int32_t* floored);
+/* denormalize (metrics.hpp:174-197): out = y * scale[f] + offset[f]. */
+HTR_API htr_status htr_denormalize(htr_context* ctx, const double* y, int32_t y_on_device, const int64_t* shape,
+                                   int32_t order, int32_t method, int32_t field_axis, const double* scale,
+                                   const double* offset, double* out, int32_t out_on_device);
+
 /* compute_residual (ht_rise.hpp:31-38): R = C - U (U^T C). */
 HTR_API htr_status htr_compute_residual(htr_context* ctx, const double* u, int64_t rows, int64_t r, const double* c,
                                 int64_t cols, double* out);

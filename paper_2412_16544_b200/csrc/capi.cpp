@@ -602,6 +602,160 @@ htr_status htr_permute_axes(htr_context* ctx, const double* t, const int64_t* sh
     });
 }
 
+htr_status htr_device_alloc(htr_context* ctx, int64_t n, double** ptr) {
+    return guarded(ctx, [&] {
+        htr::Context& c = C(ctx);
+        (void)c;
+        if (!ptr || n < 0) htr::raise(HTR_ERR_INVALID_ARGUMENT, "device_alloc: bad arguments");
+        *ptr = nullptr;
+        if (n > 0) HTR_CUDA(cudaMalloc(reinterpret_cast<void**>(ptr), static_cast<size_t>(n) * sizeof(double)));
+    });
+}
+
+htr_status htr_device_free(htr_context* ctx, double* ptr) {
+    return guarded(ctx, [&] {
+        htr::Context& c = C(ctx);
+        if (ptr) {
+            HTR_CUDA(cudaStreamSynchronize(c.s));  // the context's work on it is done
+            HTR_CUDA(cudaFree(ptr));
+        }
+    });
+}
+
+htr_status htr_copy(htr_context* ctx, double* dst, int32_t dst_on_device, const double* src, int32_t src_on_device,
+                    int64_t n) {
+    return guarded(ctx, [&] {
+        htr::Context& c = C(ctx);
+        if (n <= 0) return;
+        if (!dst || !src) htr::raise(HTR_ERR_INVALID_ARGUMENT, "copy: null pointer");
+        const cudaMemcpyKind kind = dst_on_device ? (src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice)
+                                                  : (src_on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost);
+        HTR_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * static_cast<size_t>(n), kind, c.s));
+        HTR_CUDA(cudaStreamSynchronize(c.s));
+    });
+}
+
+namespace {
+/// (inner, fields) of the field view of a canonical tensor (metrics.hpp:60-74)
+std::pair<int64_t, int> field_view(const Shape& s, int32_t field_axis, int32_t order) {
+    if (field_axis < 0) return {htrise::shape_product(s), 1};
+    if (field_axis >= order)
+        htr::raise(HTR_ERR_INVALID_ARGUMENT, "normalize: mode " + std::to_string(field_axis) +
+                                                 " out of range for order " + std::to_string(order));
+    int64_t inner = 1;
+    for (int32_t k = 0; k < field_axis; ++k) inner *= s[static_cast<size_t>(k)];
+    return {inner, static_cast<int>(s[static_cast<size_t>(field_axis)])};
+}
+}  // namespace
+
+htr_status htr_normalize(htr_context* ctx, const double* y, int32_t y_on_device, const int64_t* shape, int32_t order,
+                         int32_t method, int32_t field_axis, double* out, int32_t out_on_device, double* scale,
+                         double* offset, int32_t* floored) {
+    return guarded(ctx, [&] {
+        htr::Context& c = C(ctx);
+        Shape s = to_shape(shape, order);
+        if (method < 0 || method > 3) htr::raise(HTR_ERR_INVALID_ARGUMENT, "unknown normalization method");
+        const auto [inner, F] = field_view(s, field_axis, order);
+        const int64_t n = htrise::shape_product(s);
+        DT yt = input(c, y, y_on_device != 0, s);
+        std::vector<double> sc(static_cast<size_t>(F), method == 0 ? 1.0 : 0.0), mu(static_cast<size_t>(F), 0.0);
+        std::vector<int32_t> fl(static_cast<size_t>(F), 0);
+        BufPtr parts = c.alloc(static_cast<int64_t>(htr::field_stat_blocks(c.num_sms)) * 16);
+        BufPtr stat = c.alloc(F), dmu = c.alloc(F), dsc = c.alloc(F);
+        auto stat_of = [&](int kind, const double* mup) {
+            htr::launch_field_stat(yt.data(), n, inner, F, kind, mup, parts->p, stat->p, c.num_sms, c.s, &c.launches);
+            HTR_CUDA(cudaGetLastError());
+            std::vector<double> v(static_cast<size_t>(F));
+            c.fetch(stat->p, F, v.data());
+            return v;
+        };
+        const double count = static_cast<double>(n / F);
+        if (method == 1) {
+            sc = stat_of(0, nullptr);
+        } else if (method == 2) {
+            sc = stat_of(1, nullptr);
+            for (double& m : sc) m = std::sqrt(m);
+        } else if (method == 3) {
+            mu = stat_of(2, nullptr);
+            for (double& m : mu) m /= count;
+            HTR_CUDA(cudaMemcpyAsync(dmu->p, mu.data(), sizeof(double) * static_cast<size_t>(F), cudaMemcpyHostToDevice,
+                                     c.s));
+            sc = stat_of(3, dmu->p);
+            for (double& m : sc) m = std::sqrt(m / count);
+        }
+        for (int f = 0; f < F; ++f)
+            if (sc[static_cast<size_t>(f)] == 0.0) {
+                sc[static_cast<size_t>(f)] = 1.0;
+                fl[static_cast<size_t>(f)] = 1;
+            }
+        if (scale) std::memcpy(scale, sc.data(), sizeof(double) * static_cast<size_t>(F));
+        if (offset) std::memcpy(offset, mu.data(), sizeof(double) * static_cast<size_t>(F));
+        if (floored) std::memcpy(floored, fl.data(), sizeof(int32_t) * static_cast<size_t>(F));
+        if (!out) htr::raise(HTR_ERR_INVALID_ARGUMENT, "null output pointer");
+        HTR_CUDA(cudaMemcpyAsync(dsc->p, sc.data(), sizeof(double) * static_cast<size_t>(F), cudaMemcpyHostToDevice, c.s));
+        HTR_CUDA(cudaMemcpyAsync(dmu->p, mu.data(), sizeof(double) * static_cast<size_t>(F), cudaMemcpyHostToDevice, c.s));
+        if (out_on_device) {
+            if (method == 0) {
+                if (out != yt.data())
+                    HTR_CUDA(cudaMemcpyAsync(out, yt.data(), sizeof(double) * static_cast<size_t>(n),
+                                             cudaMemcpyDeviceToDevice, c.s));
+            } else {
+                htr::launch_field_apply(yt.data(), n, inner, F, method == 3 ? dmu->p : nullptr, dsc->p, false, out,
+                                        c.num_sms, c.s, &c.launches);
+            }
+            HTR_CUDA(cudaGetLastError());
+            HTR_CUDA(cudaStreamSynchronize(c.s));
+            return;
+        }
+        DT o = c.tensor(s);
+        if (method == 0)
+            HTR_CUDA(cudaMemcpyAsync(o.data(), yt.data(), sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToDevice,
+                                     c.s));
+        else
+            htr::launch_field_apply(yt.data(), n, inner, F, method == 3 ? dmu->p : nullptr, dsc->p, false, o.data(),
+                                    c.num_sms, c.s, &c.launches);
+        HTR_CUDA(cudaGetLastError());
+        output(c, o.data(), n, out, false);
+    });
+}
+
+htr_status htr_denormalize(htr_context* ctx, const double* y, int32_t y_on_device, const int64_t* shape, int32_t order,
+                           int32_t method, int32_t field_axis, const double* scale, const double* offset, double* out,
+                           int32_t out_on_device) {
+    return guarded(ctx, [&] {
+        htr::Context& c = C(ctx);
+        Shape s = to_shape(shape, order);
+        if (method < 0 || method > 3) htr::raise(HTR_ERR_INVALID_ARGUMENT, "unknown normalization method");
+        const auto [inner, F] = field_view(s, field_axis, order);
+        const int64_t n = htrise::shape_product(s);
+        DT yt = input(c, y, y_on_device != 0, s);
+        if (!out || !scale) htr::raise(HTR_ERR_INVALID_ARGUMENT, "null pointer");
+        BufPtr dsc = c.alloc(F), dmu = c.alloc(F);
+        HTR_CUDA(cudaMemcpyAsync(dsc->p, scale, sizeof(double) * static_cast<size_t>(F), cudaMemcpyHostToDevice, c.s));
+        if (method == 3) {
+            if (!offset) htr::raise(HTR_ERR_INVALID_ARGUMENT, "null offset");
+            HTR_CUDA(cudaMemcpyAsync(dmu->p, offset, sizeof(double) * static_cast<size_t>(F), cudaMemcpyHostToDevice, c.s));
+        }
+        DT o;
+        double* dst = out;
+        if (!out_on_device) {
+            o = c.tensor(s);
+            dst = o.data();
+        }
+        if (method == 0) {
+            if (dst != yt.data())
+                HTR_CUDA(cudaMemcpyAsync(dst, yt.data(), sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToDevice,
+                                         c.s));
+        } else {
+            htr::launch_field_apply(yt.data(), n, inner, F, method == 3 ? dmu->p : nullptr, dsc->p, true, dst, c.num_sms,
+                                    c.s, &c.launches);
+        }
+        HTR_CUDA(cudaGetLastError());
+        if (!out_on_device) output(c, dst, n, out, false);
+        else HTR_CUDA(cudaStreamSynchronize(c.s));
+    });
+}
+
 htr_status htr_compute_residual(htr_context* ctx, const double* u, int64_t rows, int64_t r, const double* cm,
                                 int64_t cols, double* out) {
     return guarded(ctx, [&] {

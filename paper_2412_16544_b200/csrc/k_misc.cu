@@ -628,6 +628,123 @@ void launch_basis_defect(const double* const* U, const int64_t* alpha, const int
     }
 }
 
+// ---- per-field normalisation (metrics.hpp:93-197) ---------------------------
+// The tensor as runs of `inner` elements cycling through F fields (field f of
+// flat index e is (e / inner) % F). Each thread walks its grid-stride
+// elements tracking (position in run, field) incrementally; per-field
+// accumulators live in shared memory [field][thread] (fields [f0, f0 + nf),
+// nf <= 16), reduced per CTA in a fixed order, then over CTAs.
+constexpr int kFieldThreads = 256;
+constexpr int kFieldMax = 16;
+
+__global__ void __launch_bounds__(kFieldThreads) field_stat_kernel(const double* __restrict__ x, int64_t n,
+                                                                   int64_t inner, int F, int kind,
+                                                                   const double* __restrict__ mu, int f0, int nf,
+                                                                   double* __restrict__ partials) {
+    __shared__ double acc[kFieldMax][kFieldThreads];
+    const int tid = threadIdx.x;
+    for (int f = 0; f < nf; ++f) acc[f][tid] = 0.0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kFieldThreads;
+    int64_t e = blockIdx.x * static_cast<int64_t>(kFieldThreads) + tid;
+    int64_t r = e % inner;
+    int f = static_cast<int>((e / inner) % F);
+    const int64_t dr = stride % inner;
+    const int df = static_cast<int>((stride / inner) % F);
+    for (; e < n; e += stride) {
+        const int lf = f - f0;
+        if (lf >= 0 && lf < nf) {
+            const double v = x[e];
+            double& a = acc[lf][tid];
+            if (kind == 0) a = fmax(a, fabs(v));
+            else if (kind == 1) a = fma(v, v, a);
+            else if (kind == 2) a += v;
+            else {
+                const double d = v - mu[f];
+                a = fma(d, d, a);
+            }
+        }
+        r += dr;
+        f += df;
+        if (r >= inner) {
+            r -= inner;
+            ++f;
+        }
+        if (f >= F) f -= F;
+    }
+    __syncthreads();
+    // field lf: 32 lanes of warp (lf % warps) sum its 256 thread slots in a fixed tree
+    const int warp = tid >> 5, lane = tid & 31, nw = kFieldThreads / 32;
+    for (int lf = warp; lf < nf; lf += nw) {
+        double v = kind == 0 ? 0.0 : 0.0;
+        for (int t = lane; t < kFieldThreads; t += 32) v = kind == 0 ? fmax(v, acc[lf][t]) : v + acc[lf][t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double w = __shfl_xor_sync(0xffffffffu, v, o);
+            v = kind == 0 ? fmax(v, w) : v + w;
+        }
+        if (lane == 0) partials[static_cast<int64_t>(blockIdx.x) * nf + lf] = v;
+    }
+}
+
+__global__ void field_finish_kernel(const double* __restrict__ partials, int nparts, int nf, int kind,
+                                    double* __restrict__ out) {
+    const int lf = blockIdx.x;
+    double v = 0.0;
+    for (int p = threadIdx.x; p < nparts; p += 32) {
+        const double w = partials[static_cast<int64_t>(p) * nf + lf];
+        v = kind == 0 ? fmax(v, w) : v + w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = kind == 0 ? fmax(v, w) : v + w;
+    }
+    if (threadIdx.x == 0) out[lf] = v;
+}
+
+__global__ void field_apply_kernel(const double* __restrict__ x, int64_t n, int64_t inner, int F,
+                                   const double* __restrict__ mu, const double* __restrict__ sc, int inverse,
+                                   double* __restrict__ out) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    int64_t r = e % inner;
+    int f = static_cast<int>((e / inner) % F);
+    const int64_t dr = stride % inner;
+    const int df = static_cast<int>((stride / inner) % F);
+    for (; e < n; e += stride) {
+        const double m = mu ? mu[f] : 0.0;
+        out[e] = inverse ? fma(x[e], sc[f], m) : (x[e] - m) / sc[f];
+        r += dr;
+        f += df;
+        if (r >= inner) {
+            r -= inner;
+            ++f;
+        }
+        if (f >= F) f -= F;
+    }
+}
+
+int field_stat_blocks(int num_sms) { return 2 * num_sms; }
+
+void launch_field_stat(const double* x, int64_t n, int64_t inner, int F, int kind, const double* mu, double* partials,
+                       double* out, int num_sms, cudaStream_t s, int64_t* launches) {
+    const int grid = field_stat_blocks(num_sms);
+    for (int f0 = 0; f0 < F; f0 += kFieldMax) {
+        const int nf = std::min(kFieldMax, F - f0);
+        field_stat_kernel<<<grid, kFieldThreads, 0, s>>>(x, n, inner, F, kind, mu, f0, nf, partials);
+        field_finish_kernel<<<nf, 32, 0, s>>>(partials, grid, nf, kind, out + f0);
+        *launches += 2;
+    }
+}
+
+void launch_field_apply(const double* x, int64_t n, int64_t inner, int F, const double* mu, const double* sc,
+                        bool inverse, double* out, int num_sms, cudaStream_t s, int64_t* launches) {
+    if (n == 0) return;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4 * num_sms, (n + 255) / 256)));
+    field_apply_kernel<<<grid, 256, 0, s>>>(x, n, inner, F, mu, sc, inverse ? 1 : 0, out);
+    ++*launches;
+}
+
 constexpr int kPermMax = 16;
 struct PermArgs {
     int d;

@@ -163,6 +163,18 @@ void launch_unfold(const double* src, int64_t inner, int64_t ext, int64_t outer,
 void launch_orthonormalize_new(const double* U, int64_t alpha, int64_t r, double* W, int64_t q, double* info,
                                double* work, cudaStream_t s, int64_t* launches);
 
+// Per-field statistics of x (n elements; field of flat index e is
+// (e / inner) % F): kind 0 max |v|, 1 sum v^2, 2 sum v, 3 sum (v - mu[f])^2;
+// out[f] for every field (deterministic: fixed per-CTA and cross-CTA
+// orders). partials: field_stat_blocks(num_sms) * 16 doubles.
+int field_stat_blocks(int num_sms);
+void launch_field_stat(const double* x, int64_t n, int64_t inner, int F, int kind, const double* mu, double* partials,
+                       double* out, int num_sms, cudaStream_t s, int64_t* launches);
+// out = (x - mu[f]) / sc[f], or with `inverse` out = x * sc[f] + mu[f]
+// (mu may be null: 0).
+void launch_field_apply(const double* x, int64_t n, int64_t inner, int F, const double* mu, const double* sc,
+                        bool inverse, double* out, int num_sms, cudaStream_t s, int64_t* launches);
+
 // dst = src with its axes permuted: output mode k is input mode perm[k]
 // (d <= 16, canonical layouts).
 void launch_permute(const double* src, const int64_t* shape, int d, const int64_t* perm, double* dst, cudaStream_t s,

@@ -142,6 +142,13 @@ _SIGNATURES = {
     "htr_matmul": (C.c_int32, [_P, _D, C.c_int64, C.c_int64, _D, C.c_int64, _D]),
     "htr_contract": (C.c_int32, [_P, _D, _I64, C.c_int32, C.c_int32, _D, _I64, C.c_int32, C.c_int32, _D]),
     "htr_permute_axes": (C.c_int32, [_P, _D, _I64, C.c_int32, _I64, _D]),
+    "htr_device_alloc": (C.c_int32, [_P, C.c_int64, C.POINTER(_D)]),
+    "htr_device_free": (C.c_int32, [_P, _D]),
+    "htr_copy": (C.c_int32, [_P, _D, C.c_int32, _D, C.c_int32, C.c_int64]),
+    "htr_normalize": (C.c_int32, [_P, _D, C.c_int32, _I64, C.c_int32, C.c_int32, C.c_int32, _D, C.c_int32, _D, _D,
+                                  C.POINTER(C.c_int32)]),
+    "htr_denormalize": (C.c_int32, [_P, _D, C.c_int32, _I64, C.c_int32, C.c_int32, C.c_int32, _D, _D, _D,
+                                    C.c_int32]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
@@ -968,6 +975,61 @@ def relative_error(h: HTRepresentation, y) -> float:
     ctx.check(lib().htr_relative_error(ctx.handle, h.handle, p, on_dev, _shape_arr(shape), len(shape), C.byref(out)))
     del keep
     return float(out.value)
+
+
+_NORM_METHODS = {"none": 0, "maxabs": 1, "unitvec": 2, "zscore": 3}
+
+
+@dataclass
+class NormalizationParams:
+    """metrics.hpp:38-46."""
+    method: str
+    field_axis: Optional[int]
+    scale: List[float]
+    offset: List[float]
+    floored: List[bool]
+
+
+def normalize(y, method: str = "none", field_axis: Optional[int] = None, ctx: Optional[Context] = None):
+    """metrics.hpp:93-171 on the device (htr_normalize). Host arrays in,
+    host array out; a DeviceTensor is scaled in place. Returns (scaled,
+    NormalizationParams)."""
+    ctx = ctx or default_context()
+    if method not in _NORM_METHODS:
+        raise ValueError("unknown normalization method: " + str(method))
+    p, on_dev, shape, keep = _tensor_arg(y, ctx)
+    fields = 1 if field_axis is None else int(shape[field_axis]) if 0 <= field_axis < len(shape) else 1
+    sc = np.zeros(fields)
+    off = np.zeros(fields)
+    fl = (C.c_int32 * fields)()
+    if on_dev:
+        out_p, out = p, y
+    else:
+        out = np.zeros(int(np.prod(shape)), dtype=np.float64)
+        out_p = _ptr(out)
+    ctx.check(lib().htr_normalize(ctx.handle, p, on_dev, _shape_arr(shape), len(shape), _NORM_METHODS[method],
+                                  -1 if field_axis is None else int(field_axis), out_p, on_dev, _ptr(sc), _ptr(off),
+                                  fl))
+    del keep
+    params = NormalizationParams(method, field_axis, sc.tolist(), off.tolist(), [bool(x) for x in fl])
+    if not on_dev:
+        out = out.reshape(shape, order="F")
+    return out, params
+
+
+def denormalize(y, params: NormalizationParams, ctx: Optional[Context] = None):
+    """metrics.hpp:174-197 on the device (htr_denormalize)."""
+    ctx = ctx or default_context()
+    p, on_dev, shape, keep = _tensor_arg(y, ctx)
+    sc = np.asarray(params.scale, dtype=np.float64)
+    off = np.asarray(params.offset, dtype=np.float64)
+    out = np.zeros(int(np.prod(shape)), dtype=np.float64)
+    ctx.check(lib().htr_denormalize(ctx.handle, p, on_dev, _shape_arr(shape), len(shape),
+                                    _NORM_METHODS[params.method],
+                                    -1 if params.field_axis is None else int(params.field_axis), _ptr(sc),
+                                    _ptr(off), _ptr(out), 0))
+    del keep
+    return out.reshape(shape, order="F")
 
 
 def relative_test_error(h: HTRepresentation, test_set) -> float:
