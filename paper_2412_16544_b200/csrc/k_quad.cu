@@ -99,6 +99,14 @@ __global__ void __launch_bounds__(NW * 32, 1) quad_stream_kernel(const QuadArgs 
             "l"(src), "r"(kQ2Chunk * 8), "r"(q_smem(&bar[st]))
             : "memory");
     };
+    if constexpr (FINISH) {
+        // launched as a programmatic dependent of the streaming pass: the
+        // bases above were staged while that grid drained; its output (this
+        // launch's input) and ||y||^2 partials are complete past this point
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    } else {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
     if (lane == 0) {
         for (int k = 0; k < NST; ++k)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(q_smem(&bar[k])) : "memory");
@@ -355,7 +363,18 @@ int launch_quad(const QuadArgs& a, bool finish, int num_sms, cudaStream_t s, int
     auto kfn = split ? quad_stream_kernel<true, true, kQ2Warps, kQ2Stages>
                      : quad_stream_kernel<true, false, kQ2Warps, kQ2Stages>;
     ensure_smem_limit(reinterpret_cast<const void*>(kfn), smem);
-    kfn<<<grid, kQ2Threads, smem, s>>>(a);
+    // programmatic dependent launch after the streaming pass (griddepcontrol.wait in the kernel)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kQ2Threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kfn, a);
     ++*launches;
     return grid;
 }
