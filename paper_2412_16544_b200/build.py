@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhtrise_cuda.so")
-SOURCES = ["k_gemm.cu", "k_misc.cu", "k_eig.cu", "k_fused3.cu", "k_tail3.cu", "k_quad.cu", "k_decode.cu", "k_gram.cu", "k_tridiag.cu", "k_proj2.cu"]
+SOURCES = ["k_gemm.cu", "k_misc.cu", "k_eig.cu", "k_fused3.cu", "k_tail3.cu", "k_tail4.cu", "k_quad.cu", "k_decode.cu", "k_gram.cu", "k_tridiag.cu", "k_proj2.cu"]
 HOST_SOURCES = ["runtime.cpp", "capi.cpp"]
 CXX = os.environ.get("CXX", "g++")
 CUDA_INC = "/usr/local/cuda/include"

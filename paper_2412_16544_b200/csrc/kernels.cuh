@@ -255,6 +255,30 @@ struct Tail3Args {
     bool identity_transfer = false;  // B == I (rt == r1 r2): latent = Z, no projection
 };
 bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2);
+
+// Skip-path tail for balanced 4-way trees ((1,2),(3,4)), one CTA per sample
+// (k_tail4.cu): from fused3's per-slab W = [R01 = r0 r1, n2, n3, S] to the
+// latent [r12, r34, S] through B12 (R01 x r12), U2 (n2 x r2), U3 (n3 x r3)
+// and B34 (r2 r3 x r34), with ||latent_s||^2 and the final scalar reductions
+// as in Tail3Args.
+struct Tail4Args {
+    const double* W = nullptr;
+    const double* B12 = nullptr;
+    const double* U2 = nullptr;
+    const double* U3 = nullptr;
+    const double* B34 = nullptr;
+    int R01 = 0, r12 = 0, r2 = 0, r3 = 0, r34 = 0;
+    int64_t n2 = 0, n3 = 0, S = 0;
+    double* latent = nullptr;
+    double* latsq = nullptr;  // S entries
+    const double* ysq_partials = nullptr;
+    int64_t n_ysq = 0;
+    double* out = nullptr;
+    double* host_out = nullptr;
+    unsigned int* ticket = nullptr;  // zero on entry, left zero on exit
+};
+bool tail4_supported(int R01, int r12, int r34, int r2, int r3, int64_t n2, int64_t n3);
+void launch_tail4(const Tail4Args& a, cudaStream_t s, int64_t* launches);
 // (identity_transfer is honoured by the per-sample/cluster kernel; the
 // sample-pair variant falls back to it)
 

@@ -1571,9 +1571,90 @@ bool launch_skip_encode8(Context& c, const Rep& h, const DT& y, const DT* latent
     return true;
 }
 
+/// Balanced 4-way trees ((1,2),(3,4)) (config 3): fused3 over the [n0, n1]
+/// slabs (modes 0, 1 and ||y||^2) + the per-sample tail (k_tail4.cu).
+bool launch_skip_encode4(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc, DT* latent,
+                         cudaEvent_t ev0, cudaEvent_t ev1, double* host_out) {
+    const DimensionTree& tree = h.tree;
+    if (tree.dims() != 4 || tree.depth() != 2 || tree.layer_size(1) != 2) return false;
+    const TreeNode* tr[2];
+    const TreeNode* leaf[4];
+    for (int side = 0; side < 2; ++side) {
+        tr[side] = &tree.node(NodeId{1, side});
+        if (tr[side]->kind != NodeKind::Transfer) return false;
+        for (int k = 0; k < 2; ++k) {
+            const TreeNode& l = tree.node(tr[side]->successors[static_cast<size_t>(k)]);
+            if (l.kind != NodeKind::Leaf || l.leaf_dim != 2 * side + k) return false;
+            leaf[2 * side + k] = &l;
+        }
+    }
+    const Basis b0 = basis_of(h, leaf[0]->id), b1 = basis_of(h, leaf[1]->id), b2 = basis_of(h, leaf[2]->id),
+                b3 = basis_of(h, leaf[3]->id), B12 = basis_of(h, tr[0]->id), B34 = basis_of(h, tr[1]->id);
+    const int64_t n0 = y.shape[0], n1 = y.shape[1], n2 = y.shape[2], n3 = y.shape[3], batch = y.shape[4];
+    const int64_t R01 = b0.r * b1.r;
+    if (b0.r > 24 || b1.r > 24 || b2.r > 24 || b3.r > 24 || B12.r > 24 || B34.r > 1024 || batch < 1) return false;
+    if (!fused3_supported(n0, n1, n2 * n3 * batch, static_cast<int>(b0.r), static_cast<int>(b1.r), 1) ||
+        !tail4_supported(static_cast<int>(R01), static_cast<int>(B12.r), static_cast<int>(B34.r),
+                         static_cast<int>(b2.r), static_cast<int>(b3.r), n2, n3) ||
+        (reinterpret_cast<uintptr_t>(y.data()) & 15u) != 0)
+        return false;
+    DT W = c.tensor({b0.r, b1.r, n2, n3, batch});
+    Fused3Args fa;
+    fa.Y = y.data();
+    fa.n2 = n2 * n3 * batch;
+    fa.S = 1;
+    fa.U0 = b0.p;
+    fa.U1 = b1.p;
+    fa.r0 = static_cast<int>(b0.r);
+    fa.r1 = static_cast<int>(b1.r);
+    fa.r2 = 1;
+    fa.slab_gemm = false;
+    fa.wslab = W.data();
+    BufPtr parts = c.alloc(c.num_sms + static_cast<int64_t>(c.num_sms) * 24 * R01);
+    fa.ysq_partials = parts->p;
+    if (ev0) HTR_CUDA(cudaEventRecord(ev0, c.s));
+    const int grid = launch_fused3(n0, n1, fa, c.num_sms, c.s, &c.launches);
+    if (ev1) HTR_CUDA(cudaEventRecord(ev1, c.s));
+    HTR_CUDA(cudaGetLastError());
+    if (grid <= 0) return false;  // no tensor map for this pointer: nothing was launched
+    Tail4Args ta;
+    ta.W = W.data();
+    ta.B12 = B12.p;
+    ta.U2 = b2.p;
+    ta.U3 = b3.p;
+    ta.B34 = B34.p;
+    ta.R01 = static_cast<int>(R01);
+    ta.r12 = static_cast<int>(B12.r);
+    ta.r2 = static_cast<int>(b2.r);
+    ta.r3 = static_cast<int>(b3.r);
+    ta.r34 = static_cast<int>(B34.r);
+    ta.n2 = n2;
+    ta.n3 = n3;
+    ta.S = batch;
+    DT lat;
+    if (latent_target && latent_target->shape == Shape{B12.r, B34.r, batch}) {
+        lat = *latent_target;
+    } else {
+        lat = c.tensor({B12.r, B34.r, batch});
+    }
+    ta.latent = lat.data();
+    BufPtr lsq = c.alloc(batch);
+    ta.latsq = lsq->p;
+    ta.ysq_partials = parts->p;
+    ta.n_ysq = grid;
+    ta.out = sc;
+    ta.host_out = host_out;
+    ta.ticket = c.d_ticket;
+    launch_tail4(ta, c.s, &c.launches);
+    HTR_CUDA(cudaGetLastError());
+    *latent = lat;
+    return true;
+}
+
 bool launch_skip_encode_fused(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc,
                               DT* latent, cudaEvent_t ev0, cudaEvent_t ev1, double* host_out) {
     return launch_skip_encode3(c, h, y, latent_target, sc, latent, ev0, ev1, host_out) ||
+           launch_skip_encode4(c, h, y, latent_target, sc, latent, ev0, ev1, host_out) ||
            launch_skip_encode8(c, h, y, latent_target, sc, latent, ev0, ev1, host_out);
 }
 
@@ -1689,10 +1770,12 @@ EncodeOut encode(Context& c, const Rep& h, const DT& y, bool exact, const DT* la
                 }
             }
         }
-    } else if (!exact && c.fused && d == 8) {
+    } else if (!exact && c.fused && (d == 8 || d == 4)) {
         DT lat;
-        if (launch_skip_encode8(c, h, y, latent_target, sc, &lat, prof ? c.ev[0] : nullptr,
-                                prof ? c.ev[1] : nullptr, host_out)) {
+        if (d == 8 ? launch_skip_encode8(c, h, y, latent_target, sc, &lat, prof ? c.ev[0] : nullptr,
+                                         prof ? c.ev[1] : nullptr, host_out)
+                   : launch_skip_encode4(c, h, y, latent_target, sc, &lat, prof ? c.ev[0] : nullptr,
+                                         prof ? c.ev[1] : nullptr, host_out)) {
             leaves_done = tail_done = out.fused = true;
             cur = lat;
         }

@@ -280,7 +280,11 @@ bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent
 /// 4-leaf subtree launches, config 4).
 bool launch_skip_encode8(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc, DT* latent,
                          cudaEvent_t ev0, cudaEvent_t ev1, double* host_out = nullptr);
-/// Whichever fused skip-path encode applies (3-way or 8-way); false when none.
+/// The same for balanced 4-way trees ((1,2),(3,4)) whose leading slabs fit the
+/// fused leaf kernel (config 3): fused3 over modes 0, 1 + the per-sample tail.
+bool launch_skip_encode4(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc, DT* latent,
+                         cudaEvent_t ev0, cudaEvent_t ev1, double* host_out = nullptr);
+/// Whichever fused skip-path encode applies (3-, 4- or 8-way); false when none.
 bool launch_skip_encode_fused(Context& c, const Rep& h, const DT& y, const DT* latent_target, double* sc,
                               DT* latent, cudaEvent_t ev0, cudaEvent_t ev1, double* host_out = nullptr);
 

@@ -389,6 +389,63 @@ def test_fused_tail_tile_cases(ht, ranks, n2, nsamp, n01):
     assert g2.ranks() == r2.ranks()
 
 
+@pytest.mark.parametrize("dims,ranks,nsamp", [
+    ((32, 32, 32, 8), (6, 6, 6, 6), 16),     # the c3 shape before its rank growth
+    ((32, 32, 32, 8), (12, 12, 12, 8), 5),   # after it: r0 r1 = 144 rows, two tiles of r12
+    ((32, 32, 5, 7), (3, 5, 2, 4), 3),       # ragged columns (35: a partial 8-column tile), odd ranks
+    ((64, 64, 9, 3), (7, 2, 9, 3), 2),       # 64 x 64 slabs, r0 r1 = 14 (k tail), full-rank last leaf
+    ((32, 32, 1, 6), (4, 4, 1, 2), 4),       # a singleton mode
+    ((128, 64, 4, 4), (17, 3, 4, 4), 1),     # mixed slab extents, one sample, r12 over three tiles
+])
+def test_balanced4_fused_tail_cases(ht, dims, ranks, nsamp):
+    """fused3 (modes 0, 1) + tail4 (k_tail4.cu), the skip-path encode of
+    balanced ((1,2),(3,4)) trees, against the generic per-mode chain and the
+    oracle across the tail's tile counts (bht.hpp:381-399)."""
+    rng = np.random.default_rng(sum(dims) * 100 + sum(ranks))
+    bases = [ro.random_orthonormal(n, r, rng) for n, r in zip(dims, ranks)]
+
+    def fam(n):
+        core = rng.standard_normal(tuple(ranks) + (n,))
+        return np.asfortranarray(np.einsum("abcds,ia,jb,kc,ld->ijkls", core, *bases))
+
+    y0 = fam(max(nsamp, int(np.prod(ranks[:2])) + 3))
+    rep, _ = ht.bht_l2r(y0, ht.DimensionTree.balanced(4), 1e-9)
+    ref, _ = ho.bht_l2r(y0, ho.DimensionTree.balanced(4), 1e-9)
+    assert rep.ranks() == ref.ranks()
+    y1 = fam(nsamp)
+    ctx = rep.ctx
+    n0 = ctx.launch_count()
+    la, pa = ht.encode(rep, y1)
+    assert ctx.launch_count() - n0 <= 3  # fused3 + tail4 (+ the explicit loss when below the floor)
+    ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+    try:
+        lb, pb = ht.encode(rep, y1)
+    finally:
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    lr, _ = ho.encode(ref, y1)
+    assert la.shape == lb.shape == lr.shape
+    assert np.linalg.norm(la - lb) <= 1e-12 * np.linalg.norm(lb)
+    assert np.allclose(np.linalg.norm(la, axis=(0, 1)), np.linalg.norm(lr, axis=(0, 1)), rtol=1e-10, atol=0)
+    rec, rec_ref = ht.decode(rep, la), ho.decode(ref, lr)
+    assert np.linalg.norm(rec - rec_ref) <= 1e-9 * np.linalg.norm(rec_ref)
+    assert np.linalg.norm(rec - y1) <= 1e-9 * np.linalg.norm(y1)
+    g2, upd = ht.ht_rise_update(rep, y1)
+    r2, ur = ho.ht_rise_update(ref, y1)
+    assert upd.skipped == ur.skipped
+    assert g2.ranks() == r2.ranks()
+    # the stream API takes the same kernels; a looser eps keeps the decision
+    # away from the guard band so the fused launch pair decides alone
+    rep3, _ = ht.bht_l2r(y0, ht.DimensionTree.balanced(4), 1e-4)
+    ref3, _ = ho.bht_l2r(y0, ho.DimensionTree.balanced(4), 1e-4)
+    ys = [fam(nsamp) for _ in range(3)]
+    vals, reps = ht.ht_rise_update_many(rep3, ys)
+    for yb, u in zip(ys, reps):
+        ref3, ur = ho.ht_rise_update(ref3, yb)
+        assert u.skipped == ur.skipped and u.used_fused_path
+        assert abs(u.proj_error - ur.proj_error) <= 1e-9 * np.linalg.norm(yb)
+    compare_reps(ht, vals[-1], ref3, check_slices=True)
+
+
 def test_fused_skip_writes_root_slot_with_value_semantics(ht):
     """On the fused path the tail writes a skipped batch's latent straight into
     the shared root store's next slices. Branching from an older value must
