@@ -109,17 +109,24 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 
 struct RangeInfo {
     int64_t T;  // total slabs = n2 * S
+    int n0, n1; // slab extents (<= the kernel's N0, N1; n0 even)
 };
 
 __host__ __device__ __forceinline__ int64_t cta_begin(int64_t T, int64_t b, int64_t B) { return (T * b) / B; }
 
-template <int N0, int N1, int MT0, int MT1>
+// EXACT: the slabs are N0 x N1 (all step counts compile-time). Otherwise the
+// slabs are n0 x n1 with n0 <= N0 (even), n1 <= N1: the tensor map carries
+// the true extents, TMA zero-fills the out-of-range part of a box, the basis
+// fragments are zero beyond n0 / n1, and only the steps that touch the slab
+// are walked (n0 = 96 on the 128-row kernel: 3 of 4 row quarters).
+template <int N0, int N1, int MT0, int MT1, bool EXACT>
 __global__ void __launch_bounds__(kThreads, 1)
     fused3_kernel(const Fused3Args a, const RangeInfo ri, const __grid_constant__ CUtensorMap tmap) {
     constexpr int NC = N0 / 8;      // 8-row chunks per column block
-    constexpr int NQ = N0 / kRows;  // steps per column pair
-    constexpr int NP = N1 / kCols;  // column pairs per slab
-    constexpr int IPS = NP * NQ;    // steps per slab
+    const int n0 = EXACT ? N0 : ri.n0, n1 = EXACT ? N1 : ri.n1;
+    const int NQ = EXACT ? N0 / kRows : (ri.n0 + kRows - 1) / kRows;  // steps per column pair
+    const int NP = EXACT ? N1 / kCols : (ri.n1 + kCols - 1) / kCols;  // column pairs per slab
+    const int IPS = NP * NQ;        // steps per slab
     extern __shared__ __align__(1024) double smem_raw[];
     // stages first: the 128-byte swizzle needs 1024-byte aligned boxes
     double* stages = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u) / sizeof(double);  // [warp][stage][box][col][16]
@@ -191,8 +198,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int l = idx & 31, mt = (idx >> 5) % MT0, c = idx / (32 * MT0);
         const int i0 = 8 * c + 2 * (l & 3), col = 8 * mt + (l >> 2);
         double2 v;
-        v.x = col < a.r0 ? a.U0[i0 + static_cast<int64_t>(N0) * col] : 0.0;
-        v.y = col < a.r0 ? a.U0[i0 + 1 + static_cast<int64_t>(N0) * col] : 0.0;
+        const bool ok = col < a.r0 && i0 < n0;  // (n0 even: i0 + 1 < n0 too)
+        v.x = ok ? a.U0[i0 + static_cast<int64_t>(n0) * col] : 0.0;
+        v.y = ok ? a.U0[i0 + 1 + static_cast<int64_t>(n0) * col] : 0.0;
         U0f[idx] = v;
     }
     for (int idx = tid; idx < (N1 / 8) * MT1 * 32; idx += kThreads) {
@@ -200,8 +208,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int i1x = 8 * nt + col_perm(2 * (l & 3)), i1y = 8 * nt + col_perm(2 * (l & 3) + 1);
         const int col = 8 * mt + (l >> 2);
         double2 v;
-        v.x = col < a.r1 ? a.U1[i1x + static_cast<int64_t>(N1) * col] : 0.0;
-        v.y = col < a.r1 ? a.U1[i1y + static_cast<int64_t>(N1) * col] : 0.0;
+        v.x = (col < a.r1 && i1x < n1) ? a.U1[i1x + static_cast<int64_t>(n1) * col] : 0.0;
+        v.y = (col < a.r1 && i1y < n1) ? a.U1[i1y + static_cast<int64_t>(n1) * col] : 0.0;
         U1f[idx] = v;
     }
     __syncthreads();
@@ -375,18 +383,18 @@ bool make_batch_map(CUtensorMap* map, const double* Y, int64_t N0, int64_t N1, i
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int N0, int N1, int MT0, int MT1>
-int launch_impl(const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {
+template <int N0, int N1, int MT0, int MT1, bool EXACT>
+int launch_impl(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {
     const int64_t T = a.n2 * a.S;
     const int64_t B = std::min<int64_t>(num_sms, T);
-    RangeInfo ri{T};
+    RangeInfo ri{T, static_cast<int>(n0), static_cast<int>(n1)};
     Fused3Args args = a;
     args.wpart = a.ysq_partials + B;  // B * kWarps * 2 * r0 r1 doubles (fused3_workspace_doubles)
     alignas(64) CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
-    if (!make_batch_map(&map, a.Y, N0, N1, T)) return -1;
+    if (!make_batch_map(&map, a.Y, n0, n1, T)) return -1;
     const size_t smem = smem_bytes<N0, N1, MT0, MT1>();
-    auto kfn = fused3_kernel<N0, N1, MT0, MT1>;
+    auto kfn = fused3_kernel<N0, N1, MT0, MT1, EXACT>;
     ensure_smem_limit(reinterpret_cast<const void*>(kfn), smem);
     kfn<<<static_cast<unsigned>(B), kThreads, smem, s>>>(args, ri, map);
     ++*launches;
@@ -414,12 +422,12 @@ int launch_impl(const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launc
     return static_cast<int>(B);
 }
 
-template <int N0, int N1>
-int dispatch_mt(int mt, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {
+template <int N0, int N1, bool EXACT>
+int dispatch_mt(int mt, int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {
     switch (mt) {
-        case 1: return launch_impl<N0, N1, 1, 1>(a, num_sms, s, launches);
-        case 2: return launch_impl<N0, N1, 2, 2>(a, num_sms, s, launches);
-        case 3: return launch_impl<N0, N1, 3, 3>(a, num_sms, s, launches);
+        case 1: return launch_impl<N0, N1, 1, 1, EXACT>(n0, n1, a, num_sms, s, launches);
+        case 2: return launch_impl<N0, N1, 2, 2, EXACT>(n0, n1, a, num_sms, s, launches);
+        case 3: return launch_impl<N0, N1, 3, 3, EXACT>(n0, n1, a, num_sms, s, launches);
         default: return -1;
     }
 }
@@ -428,8 +436,9 @@ int dispatch_mt(int mt, const Fused3Args& a, int num_sms, cudaStream_t s, int64_
 
 bool fused3_supported(int64_t n0, int64_t n1, int64_t n2, int r0, int r1, int r2) {
     (void)n2;
-    const bool sq32 = n0 == 32 && n1 == 32;  // leading 32 x 32 slabs (config 3's modes 0, 1)
-    if (!sq32 && ((n0 != 64 && n0 != 128) || (n1 != 64 && n1 != 128))) return false;
+    // slabs up to 128 x 128; n0 even (16-byte rows for the tensor map) and a
+    // slab large enough that the 16 x 32 steps are not mostly padding
+    if (n0 < 16 || n1 < 16 || n0 > 128 || n1 > 128 || (n0 & 1)) return false;
     if (r0 < 1 || r1 < 1 || r2 < 1 || r0 > 24 || r1 > 24) return false;
     return true;
 }
@@ -447,12 +456,19 @@ int64_t fused3_workspace_doubles(int64_t n0, int64_t n1, int64_t n2, int64_t S, 
 
 int launch_fused3(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {
     const int mt = (std::max(a.r0, a.r1) + 7) / 8;
-    if (n0 == 128 && n1 == 128) return dispatch_mt<128, 128>(mt, a, num_sms, s, launches);
-    if (n0 == 64 && n1 == 64) return dispatch_mt<64, 64>(mt, a, num_sms, s, launches);
-    if (n0 == 128 && n1 == 64) return dispatch_mt<128, 64>(mt, a, num_sms, s, launches);
-    if (n0 == 64 && n1 == 128) return dispatch_mt<64, 128>(mt, a, num_sms, s, launches);
-    if (n0 == 32 && n1 == 32) return dispatch_mt<32, 32>(mt, a, num_sms, s, launches);
-    return -1;
+    if (n0 == 128 && n1 == 128) return dispatch_mt<128, 128, true>(mt, n0, n1, a, num_sms, s, launches);
+    if (n0 == 64 && n1 == 64) return dispatch_mt<64, 64, true>(mt, n0, n1, a, num_sms, s, launches);
+    if (n0 == 128 && n1 == 64) return dispatch_mt<128, 64, true>(mt, n0, n1, a, num_sms, s, launches);
+    if (n0 == 64 && n1 == 128) return dispatch_mt<64, 128, true>(mt, n0, n1, a, num_sms, s, launches);
+    if (n0 == 32 && n1 == 32) return dispatch_mt<32, 32, true>(mt, n0, n1, a, num_sms, s, launches);
+    // any other slab: the smallest kernel that holds it (the basis fragments
+    // in shared memory are sized by the kernel's extents)
+    if (n0 < 2 || n0 > 128 || n1 < 1 || n1 > 128 || (n0 & 1)) return -1;
+    if (n0 <= 32 && n1 <= 32) return dispatch_mt<32, 32, false>(mt, n0, n1, a, num_sms, s, launches);
+    if (n0 <= 64 && n1 <= 64) return dispatch_mt<64, 64, false>(mt, n0, n1, a, num_sms, s, launches);
+    if (n0 <= 64) return dispatch_mt<64, 128, false>(mt, n0, n1, a, num_sms, s, launches);
+    if (n1 <= 64) return dispatch_mt<128, 64, false>(mt, n0, n1, a, num_sms, s, launches);
+    return dispatch_mt<128, 128, false>(mt, n0, n1, a, num_sms, s, launches);
 }
 
 }  // namespace htr

@@ -235,6 +235,10 @@ constexpr int FPK = FBK + 8;
 struct FastArgs {
     int64_t M, N, K;
     int64_t sam, sak, sbk, sbn;  // single-level operand strides
+    // two-level K whose inner extent k1 is a multiple of the k tile (a tile
+    // never straddles the outer index): k = kr + k1 kq sits at kr sak + kq sak2
+    // (A) / kr sbk + kq sbk2 (B); k1 = 0 for a single level
+    int64_t k1, sak2, sbk2;
     int64_t kchunk, splits;
     double* partial;             // split-K partials or nullptr
     double* sq_partials;         // per-CTA sum of squares of C, or nullptr
@@ -294,19 +298,26 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, 2)
         const int64_t k0 = kbeg + static_cast<int64_t>(kt) * FBK;
         double* as = As + st * SA;
         double* bs = Bs + st * SB;
+        // operand offsets of the tile's first k (one or two K levels)
+        int64_t ka = k0 * f.sak, kb = k0 * f.sbk;
+        if (f.k1) {
+            const int64_t kq = k0 / f.k1, kr = k0 - kq * f.k1;
+            ka = kr * f.sak + kq * f.sak2;
+            kb = kr * f.sbk + kq * f.sbk2;
+        }
         if constexpr (AK) {
 #pragma unroll
             for (int c = t; c < BM * (FBK / 2); c += NTH) {
                 const int m = c / (FBK / 2), kk = 2 * (c % (FBK / 2));
                 const bool ok = m0 + m < f.M && k0 + kk < kend;
-                cp_async16(as + m * FPK + kk, ok ? A + (m0 + m) * f.sam + (k0 + kk) : A, ok);
+                cp_async16(as + m * FPK + kk, ok ? A + (m0 + m) * f.sam + (ka + kk) : A, ok);
             }
         } else {
 #pragma unroll
             for (int c = t; c < FBK * (BM / 2); c += NTH) {
                 const int kk = c / (BM / 2), m = 2 * (c % (BM / 2));
                 const bool ok = m0 + m < f.M && k0 + kk < kend;
-                cp_async16(as + kk * PAM + m, ok ? A + (k0 + kk) * f.sak + (m0 + m) : A, ok);
+                cp_async16(as + kk * PAM + m, ok ? A + ka + kk * f.sak + (m0 + m) : A, ok);
             }
         }
         if constexpr (BKF) {
@@ -314,14 +325,14 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, 2)
             for (int c = t; c < BN * (FBK / 2); c += NTH) {
                 const int n = c / (FBK / 2), kk = 2 * (c % (FBK / 2));
                 const bool ok = n0 + n < f.N && k0 + kk < kend;
-                cp_async16(bs + n * FPK + kk, ok ? B + (n0 + n) * f.sbn + (k0 + kk) : B, ok);
+                cp_async16(bs + n * FPK + kk, ok ? B + (n0 + n) * f.sbn + (kb + kk) : B, ok);
             }
         } else {
 #pragma unroll
             for (int c = t; c < FBK * (BN / 2); c += NTH) {
                 const int kk = c / (BN / 2), n = 2 * (c % (BN / 2));
                 const bool ok = n0 + n < f.N && k0 + kk < kend;
-                cp_async16(bs + kk * PBN + n, ok ? B + (k0 + kk) * f.sbk + (n0 + n) : B, ok);
+                cp_async16(bs + kk * PBN + n, ok ? B + kb + kk * f.sbk + (n0 + n) : B, ok);
             }
         }
     };
@@ -575,6 +586,7 @@ struct Plan {
     int64_t tiles_n, tiles_m, splits, kchunk;
     bool fast = false, ak = false, bkf = false;
     int64_t sam = 0, sak = 0, sbk = 0, sbn = 0;
+    int64_t k1 = 0, sak2 = 0, sbk2 = 0;  // two-level K (fast kernel), see FastArgs
 };
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -593,6 +605,14 @@ bool fast_eligible(const GemmDesc& d, Plan& p) {
     } else if (d.sak2 == d.K1 * d.sak1 && d.sbk2 == d.K1 * d.sbk1) {
         p.sak = d.sak1;
         p.sbk = d.sbk1;
+    } else if (d.K1 % FBK == 0 && ((d.sak2 | d.sbk2) & 1) == 0) {
+        // two K levels, the inner a whole number of k tiles (the transfer
+        // Grams of a projected layer: K = leading extent x batch)
+        p.sak = d.sak1;
+        p.sbk = d.sbk1;
+        p.k1 = d.K1;
+        p.sak2 = d.sak2;
+        p.sbk2 = d.sbk2;
     } else {
         return false;
     }
@@ -722,7 +742,7 @@ int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t 
         const int64_t c_sn = d.N2 == 1 ? d.scn1 : (d.N1 == 1 ? d.scn2 : d.scn1);
         const int staged = c_flat && c_sn == 1 && aligned16(d.C) && (d.scm % 2 == 0) &&
                            (d.batch == 1 || d.scb % 2 == 0);
-        FastArgs f{d.M, N, K, p.sam, p.sak, p.sbk, p.sbn, p.kchunk, p.splits, partial, sq_partials, staged};
+        FastArgs f{d.M, N, K, p.sam, p.sak, p.sbk, p.sbn, p.k1, p.sak2, p.sbk2, p.kchunk, p.splits, partial, sq_partials, staged};
         launch_fast(p, d, f, L, grid, s);
         ++*launches;
         if (p.splits > 1) {

@@ -70,6 +70,28 @@ __host__ __device__ constexpr int consumer_warps() {
     return MB * (MB + 1) / 2;
 }
 
+/// Lower-triangle block (mb >= nb) of consumer warp w. The FP64 tensor pipe is
+/// fed per scheduler (warp % 4), a diagonal block issues 10 of an off-diagonal
+/// block's 16 DMMAs per k-step, and the row-major order would give the four
+/// schedulers 42/36/26/32 DMMAs per k-step at MB = 4; this order gives
+/// 36/36/32/32 (warp 10, the TMA producer, shares scheduler 2).
+template <int MB>
+__device__ __forceinline__ void block_of_warp(int w, int& mb, int& nb) {
+    if constexpr (MB == 4) {
+        // warps 0,4,8 | 1,5,9 | 2,6 | 3,7
+        // mb = {1, 2, 2, 3, 0, 2, 3, 3, 1, 3}, nb = {0, 0, 1, 1, 0, 2, 0, 2, 1, 3}, two bits per warp
+        mb = (0xdf8e9u >> (2 * w)) & 3;
+        nb = (0xd8850u >> (2 * w)) & 3;
+    } else {
+        mb = 0;
+        nb = w;
+        while (nb > mb) {
+            nb -= mb + 1;
+            ++mb;
+        }
+    }
+}
+
 template <int MB>
 __global__ void __launch_bounds__((consumer_warps<MB>() + 1) * 32, 1)
     gram_stream_kernel(int64_t units, int64_t kchunks, int M, double* __restrict__ partials,
@@ -77,7 +99,10 @@ __global__ void __launch_bounds__((consumer_warps<MB>() + 1) * 32, 1)
     constexpr int CW = consumer_warps<MB>();
     constexpr int MP = 32 * MB;  // padded rows per chunk
     extern __shared__ __align__(1024) unsigned char gsm_raw[];
-    double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned ring (the swizzle's span); the offset is applied to the
+    // shared array itself so the compiler keeps the shared address space (LDS)
+    const uint32_t pad = (1024u - (saddr(gsm_raw) & 1023u)) & 1023u;
+    double* ring = reinterpret_cast<double*>(gsm_raw + pad);
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + kGStages * MP * kGChunk);
     uint64_t* empty = full + kGStages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -108,11 +133,8 @@ __global__ void __launch_bounds__((consumer_warps<MB>() + 1) * 32, 1)
         return;
     }
     // consumer warp -> lower-triangle block (mb >= nb)
-    int mb = 0, nb = warp;
-    while (nb > mb) {
-        nb -= mb + 1;
-        ++mb;
-    }
+    int mb, nb;
+    block_of_warp<MB>(warp, mb, nb);
     const bool diag = mb == nb;
     const int g4 = lane >> 2, t4 = lane & 3;
     double acc[4][4][2];
@@ -197,11 +219,8 @@ __global__ void __launch_bounds__(consumer_warps<MB>() * 32, 1)
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    int mb = 0, nb = warp;
-    while (nb > mb) {
-        nb -= mb + 1;
-        ++mb;
-    }
+    int mb, nb;
+    block_of_warp<MB>(warp, mb, nb);
     const bool diag = mb == nb;
     const int g4 = lane >> 2, t4 = lane & 3;
     double acc[4][4][2];

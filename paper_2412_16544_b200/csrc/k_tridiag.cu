@@ -397,6 +397,10 @@ constexpr int kVecSmemRefN = 128;
 /// Above this n the vector kernel keeps T and its scratch in the workspace.
 constexpr int kVecSmemN = 1024;
 constexpr int kTriMaxN = 8192;
+/// Clusters of 2..kBlockMax close eigenvalues are iterated by the whole CTA
+/// (solves dealt to the warps, block re-orthonormalisation by CholeskyQR2).
+constexpr int kBlockMax = 48;
+constexpr int kBlockGramDoubles = kBlockMax * (kBlockMax + 1);
 /// Eigenvectors built in shared memory up to n * r doubles (n <= 128).
 __host__ __device__ __forceinline__ bool jobs_z_smem(int n, int r) { return n <= kVecSmemRefN && n * r <= 4096; }
 __device__ __forceinline__ int refl_off(int k, int n) { return k * (n - 2) - (k * (k - 1)) / 2; }
@@ -488,10 +492,17 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const __gr
         for (int i = lane; i < n; i += 32) v[i] *= inv;
         __syncwarp();
     };
+    // clusters the whole CTA iterates together (below): 2..kBlockMax members
+    // with the vectors in shared memory; larger ones stay with one warp
+    auto block_cluster = [&](int cl) {
+        const int m = cstart[cl + 1] - cstart[cl];
+        return !big && m > 1 && m <= kBlockMax;
+    };
     for (int cl = warp; cl < ncl && warp < vec_warps; cl += vec_warps) {
         double* ws = scratch + static_cast<int64_t>(warp) * per;
         TriLU f{ws, ws + n, ws + 2 * n, ws + 3 * n, reinterpret_cast<unsigned char*>(ws + 5 * n)};
         const int j0 = cstart[cl], j1 = cstart[cl + 1];
+        if (block_cluster(cl)) continue;
         if (j1 - j0 == 1) {
             // an isolated eigenvalue: two inverse-iteration steps
             double* y = Zc + static_cast<int64_t>(n) * (n - 1 - j0);
@@ -548,6 +559,97 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const __gr
         }
     }
     __syncthreads();
+    // ---- clusters iterated by the whole CTA: three rounds of (every member
+    // solved from its current vector, one member per warp at a time; then the
+    // block re-orthonormalised by CholeskyQR2: S = Y^T Y, S = R^T R, Y <- Y R^-1,
+    // twice). The same scheme as the one-warp path above (solve all, then
+    // Gram-Schmidt in member order -- CholeskyQR yields that same QR factor),
+    // with the serial work spread over the CTA: a noise-floor cluster of 20
+    // vectors of a 25-row Gram took 0.39 ms on one warp.
+    if (!big) {
+        double* S = scratch + static_cast<int64_t>(vec_warps) * per;  // [m][m + 1]
+        for (int cl = 0; cl < ncl; ++cl) {
+            if (!block_cluster(cl)) continue;
+            const int j0 = cstart[cl], j1 = cstart[cl + 1], m = j1 - j0, sp = m + 1;
+            // member q (eigenvalue j0 + q) is column n - 1 - j0 - q: Yb[-n q]
+            double* Yb = Zc + static_cast<int64_t>(n) * (n - 1 - j0);
+            for (int e = tid; e < n * m; e += nt) {
+                const int q = e / n, i = e - q * n;
+                Yb[i - static_cast<int64_t>(n) * q] = hash_uniform(static_cast<uint32_t>(j0 + q), static_cast<uint32_t>(i));
+            }
+            __syncthreads();
+            for (int it = 0; it < 3; ++it) {
+                if (warp < vec_warps) {
+                    double* ws = scratch + static_cast<int64_t>(warp) * per;
+                    TriLU f{ws, ws + n, ws + 2 * n, ws + 3 * n, reinterpret_cast<unsigned char*>(ws + 5 * n)};
+                    for (int q = warp; q < m; q += vec_warps) {
+                        // coincident eigenvalues separated slightly (dstein): the
+                        // shift of member q is at least 10 u |x| above member q - 1's
+                        double xj = lam_asc[j0];
+                        for (int t = 1; t <= q; ++t) {
+                            const double xt = lam_asc[j0 + t], pertol = 10.0 * fabs(DBL_EPSILON * xt);
+                            xj = xt - xj < pertol ? xj + pertol : xt;
+                        }
+                        double* y = Yb - static_cast<int64_t>(n) * q;
+                        if (lane == 0) {
+                            tri_factor(d, e, n, xj, tol, f);
+                            tri_solve(n, f, y);
+                        }
+                        __syncwarp();
+                        normalise(y, false);
+                    }
+                }
+                __syncthreads();
+                for (int pass = 0; pass < 2; ++pass) {
+                    // S = Y^T Y (lower triangle)
+                    for (int idx = tid; idx < m * m; idx += nt) {
+                        const int p = idx / m, q = idx - p * m;
+                        if (q > p) continue;
+                        const double* yp = Yb - static_cast<int64_t>(n) * p;
+                        const double* yq = Yb - static_cast<int64_t>(n) * q;
+                        double acc = 0.0;
+                        for (int i = 0; i < n; ++i) acc = fma(yp[i], yq[i], acc);
+                        S[p * sp + q] = acc;
+                    }
+                    __syncthreads();
+                    // Cholesky S = L L^T in place (one warp; R = L^T). A
+                    // non-positive pivot (a numerically dependent member) is
+                    // replaced by 1: that column keeps its current direction
+                    // and the next round's solve separates it.
+                    if (warp == 0) {
+                        for (int k = 0; k < m; ++k) {
+                            double dk = S[k * sp + k];
+                            dk = dk > 0.0 ? sqrt(dk) : 1.0;
+                            const double inv = 1.0 / dk;
+                            __syncwarp();
+                            for (int i = k + 1 + lane; i < m; i += 32) S[i * sp + k] *= inv;
+                            if (lane == 0) S[k * sp + k] = dk;
+                            __syncwarp();
+                            for (int idx = lane; idx < (m - k - 1) * (m - k - 1); idx += 32) {
+                                const int i = k + 1 + idx / (m - k - 1), j = k + 1 + idx % (m - k - 1);
+                                if (j <= i) S[i * sp + j] = fma(-S[i * sp + k], S[j * sp + k], S[i * sp + j]);
+                            }
+                            __syncwarp();
+                        }
+                    }
+                    __syncthreads();
+                    // Y <- Y R^-1: row i of Y by forward substitution (column q
+                    // needs the finished columns p < q), one thread per row
+                    for (int i = tid; i < n; i += nt) {
+                        for (int q = 0; q < m; ++q) {
+                            double v = Yb[i - static_cast<int64_t>(n) * q];
+                            for (int p = 0; p < q; ++p) v = fma(-Yb[i - static_cast<int64_t>(n) * p], S[q * sp + p], v);
+                            Yb[i - static_cast<int64_t>(n) * q] = v / S[q * sp + q];
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            // unit norm and a fixed sign (largest entry positive), a warp per member
+            for (int q = warp; q < m; q += nt >> 5) normalise(Yb - static_cast<int64_t>(n) * q, true);
+            __syncthreads();
+        }
+    }
     // U = H_0 H_1 ... H_{n-3} Z: 8 lanes per column, every reflector applied
     // last-to-first (no block barrier: a group owns its column)
     const int g = tid >> 3, gl = tid & 7, ngroups = nt >> 3;
@@ -650,10 +752,11 @@ void launch_tridiag_vectors(const double* const* W, const double* const* info, c
             if (jobs_z_smem(jobs.n[i], jobs.r[i])) zs = std::max<int64_t>(zs, static_cast<int64_t>(jobs.n[i]) * jobs.r[i]);
         const int64_t per = 5 * nmax + (nmax + 7) / 8;
         const bool big = nmax > kVecSmemN;
-        const int64_t budget = 200 * 1024 / 8 - 3 * nmax - refl - zs;
+        const int64_t budget = 200 * 1024 / 8 - 3 * nmax - refl - zs - kBlockGramDoubles;
         const int vw = big ? kVecThreads / 32
                            : static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kVecThreads / 32, budget / per)));
-        const size_t smem = big ? 0 : sizeof(double) * static_cast<size_t>(3 * nmax + refl + zs + vw * per);
+        const size_t smem =
+            big ? 0 : sizeof(double) * static_cast<size_t>(3 * nmax + refl + zs + vw * per + kBlockGramDoubles);
         if (smem > 0) ensure_smem_limit(reinterpret_cast<const void*>(tridiag_vectors_kernel), smem);
         tridiag_vectors_kernel<<<k, kVecThreads, smem, s>>>(jobs, vw);
         ++*launches;

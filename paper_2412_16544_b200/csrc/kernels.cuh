@@ -276,9 +276,10 @@ struct Tail4Args {
     double* out = nullptr;
     double* host_out = nullptr;
     unsigned int* ticket = nullptr;  // zero on entry, left zero on exit
+    int csize = 1;  // CTAs per sample (a thread-block cluster over the i3 slices), set by the launcher
 };
 bool tail4_supported(int R01, int r12, int r34, int r2, int r3, int64_t n2, int64_t n3);
-void launch_tail4(const Tail4Args& a, cudaStream_t s, int64_t* launches);
+void launch_tail4(const Tail4Args& a, int num_sms, cudaStream_t s, int64_t* launches);
 // (identity_transfer is honoured by the per-sample/cluster kernel; the
 // sample-pair variant falls back to it)
 

@@ -40,15 +40,50 @@ Stream::Stream(int dev) : device(dev) {
 Stream::~Stream() {
     if (s) {
         cudaStreamSynchronize(s);
+        for (auto& bin : bins)
+            for (double* p : bin) cudaFreeAsync(p, s);
+        cudaStreamSynchronize(s);
         cudaStreamDestroy(s);
     }
 }
 
+int Stream::size_class(int64_t n) {
+    if (n <= 0 || n > (int64_t{1} << kMaxClass)) return -1;
+    int c = kMinClass;
+    while ((int64_t{1} << c) < n) ++c;
+    return c;
+}
+
+double* Stream::take(int cls) {
+    std::lock_guard<std::mutex> g(mu);
+    auto& bin = bins[cls];
+    if (bin.empty()) return nullptr;
+    double* p = bin.back();
+    bin.pop_back();
+    cached_bytes -= sizeof(double) << cls;
+    return p;
+}
+
+bool Stream::give(int cls, double* p) {
+    std::lock_guard<std::mutex> g(mu);
+    const size_t bytes = sizeof(double) << cls;
+    if (cached_bytes + bytes > kCacheCapBytes) return false;
+    bins[cls].push_back(p);
+    cached_bytes += bytes;
+    return true;
+}
+
 Buf::Buf(StreamPtr st_, int64_t n_) : st(std::move(st_)), n(n_) {
-    if (n > 0) HTR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(n) * sizeof(double), st->s));
+    if (n <= 0) return;
+    cls = Stream::size_class(n);
+    if (cls >= 0 && (p = st->take(cls)) != nullptr) return;
+    const size_t doubles = cls >= 0 ? size_t{1} << cls : static_cast<size_t>(n);
+    HTR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), doubles * sizeof(double), st->s));
 }
 Buf::~Buf() {
-    if (p && owned) cudaFreeAsync(p, st->s);
+    if (!p || !owned) return;
+    if (cls >= 0 && st->give(cls, p)) return;
+    cudaFreeAsync(p, st->s);
 }
 
 Index Rep::rank(NodeId id) const {
@@ -1592,7 +1627,7 @@ bool launch_skip_encode4(Context& c, const Rep& h, const DT& y, const DT* latent
                 b3 = basis_of(h, leaf[3]->id), B12 = basis_of(h, tr[0]->id), B34 = basis_of(h, tr[1]->id);
     const int64_t n0 = y.shape[0], n1 = y.shape[1], n2 = y.shape[2], n3 = y.shape[3], batch = y.shape[4];
     const int64_t R01 = b0.r * b1.r;
-    if (b0.r > 24 || b1.r > 24 || b2.r > 24 || b3.r > 24 || B12.r > 24 || B34.r > 1024 || batch < 1) return false;
+    if (b0.r > 24 || b1.r > 24 || b2.r > 24 || b3.r > 24 || B12.r > 96 || B34.r > 1024 || batch < 1) return false;
     if (!fused3_supported(n0, n1, n2 * n3 * batch, static_cast<int>(b0.r), static_cast<int>(b1.r), 1) ||
         !tail4_supported(static_cast<int>(R01), static_cast<int>(B12.r), static_cast<int>(B34.r),
                          static_cast<int>(b2.r), static_cast<int>(b3.r), n2, n3) ||
@@ -1645,7 +1680,7 @@ bool launch_skip_encode4(Context& c, const Rep& h, const DT& y, const DT* latent
     ta.out = sc;
     ta.host_out = host_out;
     ta.ticket = c.d_ticket;
-    launch_tail4(ta, c.s, &c.launches);
+    launch_tail4(ta, c.num_sms, c.s, &c.launches);
     HTR_CUDA(cudaGetLastError());
     *latent = lat;
     return true;
