@@ -49,6 +49,12 @@ constexpr size_t decode2_smem_doubles() {
     return static_cast<size_t>(N0T) * MT0 * 64 + (kDecMaxN1 / 8) * 3 * 64 + kDecWarps * 2 * kDecWS;
 }
 
+struct DecodeFinal {
+    double* out;           // residual mode: the total sum (X - Y)^2, or null (partials only)
+    double* host_out;      // optional mapped-host copy
+    unsigned int* ticket;  // zero on entry, left zero
+};
+
 // N0T: n0 / 8 (i0 n-tiles); MT0: ceil(r0 / 8) (a0 tiles of step A's output)
 // RESID: instead of storing X, accumulate sum (X - Y)^2 (relative_test_error,
 // metrics.hpp:218-237) into one partial per warp; the reconstruction is never
@@ -57,7 +63,7 @@ template <int N0T, int MT0, bool RESID>
 __global__ void __launch_bounds__(kDecWarps * 32, 1)
     decode2_kernel(const double* __restrict__ W, int64_t T, int r0, int r1, int n1, const double* __restrict__ U0,
                    const double* __restrict__ U1, double* __restrict__ X, const double* __restrict__ Y,
-                   double* __restrict__ partials) {
+                   double* __restrict__ partials, const DecodeFinal fin) {
     constexpr int HT = N0T > 8 ? 8 : N0T;  // n-tiles per pass (accumulator budget)
     constexpr int NH = N0T / HT;
     constexpr int n0 = 8 * N0T;
@@ -220,6 +226,35 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
         if (lane == 0) partials[gw] = rs;
+        if (fin.out == nullptr) return;
+        // the last CTA to finish (ticket counter) sums every warp's partial in
+        // a fixed order and publishes the total, also into mapped host memory
+        // when given: the stream API's explicit loss needs neither a reduction
+        // launch nor a device-to-host copy
+        __shared__ bool last;
+        __shared__ double fred[kDecWarps];
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            last = atomicAdd(fin.ticket, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        const int64_t np = static_cast<int64_t>(gridDim.x) * kDecWarps;
+        double t = 0.0;
+        for (int64_t i = tid; i < np; i += kDecWarps * 32) t += __ldcg(partials + i);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) fred[warp] = t;
+        __syncthreads();
+        if (tid == 0) {
+            double sum = 0.0;
+            for (int w = 0; w < kDecWarps; ++w) sum += fred[w];
+            fin.out[0] = sum;
+            if (fin.host_out) fin.host_out[0] = sum;
+            *fin.ticket = 0u;
+        }
     }
 }
 
@@ -229,7 +264,8 @@ int launch_t(const Decode2Args& a, int num_sms, cudaStream_t s) {
     ensure_smem_limit(reinterpret_cast<const void*>(decode2_kernel<N0T, MT0, RESID>), smem);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, (a.T + kDecWarps - 1) / kDecWarps)));
     decode2_kernel<N0T, MT0, RESID><<<grid, kDecWarps * 32, smem, s>>>(a.W, a.T, a.r0, a.r1, static_cast<int>(a.n1),
-                                                                        a.U0, a.U1, a.X, a.Y, a.partials);
+                                                                        a.U0, a.U1, a.X, a.Y, a.partials,
+                                                                        DecodeFinal{a.final_out, a.final_host, a.ticket});
     return grid;
 }
 
@@ -280,6 +316,7 @@ int launch_decode2(const Decode2Args& a, int num_sms, cudaStream_t s, int64_t* l
     if (!decode2_supported(a.n0, a.n1, a.r0, a.r1) || a.T < 1) return -1;
     if ((!a.Y && (reinterpret_cast<uintptr_t>(a.X) & 15u) != 0) || (reinterpret_cast<uintptr_t>(a.W) & 7u) != 0) return -1;
     if (a.Y && (!a.partials || (reinterpret_cast<uintptr_t>(a.Y) & 15u) != 0)) return -1;
+    if (a.final_out && !a.ticket) return -1;
     const int grid = a.Y ? launch_r<true>(a, num_sms, s) : launch_r<false>(a, num_sms, s);
     ++*launches;
     return grid;

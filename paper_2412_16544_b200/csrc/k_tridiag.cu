@@ -450,8 +450,15 @@ __global__ void __launch_bounds__(kVecThreads) tridiag_vectors_kernel(const __gr
         e[i] = eg[i];
         lam_asc[i] = lam_g[i];
     }
-    for (int k = 0; k + 2 < n && refl_smem; ++k)
-        for (int i = tid; i < n - k - 2; i += nt) refl[refl_off(k, n) + i] = W[(k + 2 + i) + static_cast<int64_t>(n) * k];
+    // (one flat loop over the (n - 2) x (n - 2) index square: every thread has
+    // its loads in flight at once instead of one short column per iteration)
+    if (refl_smem && n > 2) {
+        const int q = n - 2;
+        for (int idx = tid; idx < q * q; idx += nt) {
+            const int k = idx / q, i = idx - k * q;
+            if (i < q - k) refl[refl_off(k, n) + i] = W[(k + 2 + i) + static_cast<int64_t>(n) * k];
+        }
+    }
     __syncthreads();
     __shared__ double onenrm;
     if (tid == 0) {

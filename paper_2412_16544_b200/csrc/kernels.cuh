@@ -351,6 +351,11 @@ struct Decode2Args {
     double* X;         // [n0][n1][T]
     const double* Y = nullptr;  // set: no X; one sum (X - Y)^2 per warp into partials
     double* partials = nullptr;
+    // residual mode, optional: the last CTA sums the partials (fixed order)
+    // into final_out[0] and, when given, final_host[0] (mapped host memory)
+    double* final_out = nullptr;
+    double* final_host = nullptr;
+    unsigned int* ticket = nullptr;  // zero on entry, left zero on exit
 };
 bool decode2_supported(int64_t n0, int64_t n1, int64_t r0, int64_t r1);
 int launch_decode2(const Decode2Args& a, int num_sms, cudaStream_t s, int64_t* launches);

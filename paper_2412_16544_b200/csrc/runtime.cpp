@@ -1525,6 +1525,8 @@ bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent
         lat = c.tensor({t.r0, t.rt, batch});
     }
     ta.latent = lat.data();
+    ta.variant = c.tail_kernel;
+    ta.num_sms = c.num_sms;
     BufPtr lsq = c.alloc(8 * batch);  // per-CTA partials (up to 8 CTAs per sample)
     ta.latsq = lsq->p;
     ta.ysq_partials = fa.ysq_partials;
@@ -1532,8 +1534,6 @@ bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent
     ta.out = sc;
     ta.host_out = host_out;
     ta.ticket = c.d_ticket;
-    ta.variant = c.tail_kernel;
-    ta.num_sms = c.num_sms;
     launch_tail3(ta, c.s, &c.launches);
     HTR_CUDA(cudaGetLastError());
     *latent = lat;
@@ -2232,6 +2232,8 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         bool used_fused = false;   // (report) any fused kernel in the encode
         bool scan_valid = false;   // dsc[1] is the non-finite flag of a full scan
         bool resid = false;        // dsc[4] holds ||y - decode(latent)||^2 (explicit loss, enqueued ahead)
+        bool resid_mapped = false;  // ... and the kernel mirrored it into mapped[4]
+        bool from_mapped = false;   // the decision reads the mapped block (no device-to-host copy)
         cudaEvent_t done = nullptr, t0 = nullptr, t1 = nullptr;
         int64_t launches = 0;
         std::chrono::steady_clock::time_point started;
@@ -2310,14 +2312,19 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
         // as every batch of a stream near the floor does): the decision then
         // reads it without another host round trip
         sl.resid = refine_hint;
-        if (sl.resid) decode_residual_sq(c, h, sl.latent, sl.y, sl.dsc->p + 4);
+        // (the fused reconstruction kernel mirrors it into the slot's mapped block)
+        sl.resid_mapped = false;
+        if (sl.resid)
+            sl.resid_mapped = decode_residual_sq(c, h, sl.latent, sl.y, sl.dsc->p + 4,
+                                                 c.sharded() ? nullptr : mapped_dev + 4);
         if (c.sharded()) {
             // the global batch count rides on the skip test's all-reduce
             sl.host[8] = static_cast<double>(nb);
             HTR_CUDA(cudaMemcpyAsync(sl.dsc->p + 8, sl.host + 8, sizeof(double), cudaMemcpyHostToDevice, c.s));
             c.allreduce(sl.dsc->p, 9);
         }
-        if (c.sharded() || !sl.fused || sl.resid)
+        sl.from_mapped = !c.sharded() && sl.fused && (!sl.resid || sl.resid_mapped);
+        if (!sl.from_mapped)
             HTR_CUDA(cudaMemcpyAsync(sl.host, sl.dsc->p, 9 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
         HTR_CUDA(cudaEventRecord(sl.done, c.s));
         mark();
@@ -2332,7 +2339,7 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
     auto decide = [&](Slot& sl, const Rep& h) -> std::shared_ptr<Rep> {
         HTR_CUDA(cudaEventSynchronize(sl.done));
         const int64_t nb = sl.y.shape[static_cast<size_t>(d)];
-        const double* v = (c.sharded() || !sl.fused || sl.resid) ? sl.host : sl.mapped;
+        const double* v = sl.from_mapped ? sl.mapped : sl.host;
         const double ysq = v[0], latsq = v[2];
         const int64_t gbatch = c.sharded() ? static_cast<int64_t>(std::llround(v[8])) : nb;
         // non-finite input (the per-call path raises); sharded, the flag is
@@ -2441,17 +2448,21 @@ std::vector<UpdateOut> ht_rise_update_many(Context& c, const std::shared_ptr<Rep
 // ---------------------------------------------------------------------------
 
 namespace {
-DT decode_impl(Context& c, const Rep& h, const DT& latent, double* dst, const DT* ref, double* resid_out);
+DT decode_impl(Context& c, const Rep& h, const DT& latent, double* dst, const DT* ref, double* resid_out,
+               double* resid_host = nullptr, bool* host_written = nullptr);
 }
 
 DT decode(Context& c, const Rep& h, const DT& latent, double* dst) { return decode_impl(c, h, latent, dst, nullptr, nullptr); }
 
-void decode_residual_sq(Context& c, const Rep& h, const DT& latent, const DT& y, double* out) {
-    decode_impl(c, h, latent, nullptr, &y, out);
+bool decode_residual_sq(Context& c, const Rep& h, const DT& latent, const DT& y, double* out, double* host_out) {
+    bool written = false;
+    decode_impl(c, h, latent, nullptr, &y, out, host_out, &written);
+    return written;
 }
 
 namespace {
-DT decode_impl(Context& c, const Rep& h, const DT& latent, double* dst, const DT* ref, double* resid_out) {
+DT decode_impl(Context& c, const Rep& h, const DT& latent, double* dst, const DT* ref, double* resid_out,
+               double* resid_host, bool* host_written) {
     const int64_t r11 = h.root->r11, r12 = h.root->r12;
     if (latent.shape.size() != 3 || latent.shape[0] != r11 || latent.shape[1] != r12)
         raise(HTR_ERR_INVALID_ARGUMENT, "decode: latent ranks " + htrise::shape_to_string(latent.shape) +
@@ -2540,13 +2551,18 @@ DT decode_impl(Context& c, const Rep& h, const DT& latent, double* dst, const DT
             a.Y = ref->data();
             parts = c.alloc(decode2_partials(a.T, c.num_sms));
             a.partials = parts->p;
+            // the kernel's last CTA sums the partials (and mirrors the total
+            // into mapped host memory when asked)
+            a.final_out = resid_out;
+            a.final_host = resid_host;
+            a.ticket = c.d_ticket;
         } else {
             a.X = out.data();
         }
         if (a.T > 0) {
             if (launch_decode2(a, c.num_sms, c.s, &c.launches) < 0) raise(HTR_ERR_RUNTIME, "decode: fused leaf kernel rejected its operands");
             HTR_CUDA(cudaGetLastError());
-            if (ref) launch_sum_partials(parts->p, decode2_partials(a.T, c.num_sms), resid_out, c.s, &c.launches);
+            if (ref && host_written) *host_written = resid_host != nullptr;
         } else if (ref) {
             HTR_CUDA(cudaMemsetAsync(resid_out, 0, sizeof(double), c.s));
         }

@@ -321,7 +321,12 @@ DT decode(Context& c, const Rep& h, const DT& latent, double* dst = nullptr);
 /// sum (decode(latent) - y)^2 over this rank's samples into the device scalar
 /// `out`, without materialising the reconstruction where the fused decode
 /// kernel applies (relative_test_error, metrics.hpp:218-237).
-void decode_residual_sq(Context& c, const Rep& h, const DT& latent, const DT& y, double* out);
+/// out[0] = ||y - decode(latent)||^2 (enqueued). With host_out (device address
+/// of mapped host memory) the fused reconstruction kernel also writes the
+/// value there; returns whether it did (false: the generic chain ran and the
+/// caller copies out[0] back).
+bool decode_residual_sq(Context& c, const Rep& h, const DT& latent, const DT& y, double* out,
+                        double* host_out = nullptr);
 
 /// Append latent slices [r11, r12, N] to a representation's root (value
 /// semantics: returns the new root view).
