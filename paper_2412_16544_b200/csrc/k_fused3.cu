@@ -119,7 +119,7 @@ __host__ __device__ __forceinline__ int64_t cta_begin(int64_t T, int64_t b, int6
 // the true extents, TMA zero-fills the out-of-range part of a box, the basis
 // fragments are zero beyond n0 / n1, and only the steps that touch the slab
 // are walked (n0 = 96 on the 128-row kernel: 3 of 4 row quarters).
-template <int N0, int N1, int MT0, int MT1, bool EXACT>
+template <int N0, int N1, int MT0, int MT1, bool EXACT, int ST = kStages>
 __global__ void __launch_bounds__(kThreads, 1)
     fused3_kernel(const Fused3Args a, const RangeInfo ri, const __grid_constant__ CUtensorMap tmap) {
     constexpr int NC = N0 / 8;      // 8-row chunks per column block
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) double smem_raw[];
     // stages first: the 128-byte swizzle needs 1024-byte aligned boxes
     double* stages = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u) / sizeof(double);  // [warp][stage][box][col][16]
-    double2* U0f = reinterpret_cast<double2*>(stages + kWarps * kStages * kStageDoubles);  // [NC][MT0][32]
+    double2* U0f = reinterpret_cast<double2*>(stages + kWarps * ST * kStageDoubles);  // [NC][MT0][32]
     double2* U1f = U0f + NC * MT0 * 32;                                              // [N1/8][MT1][32]
     uint64_t* full = reinterpret_cast<uint64_t*>(U1f + (N1 / 8) * MT1 * 32);  // [warp][stage]
     __shared__ double red[kWarps];
@@ -171,13 +171,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             t = tr + u / NP;
         }
     };
-    double* my_stages = stages + warp * kStages * kStageDoubles;
-    uint64_t* my_full = full + warp * kStages;
+    double* my_stages = stages + warp * ST * kStageDoubles;
+    uint64_t* my_full = full + warp * ST;
     const uint64_t policy = evict_first_policy();
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
 
     auto issue = [&](int i) {  // lane 0 only
-        const int st = i % kStages;
+        const int st = i % ST;
         int t, u, pair, q;
         coords(i, t, pair, q, u);
         mbar_expect_tx(&my_full[st], kStageBytes);
@@ -188,9 +188,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // lane 0 sets up its warp's ring and starts the stream before the basis
     // fragments are staged (the first loads' latency overlaps the staging)
     if (lane == 0) {
-        for (int k = 0; k < kStages; ++k) mbar_init(&my_full[k], 1);
+        for (int k = 0; k < ST; ++k) mbar_init(&my_full[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int k = 0; k < kStages; ++k)
+        for (int k = 0; k < ST; ++k)
             if (k < total) issue(k);
     }
     // ---- stage basis fragments (zero-padded to 8-multiples) ----
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < MT1; ++j) wacc[i][j][0] = wacc[i][j][1] = 0.0;
 
     for (int i = 0; i < total; ++i) {
-        const int st = i % kStages;
+        const int st = i % ST;
         int t, u, pair, q;
         coords(i, t, pair, q, u);
         if (q == 0) {
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int y = 0; y < 2; ++y) pacc[x][y][0] = pacc[x][y][1] = 0.0;
         }
-        mbar_wait(&my_full[st], static_cast<uint32_t>((i / kStages) & 1));
+        mbar_wait(&my_full[st], static_cast<uint32_t>((i / ST) & 1));
         const double* sb = my_stages + st * kStageDoubles;
         const int pc0 = col_perm(g4), pc1 = 8 + col_perm(g4);
 #pragma unroll
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (i + kStages < total) issue(i + kStages);
+            if (i + ST < total) issue(i + ST);
         }
 
         if (q == NQ - 1) {
@@ -351,11 +351,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int N0, int N1, int MT0, int MT1>
+template <int N0, int N1, int MT0, int MT1, int ST>
 size_t smem_bytes() {
     return sizeof(double) * (static_cast<size_t>(N0 / 8) * MT0 * 64 + static_cast<size_t>(N1 / 8) * MT1 * 64 +
-                             static_cast<size_t>(kWarps) * kStages * kStageDoubles) +
-           sizeof(uint64_t) * kWarps * kStages + 1024;  // + alignment slack
+                             static_cast<size_t>(kWarps) * ST * kStageDoubles) +
+           sizeof(uint64_t) * kWarps * ST + 1024;  // + alignment slack
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -383,7 +383,7 @@ bool make_batch_map(CUtensorMap* map, const double* Y, int64_t N0, int64_t N1, i
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int N0, int N1, int MT0, int MT1, bool EXACT>
+template <int N0, int N1, int MT0, int MT1, bool EXACT, int ST = kStages>
 int launch_impl(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {
     const int64_t T = a.n2 * a.S;
     const int64_t B = std::min<int64_t>(num_sms, T);
@@ -393,8 +393,8 @@ int launch_impl(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaSt
     alignas(64) CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
     if (!make_batch_map(&map, a.Y, n0, n1, T)) return -1;
-    const size_t smem = smem_bytes<N0, N1, MT0, MT1>();
-    auto kfn = fused3_kernel<N0, N1, MT0, MT1, EXACT>;
+    const size_t smem = smem_bytes<N0, N1, MT0, MT1, ST>();
+    auto kfn = fused3_kernel<N0, N1, MT0, MT1, EXACT, ST>;
     ensure_smem_limit(reinterpret_cast<const void*>(kfn), smem);
     kfn<<<static_cast<unsigned>(B), kThreads, smem, s>>>(args, ri, map);
     ++*launches;
@@ -422,12 +422,12 @@ int launch_impl(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaSt
     return static_cast<int>(B);
 }
 
-template <int N0, int N1, bool EXACT>
+template <int N0, int N1, bool EXACT, int ST = kStages>
 int dispatch_mt(int mt, int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cudaStream_t s, int64_t* launches) {
     switch (mt) {
-        case 1: return launch_impl<N0, N1, 1, 1, EXACT>(n0, n1, a, num_sms, s, launches);
-        case 2: return launch_impl<N0, N1, 2, 2, EXACT>(n0, n1, a, num_sms, s, launches);
-        case 3: return launch_impl<N0, N1, 3, 3, EXACT>(n0, n1, a, num_sms, s, launches);
+        case 1: return launch_impl<N0, N1, 1, 1, EXACT, ST>(n0, n1, a, num_sms, s, launches);
+        case 2: return launch_impl<N0, N1, 2, 2, EXACT, ST>(n0, n1, a, num_sms, s, launches);
+        case 3: return launch_impl<N0, N1, 3, 3, EXACT, ST>(n0, n1, a, num_sms, s, launches);
         default: return -1;
     }
 }
@@ -436,9 +436,9 @@ int dispatch_mt(int mt, int64_t n0, int64_t n1, const Fused3Args& a, int num_sms
 
 bool fused3_supported(int64_t n0, int64_t n1, int64_t n2, int r0, int r1, int r2) {
     (void)n2;
-    // slabs up to 128 x 128; n0 even (16-byte rows for the tensor map) and a
+    // slabs up to 256 x 256; n0 even (16-byte rows for the tensor map) and a
     // slab large enough that the 16 x 32 steps are not mostly padding
-    if (n0 < 16 || n1 < 16 || n0 > 128 || n1 > 128 || (n0 & 1)) return false;
+    if (n0 < 16 || n1 < 16 || n0 > 256 || n1 > 256 || (n0 & 1)) return false;
     if (r0 < 1 || r1 < 1 || r2 < 1 || r0 > 24 || r1 > 24) return false;
     return true;
 }
@@ -463,7 +463,10 @@ int launch_fused3(int64_t n0, int64_t n1, const Fused3Args& a, int num_sms, cuda
     if (n0 == 32 && n1 == 32) return dispatch_mt<32, 32, true>(mt, n0, n1, a, num_sms, s, launches);
     // any other slab: the smallest kernel that holds it (the basis fragments
     // in shared memory are sized by the kernel's extents)
-    if (n0 < 2 || n0 > 128 || n1 < 1 || n1 > 128 || (n0 & 1)) return -1;
+    if (n0 < 2 || n0 > 256 || n1 < 1 || n1 > 256 || (n0 & 1)) return -1;
+    // above 128: the 256 x 256 kernel with two-stage rings (the basis
+    // fragments of both modes take 96 KB of shared memory at ranks 17..24)
+    if (n0 > 128 || n1 > 128) return dispatch_mt<256, 256, false, 2>(mt, n0, n1, a, num_sms, s, launches);
     if (n0 <= 32 && n1 <= 32) return dispatch_mt<32, 32, false>(mt, n0, n1, a, num_sms, s, launches);
     if (n0 <= 64 && n1 <= 64) return dispatch_mt<64, 64, false>(mt, n0, n1, a, num_sms, s, launches);
     if (n0 <= 64) return dispatch_mt<64, 128, false>(mt, n0, n1, a, num_sms, s, launches);

@@ -24,8 +24,10 @@
 namespace htr {
 namespace {
 
-constexpr int kGStages = 8;
-constexpr int kGChunk = 16;  // k rows per chunk (128 B: the swizzle span)
+constexpr int kGStages = 4;
+constexpr int kGChunk = 16;  // k rows per TMA box (128 B: the swizzle span)
+constexpr int kGBoxes = 2;   // boxes per stage: 32 k rows between two barrier hand-overs
+constexpr int kGUnit = kGChunk * kGBoxes;
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -103,7 +105,8 @@ __global__ void __launch_bounds__((consumer_warps<MB>() + 1) * 32, 1)
     // shared array itself so the compiler keeps the shared address space (LDS)
     const uint32_t pad = (1024u - (saddr(gsm_raw) & 1023u)) & 1023u;
     double* ring = reinterpret_cast<double*>(gsm_raw + pad);
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + kGStages * MP * kGChunk);
+    constexpr int SD = kGBoxes * MP * kGChunk;  // doubles per stage
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + kGStages * SD);
     uint64_t* empty = full + kGStages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
@@ -120,14 +123,16 @@ __global__ void __launch_bounds__((consumer_warps<MB>() + 1) * 32, 1)
         if (lane == 0) {
             uint64_t pol;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-            const uint32_t bytes = static_cast<uint32_t>(MP * kGChunk * sizeof(double));
+            const uint32_t bytes = static_cast<uint32_t>(SD * sizeof(double));
             for (int64_t u = u0, i = 0; u < u1; ++u, ++i) {
                 const int s = static_cast<int>(i % kGStages);
                 if (i >= kGStages) bar_wait(empty + s, static_cast<uint32_t>(((i / kGStages) - 1) & 1));
                 bar_expect_tx(full + s, bytes);
                 const int64_t b = u / kchunks, kc = u - b * kchunks;
-                tma3d(ring + s * MP * kGChunk, &tmap, static_cast<int>(kc * kGChunk), 0, static_cast<int>(b),
-                      full + s, pol);
+#pragma unroll
+                for (int x = 0; x < kGBoxes; ++x)  // (rows beyond K are zero-filled)
+                    tma3d(ring + s * SD + x * MP * kGChunk, &tmap, static_cast<int>(kc * kGUnit + x * kGChunk), 0,
+                          static_cast<int>(b), full + s, pol);
             }
         }
         return;
@@ -145,10 +150,10 @@ __global__ void __launch_bounds__((consumer_warps<MB>() + 1) * 32, 1)
     for (int64_t u = u0, i = 0; u < u1; ++u, ++i) {
         const int s = static_cast<int>(i % kGStages);
         bar_wait(full + s, static_cast<uint32_t>((i / kGStages) & 1));
-        const double* ch = ring + s * MP * kGChunk;
 #pragma unroll
-        for (int ks = 0; ks < kGChunk / 4; ++ks) {
-            const int k = 4 * ks + t4;
+        for (int ks8 = 0; ks8 < kGUnit / 4; ++ks8) {
+            const double* ch = ring + s * SD + (ks8 / (kGChunk / 4)) * MP * kGChunk;
+            const int k = 4 * (ks8 % (kGChunk / 4)) + t4;
             double af[4], bf[4];
 #pragma unroll
             for (int t = 0; t < 4; ++t) af[t] = ch[swz(32 * mb + 8 * t + g4, k)];
@@ -455,13 +460,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 
 template <int MB>
 size_t gram_smem_bytes() {
-    return sizeof(double) * kGStages * 32 * MB * kGChunk + 2 * kGStages * sizeof(uint64_t) + 1024;
+    return sizeof(double) * kGStages * kGBoxes * 32 * MB * kGChunk + 2 * kGStages * sizeof(uint64_t) + 1024;
 }
 
 template <int MB>
 int launch_mb(const double* Y, int64_t K, int64_t M, int64_t B, double* partials, int grid, const CUtensorMap& map,
               cudaStream_t s) {
-    const int64_t kchunks = (K + kGChunk - 1) / kGChunk;
+    const int64_t kchunks = (K + kGUnit - 1) / kGUnit;
     const size_t smem = gram_smem_bytes<MB>();
     ensure_smem_limit(reinterpret_cast<const void*>(gram_stream_kernel<MB>), smem);
     gram_stream_kernel<MB><<<grid, (consumer_warps<MB>() + 1) * 32, smem, s>>>(B * kchunks, kchunks, static_cast<int>(M),
@@ -568,7 +573,7 @@ int launch_gram_stream(const double* Y, int64_t K, int64_t M, int64_t B, double*
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return -1;
-    const int64_t units = B * ((K + kGChunk - 1) / kGChunk);
+    const int64_t units = B * ((K + kGUnit - 1) / kGUnit);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, units)));
     if (MB == 1) launch_mb<1>(Y, K, M, B, partials, grid, map, s);
     else if (MB == 2) launch_mb<2>(Y, K, M, B, partials, grid, map, s);

@@ -346,6 +346,8 @@ def test_fused_path_matches_generic(ht):
     ((5, 4, 3), 7, 5, (50, 18)),       # ragged in both (50 rows: a partial quarter; 18 columns: a partial pair)
     ((4, 4, 2), 5, 2, (16, 16)),       # the smallest slab the fused kernel takes
     ((8, 3, 6), 10, 3, (34, 100)),     # 64 x 128 kernel
+    ((12, 9, 4), 6, 2, (256, 256)),    # above 128: the 256 x 256 kernel with two-stage rings
+    ((20, 5, 3), 5, 2, (160, 200)),    # ... padded in both modes, MT = 3
 ])
 def test_fused_tail_tile_cases(ht, ranks, n2, nsamp, n01):
     """fused3 + tail3 (skip-path encode) against the generic GEMM chain across

@@ -19,9 +19,20 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -c
 timeout 300 python tools/ncu_targets.py c5 c1 > gpurun_out/targets_plain.log 2>&1 &&
 timeout 1500 ncu --set full --clock-control none --import-source on \
   -k 'regex:^(tridiag_reduce|tridiag_bisect|tridiag_vectors|chol_panel|gram_stream|gram_mode0|gram_mid|proj2|gemm_fast)' \
-  -c 40 -o gpurun_out/r2_targets python tools/ncu_targets.py c5 c1 > gpurun_out/ncu_targets.log 2>&1
+  -c 40 -o /tmp/r2_targets python tools/ncu_targets.py c5 c1 > gpurun_out/ncu_targets.log 2>&1
+# (the reports are summarised here: gpurun brings back at most 64 MiB)
+python tools/ncu_multi_summary.py /tmp/r2_targets.ncu-rep > gpurun_out/r2_bht_kernels_ncu_summary.txt 2>&1
+for k in gram_stream tridiag_reduce tridiag_vectors proj2; do
+  echo "== $k" >> gpurun_out/r2_bht_kernels_ncu_lines.txt
+  python tools/ncu_lines.py /tmp/r2_targets.ncu-rep $k 12 >> gpurun_out/r2_bht_kernels_ncu_lines.txt 2>&1
+done
 timeout 300 python tools/ncu_targets_update.py > gpurun_out/targets_update_plain.log 2>&1 &&
 timeout 1500 ncu --set full --clock-control none --import-source on \
   -k 'regex:^(fused3|tail3|tail4|quad|field|expand|decode2)' \
-  -c 40 -o gpurun_out/r2_update_targets python tools/ncu_targets_update.py > gpurun_out/ncu_update_targets.log 2>&1
+  -c 40 -o /tmp/r2_update_targets python tools/ncu_targets_update.py > gpurun_out/ncu_update_targets.log 2>&1
+python tools/ncu_multi_summary.py /tmp/r2_update_targets.ncu-rep > gpurun_out/r2_update_kernels_ncu_summary.txt 2>&1
+for k in fused3_kernel tail3_kernel tail4_kernel quad_stream; do
+  echo "== $k" >> gpurun_out/r2_update_kernels_ncu_lines.txt
+  python tools/ncu_lines.py /tmp/r2_update_targets.ncu-rep $k 12 >> gpurun_out/r2_update_kernels_ncu_lines.txt 2>&1
+done
 echo done

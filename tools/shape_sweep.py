@@ -25,11 +25,12 @@ CASES = [
     ("50^3 r8", (50, 50, 50), 8, "1_23", 512),
     ("128x64x32 r10", (128, 64, 32), 10, "1_23", 512),
     ("63^3 r8 (odd leading extent: generic engine)", (63, 63, 63), 8, "1_23", 256),
-    ("256x256x16 r12 (extent > 128: generic engine)", (256, 256, 16), 12, "1_23", 128),
+    ("256x256x16 r12 (2-D grids x channels; the 256 x 256 kernel)", (256, 256, 16), 12, "1_23", 128),
+    ("512x512x4 r12 (extent > 256: generic engine)", (512, 512, 4), 12, "1_23", 128),
     ("64x64x64x5 r6 balanced (3-D fields x variables)", (64, 64, 64, 5), 6, "balanced", 64),
     ("120x120x12x4 r6 balanced", (120, 120, 12, 4), 4, "balanced", 128),
     ("64x64x3x16 r6 balanced (video clips)", (64, 64, 3, 16), 3, "balanced", 512),
-    ("24^4 r5 balanced (small extents: generic engine)", (24, 24, 24, 24), 5, "balanced", 256),
+    ("24^4 r5 balanced (padded 32 x 32 kernel)", (24, 24, 24, 24), 5, "balanced", 256),
 ]
 K = 12
 
