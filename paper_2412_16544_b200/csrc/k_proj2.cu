@@ -122,30 +122,10 @@ __global__ void __launch_bounds__(kP2Warps * 32, 1) proj2_kernel(const Proj2Args
             const int st = r % kP2Stages;
             mbar_wait(&my_full[st], static_cast<uint32_t>((r / kP2Stages) & 1));
             const double* X = my_stages + st * stage_doubles;  // [i1][8]
-            // two independent accumulator sets over alternate k-steps: each
-            // DMMA chain is half as long and twice as many are in flight
-            double q2[NT1][2];
-#pragma unroll
-            for (int nt = 0; nt < NT1; ++nt) q2[nt][0] = q2[nt][1] = 0.0;
-            const int nks = n1 / 4;
-            int ks = 0;
-            for (; ks + 1 < nks; ks += 2) {
-                const double av0 = X[(4 * ks + t) * 8 + g];
-                const double av1 = X[(4 * ks + 4 + t) * 8 + g];
-#pragma unroll
-                for (int nt = 0; nt < NT1; ++nt) dmma(q[nt], av0, U1s[(4 * ks + t) * kP2Pad + 8 * nt + g]);
-#pragma unroll
-                for (int nt = 0; nt < NT1; ++nt) dmma(q2[nt], av1, U1s[(4 * ks + 4 + t) * kP2Pad + 8 * nt + g]);
-            }
-            if (ks < nks) {
+            for (int ks = 0; ks < n1 / 4; ++ks) {
                 const double av = X[(4 * ks + t) * 8 + g];
 #pragma unroll
                 for (int nt = 0; nt < NT1; ++nt) dmma(q[nt], av, U1s[(4 * ks + t) * kP2Pad + 8 * nt + g]);
-            }
-#pragma unroll
-            for (int nt = 0; nt < NT1; ++nt) {
-                q[nt][0] += q2[nt][0];
-                q[nt][1] += q2[nt][1];
             }
             __syncwarp();
             if (lane == 0) {
