@@ -57,8 +57,11 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self.source = "nvidia-smi"
 
     def _run(self):
+        if self._run_nvml():
+            return
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -72,6 +75,45 @@ class ClockSampler:
             except Exception:
                 pass
             self._stop.wait(0.2)
+
+    def _run_nvml(self) -> bool:
+        """Poll NVML directly every millisecond (the timed region of a default
+        run is ~10 ms: one nvidia-smi process start would cover it with a
+        single sample). False when NVML is unavailable (nvidia-smi fallback)."""
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            try:
+                uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(("GPU-" + uuid if not uuid.startswith("GPU-") else uuid).encode())
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            reasons(h)
+        except Exception:
+            return False
+        bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal_slowdown, sw_thermal_slowdown, sw_power_cap
+        while True:
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = int(reasons(h))
+                try:
+                    pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                except Exception:
+                    pw = 0.0
+                self.samples.append([str(sm), str(mx), f"{pw:.1f}", hex(r)] +
+                                    ["Active" if r & b else "Not Active" for b in bits])
+            except Exception:
+                pass
+            if self._stop.wait(0.001):
+                break
+        self.source = "nvml"
+        return True
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -94,7 +136,7 @@ class ClockSampler:
                 if len(s) > 4 + i and s[4 + i].lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "source": self.source}
 
 
 def _dist_env():

@@ -102,6 +102,23 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
     return c;
 }
 
+/// The Householder scalars of a column (alpha its first entry, xn2 the squared
+/// norm of the rest): hs[0] = tau, hs[1] = 1 / (alpha - beta), hs[2] = beta.
+/// FP64 sqrt and divisions are long instruction sequences; they are computed
+/// by one thread and read by everyone (all 32 warps computing them
+/// redundantly cost more issue slots per step than the matrix update).
+__device__ __forceinline__ void house_scalars(double alpha, double xn2, double* hs) {
+    double tau = 0.0, beta = alpha, scale = 0.0;
+    if (xn2 > 0.0) {
+        beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+    }
+    hs[0] = tau;
+    hs[1] = scale;
+    hs[2] = beta;
+}
+
 /// Householder reduction Q^T G Q = T (dsytd2, lower) of one Gram per CTA.
 /// Three block barriers per column: the reflector is formed from the
 /// column's norm (accumulated by the previous column's update), the
@@ -121,7 +138,7 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_reduce_kernel(const __gri
     extern __shared__ double smem[];
     __shared__ double red[32];
     __shared__ double pdp[32];
-    __shared__ double xn2_next;
+    __shared__ double hs[4];  // the current column's tau, scale, beta (house_scalars)
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     const int64_t nn = static_cast<int64_t>(n) * n;
     double* A = use_smem ? smem : W;
@@ -147,16 +164,15 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_reduce_kernel(const __gri
         for (int i = 2 + tid; i < n; i += nt) ps = fma(A[i], A[i], ps);
         xn2 = block_sum(ps, red);
     }
+    if (tid == 0 && n > 2) house_scalars(A[1], xn2, hs);
+    __syncthreads();
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1;
         double* x = A + (k + 1) + static_cast<int64_t>(n) * k;
-        const double alpha = x[0];
-        double tau = 0.0, beta = alpha, scale = 0.0;
-        if (xn2 > 0.0) {
-            beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
-            tau = (beta - alpha) / beta;
-            scale = 1.0 / (alpha - beta);
-        }
+        // written for this column by the previous step (the warp that updated
+        // it) before that step's closing barrier; rewritten after this step's
+        // second barrier
+        const double tau = hs[0], scale = hs[1], beta = hs[2];
         for (int i = tid; i < m; i += nt) {
             const double vi = i == 0 ? 1.0 : x[i] * scale;
             vv[i] = vi;
@@ -173,6 +189,8 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_reduce_kernel(const __gri
             double ps = 0.0;
             for (int i = 2 + tid; i < m; i += nt) ps = fma(A22[i], A22[i], ps);
             xn2 = block_sum(ps, red);
+            if (tid == 0 && m >= 2) house_scalars(A22[1], xn2, hs);
+            __syncthreads();
             continue;
         }
         // p = tau A22 v (column j dotted with v), and p . v per warp
@@ -202,19 +220,22 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_reduce_kernel(const __gri
             for (int j = warp; j < m; j += nw) {
                 double* col = A22 + static_cast<int64_t>(n) * j;
                 const double vj = vv[j], wj = fma(-K, vj, pw[j]);
-                double s = 0.0;
+                double s = 0.0, a0 = 0.0;  // a0: the updated entry i = lane (t = 0)
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
                     const int i = lane + 32 * t;
                     if (i < m) {
                         const double a = col[i] - fma(vr[t], wj, wr[t] * vj);
                         col[i] = a;
+                        if (t == 0) a0 = a;
                         if (i >= 2) s = fma(a, a, s);
                     }
                 }
                 if (j == 0) {
+                    // the next column: its head (row 1) and the rest's norm
                     s = warp_sum(s);
-                    if (lane == 0) xn2_next = s;
+                    const double head = __shfl_sync(0xffffffffu, a0, 1);
+                    if (lane == 0) house_scalars(head, s, hs);
                 }
             }
         } else {
@@ -232,21 +253,22 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_reduce_kernel(const __gri
             for (int j = warp; j < m; j += nw) {
                 double* col = A22 + static_cast<int64_t>(n) * j;
                 const double vj = vv[j], wj = fma(-K, vj, pw[j]);
-                double s = 0.0;
+                double s = 0.0, a0 = 0.0;
                 for (int i = lane; i < m; i += 32) {
                     const double wi = fma(-K, vv[i], pw[i]);
                     const double a = col[i] - fma(vv[i], wj, wi * vj);
                     col[i] = a;
+                    if (i == lane) a0 = a;
                     if (j == 0 && i >= 2) s = fma(a, a, s);
                 }
                 if (j == 0) {
                     s = warp_sum(s);
-                    if (lane == 0) xn2_next = s;
+                    const double head = __shfl_sync(0xffffffffu, a0, 1);
+                    if (lane == 0) house_scalars(head, s, hs);
                 }
             }
         }
         __syncthreads();
-        xn2 = xn2_next;
     }
     // T: diagonal and subdiagonal; reflectors to the workspace
     for (int i = tid; i < n; i += nt) {
@@ -713,8 +735,10 @@ void launch_tridiag_eigvals(const double* const* G, const int64_t* n, double* co
             nmax = std::max(nmax, n[i0 + k]);
             ++k;
         }
-        const size_t smem = sm ? sizeof(double) * static_cast<size_t>(nmax * nmax + 2 * nmax) : 0;
         const int T = sm ? static_cast<int>((nmax - 1 + 31) / 32) : 0;  // m = n - 1 rows at most
+        // (small matrices: fewer threads, cheaper barriers and loop overhead)
+        const int threads = nmax <= 32 ? 128 : (nmax <= 64 ? 256 : kTriThreads);
+        const size_t smem = sm ? sizeof(double) * static_cast<size_t>(nmax * nmax + 2 * nmax) : 0;
         auto kfn = T == 0 ? tridiag_reduce_kernel<0>
                  : T == 1 ? tridiag_reduce_kernel<1>
                  : T == 2 ? tridiag_reduce_kernel<2>
@@ -722,8 +746,6 @@ void launch_tridiag_eigvals(const double* const* G, const int64_t* n, double* co
                  : T == 4 ? tridiag_reduce_kernel<4>
                           : tridiag_reduce_kernel<5>;
         if (smem > 0) ensure_smem_limit(reinterpret_cast<const void*>(kfn), smem);
-        // (small matrices: fewer threads, cheaper barriers and loop overhead)
-        const int threads = nmax <= 32 ? 128 : (nmax <= 64 ? 256 : kTriThreads);
         kfn<<<k, threads, smem, s>>>(jobs, sm ? 1 : 0);
         // eigenvalues: a warp per eigenvalue over many CTAs
         dim3 grid(static_cast<unsigned>((nmax + kBisWarps - 1) / kBisWarps), static_cast<unsigned>(k));

@@ -115,8 +115,11 @@ def test_two_ranks_all_configs(cuda, tmp_path):
     c2 (fused 3-way leaf + tail kernels on 16-sample shards), c3 through its
     batch-25 expansion (residual Grams all-reduced), c4 (fused 8-way subtree
     kernels), c5's 128^3 rank-20 shapes (fused path, 3-sample shards)."""
+    # + a 48 x 34 x 12 family: slabs that are no multiple of the fused kernel's
+    # steps (the padded 64 x 64 kernel) through skip updates on 4-sample shards
+    padded = {"dims": [48, 34, 12], "ranks": [5, 4, 3], "batch": 8, "eps": 1e-6, "seed": 11}
     cases = [_oracle_case("c1", 1), _oracle_case("c2", 4), _oracle_case("c3", 26),
-             _oracle_case("c4", 2), _oracle_case("c5", 3, batch=6)]
+             _oracle_case("c4", 2), _oracle_case("c5", 3, batch=6), _oracle_case("padded", 4, custom=padded)]
     _check(_run_world(2, cases, tmp_path), len(cases), 2)
 
 
