@@ -24,8 +24,11 @@
 // per-CTA partials) and ||latent||^2 in a fixed order. Replaces two generic
 // GEMM launches, the latent norm pass and two scalar reductions.
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "kernels.cuh"
 
@@ -349,6 +352,252 @@ __global__ void __launch_bounds__(kThreads, 2) tail3_kernel(const Tail3Args a) {
     }
 }
 
+// ---- identity transfer basis: the latent is Z itself -----------------------
+// A full-rank transfer node carries the identity basis (BHT-l2r's Cholesky
+// certificate; config 5: rt = r1 r2 = 400), so the tail is phase A alone and
+// Z_s needs no shared-memory staging. Work units (sample, 16 rows p of Z_s =
+// two m-tiles) are dealt round-robin to every warp of a grid two CTAs per SM
+// deep. W arrives by TMA: a [R01, n2, S] tensor map, 16 x 16 boxes (128-byte
+// rows, 128-byte swizzle) into the warp's own four-stage ring, one lane
+// issuing the copies and an mbarrier per stage, so a warp keeps 8 KB of W in
+// flight without holding the loads in registers (register prefetch is capped
+// by the six scoreboards of a warp: a variant with sixteen loads per lane in
+// flight measured 69 us). Per stage 4 k-steps x 2 x NT DMMAs; the tiles are
+// stored straight into the latent; per-CTA ||latent||^2 partials, the final
+// reductions by the last CTA. c5: 42.7 us against 53.7 us for the
+// one-CTA-per-sample kernel. (Writing W in 16-row blocks from fused3 so that a
+// unit is one contiguous range was measured too: the scattered 128-byte
+// writes cost fused3 5 % and the tail gained nothing.)
+constexpr int kIdStages = 4;
+constexpr int kIdBox = 16;                    // rows p and steps k per box
+constexpr int kIdStageDoubles = kIdBox * kIdBox;
+
+__device__ __forceinline__ uint32_t id_saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// element (k, p) of a swizzled 16 x 16 box (rows k of 128 bytes)
+__device__ __forceinline__ int id_swz(int k, int p) { return k * kIdBox + ((((p >> 1) ^ (k & 7))) << 1) + (p & 1); }
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 2)
+    tail3_identity_kernel(const Tail3Args a, const __grid_constant__ CUtensorMap wmap) {
+    extern __shared__ __align__(1024) unsigned char idsm_raw[];
+    const int r0 = a.r0, r1 = a.r1, r2 = a.r2;
+    const int R01 = r0 * r1;
+    const int n2 = static_cast<int>(a.n2);
+    const int spu = (n2 + kIdBox - 1) / kIdBox;  // stages per unit
+    const int n2p = spu * kIdBox;
+    // rings first (1024-byte aligned for the swizzle), then U2 (zero rows beyond n2)
+    const uint32_t pad = (1024u - (id_saddr(idsm_raw) & 1023u)) & 1023u;
+    double* rings = reinterpret_cast<double*>(idsm_raw + pad);  // [warp][stage][16][16]
+    double* U2s = rings + kWarps * kIdStages * kIdStageDoubles;  // [n2p][kU2Pitch]
+    __shared__ __align__(8) uint64_t full[kWarps][kIdStages];
+    __shared__ double red[kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g4 = lane >> 2, t4 = lane & 3;
+
+    const int mtA = (R01 + 7) / 8;
+    const int upg = (mtA + 1) / 2;  // units (pairs of m-tiles) per sample
+    const int64_t units = a.S * upg;
+    const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + warp, nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int64_t my_units = gw < units ? (units - gw + nw - 1) / nw : 0;
+    const int64_t total = my_units * spu;  // stages this warp consumes
+    double* ring = rings + warp * kIdStages * kIdStageDoubles;
+    uint64_t* bar = full[warp];
+    auto issue = [&](int64_t i) {  // lane 0: stage i of this warp's sequence
+        const int st = static_cast<int>(i % kIdStages);
+        const int64_t u = gw + (i / spu) * nw;
+        const int kc = static_cast<int>(i % spu);
+        const int64_t s = u / upg;
+        const int p0 = static_cast<int>(u - s * upg) * kIdBox;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(id_saddr(&bar[st])),
+                     "r"(static_cast<uint32_t>(kIdStageDoubles * sizeof(double)))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(id_saddr(ring + st * kIdStageDoubles)),
+            "l"(reinterpret_cast<uint64_t>(&wmap)), "r"(p0), "r"(kc * kIdBox), "r"(static_cast<int>(s)),
+            "r"(id_saddr(&bar[st]))
+            : "memory");
+    };
+    if (lane == 0) {
+        for (int k = 0; k < kIdStages; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(id_saddr(&bar[k])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int e = tid; e < n2p * kU2Pitch; e += kThreads) {
+        const int i2 = e / kU2Pitch, c = e - i2 * kU2Pitch;
+        U2s[e] = (c < r2 && i2 < n2) ? a.U2[i2 + static_cast<int64_t>(n2) * c] : 0.0;
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // fused3's W and ||y||^2 partials are complete
+    if (lane == 0)
+        for (int64_t i = 0; i < kIdStages && i < total; ++i) issue(i);
+
+    double lsq = 0.0;
+    int64_t i = 0;
+    for (int64_t uu = 0; uu < my_units; ++uu) {
+        const int64_t u = gw + uu * nw;
+        const int64_t s = u / upg;
+        const int mt0 = static_cast<int>(u - s * upg) * 2;
+        double acc[2][NT][2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) acc[x][j][0] = acc[x][j][1] = 0.0;
+        for (int kc = 0; kc < spu; ++kc, ++i) {
+            const int st = static_cast<int>(i % kIdStages);
+            const uint32_t parity = static_cast<uint32_t>((i / kIdStages) & 1);
+            asm volatile(
+                "{\n\t.reg .pred p;\nWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n}\n" ::"r"(
+                    id_saddr(&bar[st])),
+                "r"(parity)
+                : "memory");
+            const double* box = ring + st * kIdStageDoubles;
+#pragma unroll
+            for (int ks = 0; ks < kIdBox / 4; ++ks) {
+                const int kk = 4 * ks + t4;
+                const double a0 = box[id_swz(kk, g4)], a1 = box[id_swz(kk, 8 + g4)];
+                const double* u2 = U2s + (kc * kIdBox + kk) * kU2Pitch + g4;
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    const double b = u2[8 * j];
+                    dmma(acc[0][j], a0, b);
+                    dmma(acc[1][j], a1, b);
+                }
+            }
+            // the stage is consumed: refill it (generic-proxy reads before the async-proxy write)
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                if (i + kIdStages < total) issue(i + kIdStages);
+            }
+        }
+        double* out = a.latent + s * static_cast<int64_t>(R01) * r2;
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            const int p = 8 * (mt0 + x) + g4;
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int a2 = 8 * j + 2 * t4 + h;
+                    if (p < R01 && a2 < r2) {
+                        const double v = acc[x][j][h];
+                        out[p + static_cast<int64_t>(R01) * a2] = v;
+                        lsq = fma(v, v, lsq);
+                    }
+                }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsq += __shfl_xor_sync(0xffffffffu, lsq, o);
+    if (lane == 0) red[warp] = lsq;
+    __syncthreads();
+    __shared__ bool last;
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kWarps; ++w) t += red[w];
+        a.latsq[blockIdx.x] = t;
+        __threadfence();
+        last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double ys = 0.0, ls = 0.0;
+    for (int64_t k = tid; k < a.n_ysq; k += kThreads) ys += __ldcg(a.ysq_partials + k);
+    for (int64_t k = tid; k < gridDim.x; k += kThreads) ls += __ldcg(a.latsq + k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ys += __shfl_xor_sync(0xffffffffu, ys, o);
+        ls += __shfl_xor_sync(0xffffffffu, ls, o);
+    }
+    __shared__ double red2[2][kWarps];
+    if (lane == 0) {
+        red2[0][warp] = ys;
+        red2[1][warp] = ls;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int w = 0; w < kWarps; ++w) {
+            t0 += red2[0][w];
+            t1 += red2[1][w];
+        }
+        a.out[0] = t0;
+        a.out[2] = t1;
+        if (a.host_out) {
+            a.host_out[0] = t0;
+            a.host_out[2] = t1;
+        }
+        *a.ticket = 0u;
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 id_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+int tail3_identity_grid(const Tail3Args& a) {
+    const int64_t mtA = (static_cast<int64_t>(a.r0) * a.r1 + 7) / 8;
+    const int64_t units = a.S * ((mtA + 1) / 2);
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(2 * a.num_sms, (units + kWarps - 1) / kWarps)));
+}
+
+size_t tail3_identity_smem(int64_t n2) {
+    const int64_t n2p = (n2 + kIdBox - 1) / kIdBox * kIdBox;
+    return sizeof(double) * static_cast<size_t>(kWarps * kIdStages * kIdStageDoubles + n2p * kU2Pitch) + 1024;
+}
+
+/// Launches the identity-transfer tail; false (nothing launched) when the
+/// operands do not fit it (odd r0 r1, unaligned W, no tensor-map encoder).
+bool launch_identity(const Tail3Args& a, cudaStream_t s) {
+    const int64_t R01 = static_cast<int64_t>(a.r0) * a.r1;
+    auto enc = id_encoder();
+    if (!enc || (R01 & 1) || (reinterpret_cast<uintptr_t>(a.wslab) & 15u) || a.n2 > 4096 || a.S >= (int64_t{1} << 31))
+        return false;
+    const size_t smem = tail3_identity_smem(a.n2);
+    if (smem > 100 * 1024) return false;  // two CTAs per SM
+    alignas(64) CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(R01), static_cast<cuuint64_t>(a.n2), static_cast<cuuint64_t>(a.S)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(R01 * 8), static_cast<cuuint64_t>(R01 * a.n2 * 8)};
+    cuuint32_t box[3] = {kIdBox, kIdBox, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(a.wslab), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(tail3_identity_grid(a)));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    auto run = [&](auto kfn) {
+        if (smem > 46 * 1024) ensure_smem_limit(reinterpret_cast<const void*>(kfn), smem);
+        cudaLaunchKernelEx(&cfg, kfn, a, map);
+    };
+    switch ((a.r2 + 7) / 8) {
+        case 1: run(tail3_identity_kernel<1>); break;
+        case 2: run(tail3_identity_kernel<2>); break;
+        default: run(tail3_identity_kernel<3>); break;
+    }
+    return true;
+}
+
 // ---- sample-pair variant --------------------------------------------------
 // One CTA per pair of samples (s0, s0 + 1), 10 warps:
 //   phase A  Z_s = W_s U2 for both samples (as above), written transposed
@@ -637,12 +886,21 @@ void launch_nt(const Tail3Args& a, size_t smem, cudaStream_t s) {
 
 }  // namespace
 
+int64_t tail3_latsq_entries(int64_t S, int num_sms) { return std::max<int64_t>(8 * S, 2 * static_cast<int64_t>(num_sms)); }
+
 bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2) {
     if (r0 < 1 || r1 < 1 || r2 < 1 || rt < 1 || r0 > 24 || r2 > 24) return false;
     return tail3_smem(n2, r0, r1, r2) <= 200 * 1024;
 }
 
 void launch_tail3(const Tail3Args& a, cudaStream_t s, int64_t* launches) {
+    // identity transfer basis: the unit-dealt TMA kernel (HTR_OPT_TAIL_KERNEL
+    // = 1 keeps the one-CTA-per-sample kernel); a small batch stays with the
+    // cluster-split kernel below
+    if (a.identity_transfer && a.variant == 0 && 2 * a.S > static_cast<int64_t>(a.num_sms) && launch_identity(a, s)) {
+        ++*launches;
+        return;
+    }
     if (a.variant == 2 && !a.identity_transfer) {
         const size_t psmem = tail3_pair_smem(a.n2, a.r0, a.r1, a.r2);
         if (psmem <= 220 * 1024) {

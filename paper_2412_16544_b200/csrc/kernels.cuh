@@ -255,6 +255,8 @@ struct Tail3Args {
     bool identity_transfer = false;  // B == I (rt == r1 r2): latent = Z, no projection
 };
 bool tail3_supported(int r0, int r1, int r2, int rt, int64_t n2);
+/// Entries the tail writes into Tail3Args::latsq (whichever kernel it picks).
+int64_t tail3_latsq_entries(int64_t S, int num_sms);
 
 // Skip-path tail for balanced 4-way trees ((1,2),(3,4)), one CTA per sample
 // (k_tail4.cu): from fused3's per-slab W = [R01 = r0 r1, n2, n3, S] to the

@@ -1527,7 +1527,7 @@ bool launch_skip_encode3(Context& c, const Rep& h, const DT& y, const DT* latent
     ta.latent = lat.data();
     ta.variant = c.tail_kernel;
     ta.num_sms = c.num_sms;
-    BufPtr lsq = c.alloc(8 * batch);  // per-CTA partials (up to 8 CTAs per sample)
+    BufPtr lsq = c.alloc(tail3_latsq_entries(batch, c.num_sms));  // per-CTA partials
     ta.latsq = lsq->p;
     ta.ysq_partials = fa.ysq_partials;
     ta.n_ysq = grid;

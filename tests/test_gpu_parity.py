@@ -628,6 +628,30 @@ def test_identity_transfer_tail_vs_generic_and_oracle(ht):
     r2, ur = ho.ht_rise_update(ref, y1)
     assert ug.used_fused_path and ug.skipped == ur.skipped
     compare_reps(ht, g2, r2, check_slices=True)
+    # a batch of more than half an SM count of samples takes the unit-dealt
+    # TMA kernel (tail3_identity_kernel) instead of the cluster-split one
+    y3 = ro.tucker_family_batch(bases, 80, rng)
+    la3, pa3 = ht.encode(gpu, y3)
+    ctx.set_option(ht.OPT_TAIL_KERNEL, 1)  # one CTA per sample
+    try:
+        lc3, _ = ht.encode(gpu, y3)
+    finally:
+        ctx.set_option(ht.OPT_TAIL_KERNEL, 0)
+    ctx.set_option(ht.OPT_FUSED_ENCODE, 0)
+    try:
+        lb3, pb3 = ht.encode(gpu, y3)
+    finally:
+        ctx.set_option(ht.OPT_FUSED_ENCODE, 1)
+    assert np.linalg.norm(la3 - lb3) <= 1e-12 * np.linalg.norm(lb3)
+    assert np.linalg.norm(lc3 - lb3) <= 1e-12 * np.linalg.norm(lb3)
+    g3, ug3 = ht.ht_rise_update(g2, y3)
+    r3, ur3 = ho.ht_rise_update(r2, y3)
+    assert ug3.used_fused_path and ug3.skipped == ur3.skipped
+    assert abs(ug3.proj_error - ur3.proj_error) <= 1e-9 * np.linalg.norm(y3)
+    assert g3.ranks() == r3.ranks()
+    for m in (g3.accumulated, g3.accumulated - 40, g3.accumulated - 79):
+        a, b = ht.reconstruct_slice(g3, m), ho.reconstruct_slice(r3, m)
+        assert np.linalg.norm(a - b) <= 1e-9 * np.linalg.norm(b)
 
 
 def test_leading_modes_fused_matches_generic(ht):
