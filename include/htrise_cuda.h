@@ -110,7 +110,7 @@ HTR_API htr_status htr_synchronize(htr_context* ctx);
 #define HTR_OPT_EXACT_LOSS 1      /* 1: per-step explicit residual loss like bht.hpp:357-365 (default 0 = telescoped with guard band) */
 #define HTR_OPT_FUSED_ENCODE 2    /* 1 (default): fused DMMA leaf-projection kernel where it applies */
 #define HTR_OPT_PROFILE_EVENTS 3  /* 1: record per-kernel CUDA events for the bench */
-#define HTR_OPT_TAIL_KERNEL 4     /* skip-path tail of (1,(2,3)) trees: 0 auto (default: one sample per CTA), 1 one sample per CTA, 2 sample pairs */
+#define HTR_OPT_TAIL_KERNEL 4     /* skip-path tail of (1,(2,3)) trees: 0 auto (default: one sample per CTA, split over a cluster for small batches; the unit-dealt TMA kernel when the transfer basis is the identity), 1 one sample per CTA, 2 sample pairs */
 #define HTR_OPT_EIG_SOLVER 5      /* truncation eigensolver: 1 (default) Householder tridiagonal + bisection + inverse iteration, 0 Jacobi */
 HTR_API htr_status htr_context_set_option(htr_context* ctx, int32_t option, double value);
 /* Kernel launches issued on this context so far (monotonic counter). */
