@@ -628,8 +628,8 @@ def test_identity_transfer_tail_vs_generic_and_oracle(ht):
     r2, ur = ho.ht_rise_update(ref, y1)
     assert ug.used_fused_path and ug.skipped == ur.skipped
     compare_reps(ht, g2, r2, check_slices=True)
-    # a batch of more than half an SM count of samples takes the unit-dealt
-    # TMA kernel (tail3_identity_kernel) instead of the cluster-split one
+    # a larger batch (several units per warp of the unit-dealt TMA kernel,
+    # tail3_identity_kernel) against the one-CTA-per-sample kernel
     y3 = ro.tucker_family_batch(bases, 80, rng)
     la3, pa3 = ht.encode(gpu, y3)
     ctx.set_option(ht.OPT_TAIL_KERNEL, 1)  # one CTA per sample
