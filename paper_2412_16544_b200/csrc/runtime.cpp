@@ -548,6 +548,83 @@ Truncation finish_tri(Context& c, const TriSolve& ts, const DT& G, int64_t rows,
     return t;
 }
 
+/// finish_tri for the nodes of one layer at once: every node's rank rule is
+/// enqueued before the first result is read back, and the retained
+/// eigenvectors of all nodes are formed by ONE launch (a CTA per node) instead
+/// of one launch per node behind a host round trip each (c1's four leaves:
+/// 4 x 76 us of single-CTA launches -> one). Results equal finish_tri's bit
+/// for bit.
+std::vector<Truncation> finish_tri_batch(Context& c, const std::vector<TriSolve>& ts, const std::vector<DT>& G,
+                                         const std::vector<int64_t>& rows, const std::vector<int64_t>& cols,
+                                         double eps_abs, int64_t min_rank, const std::vector<ProjectedGram>& refine,
+                                         const std::vector<double>& noise) {
+    const size_t m = ts.size();
+    std::vector<Truncation> out(m);
+    std::vector<char> done(m, 0);
+    for (size_t j = 0; j < m; ++j) {
+        if (!refine[j]) continue;
+        const int64_t n = rows[j];
+        std::vector<double> lh(static_cast<size_t>(n));
+        c.fetch(ts[j].lam->p, n, lh.data());
+        const double lmax = std::max({lh[0], noise[j], 0.0});
+        if (lmax > 0.0 && eps_abs * eps_abs < refine_threshold(n) * lmax) {
+            int64_t s0 = 0;
+            while (s0 < n && lh[static_cast<size_t>(s0)] >= 1e-6 * lmax) ++s0;
+            if (s0 < n) {
+                out[j] = truncate_jacobi(c, G[j], rows[j], cols[j], eps_abs, min_rank, refine[j], noise[j]);
+                done[j] = 1;
+            }
+        }
+    }
+    std::vector<BufPtr> infos(m);
+    for (size_t j = 0; j < m; ++j) {
+        if (done[j]) continue;
+        infos[j] = c.alloc(4);
+        launch_rank_rule(ts[j].lam->p, std::min(rows[j], cols[j]), rows[j], eps_abs, min_rank, nullptr, infos[j]->p, c.s,
+                         &c.launches);
+    }
+    HTR_CUDA(cudaGetLastError());
+    std::vector<char> zero(m, 0);
+    std::vector<const double*> Wp, ip;
+    std::vector<int64_t> nn, rr;
+    std::vector<double*> up;
+    for (size_t j = 0; j < m; ++j) {
+        if (done[j]) continue;
+        double h[4];
+        c.fetch(infos[j]->p, 3, h);
+        Truncation& t = out[j];
+        t.rank = static_cast<int64_t>(h[0]);
+        t.discarded = h[1];
+        zero[j] = h[2] == 0.0;
+        if (t.rank > 0) {
+            std::vector<double> l(static_cast<size_t>(t.rank));
+            c.fetch(ts[j].lam->p, t.rank, l.data());
+            t.sigma.resize(static_cast<size_t>(t.rank));
+            for (int64_t i = 0; i < t.rank; ++i)
+                t.sigma[static_cast<size_t>(i)] = zero[j] ? 0.0 : std::sqrt(std::max(0.0, l[static_cast<size_t>(i)]));
+        }
+        t.u = c.tensor({rows[j], t.rank});
+        if (t.rank > 0) {
+            Wp.push_back(ts[j].W->p);
+            ip.push_back(infos[j]->p);
+            nn.push_back(rows[j]);
+            rr.push_back(t.rank);
+            up.push_back(t.u.data());
+        }
+    }
+    if (!Wp.empty())
+        launch_tridiag_vectors(Wp.data(), ip.data(), nn.data(), rr.data(), up.data(), static_cast<int>(Wp.size()), c.s,
+                               &c.launches);
+    for (size_t j = 0; j < m; ++j) {
+        if (done[j] || out[j].rank <= 0 || zero[j]) continue;
+        BufPtr oinfo = c.alloc(4);  // CholeskyQR2 polish (as finish_tri)
+        BufPtr work = c.alloc(out[j].rank * out[j].rank + 16);
+        launch_orthonormalize_new(nullptr, rows[j], 0, out[j].u.data(), out[j].rank, oinfo->p, work->p, c.s, &c.launches);
+    }
+    HTR_CUDA(cudaGetLastError());
+    return out;
+}
+
 Truncation truncate_gram(Context& c, const DT& G, int64_t rows, int64_t cols, double eps_abs, int64_t min_rank,
                          const ProjectedGram& refine, double noise_scale) {
     if (c.tridiag && tridiag_supported(rows)) {
@@ -1174,10 +1251,16 @@ std::vector<Truncation> truncate_modes(Context& c, const DT& t, const std::vecto
         launch_jacobi_eig_batch(gp.data(), ns.data(), lp.data(), vp.data(), nb, c.s, &c.launches);
     }
     HTR_CUDA(cudaGetLastError());
+    std::vector<Truncation> tri_out;
+    if (c.tridiag) {
+        std::vector<int64_t> bcols;
+        for (size_t i = 0; i < modes.size(); ++i)
+            if (batch[i]) bcols.push_back(cols_global[i]);
+        tri_out = finish_tri_batch(c, tris, grams, ns, bcols, eps_abs, min_rank, refiners, noise);
+    }
     for (size_t i = 0, j = 0; i < modes.size(); ++i) {
         if (batch[i]) {
-            out[i] = c.tridiag ? finish_tri(c, tris[j], grams[j], ns[j], cols_global[i], eps_abs, min_rank,
-                                            refiners[j], noise[j])
+            out[i] = c.tridiag ? std::move(tri_out[j])
                                : truncate_eig(c, lams[j], vs[j], ns[j], cols_global[i], eps_abs, min_rank,
                                               refiners[j], noise[j]);
             ++j;
