@@ -243,6 +243,7 @@ struct FastArgs {
     double* partial;             // split-K partials or nullptr
     double* sq_partials;         // per-CTA sum of squares of C, or nullptr
     int staged;                  // C is n-contiguous, rows 16-byte aligned: coalesced epilogue
+    int sym_lower;               // skip tiles strictly above the diagonal (mirrored afterwards)
 };
 
 template <int BM, int BN, bool AK>
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, 2)
     const double* B = d.B + zb * d.sbb;
     const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
     const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
+    if (f.sym_lower && n0 >= m0 + BM) return;  // strictly above the diagonal: mirrored from the lower triangle
     const int64_t kbeg = zs * f.kchunk;
     const int64_t kend = min(f.K, kbeg + f.kchunk);
     const int ntiles = static_cast<int>((kend - kbeg + FBK - 1) / FBK);
@@ -568,6 +570,17 @@ __global__ void __launch_bounds__(XT, 2) expand_kernel(const double* __restrict_
     }
 }
 
+// C[m, n] = C[n, m] for n > m of a square single-level C (the symmetric
+// contractions whose upper tiles were skipped)
+__global__ void sym_mirror_kernel(double* C, int64_t n, int64_t scm, int64_t scn) {
+    const int64_t total = n * n;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t m = idx % n, c = idx / n;
+        if (c > m) C[m * scm + c * scn] = C[c * scm + m * scn];
+    }
+}
+
 __global__ void splitk_reduce_kernel(const GemmDesc d, const double* partial, int64_t splits, const Launch L) {
     const int64_t M = d.M, N = d.N1 * d.N2, MN = M * N, total = MN * d.batch;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -742,13 +755,22 @@ int launch_gemm(const GemmDesc& d, double* workspace, int num_sms, cudaStream_t 
         const int64_t c_sn = d.N2 == 1 ? d.scn1 : (d.N1 == 1 ? d.scn2 : d.scn1);
         const int staged = c_flat && c_sn == 1 && aligned16(d.C) && (d.scm % 2 == 0) &&
                            (d.batch == 1 || d.scb % 2 == 0);
-        FastArgs f{d.M, N, K, p.sam, p.sak, p.sbk, p.sbn, p.k1, p.sak2, p.sbk2, p.kchunk, p.splits, partial, sq_partials, staged};
+        // symmetric results: lower tiles only (square, single-level C, no
+        // accumulation into C, no per-CTA sums of squares)
+        const int sym = d.symmetric && d.M == N && d.batch == 1 && d.beta == 0.0 && !sq_partials && (d.N2 == 1 || d.N1 == 1);
+        FastArgs f{d.M, N, K, p.sam, p.sak, p.sbk, p.sbn, p.k1, p.sak2, p.sbk2, p.kchunk, p.splits, partial, sq_partials, staged, sym};
         launch_fast(p, d, f, L, grid, s);
         ++*launches;
         if (p.splits > 1) {
             const int64_t total = d.M * N * d.batch;
             const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * num_sms));
             splitk_reduce_kernel<<<blocks, 256, 0, s>>>(d, partial, p.splits, L);
+            ++*launches;
+        }
+        if (sym) {
+            const int64_t scn = d.N2 == 1 ? d.scn1 : d.scn2;
+            const int blocks = static_cast<int>(std::min<int64_t>((d.M * d.M + 255) / 256, 8 * num_sms));
+            sym_mirror_kernel<<<blocks, 256, 0, s>>>(d.C, d.M, d.scm, scn);
             ++*launches;
         }
         return 0;

@@ -62,6 +62,11 @@ struct GemmDesc {
     // sum (D(m,n) - acc)^2 with D addressed like C; one partial per CTA.
     const double* D = nullptr;
     double* energy_partials = nullptr;  // >= grid size entries
+    // C = A A^T-like symmetric result (M == N, C column- or row-major square):
+    // on the fast kernel only the tiles touching the lower triangle are
+    // computed and the strict upper triangle is mirrored from it afterwards
+    // (ignored, i.e. everything computed, on the general kernel)
+    bool symmetric = false;
 };
 
 // Enqueue; returns the number of CTAs used for the energy epilogue (0 when

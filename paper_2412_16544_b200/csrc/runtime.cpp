@@ -428,6 +428,7 @@ DT gram(Context& c, const DT& t, int mode, bool reduce) {
     d.C = G.data();
     d.scm = 1;
     d.scn1 = sp.J;
+    d.symmetric = true;
     run_gemm(c, d);
     if (reduce) c.allreduce(G.data(), sp.J * sp.J);
     return G;
