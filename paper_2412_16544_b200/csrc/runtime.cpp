@@ -561,12 +561,43 @@ std::vector<Truncation> finish_tri_batch(Context& c, const std::vector<TriSolve>
                                          const std::vector<double>& noise) {
     const size_t m = ts.size();
     std::vector<Truncation> out(m);
+    if (m > 200) {  // (the pinned staging block holds 4 doubles per node) one by one
+        for (size_t j = 0; j < m; ++j)
+            out[j] = finish_tri(c, ts[j], G[j], rows[j], cols[j], eps_abs, min_rank, refine[j], noise[j]);
+        return out;
+    }
     std::vector<char> done(m, 0);
+    // every node's eigenvalues in one read-back (pinned staging, one stream
+    // synchronisation for the layer instead of one per node)
+    std::vector<std::vector<double>> lam(m);
+    {
+        int64_t total = 0;
+        for (size_t j = 0; j < m; ++j) total += rows[j];
+        const bool staged = total <= 896;  // h_sc holds 1024 doubles; [960..) belongs to the stream slots
+        int64_t off = 0;
+        for (size_t j = 0; j < m; ++j) {
+            lam[j].resize(static_cast<size_t>(rows[j]));
+            if (staged) {
+                HTR_CUDA(cudaMemcpyAsync(c.h_sc + off, ts[j].lam->p, sizeof(double) * static_cast<size_t>(rows[j]),
+                                         cudaMemcpyDeviceToHost, c.s));
+                off += rows[j];
+            } else {
+                c.fetch(ts[j].lam->p, rows[j], lam[j].data());
+            }
+        }
+        if (staged) {
+            HTR_CUDA(cudaStreamSynchronize(c.s));
+            off = 0;
+            for (size_t j = 0; j < m; ++j) {
+                std::copy(c.h_sc + off, c.h_sc + off + rows[j], lam[j].begin());
+                off += rows[j];
+            }
+        }
+    }
     for (size_t j = 0; j < m; ++j) {
         if (!refine[j]) continue;
         const int64_t n = rows[j];
-        std::vector<double> lh(static_cast<size_t>(n));
-        c.fetch(ts[j].lam->p, n, lh.data());
+        const std::vector<double>& lh = lam[j];
         const double lmax = std::max({lh[0], noise[j], 0.0});
         if (lmax > 0.0 && eps_abs * eps_abs < refine_threshold(n) * lmax) {
             int64_t s0 = 0;
@@ -578,31 +609,34 @@ std::vector<Truncation> finish_tri_batch(Context& c, const std::vector<TriSolve>
         }
     }
     std::vector<BufPtr> infos(m);
+    size_t pending = 0;
     for (size_t j = 0; j < m; ++j) {
         if (done[j]) continue;
         infos[j] = c.alloc(4);
         launch_rank_rule(ts[j].lam->p, std::min(rows[j], cols[j]), rows[j], eps_abs, min_rank, nullptr, infos[j]->p, c.s,
                          &c.launches);
+        HTR_CUDA(cudaMemcpyAsync(c.h_sc + 4 * pending, infos[j]->p, 3 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        ++pending;
     }
     HTR_CUDA(cudaGetLastError());
+    HTR_CUDA(cudaStreamSynchronize(c.s));
     std::vector<char> zero(m, 0);
     std::vector<const double*> Wp, ip;
     std::vector<int64_t> nn, rr;
     std::vector<double*> up;
+    size_t slot = 0;
     for (size_t j = 0; j < m; ++j) {
         if (done[j]) continue;
-        double h[4];
-        c.fetch(infos[j]->p, 3, h);
+        const double* h = c.h_sc + 4 * slot++;
         Truncation& t = out[j];
         t.rank = static_cast<int64_t>(h[0]);
         t.discarded = h[1];
         zero[j] = h[2] == 0.0;
         if (t.rank > 0) {
-            std::vector<double> l(static_cast<size_t>(t.rank));
-            c.fetch(ts[j].lam->p, t.rank, l.data());
+            // (the rank rule does not change the eigenvalues read above)
             t.sigma.resize(static_cast<size_t>(t.rank));
             for (int64_t i = 0; i < t.rank; ++i)
-                t.sigma[static_cast<size_t>(i)] = zero[j] ? 0.0 : std::sqrt(std::max(0.0, l[static_cast<size_t>(i)]));
+                t.sigma[static_cast<size_t>(i)] = zero[j] ? 0.0 : std::sqrt(std::max(0.0, lam[j][static_cast<size_t>(i)]));
         }
         t.u = c.tensor({rows[j], t.rank});
         if (t.rank > 0) {
