@@ -40,14 +40,16 @@ struct Stream {
     int device = 0;
     explicit Stream(int dev);
     ~Stream();
-    // Host-side free lists of small stream-ordered blocks (power-of-two size
-    // classes up to 32 MB): a block released by one Buf is handed to the next
+    // Host-side free lists of stream-ordered blocks (power-of-two size
+    // classes up to 256 MB, at most 1 GB held): a block released by one Buf is handed to the next
     // allocation of its class without a driver call. All work is enqueued on
     // `s`, so the hand-over has exactly cudaFreeAsync + cudaMallocAsync's
     // ordering on that stream; it saves their ~2 us of host time per buffer,
-    // which the latency-bound skip updates (configs 2, 3) pay 5-6 times a batch.
-    static constexpr int kMinClass = 5, kMaxClass = 22;  // 2^5 .. 2^22 doubles
-    static constexpr size_t kCacheCapBytes = size_t{512} << 20;
+    // which the latency-bound skip updates (configs 2, 3) pay 5-6 times a batch,
+    // and the ~0.4 ms a 100 MB cudaMallocAsync can take (config 5's BHT-l2r
+    // waited that long for its projected tensor).
+    static constexpr int kMinClass = 5, kMaxClass = 25;  // 2^5 .. 2^25 doubles
+    static constexpr size_t kCacheCapBytes = size_t{1024} << 20;
     std::mutex mu;
     std::vector<double*> bins[kMaxClass + 1];
     size_t cached_bytes = 0;
