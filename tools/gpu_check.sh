@@ -6,7 +6,7 @@
 # committed under profiles/ are made from them with tools/ncu_multi_summary.py.
 set -u
 mkdir -p gpurun_out
-K='regex:^(fused3|tail3|tail4|quad|gram|tridiag|chol|proj2|gemm|rank_rule|sumsq|sum_partials|basis_defect|take_columns|expand|decode2|cholqr2|orthonormalize|pair_project|mode_small|pad_axis|fill|unfold|field|permute|posdef|jacobi|diff_sumsq|splitk)'
+K='regex:^(fused3|tail3|tail4|quad|gram|tridiag|chol|proj2|gemm|rank_rule|sumsq|sum_partials|basis_defect|take_columns|expand|decode2|cholqr2|orthonormalize|pair_project|mode_small|pad_axis|fill|unfold|field|permute|posdef|jacobi|diff_sumsq|splitk|sym_mirror)'
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.txt 2>&1; echo "TESTS_EXIT=$?" >> gpurun_out/gpu_tests.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; echo "SMOKE_EXIT=$?" >> gpurun_out/smoke.txt
